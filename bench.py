@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""bench.py — particle-steps/s of the GranularGym timestep on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload hero50k|bed1m]
+    python bench.py --impl reference ...        # the reference CPU path (oracle port)
+
+Workloads (BASELINE.json configs):
+  hero50k  config 2: 50k settled column bed (floor + tube wall) with the
+           ExcavationEnv Box scoop on its 7-joint chain, joints at 0.3 x limits,
+           dt = 5e-4, 10 PJA sweeps.  Initial state: bench_data/hero50k_settled.npz
+           (settled once on the GPU, shared by both arms), else settled at start.
+  bed1m    config 4 scale: lattice_bed(1e6) on a floor with a spinning grid SDF tool.
+
+One JSON line on rank 0.  ``value`` is device time (CUDA events per step, L2
+flushed by a 512 MB write before every step); ``e2e`` is wall time through
+the public ``run()`` API with host state uploaded from pinned memory and the
+final state + every step's report read back.  N > 1: independent replicas
+(one per GPU, no data-path collective), max time over ranks.
+"""
+
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import argparse
+import ctypes
+import json
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "particle-steps/s at 50k & 1M particles (1/2/4/8 B200); % of HBM roofline"
+UNIT = "particle-steps/s"
+SETTLED = ROOT / "bench_data" / "hero50k_settled.npz"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="hero50k", choices=["hero50k", "bed1m"])
+    ap.add_argument("--settle", type=int, default=3000)
+    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as td
+
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            td.init_process_group(backend)
+            self.pg = td
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        dev = f"cuda:{self.local}" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def analytic_box_grid(half, spacing):
+    """SdfGrid of a box sampled from its exact SDF (stand-in for a baked mesh)."""
+    from paper_2306_01369_b200.sdf import SdfGrid
+
+    half = np.asarray(half, float)
+    lo = -half - 3 * spacing
+    dims = np.ceil((2 * half + 6 * spacing) / spacing).astype(int) + 1
+    ax = [lo[a] + spacing * np.arange(dims[a]) for a in range(3)]
+    P = np.stack(np.meshgrid(*ax, indexing="ij"), -1).reshape(-1, 3)
+    q = np.abs(P) - half
+    d = np.linalg.norm(np.maximum(q, 0), axis=1) + np.minimum(q.max(1), 0)
+    return SdfGrid(lo, np.full(3, spacing), dims, d.reshape(tuple(dims)))
+
+
+def hero_initial_state(args, with_gpu: bool):
+    """(x, v, t) of the settled 50k column."""
+    if SETTLED.exists():
+        z = np.load(SETTLED)
+        return z["x"].astype(np.float64), z["v"].astype(np.float64), float(z["t"])
+    if not with_gpu:
+        return None
+    import paper_2306_01369_b200 as gg
+
+    sc = gg.hero_scene(50_000)
+    gg.run(sc, args.settle)
+    x = sc.particles.positions.astype(np.float32).astype(np.float64)
+    v = sc.particles.velocities.astype(np.float32).astype(np.float64)
+    return x, v, float(sc.t)
+
+
+def make_scene(args, with_gpu=True):
+    import paper_2306_01369_b200 as gg
+    from paper_2306_01369_b200.beds import add_scoop
+
+    if args.workload == "hero50k":
+        st = hero_initial_state(args, with_gpu)
+        if st is None:
+            raise RuntimeError("no settled state file and no GPU to settle one")
+        x, v, t = st
+        sc = gg.hero_scene(50_000)
+        sc.particles = gg.ParticleSet(x, v)
+        sc.t = t
+        sc.params.timestep = 5e-4
+        add_scoop(sc, action=0.3, depth=0.05)
+        desc = {"workload": "hero50k", "config": "BASELINE configs[1]: 50k bed + kinematic scoop",
+                "n_particles": 50_000, "dt": 5e-4, "solver_iterations": 10,
+                "bodies": "floor + tube wall + Box(0.15,0.1,0.04) scoop on 7-joint chain @0.3 limits"}
+    else:
+        x = gg.lattice_bed(1_000_000).astype(np.float32).astype(np.float64)
+        params = gg.MaterialParams(timestep=5e-4)
+        grid = analytic_box_grid([0.6, 0.4, 0.2], 0.04)
+        top = float(x[:, 2].max())
+        cx, cy = float(np.median(x[:, 0])), float(np.median(x[:, 1]))
+        tool = gg.RigidBody(grid, gg.SpinDriver(axis=[0, 0, 1], rate=1.0, center=[cx, cy, top],
+                                                base_pose=gg.make_pose(np.eye(3), [cx, cy, top - 0.1])),
+                            name="tool")
+        sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
+                      bodies=[gg.RigidBody(gg.HalfSpace(), name="floor"), tool], params=params)
+        desc = {"workload": "bed1m", "config": "BASELINE configs[3] scale: 1M lattice bed + grid SDF tool",
+                "n_particles": 1_000_000, "dt": 5e-4, "solver_iterations": 10,
+                "bodies": "floor + spinning SdfGrid box tool"}
+    return sc, desc
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# byte model and roofline
+# ---------------------------------------------------------------------------
+def bytes_model(n_h: int, S: int, c_pp: float, c_b: float) -> dict:
+    P = int(np.ceil(np.log2(max(n_h, 2)) / 8))
+    per_kernel = {
+        "k_hash_count": 24.0,
+        "k_reorder": 68.0,
+        "k_narrow": 36.0 + 20.0 * c_pp + 32.0 * c_b,
+        "k_sweep": 48.0 + 20.0 * c_pp + 32.0 * c_b,
+        "k_integrate": 80.0,
+    }
+    step = 228.0 + 16.0 * P + 48.0 * S + (S + 1) * (20.0 * c_pp + 32.0 * c_b)
+    return {"per_kernel_per_particle": per_kernel, "step_per_particle": step, "radix_passes": P}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        z = json.loads(p.read_text())
+        return float(z["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    try:
+        z = json.loads(f.read_text())
+        e = z.get(workload, {}).get(kernel)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port on host cores; test infrastructure, timed only)
+# ---------------------------------------------------------------------------
+class _BodyAt:
+    def __init__(self, geometry, pose, omega, v_origin):
+        self.geometry, self.pose, self.omega, self.v_origin = geometry, pose, omega, v_origin
+
+
+def cpu_baseline(sc, x, v, budget_s: float) -> dict:
+    from oracle import granular_oracle as O
+
+    params = sc.params
+    n = len(x)
+    n_h = int(sc.hashmap_size or O.table_size(n))
+    t = sc.t
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        t += params.timestep
+        bodies = []
+        for b in sc.bodies:
+            om, vo = b.driver.twist_at(t)
+            bodies.append(_BodyAt(b.geometry, np.asarray(b.driver.pose_at(t), float), om, vo))
+        x, v, _, _, _ = O.step(x, v, params, bodies, n_h, sc.boundary)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= 200:
+            break
+    return {"value": n * steps / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{steps} oracle steps of the same workload state ({n} particles), "
+                      f"{el:.1f}s, numpy single thread (OPENBLAS_NUM_THREADS=1)"}
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, dist: Dist):
+    """--impl reference: the reference CPU path (oracle port, oracle/_ref absent:
+    the reference is Python) on the host, rank 0 only."""
+    if dist.rank != 0:
+        return
+    sc, desc = make_scene(args, with_gpu=False)
+    x = np.asarray(sc.particles._x, float).copy()
+    v = np.asarray(sc.particles._v, float).copy()
+    per_step_budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
+    # bounded: warmup W steps and K timed steps are each one oracle step sample
+    budget = min(args.cpu_seconds, 60.0)
+    cb = cpu_baseline(sc, x, v, budget)
+    del per_step_budget
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * desc["n_particles"] / cb["value"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": desc, "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, dist: Dist):
+    import paper_2306_01369_b200 as gg
+    from paper_2306_01369_b200 import _native as N
+    from paper_2306_01369_b200.engine import engine_for
+
+    dev = dist.local
+    os.environ.setdefault("CUDA_VISIBLE_DEVICES", os.environ.get("CUDA_VISIBLE_DEVICES", ""))
+    sc, desc = make_scene(args)
+    n = sc.particles.count
+    eng = engine_for(sc)
+    eng.device = dev
+    eng.prepare(sc)
+    nb = len(sc.bodies)
+    K, W = args.steps, args.warmup
+    table, _ = eng.body_tables(sc, W + K)
+    # warm-up (untimed)
+    if W:
+        reps, _, done, st, msg = eng.run_batch(table[:W], nb, 0)
+        if st:
+            raise RuntimeError(msg)
+    lib = N.lib()
+    rows = np.ascontiguousarray(table[W:])
+    step_ms = np.zeros(K, dtype=np.float32)
+    l0 = eng.kernel_launches()
+    clocks = Clocks(dev)
+    clocks.start()
+    dist.barrier()
+    st = lib.gg_bench_steps(eng.ctx, K, N.ptr(rows), nb, args.flush_mb << 20, N.ptr(step_ms))
+    N.check(eng.ctx, st, "gg_bench_steps")
+    dist.barrier()
+    clk = clocks.stop()
+    launches = eng.kernel_launches() - l0
+    rbuf = np.zeros(K, dtype=N.REPORT_DTYPE)
+    bbuf = np.zeros((K, max(nb, 1), 3))
+    nd, es = ctypes.c_int32(0), ctypes.c_int32(-1)
+    st = lib.gg_sync(eng.ctx, N.ptr(rbuf), N.ptr(bbuf), K, ctypes.byref(nd), ctypes.byref(es))
+    if st != N.GG_OK or nd.value != K:
+        raise RuntimeError(f"bench steps failed: status {st} {N.last_error(eng.ctx)}")
+    eng.device_newer = True
+    t_ms = dist.max(float(step_ms.sum()))
+    value = n * K * dist.world / (t_ms / 1000.0)
+    c_pp = float(rbuf["n_contacts"].mean()) / n
+    c_b = float(rbuf["n_body_contacts"].mean()) / n
+
+    # warm (no flush) steady-state loop, for context
+    table2, _ = eng.body_tables(sc, K)
+    t_warm = None
+    reps, _, done, st2, _ = eng.run_batch(table2, nb, 0)
+    if st2 == 0:
+        t_warm = eng.last_batch_ms()
+
+    # per-kernel roofline pass (same schedule, event after every kernel)
+    peak, peak_src = peaks()
+    P = max(args.profile_steps, 1)
+    table3, _ = eng.body_tables(sc, P)
+    kind_ms = np.zeros(11, dtype=np.float32)
+    kind_n = np.zeros(11, dtype=np.int32)
+    st = lib.gg_profile_steps(eng.ctx, P, N.ptr(np.ascontiguousarray(table3)), nb, N.ptr(kind_ms),
+                              N.ptr(kind_n))
+    N.check(eng.ctx, st, "gg_profile_steps")
+    names = [lib.gg_profile_kind_name(k).decode() for k in range(11)]
+    model = bytes_model(eng.n_h, sc.params.solver_iterations, c_pp, c_b)
+    share = {names[k]: float(kind_ms[k] / max(kind_ms.sum(), 1e-9)) for k in range(11)}
+    top = max((k for k in range(11) if names[k] in model["per_kernel_per_particle"]),
+              key=lambda k: kind_ms[k])
+    top_name = names[top]
+    avg_ms = float(kind_ms[top] / max(kind_n[top], 1))
+    bytes_launch = model["per_kernel_per_particle"][top_name] * n
+    achieved = bytes_launch / (avg_ms / 1000.0) / 1e9
+    step_bytes = model["step_per_particle"] * n
+    roofline = {"bound": "hbm", "kernel": top_name, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(top_name, desc["workload"]),
+                "algorithmic_bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
+                "peak_source": peak_src, "kernel_time_share": share,
+                "step_bytes_per_particle": model["step_per_particle"],
+                "step_frac": (value / dist.world) * model["step_per_particle"] / (peak * 1e9)}
+
+    # e2e through the public API: pinned host state -> run(K) -> reports + state back
+    x_host = sc.particles.positions.copy()
+    v_host = sc.particles.velocities.copy()
+    sc2 = sc
+    sc2.particles = gg.ParticleSet(x_host, v_host)
+    px, pv = sc2.particles._x, sc2.particles._v
+    lib.gg_host_register(N.ptr(px), px.nbytes)
+    lib.gg_host_register(N.ptr(pv), pv.nbytes)
+    dist.barrier()
+    t0 = time.perf_counter()
+    _, reports = gg.run(sc2, K)
+    xf = sc2.particles.positions  # device -> host
+    _ = float(xf[0, 0]) + sum(r.kinetic_energy for r in reports)
+    t_e2e = dist.max(time.perf_counter() - t0)
+    lib.gg_host_unregister(N.ptr(px))
+    lib.gg_host_unregister(N.ptr(pv))
+    e2e = {"value": n * K * dist.world / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": (2 * 24 * n) / K + 240 * nb,
+           "d2h_bytes_per_step": (2 * 24 * n) / K + 72 + 24 * nb,
+           "api": "paper_2306_01369_b200.run(scene, K): host state upload, per-step body "
+                  "tables, all StepReports and the final state read back",
+           "wall_s": t_e2e}
+
+    cb = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        x0 = np.asarray(sc.particles.positions, float).copy()
+        v0 = np.asarray(sc.particles.velocities, float).copy()
+        cb = cpu_baseline(sc, x0, v0, args.cpu_seconds)
+
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
+            "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
+            "data": "synthetic (seeded bed, settled on GPU)",
+            "config": {**desc, "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
+                       "l2": f"flushed before every timed step ({args.flush_mb} MB write)",
+                       "c_pp": c_pp, "c_b": c_b, "n_h": eng.n_h,
+                       "warm_ms_per_step": None if t_warm is None else t_warm / K},
+            "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,212 @@
+/*
+ * granusim_b200.h — C-ABI of the B200-native GranularGym timestep.
+ *
+ * The reference (`/root/reference/pkg/src/granusim`) has no FFI: its boundary is
+ * the Python function API.  Every entry point below replaces one reference
+ * function (cited file:line) and is what a ctypes/cffi binding of the reference
+ * package would call.  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - every function returns an int status (GG_OK == 0);  gg_last_error(ctx)
+ *     returns a human-readable message for the last failure on that context.
+ *   - a context owns one CUDA stream on one device; calls on one context are
+ *     not thread-safe, distinct contexts are independent
+ *     (bindings/tests/test_bindings.py:112-124 "concurrent handles").
+ *   - positions / velocities cross the boundary as float64 (n,3) row-major
+ *     host arrays (the reference's ParticleSet layout, scene.py:85-93) or as
+ *     float32 float4 device arrays (the resident layout).
+ *   - gg_step is asynchronous on the context stream; gg_sync waits and returns
+ *     the per-step reports.
+ */
+#ifndef GRANUSIM_B200_H
+#define GRANUSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped back to the reference's exception types) ------ */
+#define GG_OK 0
+#define GG_EINVAL 1        /* ValueError / ValidationError (bad argument)            */
+#define GG_ENONFINITE 2    /* SolverError, contact.py:503-509                        */
+#define GG_ECAPACITY 3     /* per-owner contact slots exhausted (host grows + retries)*/
+#define GG_ECUDA 4         /* CUDA runtime failure                                    */
+#define GG_EPOSITIONS 5    /* ValueError("positions must be finite"), broadphase.py:104-107 */
+
+/* ---- geometry kinds (sdf.py:44-241) -------------------------------------- */
+#define GG_GEOM_SPHERE 1
+#define GG_GEOM_HALFSPACE 2
+#define GG_GEOM_BOX 3
+#define GG_GEOM_CYLINDER 4
+#define GG_GEOM_TUBE 5
+#define GG_GEOM_GRID 6
+
+/* ---- pipeline modes (stepper.py:34-37) ----------------------------------- */
+#define GG_MODE_TWO_LOOPS_SPLIT 0
+#define GG_MODE_TWO_LOOPS_FUSED 1
+#define GG_MODE_ONE_LOOP 2
+
+/* MaterialParams (scene.py:47-82) + CyclicBoundary (scene.py:115-124).
+ * Derived constants are computed on the host exactly as the reference writes
+ * them so device decisions are bit-identical:
+ *   contact_d2   = (2.0 * r) ** 2                       contact.py:261
+ *   coincident_d2 = COINCIDENT_EPS * COINCIDENT_EPS      contact.py:260
+ *   gdt          = timestep * gravity                    contact.py:452          */
+typedef struct gg_params {
+  double radius;
+  double particle_mass;
+  double friction;
+  double baumgarte_alpha;
+  double timestep;
+  double gravity[3];
+  double gamma;
+  double contact_d2;
+  double coincident_d2;
+  double gdt[3];
+  int32_t solver_iterations;
+  int32_t has_boundary;
+  double z_min;
+  double z_max;
+} gg_params;
+
+/* One kinematic body at one step, after RigidBody.update(t) (scene.py:150-153).
+ * aabb_lo/hi are the world AABB `_near_body` computes (contact.py:187-203);
+ * bounded == 0 for geometries whose contact_bounds is None (HalfSpace, Tube). */
+typedef struct gg_body {
+  int32_t kind;      /* GG_GEOM_*                                       */
+  int32_t grid_id;   /* from gg_upload_grid, GG_GEOM_GRID only           */
+  int32_t bounded;
+  int32_t reserved;
+  double shape[4];   /* sphere {R}; halfspace {nx,ny,nz,offset}; box {hx,hy,hz};
+                        cylinder {R, half_height}; tube {R}              */
+  double rot[9];     /* pose[:3,:3], row-major                           */
+  double trans[3];   /* pose[:3,3]                                       */
+  double omega[3];   /* RigidBody.omega                                  */
+  double v_origin[3];/* RigidBody.v_origin                               */
+  double aabb_lo[3];
+  double aabb_hi[3];
+} gg_body;
+
+/* StepReport (stepper.py:40-54), minus wall_time/step_index/body_momentum,
+ * which the host fills (body momentum comes from gg_sync's bm array). */
+typedef struct gg_report {
+  int64_t n_contacts;
+  int64_t n_candidates;
+  int64_t n_body_contacts;
+  int64_t n_coincident;
+  int64_t n_degenerate;
+  double max_penetration;
+  double kinetic_energy;
+  double max_cone_violation;
+  double min_normal_impulse; /* +inf when no contact was live: host maps to 0.0 */
+} gg_report;
+
+typedef struct gg_ctx gg_ctx;
+
+/* Create a context for n particles and an n_h-bucket hash table.
+ * Replaces the implicit state of stepper.step (stepper.py:57-72):
+ * n_h == scene.hashmap_size or default_table_size(n) (broadphase.py:58-60).
+ * max_contacts = per-owner contact slots (grown on GG_ECAPACITY). */
+int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h,
+              int32_t max_bodies, int32_t max_contacts, gg_ctx** out);
+int gg_destroy(gg_ctx* ctx);
+const char* gg_last_error(const gg_ctx* ctx);
+int gg_set_params(gg_ctx* ctx, const gg_params* params);
+
+/* Particle state (ParticleSet.positions/velocities, scene.py:85-112).
+ * Host variants take float64 (n,3) arrays in user order; device variants take
+ * float4 (x,y,z,_) float32 arrays in user order on the context's device. */
+int gg_set_state_f64(gg_ctx* ctx, const double* x, const double* v);
+int gg_get_state_f64(gg_ctx* ctx, double* x, double* v);
+int gg_set_state_f32x4_dev(gg_ctx* ctx, const void* x4, const void* v4);
+int gg_get_state_f32x4_dev(gg_ctx* ctx, void* x4, void* v4);
+
+/* SdfGrid values (sdf.py:179-241): float64 [dims0][dims1][dims2] C-order. */
+int gg_upload_grid(gg_ctx* ctx, const double* values, const int32_t dims[3],
+                   const double origin[3], const double spacing[3], int32_t* grid_id);
+
+/* Enqueue n_steps timesteps (stepper.step, stepper.py:57-135) on the context
+ * stream.  bodies = [n_steps][n_bodies] per-step body tables.  Asynchronous. */
+int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
+            int32_t mode);
+
+/* Detection pass only (detect_contacts / narrowphase_contacts,
+ * contact.py:244-300,372-379) on the current state: broadphase + pp + body
+ * contacts, no solve, no state change.  Fills the contact/broadphase fields
+ * of *out (n_contacts, n_candidates, n_body_contacts, n_coincident,
+ * n_degenerate, max_penetration); gg_tap_contacts then reads the contacts. */
+int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* out);
+
+/* Wait for the enqueued steps.  Writes min(n_steps,cap) reports and the
+ * [n_steps][n_bodies][3] body momenta (StepReport.body_momentum,
+ * contact.py:489-495).  *n_done = steps committed; on failure returns the
+ * status of the failing step and *err_step = its index within the batch
+ * (state is left at that step's input, like the reference which raises
+ * before integrating, stepper.py:99-103). */
+int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
+            int32_t* n_done, int32_t* err_step);
+
+/* Device time of the last gg_step batch (CUDA events on the context stream). */
+int gg_last_batch_ms(gg_ctx* ctx, float* ms);
+
+/* Benchmark helpers (bench.py).  gg_bench_steps runs n_steps like gg_step
+ * but writes flush_bytes to a scratch buffer (L2 flush) before every step
+ * and times each step alone with CUDA events (step_ms[n_steps]).
+ * gg_profile_steps runs the same schedule un-graphed with an event after
+ * every kernel and returns per-kernel-kind device time (kind_ms[11]) and
+ * launch counts; gg_profile_kind_name(k) names kind k.  Both commit state. */
+int gg_bench_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
+                   int64_t flush_bytes, float* step_ms);
+int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
+                     float* kind_ms, int32_t* kind_launches);
+const char* gg_profile_kind_name(int32_t k);
+
+/* ---- parity taps (read-only views of the last committed step) ------------
+ * cells/hashes: position_cells + spatial_hash of the CURRENT state in user
+ *   order (broadphase.py:33-55, the SpatialHashmap.cells/.hashes fields);
+ * order: np.argsort(hashes, kind="stable") (broadphase.py:160), user ids.   */
+int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order);
+
+/* Contacts detected by the last step (narrowphase_contacts, contact.py:244-300)
+ * as user-id directed pairs.  kind 0 = particle (other = particle id),
+ * kind 1 = body (other = body index).  e1/psi in float64 (computed in fp64,
+ * stored fp32 on device).  *count = total; arrays must hold cap entries. */
+int gg_tap_contacts(gg_ctx* ctx, int64_t cap, int64_t* count, int32_t* owner,
+                    int32_t* other, int32_t* kind, double* psi, double* e1);
+
+/* Standalone SDF query (penetration_depth, sdf.py:472-512) for n world points
+ * against one posed body; out psi[n], normal[n*3], hit[n] (0/1), n_degenerate. */
+int gg_penetration(gg_ctx* ctx, const gg_body* body, const double* points, int64_t n,
+                   double radius, double* psi, double* normal, int32_t* hit,
+                   int64_t* n_degenerate);
+
+/* Standalone spatial hash (spatial_hash, broadphase.py:44-55) of k cells. */
+int gg_spatial_hash(gg_ctx* ctx, const int64_t* cells, int64_t k, int64_t n_h,
+                    int64_t* out);
+
+/* Contact-slot capacity.  gg_sync returns GG_ECAPACITY when an owner had more
+ * contacts than slots; gg_required_contacts reports how many it needed and
+ * gg_set_max_contacts regrows the slot arrays (the step is then re-run from
+ * its uncommitted input, "x2 growth between steps"). */
+int gg_set_max_contacts(gg_ctx* ctx, int32_t max_contacts);
+int gg_max_contacts(const gg_ctx* ctx);
+int gg_required_contacts(gg_ctx* ctx);
+
+/* Page-lock host arrays so gg_set/get_state_f64 run at full PCIe speed. */
+int gg_host_register(void* ptr, int64_t bytes);
+int gg_host_unregister(void* ptr);
+
+/* The context's cudaStream_t (for interop with torch events). */
+void* gg_stream(gg_ctx* ctx);
+
+/* Library build info: arch string and number of kernels launched so far on
+ * this context (the bench's gpu_launches evidence). */
+const char* gg_build_info(void);
+int64_t gg_kernel_launches(const gg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRANUSIM_B200_H */

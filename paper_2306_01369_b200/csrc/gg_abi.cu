@@ -1,0 +1,924 @@
+// gg_abi.cu — context, buffers, the step schedule (CUDA graph) and the
+// extern "C" entry points declared in include/granusim_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gg_kernels.cuh"
+
+using namespace gg;
+
+struct gg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  gg_params P{};
+  long long n = 0, n_h = 0;
+  int K = 16;
+  int max_bodies = 0;
+  int nblocks = 0;
+  int ntiles = 0;
+  Dev D{};
+  std::string err;
+  long long launches = 0;
+
+  // batch buffers
+  int batch_cap = 0;
+  gg_body* d_bodies = nullptr;
+  gg_body* h_bodies = nullptr;  // pinned staging
+  gg_report* d_reports = nullptr;
+  double* d_bm = nullptr;
+  Ctl* h_ctl = nullptr;  // pinned
+  int last_batch = 0;
+  int last_nb = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // grids
+  std::vector<DevGrid> grids;
+  DevGrid* d_grids = nullptr;
+  int d_grids_cap = 0;
+  double* d_gvals = nullptr;
+  long long gvals_cap = 0, gvals_used = 0;
+
+  // staging for f64 state / taps
+  double* d_stage = nullptr;  // 6n doubles
+
+  // contact taps read UID[cur ^ 1] after gg_detect (uncommitted sort)
+  bool tap_uncommitted = false;
+
+  // bench helpers
+  void* flush_buf = nullptr;
+  long long flush_bytes = 0;
+  std::vector<cudaEvent_t> evpool;
+
+  // graph of one step
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_dirty = true;
+
+  std::vector<void*> owned;  // fixed-size allocations freed at destroy
+};
+
+namespace {
+
+#define GG_STR2(x) #x
+#define GG_STR(x) GG_STR2(x)
+const char* kBuildInfo = "granusim_b200 sm_100a nvcc " GG_STR(__CUDACC_VER_MAJOR__) "." GG_STR(__CUDACC_VER_MINOR__);
+
+int fail(gg_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(gg_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, GG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                              \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);  \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(gg_ctx* ctx, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+  if (e == cudaSuccess) {
+    *p = static_cast<T*>(q);
+    ctx->owned.push_back(q);
+  }
+  return e;
+}
+
+void dfree(gg_ctx* ctx, void* p) {
+  if (!p) return;
+  auto it = std::find(ctx->owned.begin(), ctx->owned.end(), p);
+  if (it != ctx->owned.end()) ctx->owned.erase(it);
+  cudaFree(p);
+}
+
+int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock); }
+
+int validate_params(gg_ctx* ctx, const gg_params* p) {
+  if (!p) return fail(ctx, GG_EINVAL, "params is NULL");
+  if (!(p->radius > 0)) return fail(ctx, GG_EINVAL, "radius must be > 0");
+  if (!(p->particle_mass > 0)) return fail(ctx, GG_EINVAL, "particle_mass must be > 0");
+  if (!(p->friction >= 0)) return fail(ctx, GG_EINVAL, "friction must be >= 0");
+  if (!(p->timestep > 0)) return fail(ctx, GG_EINVAL, "timestep must be > 0");
+  if (p->solver_iterations < 1) return fail(ctx, GG_EINVAL, "solver_iterations must be >= 1");
+  if (p->has_boundary && !(p->z_min < p->z_max))
+    return fail(ctx, GG_EINVAL, "cyclic boundary requires z_min < z_max");
+  return GG_OK;
+}
+
+void fill_params(gg_ctx* ctx) {
+  const gg_params& P = ctx->P;
+  Dev& D = ctx->D;
+  D.r = P.radius;
+  D.two_r = 2.0 * P.radius;
+  D.contact_d2 = P.contact_d2;
+  D.coinc_d2 = P.coincident_d2;
+  D.mass = P.particle_mass;
+  D.mu = P.friction;
+  D.alpha = P.baumgarte_alpha;
+  D.dt = P.timestep;
+  D.gamma = P.gamma;
+  D.gdt0 = P.gdt[0];
+  D.gdt1 = P.gdt[1];
+  D.gdt2 = P.gdt[2];
+  D.S = P.solver_iterations;
+  D.has_boundary = P.has_boundary;
+  D.z_min = P.z_min;
+  D.band = P.z_max - P.z_min;
+}
+
+int alloc_slots(gg_ctx* ctx, int K) {
+  Dev& D = ctx->D;
+  dfree(ctx, D.cgeo);
+  dfree(ctx, D.coth);
+  dfree(ctx, D.cvb);
+  D.cgeo = nullptr;
+  D.coth = nullptr;
+  D.cvb = nullptr;
+  const size_t slots = static_cast<size_t>(K) * static_cast<size_t>(std::max<long long>(ctx->n, 1));
+  CK(dalloc(ctx, &D.cgeo, slots));
+  CK(dalloc(ctx, &D.coth, slots));
+  CK(dalloc(ctx, &D.cvb, slots));
+  ctx->K = K;
+  D.K = K;
+  ctx->graph_dirty = true;
+  return GG_OK;
+}
+
+int ensure_batch(gg_ctx* ctx, int steps, int nb) {
+  const int need = std::max(steps, 1);
+  const int nbx = std::max(nb, 1);
+  if (need <= ctx->batch_cap && nbx <= std::max(ctx->max_bodies, 1)) return GG_OK;
+  if (nb > ctx->max_bodies) {
+    // grow the body capacity: momentum partials depend on it
+    ctx->max_bodies = nb;
+    dfree(ctx, ctx->D.bm_part);
+    dfree(ctx, ctx->D.bm_glob);
+    ctx->D.bm_part = nullptr;
+    ctx->D.bm_glob = nullptr;
+    CK(dalloc(ctx, &ctx->D.bm_part, static_cast<size_t>(ctx->nblocks) * nb * 3));
+    CK(dalloc(ctx, &ctx->D.bm_glob, static_cast<size_t>(nb) * 3));
+  }
+  int cap = std::max(ctx->batch_cap, 1);
+  while (cap < need) cap *= 2;
+  dfree(ctx, ctx->d_bodies);
+  dfree(ctx, ctx->d_reports);
+  dfree(ctx, ctx->d_bm);
+  if (ctx->h_bodies) cudaFreeHost(ctx->h_bodies);
+  ctx->d_bodies = nullptr;
+  ctx->d_reports = nullptr;
+  ctx->d_bm = nullptr;
+  ctx->h_bodies = nullptr;
+  const int mb = std::max(ctx->max_bodies, 1);
+  CK(dalloc(ctx, &ctx->d_bodies, static_cast<size_t>(cap) * mb));
+  CK(dalloc(ctx, &ctx->d_reports, static_cast<size_t>(cap)));
+  CK(dalloc(ctx, &ctx->d_bm, static_cast<size_t>(cap) * mb * 3));
+  CK(cudaMallocHost(&ctx->h_bodies, sizeof(gg_body) * static_cast<size_t>(cap) * mb));
+  ctx->batch_cap = cap;
+  ctx->graph_dirty = true;
+  return GG_OK;
+}
+
+// The step schedule: 9 + S kernels and one memset, all on ctx->stream.
+int enqueue_step(gg_ctx* ctx) {
+  const Dev& D = ctx->D;
+  cudaStream_t s = ctx->stream;
+  const int nbn = ctx->nblocks;
+  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  k_hash_count<<<nbn, kBlock, 0, s>>>(D);
+  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  k_scatter<<<nbn, kBlock, 0, s>>>(D);
+  k_reorder<<<nbn, kBlock, 0, s>>>(D);
+  k_narrow<<<nbn, kBlock, 0, s>>>(D);
+  for (int it = 0; it < D.S; ++it) k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
+  k_integrate<<<nbn, kBlock, 0, s>>>(D);
+  k_finalize<<<1, kBlock, 0, s>>>(D);
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int kernels_per_step(const gg_ctx* ctx) { return 9 + ctx->D.S; }
+
+// Same schedule as enqueue_step, with an event after every kernel so each
+// kernel kind's device time can be attributed (bench roofline pass).
+constexpr int kProfKinds = 11;
+const char* kProfNames[kProfKinds] = {"memset_counts", "k_hash_count", "k_scan_tiles", "k_scan_top",
+                                      "k_scan_apply",  "k_scatter",    "k_reorder",    "k_narrow",
+                                      "k_sweep",       "k_integrate",  "k_finalize"};
+
+int ensure_events(gg_ctx* ctx, size_t n) {
+  while (ctx->evpool.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->evpool.push_back(e);
+  }
+  return GG_OK;
+}
+
+int enqueue_step_profiled(gg_ctx* ctx, cudaEvent_t* ev, int* kind_of_interval) {
+  const Dev& D = ctx->D;
+  cudaStream_t s = ctx->stream;
+  const int nbn = ctx->nblocks;
+  int e = 0;
+  auto mark = [&](int kind) {
+    cudaEventRecord(ev[e + 1], s);
+    kind_of_interval[e] = kind;
+    ++e;
+  };
+  cudaEventRecord(ev[0], s);
+  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  mark(0);
+  k_hash_count<<<nbn, kBlock, 0, s>>>(D);
+  mark(1);
+  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  mark(2);
+  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+  mark(3);
+  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  mark(4);
+  k_scatter<<<nbn, kBlock, 0, s>>>(D);
+  mark(5);
+  k_reorder<<<nbn, kBlock, 0, s>>>(D);
+  mark(6);
+  k_narrow<<<nbn, kBlock, 0, s>>>(D);
+  mark(7);
+  for (int it = 0; it < D.S; ++it) {
+    k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
+    mark(8);
+  }
+  k_integrate<<<nbn, kBlock, 0, s>>>(D);
+  mark(9);
+  k_finalize<<<1, kBlock, 0, s>>>(D);
+  mark(10);
+  CK(cudaGetLastError());
+  return e;  // number of intervals
+}
+
+int refresh_dev(gg_ctx* ctx) {
+  Dev& D = ctx->D;
+  D.bodies = ctx->d_bodies;
+  D.grids = ctx->d_grids;
+  D.gvals = ctx->d_gvals;
+  D.reports = ctx->d_reports;
+  D.bm_out = ctx->d_bm;
+  return GG_OK;
+}
+
+int build_graph(gg_ctx* ctx) {
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  refresh_dev(ctx);
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int st = enqueue_step(ctx);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (st != GG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&ctx->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+  ctx->graph_dirty = false;
+  return GG_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    cudaGetDevice(&now);
+    if (prev >= 0 && now != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* gg_build_info(void) { return kBuildInfo; }
+
+int64_t gg_kernel_launches(const gg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* gg_last_error(const gg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32_t max_bodies,
+              int32_t max_contacts, gg_ctx** out) {
+  if (!out) return GG_EINVAL;
+  *out = nullptr;
+  gg_ctx* ctx = new gg_ctx();
+  int st = validate_params(ctx, params);
+  if (st != GG_OK) {
+    // keep the context so the caller can read the message
+    *out = ctx;
+    return st;
+  }
+  if (n < 1 || n >= (1ll << 31) || n_h < 1 || n_h >= (1ll << 31)) {
+    *out = ctx;
+    return fail(ctx, GG_EINVAL, "need 1 <= n < 2^31 and 1 <= n_h < 2^31");
+  }
+  *out = ctx;
+  ctx->device = device;
+  DeviceGuard guard(device);
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ctx->ev0));
+  CK(cudaEventCreate(&ctx->ev1));
+  ctx->P = *params;
+  ctx->n = n;
+  ctx->n_h = n_h;
+  ctx->max_bodies = std::max(max_bodies, 0);
+  ctx->nblocks = blocks_for(n);
+  ctx->ntiles = static_cast<int>((n_h + kScanTile - 1) / kScanTile);
+  Dev& D = ctx->D;
+  D.n = static_cast<int>(n);
+  D.nblocks = ctx->nblocks;
+  D.H.n_h = n_h;
+  D.H.pow2 = (n_h & (n_h - 1)) == 0 ? 1 : 0;
+  D.H.mask = static_cast<uint32_t>(n_h - 1);
+  fill_params(ctx);
+  D.nb = 0;
+  for (int b = 0; b < 2; ++b) {
+    CK(dalloc(ctx, &D.X[b], n));
+    CK(dalloc(ctx, &D.V[b], n));
+    CK(dalloc(ctx, &D.UID[b], n));
+    CK(dalloc(ctx, &D.W[b], n));
+  }
+  CK(dalloc(ctx, &D.key, n));
+  CK(dalloc(ctx, &D.arrive, n));
+  CK(dalloc(ctx, &D.tmp, n));
+  CK(dalloc(ctx, &D.cnt, n_h));
+  CK(dalloc(ctx, &D.start, n_h + 1));
+  CK(dalloc(ctx, &D.tile, ctx->ntiles));
+  CK(dalloc(ctx, &D.Xs, n));
+  CK(dalloc(ctx, &D.V0, n));
+  CK(dalloc(ctx, &D.ccount, n));
+  CK(dalloc(ctx, &D.acc, 1));
+  CK(dalloc(ctx, &D.ke_part, ctx->nblocks));
+  CK(dalloc(ctx, &D.bm_part, static_cast<size_t>(ctx->nblocks) * std::max(ctx->max_bodies, 1) * 3));
+  CK(dalloc(ctx, &D.bm_glob, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3));
+  CK(dalloc(ctx, &D.ctl, 1));
+  CK(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
+  st = alloc_slots(ctx, max_contacts > 0 ? max_contacts : 16);
+  if (st != GG_OK) return st;
+  // start[n_h] = n never changes for a context
+  const uint32_t nn = static_cast<uint32_t>(n);
+  CK(cudaMemcpy(D.start + n_h, &nn, sizeof(uint32_t), cudaMemcpyHostToDevice));
+  CK(cudaMemset(D.ctl, 0, sizeof(Ctl)));
+  CK(cudaMemset(D.UID[0], 0, sizeof(int) * n));
+  st = ensure_batch(ctx, 1, ctx->max_bodies);
+  if (st != GG_OK) return st;
+  // zero-state until the caller uploads
+  CK(cudaMemset(D.X[0], 0, sizeof(float4) * n));
+  CK(cudaMemset(D.V[0], 0, sizeof(float4) * n));
+  CK(cudaDeviceSynchronize());
+  return GG_OK;
+}
+
+int gg_destroy(gg_ctx* ctx) {
+  if (!ctx) return GG_OK;
+  {
+    DeviceGuard guard(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
+    for (void* p : ctx->owned) cudaFree(p);
+    ctx->owned.clear();
+    if (ctx->h_bodies) cudaFreeHost(ctx->h_bodies);
+    if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+  return GG_OK;
+}
+
+int gg_set_params(gg_ctx* ctx, const gg_params* params) {
+  if (!ctx) return GG_EINVAL;
+  int st = validate_params(ctx, params);
+  if (st != GG_OK) return st;
+  ctx->P = *params;
+  fill_params(ctx);
+  ctx->graph_dirty = true;
+  return GG_OK;
+}
+
+int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
+  if (!ctx || K < 1) return fail(ctx, GG_EINVAL, "max_contacts must be >= 1");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return alloc_slots(ctx, K);
+}
+
+int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
+
+static int ensure_stage(gg_ctx* ctx) {
+  if (ctx->d_stage) return GG_OK;
+  CK(dalloc(ctx, &ctx->d_stage, static_cast<size_t>(ctx->n) * 6));
+  return GG_OK;
+}
+
+int gg_set_state_f64(gg_ctx* ctx, const double* x, const double* v) {
+  if (!ctx || !x || !v) return fail(ctx, GG_EINVAL, "null argument");
+  DeviceGuard guard(ctx->device);
+  int st = ensure_stage(ctx);
+  if (st != GG_OK) return st;
+  const size_t bytes = sizeof(double) * 3 * static_cast<size_t>(ctx->n);
+  CK(cudaMemcpyAsync(ctx->d_stage, x, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_stage + 3 * ctx->n, v, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  k_load_f64<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, ctx->d_stage,
+                                                        ctx->d_stage + 3 * ctx->n);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GG_OK;
+}
+
+int gg_get_state_f64(gg_ctx* ctx, double* x, double* v) {
+  if (!ctx || !x || !v) return fail(ctx, GG_EINVAL, "null argument");
+  DeviceGuard guard(ctx->device);
+  int st = ensure_stage(ctx);
+  if (st != GG_OK) return st;
+  const size_t bytes = sizeof(double) * 3 * static_cast<size_t>(ctx->n);
+  k_store_f64<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, ctx->d_stage,
+                                                         ctx->d_stage + 3 * ctx->n);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(x, ctx->d_stage, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(v, ctx->d_stage + 3 * ctx->n, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GG_OK;
+}
+
+int gg_set_state_f32x4_dev(gg_ctx* ctx, const void* x4, const void* v4) {
+  if (!ctx || !x4 || !v4) return fail(ctx, GG_EINVAL, "null argument");
+  DeviceGuard guard(ctx->device);
+  k_load_f4<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, static_cast<const float4*>(x4),
+                                                       static_cast<const float4*>(v4));
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GG_OK;
+}
+
+int gg_get_state_f32x4_dev(gg_ctx* ctx, void* x4, void* v4) {
+  if (!ctx || !x4 || !v4) return fail(ctx, GG_EINVAL, "null argument");
+  DeviceGuard guard(ctx->device);
+  k_store_f4<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, static_cast<float4*>(x4),
+                                                        static_cast<float4*>(v4));
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GG_OK;
+}
+
+int gg_upload_grid(gg_ctx* ctx, const double* values, const int32_t dims[3],
+                   const double origin[3], const double spacing[3], int32_t* grid_id) {
+  if (!ctx || !values || !dims || !origin || !spacing || !grid_id)
+    return fail(ctx, GG_EINVAL, "null argument");
+  for (int a = 0; a < 3; ++a)
+    if (dims[a] < 2) return fail(ctx, GG_EINVAL, "grid dims must be >= 2 on every axis");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const long long count = static_cast<long long>(dims[0]) * dims[1] * dims[2];
+  if (ctx->gvals_used + count > ctx->gvals_cap) {
+    long long cap = std::max<long long>(ctx->gvals_cap * 2, ctx->gvals_used + count);
+    double* nv = nullptr;
+    CK(dalloc(ctx, &nv, static_cast<size_t>(cap)));
+    if (ctx->gvals_used)
+      CK(cudaMemcpy(nv, ctx->d_gvals, sizeof(double) * ctx->gvals_used, cudaMemcpyDeviceToDevice));
+    dfree(ctx, ctx->d_gvals);
+    ctx->d_gvals = nv;
+    ctx->gvals_cap = cap;
+  }
+  CK(cudaMemcpy(ctx->d_gvals + ctx->gvals_used, values, sizeof(double) * count,
+                cudaMemcpyHostToDevice));
+  DevGrid G{};
+  for (int a = 0; a < 3; ++a) {
+    G.origin[a] = origin[a];
+    G.spacing[a] = spacing[a];
+    G.dims[a] = dims[a];
+    G.upper[a] = origin[a] + static_cast<double>(dims[a] - 1) * spacing[a];
+  }
+  G.offset = ctx->gvals_used;
+  ctx->gvals_used += count;
+  ctx->grids.push_back(G);
+  if (static_cast<int>(ctx->grids.size()) > ctx->d_grids_cap) {
+    dfree(ctx, ctx->d_grids);
+    ctx->d_grids = nullptr;
+    ctx->d_grids_cap = std::max<int>(8, 2 * static_cast<int>(ctx->grids.size()));
+    CK(dalloc(ctx, &ctx->d_grids, ctx->d_grids_cap));
+  }
+  CK(cudaMemcpy(ctx->d_grids, ctx->grids.data(), sizeof(DevGrid) * ctx->grids.size(),
+                cudaMemcpyHostToDevice));
+  *grid_id = static_cast<int32_t>(ctx->grids.size() - 1);
+  ctx->graph_dirty = true;
+  return GG_OK;
+}
+
+int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies, int32_t mode) {
+  if (!ctx) return GG_EINVAL;
+  if (n_steps < 0) return fail(ctx, GG_EINVAL, "n_steps must be >= 0");
+  if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
+  if (mode < 0 || mode > 2) return fail(ctx, GG_EINVAL, "unknown pipeline mode");
+  for (long long i = 0; i < static_cast<long long>(n_steps) * n_bodies; ++i) {
+    const gg_body& b = bodies[i];
+    if (b.kind < GG_GEOM_SPHERE || b.kind > GG_GEOM_GRID)
+      return fail(ctx, GG_EINVAL, "unknown geometry kind");
+    if (b.kind == GG_GEOM_GRID && (b.grid_id < 0 || b.grid_id >= (int)ctx->grids.size()))
+      return fail(ctx, GG_EINVAL, "unknown grid id");
+  }
+  DeviceGuard guard(ctx->device);
+  // the pinned staging buffer is reused: the previous batch must be done
+  CK(cudaStreamSynchronize(ctx->stream));
+  int st = ensure_batch(ctx, n_steps, n_bodies);
+  if (st != GG_OK) return st;
+  if (ctx->D.nb != n_bodies) {
+    ctx->D.nb = n_bodies;
+    ctx->graph_dirty = true;
+  }
+  if (n_bodies > 0) {
+    const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * n_bodies;
+    std::memcpy(ctx->h_bodies, bodies, bytes);
+    CK(cudaMemcpyAsync(ctx->d_bodies, ctx->h_bodies, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (ctx->graph_dirty) {
+    st = build_graph(ctx);
+    if (st != GG_OK) return st;
+  }
+  refresh_dev(ctx);
+  k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  for (int i = 0; i < n_steps; ++i) CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->launches += 1 + static_cast<long long>(n_steps) * kernels_per_step(ctx);
+  ctx->last_batch = n_steps;
+  ctx->last_nb = n_bodies;
+  ctx->tap_uncommitted = false;
+  return GG_OK;
+}
+
+int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* out) {
+  if (!ctx) return GG_EINVAL;
+  if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  int st = ensure_batch(ctx, 1, n_bodies);
+  if (st != GG_OK) return st;
+  if (ctx->D.nb != n_bodies) {
+    ctx->D.nb = n_bodies;
+    ctx->graph_dirty = true;
+  }
+  if (n_bodies > 0)
+    CK(cudaMemcpy(ctx->d_bodies, bodies, sizeof(gg_body) * n_bodies, cudaMemcpyHostToDevice));
+  refresh_dev(ctx);
+  const Dev& D = ctx->D;
+  cudaStream_t s = ctx->stream;
+  k_batch_begin<<<1, 1, 0, s>>>(D);
+  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  k_hash_count<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  k_scatter<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  k_reorder<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  k_narrow<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  ctx->launches += 9;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  ctx->tap_uncommitted = true;
+  CK(cudaMemcpy(ctx->h_ctl, D.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  if (ctx->h_ctl->err == GG_EPOSITIONS) return fail(ctx, GG_EPOSITIONS, "positions must be finite");
+  if (ctx->h_ctl->err == GG_ECAPACITY) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "contact capacity exceeded: an owner has %d contacts > %d slots",
+                  ctx->h_ctl->cap_needed, ctx->K);
+    return fail(ctx, GG_ECAPACITY, buf);
+  }
+  if (out) {
+    Acc a;
+    CK(cudaMemcpy(&a, D.acc, sizeof(Acc), cudaMemcpyDeviceToHost));
+    std::memset(out, 0, sizeof(gg_report));
+    out->n_contacts = static_cast<int64_t>(a.n_pp);
+    out->n_candidates = static_cast<int64_t>(a.n_cand);
+    out->n_body_contacts = static_cast<int64_t>(a.n_body);
+    out->n_coincident = static_cast<int64_t>(a.n_coinc);
+    out->n_degenerate = static_cast<int64_t>(a.n_deg);
+    double mp;
+    std::memcpy(&mp, &a.max_psi_bits, sizeof(double));
+    out->max_penetration = mp;
+  }
+  return GG_OK;
+}
+
+static int stage_bodies(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  int st = ensure_batch(ctx, n_steps, n_bodies);
+  if (st != GG_OK) return st;
+  if (ctx->D.nb != n_bodies) {
+    ctx->D.nb = n_bodies;
+    ctx->graph_dirty = true;
+  }
+  if (n_bodies > 0) {
+    const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * n_bodies;
+    std::memcpy(ctx->h_bodies, bodies, bytes);
+    CK(cudaMemcpyAsync(ctx->d_bodies, ctx->h_bodies, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (ctx->graph_dirty) {
+    st = build_graph(ctx);
+    if (st != GG_OK) return st;
+  }
+  refresh_dev(ctx);
+  return GG_OK;
+}
+
+int gg_bench_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
+                   int64_t flush_bytes, float* step_ms) {
+  if (!ctx || n_steps < 1 || !step_ms) return fail(ctx, GG_EINVAL, "bad bench arguments");
+  DeviceGuard guard(ctx->device);
+  int st = stage_bodies(ctx, n_steps, bodies, n_bodies);
+  if (st != GG_OK) return st;
+  if (flush_bytes > ctx->flush_bytes) {
+    dfree(ctx, ctx->flush_buf);
+    ctx->flush_buf = nullptr;
+    char* fb = nullptr;
+    CK(dalloc(ctx, &fb, static_cast<size_t>(flush_bytes)));
+    ctx->flush_buf = fb;
+    ctx->flush_bytes = flush_bytes;
+  }
+  st = ensure_events(ctx, 2 * static_cast<size_t>(n_steps));
+  if (st != GG_OK) return st;
+  k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
+  for (int i = 0; i < n_steps; ++i) {
+    if (flush_bytes > 0)
+      CK(cudaMemsetAsync(ctx->flush_buf, i & 0xff, static_cast<size_t>(flush_bytes), ctx->stream));
+    CK(cudaEventRecord(ctx->evpool[2 * i], ctx->stream));
+    CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    CK(cudaEventRecord(ctx->evpool[2 * i + 1], ctx->stream));
+  }
+  ctx->launches += 1 + static_cast<long long>(n_steps) * kernels_per_step(ctx);
+  ctx->last_batch = n_steps;
+  ctx->last_nb = n_bodies;
+  ctx->tap_uncommitted = false;
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n_steps; ++i)
+    CK(cudaEventElapsedTime(&step_ms[i], ctx->evpool[2 * i], ctx->evpool[2 * i + 1]));
+  return GG_OK;
+}
+
+int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
+                     float* kind_ms, int32_t* kind_launches) {
+  if (!ctx || n_steps < 1 || !kind_ms) return fail(ctx, GG_EINVAL, "bad profile arguments");
+  DeviceGuard guard(ctx->device);
+  int st = stage_bodies(ctx, n_steps, bodies, n_bodies);
+  if (st != GG_OK) return st;
+  const int per = 11 + ctx->D.S;
+  st = ensure_events(ctx, static_cast<size_t>(per + 1));
+  if (st != GG_OK) return st;
+  for (int k = 0; k < kProfKinds; ++k) {
+    kind_ms[k] = 0.f;
+    if (kind_launches) kind_launches[k] = 0;
+  }
+  std::vector<int> kinds(per + 1);
+  k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
+  for (int i = 0; i < n_steps; ++i) {
+    const int m = enqueue_step_profiled(ctx, ctx->evpool.data(), kinds.data());
+    if (m < 0) return m;
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int e = 0; e < m; ++e) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ctx->evpool[e], ctx->evpool[e + 1]));
+      kind_ms[kinds[e]] += t;
+      if (kind_launches && kinds[e] > 0) kind_launches[kinds[e]] += 1;
+    }
+  }
+  ctx->launches += 1 + static_cast<long long>(n_steps) * kernels_per_step(ctx);
+  ctx->last_batch = n_steps;
+  ctx->last_nb = n_bodies;
+  ctx->tap_uncommitted = false;
+  return GG_OK;
+}
+
+const char* gg_profile_kind_name(int32_t k) {
+  return (k >= 0 && k < kProfKinds) ? kProfNames[k] : "";
+}
+
+int gg_last_batch_ms(gg_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return GG_EINVAL;
+  DeviceGuard guard(ctx->device);
+  CK(cudaEventSynchronize(ctx->ev1));
+  CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+  return GG_OK;
+}
+
+int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
+            int32_t* n_done, int32_t* err_step) {
+  if (!ctx) return GG_EINVAL;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(ctx->h_ctl, ctx->D.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  const Ctl& c = *ctx->h_ctl;
+  const int done = std::min(c.step, ctx->last_batch);
+  if (n_done) *n_done = done;
+  if (err_step) *err_step = c.err ? c.err_step : -1;
+  const int ncopy = std::min(done, cap);
+  if (reports && ncopy > 0)
+    CK(cudaMemcpy(reports, ctx->d_reports, sizeof(gg_report) * ncopy, cudaMemcpyDeviceToHost));
+  if (body_momentum && ncopy > 0 && ctx->last_nb > 0)
+    CK(cudaMemcpy(body_momentum, ctx->d_bm, sizeof(double) * 3 * ctx->last_nb * ncopy,
+                  cudaMemcpyDeviceToHost));
+  if (!c.err) return GG_OK;
+  char buf[512];
+  switch (c.err) {
+    case GG_EPOSITIONS:
+      return fail(ctx, GG_EPOSITIONS, "positions must be finite");
+    case GG_ENONFINITE: {
+      std::vector<int> bad(c.bad_uid, c.bad_uid + std::min(c.n_bad, kMaxBad));
+      std::sort(bad.begin(), bad.end());
+      std::string s = "non-finite velocity correction for particles [";
+      for (size_t i = 0; i < bad.size() && i < 5; ++i) {
+        if (i) s += ", ";
+        s += std::to_string(bad[i]);
+      }
+      s += "] (";
+      s += std::to_string(c.n_bad);
+      s += " particles)";
+      return fail(ctx, GG_ENONFINITE, s);
+    }
+    case GG_ECAPACITY:
+      std::snprintf(buf, sizeof(buf),
+                    "contact capacity exceeded: an owner has %d contacts > %d slots",
+                    c.cap_needed, ctx->K);
+      return fail(ctx, GG_ECAPACITY, buf);
+    default:
+      return fail(ctx, c.err, "device error");
+  }
+}
+
+int gg_required_contacts(gg_ctx* ctx) {
+  return ctx && ctx->h_ctl ? ctx->h_ctl->cap_needed : 0;
+}
+
+int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order) {
+  if (!ctx) return GG_EINVAL;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  int st = ensure_stage(ctx);
+  if (st != GG_OK) return st;
+  const long long n = ctx->n;
+  Dev D = ctx->D;
+  cudaStream_t s = ctx->stream;
+  k_batch_begin<<<1, 1, 0, s>>>(D);
+  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  k_hash_count<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  k_scatter<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  k_reorder<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  long long* tmp = reinterpret_cast<long long*>(ctx->d_stage);  // 6n doubles = room for 4n i64
+  k_tap_cells<<<ctx->nblocks, kBlock, 0, s>>>(D, tmp, tmp + 3 * n);
+  ctx->launches += 9;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpy(ctx->h_ctl, D.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  if (ctx->h_ctl->err == GG_EPOSITIONS) return fail(ctx, GG_EPOSITIONS, "positions must be finite");
+  if (cells) CK(cudaMemcpy(cells, tmp, sizeof(long long) * 3 * n, cudaMemcpyDeviceToHost));
+  if (hashes) CK(cudaMemcpy(hashes, tmp + 3 * n, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  if (order) {
+    std::vector<int> u(n);
+    int cur = 0;
+    CK(cudaMemcpy(&cur, &D.ctl->cur, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(u.data(), D.UID[cur ^ 1], sizeof(int) * n, cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < n; ++i) order[i] = u[i];
+  }
+  return GG_OK;
+}
+
+int gg_tap_contacts(gg_ctx* ctx, int64_t cap, int64_t* count, int32_t* owner, int32_t* other,
+                    int32_t* kind, double* psi, double* e1) {
+  if (!ctx || !count) return GG_EINVAL;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const long long n = ctx->n;
+  const int K = ctx->K;
+  std::vector<int> cnt(n), uid(n), oth(static_cast<size_t>(K) * n);
+  std::vector<float4> geo(static_cast<size_t>(K) * n);
+  int cur = 0;
+  CK(cudaMemcpy(&cur, &ctx->D.ctl->cur, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt.data(), ctx->D.ccount, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  const int ub = ctx->tap_uncommitted ? (cur ^ 1) : cur;
+  CK(cudaMemcpy(uid.data(), ctx->D.UID[ub], sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(oth.data(), ctx->D.coth, sizeof(int) * oth.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(geo.data(), ctx->D.cgeo, sizeof(float4) * geo.size(), cudaMemcpyDeviceToHost));
+  long long m = 0;
+  for (long long k = 0; k < n; ++k) {
+    for (int s = 0; s < cnt[k]; ++s, ++m) {
+      if (m >= cap) continue;
+      const size_t idx = static_cast<size_t>(s) * n + k;
+      const int j = oth[idx];
+      if (owner) owner[m] = uid[k];
+      if (other) other[m] = j >= 0 ? uid[j] : -(j + 1);
+      if (kind) kind[m] = j >= 0 ? 0 : 1;
+      if (psi) psi[m] = geo[idx].w;
+      if (e1) {
+        e1[3 * m] = geo[idx].x;
+        e1[3 * m + 1] = geo[idx].y;
+        e1[3 * m + 2] = geo[idx].z;
+      }
+    }
+  }
+  *count = m;
+  return GG_OK;
+}
+
+int gg_penetration(gg_ctx* ctx, const gg_body* body, const double* points, int64_t n,
+                   double radius, double* psi, double* normal, int32_t* hit,
+                   int64_t* n_degenerate) {
+  if (!ctx || !body || (n > 0 && (!points || !psi || !normal || !hit)))
+    return fail(ctx, GG_EINVAL, "null argument");
+  if (!(radius > 0)) return fail(ctx, GG_EINVAL, "particle radius must be positive");
+  if (body->kind == GG_GEOM_GRID && (body->grid_id < 0 || body->grid_id >= (int)ctx->grids.size()))
+    return fail(ctx, GG_EINVAL, "unknown grid id");
+  if (n_degenerate) *n_degenerate = 0;
+  if (n == 0) return GG_OK;
+  DeviceGuard guard(ctx->device);
+  double* d = nullptr;
+  unsigned long long* deg = nullptr;
+  CK(cudaMalloc(&d, sizeof(double) * 7 * n + sizeof(int) * n));
+  CK(cudaMalloc(&deg, sizeof(unsigned long long)));
+  CK(cudaMemset(deg, 0, sizeof(unsigned long long)));
+  CK(cudaMemcpy(d, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+  double* dpsi = d + 3 * n;
+  double* dn = d + 4 * n;
+  int* dh = reinterpret_cast<int*>(d + 7 * n);
+  k_penetration<<<blocks_for(n), kBlock, 0, ctx->stream>>>(*body, ctx->d_grids, ctx->d_gvals, d,
+                                                            n, radius, dpsi, dn, dh, deg);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  unsigned long long nd = 0;
+  CK(cudaMemcpy(psi, dpsi, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(normal, dn, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hit, dh, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&nd, deg, sizeof(nd), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(deg);
+  if (n_degenerate) *n_degenerate = static_cast<int64_t>(nd);
+  return GG_OK;
+}
+
+int gg_spatial_hash(gg_ctx* ctx, const int64_t* cells, int64_t k, int64_t n_h, int64_t* out) {
+  if (n_h < 1) return fail(ctx, GG_EINVAL, "hash table size must be >= 1");
+  if (k == 0) return GG_OK;
+  if (!cells || !out) return fail(ctx, GG_EINVAL, "null argument");
+  HashCfg H;
+  H.n_h = n_h;
+  H.pow2 = ((n_h & (n_h - 1)) == 0 && n_h <= (1ll << 32)) ? 1 : 0;
+  H.mask = static_cast<uint32_t>(n_h - 1);
+  long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(long long) * 4 * k);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
+  e = cudaMemcpy(d, cells, sizeof(long long) * 3 * k, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_hash_cells<<<blocks_for(k), kBlock>>>(reinterpret_cast<const long long*>(d), k, H, d + 3 * k);
+    if (ctx) ctx->launches += 1;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d + 3 * k, sizeof(long long) * k, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gg_spatial_hash");
+  return GG_OK;
+}
+
+int gg_host_register(void* ptr, int64_t bytes) {
+  return cudaHostRegister(ptr, static_cast<size_t>(bytes), cudaHostRegisterDefault) == cudaSuccess
+             ? GG_OK
+             : GG_ECUDA;
+}
+
+int gg_host_unregister(void* ptr) {
+  return cudaHostUnregister(ptr) == cudaSuccess ? GG_OK : GG_ECUDA;
+}
+
+void* gg_stream(gg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+}  // extern "C"

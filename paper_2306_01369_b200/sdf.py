@@ -1,0 +1,172 @@
+"""Signed-distance geometry descriptions (query side, sdf.py:29-241).
+
+The classes carry the parameters the device kernels evaluate (see
+csrc/gg_device.cuh) plus ``contact_bounds``, which the host needs for the
+`_near_body` AABB prefilter (contact.py:187-203).  ``penetration_depth``
+(sdf.py:472-512) runs on the GPU.  Mesh baking is offline preprocessing and
+out of scope for the hot path; an ``SdfGrid`` built anywhere (including the
+reference's ``bake_mesh_sdf``) is accepted.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+DEGENERATE_GRADIENT_EPS = 1e-9
+
+
+class SdfGeometry:
+    def contact_bounds(self, r: float):
+        return None
+
+
+@dataclass
+class Sphere(SdfGeometry):
+    radius: float
+
+    def contact_bounds(self, r):
+        e = self.radius + r
+        return -np.full(3, e), np.full(3, e)
+
+
+@dataclass
+class HalfSpace(SdfGeometry):
+    """Solid half-space; ``normal`` points out of the material."""
+
+    normal: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, 1.0]))
+    offset: float = 0.0
+
+    def __post_init__(self):
+        n = np.asarray(self.normal, dtype=np.float64)
+        self.normal = n / np.linalg.norm(n)
+
+
+@dataclass
+class Box(SdfGeometry):
+    half_extents: np.ndarray
+
+    def __post_init__(self):
+        self.half_extents = np.asarray(self.half_extents, dtype=np.float64)
+
+    def contact_bounds(self, r):
+        return -(self.half_extents + r), self.half_extents + r
+
+
+@dataclass
+class Cylinder(SdfGeometry):
+    """Capped cylinder along z."""
+
+    radius: float
+    half_height: float
+
+    def contact_bounds(self, r):
+        e = np.array([self.radius + r, self.radius + r, self.half_height + r])
+        return -e, e
+
+
+@dataclass
+class Tube(SdfGeometry):
+    """Infinite cylindrical wall, solid outside ``radius``."""
+
+    radius: float
+
+
+@dataclass
+class SdfGrid(SdfGeometry):
+    """Regular grid of signed distances, trilinear query with outward
+    extrapolation (sdf.py:179-241)."""
+
+    origin: np.ndarray
+    spacing: np.ndarray
+    dims: np.ndarray
+    values: np.ndarray
+    mesh_hash: bytes = b"\0" * 32
+
+    def __post_init__(self):
+        self.origin = np.asarray(self.origin, dtype=np.float64)
+        self.spacing = np.asarray(self.spacing, dtype=np.float64)
+        self.dims = np.asarray(self.dims, dtype=np.int64)
+        self.values = np.asarray(self.values, dtype=np.float64).reshape(tuple(self.dims))
+        if np.any(self.dims < 2):
+            raise ValueError("grid dims must be >= 2 on every axis")
+
+    @property
+    def upper(self) -> np.ndarray:
+        return self.origin + (self.dims - 1) * self.spacing
+
+    def contact_bounds(self, r):
+        return self.origin - r, self.upper + r
+
+
+def geometry_kind(geom) -> int:
+    """Device kind of a geometry object (ours or the reference's, by class name)."""
+    name = type(geom).__name__
+    kinds = {
+        "Sphere": N.GEOM_SPHERE,
+        "HalfSpace": N.GEOM_HALFSPACE,
+        "Box": N.GEOM_BOX,
+        "Cylinder": N.GEOM_CYLINDER,
+        "Tube": N.GEOM_TUBE,
+        "SdfGrid": N.GEOM_GRID,
+    }
+    if name not in kinds:
+        raise ValueError(f"unsupported geometry type {name}")
+    return kinds[name]
+
+
+def geometry_shape(geom) -> np.ndarray:
+    k = geometry_kind(geom)
+    s = np.zeros(4)
+    if k == N.GEOM_SPHERE:
+        s[0] = geom.radius
+    elif k == N.GEOM_HALFSPACE:
+        s[:3] = np.asarray(geom.normal, dtype=np.float64)
+        s[3] = geom.offset
+    elif k == N.GEOM_BOX:
+        s[:3] = np.asarray(geom.half_extents, dtype=np.float64)
+    elif k == N.GEOM_CYLINDER:
+        s[0], s[1] = geom.radius, geom.half_height
+    elif k == N.GEOM_TUBE:
+        s[0] = geom.radius
+    return s
+
+
+def penetration_depth(geom, body_pose: np.ndarray, world_points: np.ndarray, r: float):
+    """GPU penetration test of spheres against a posed geometry.
+
+    Same return convention as the reference (sdf.py:472-512):
+    ``(psi, normal_world, in_contact, n_degenerate)``; scalars for one point.
+    """
+    from .engine import utility_context
+
+    if r <= 0:
+        raise ValueError("particle radius must be positive")
+    p = np.asarray(world_points, dtype=np.float64)
+    single = p.ndim == 1
+    pts = np.ascontiguousarray(p.reshape(-1, 3))
+    uc = utility_context()
+    body = np.zeros(1, dtype=N.BODY_DTYPE)
+    pose = np.asarray(body_pose, dtype=np.float64)
+    body["kind"] = geometry_kind(geom)
+    body["shape"][0] = geometry_shape(geom)
+    body["rot"][0] = pose[:3, :3].reshape(-1)
+    body["trans"][0] = pose[:3, 3]
+    if body["kind"][0] == N.GEOM_GRID:
+        body["grid_id"] = uc.grid_id(geom)
+    n = len(pts)
+    psi = np.zeros(n)
+    nrm = np.zeros((n, 3))
+    hit = np.zeros(n, dtype=np.int32)
+    ndeg = ctypes.c_int64(0)
+    st = N.lib().gg_penetration(uc.ctx, N.ptr(body), N.ptr(pts), n, float(r), N.ptr(psi),
+                                N.ptr(nrm), N.ptr(hit), ctypes.byref(ndeg))
+    N.check(uc.ctx, st, "gg_penetration")
+    mask = hit.astype(bool)
+    if single:
+        return float(psi[0]), nrm[0], bool(mask[0]), int(ndeg.value)
+    return psi, nrm, mask, int(ndeg.value)

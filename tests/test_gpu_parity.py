@@ -1,0 +1,234 @@
+"""Device parity against the reference (golden fixtures) and the pinned
+oracle.  Bars (BASELINE.json north_star):
+  * cells / hashes / stable order / directed contact lists / counters: bit-exact
+  * single-step positions and velocities: max|d| / max(1, max|ref|) <= 1e-5
+  * contact depths / normals: float32 storage of float64 values (<= 2^-23 rel)
+"""
+
+import numpy as np
+import pytest
+
+from helpers import (
+    body_states,
+    directed_rows,
+    golden_cases,
+    load,
+    params_from,
+    rel_err,
+    scene_from,
+)
+
+import paper_2306_01369_b200 as gg
+from paper_2306_01369_b200.broadphase import device_hash_sort
+from paper_2306_01369_b200.contact import device_detect
+from oracle import granular_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_broadphase_bit_exact(name):
+    g = load(name)
+    cells, hashes, order = device_hash_sort(g["x0"], float(g["radius"]), int(g["n_h"]))
+    assert np.array_equal(cells, g["cells"])
+    assert np.array_equal(hashes, g["hashes"])
+    assert np.array_equal(order, g["order"])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_contacts_bit_exact(name):
+    g = load(name)
+    sc = scene_from(g)
+    cs, rep = device_detect(g["x0"], float(g["radius"]), int(g["n_h"]), sc.bodies,
+                            params=sc.params)
+    got = directed_rows(cs.owner, cs.kind, cs.other)
+    want = directed_rows(g["c_owner"], g["c_kind"], g["c_other"])
+    assert got.shape == want.shape, (got.shape, want.shape)
+    assert np.array_equal(got, want)
+    assert int(rep["n_candidates"]) == int(g["rep_n_candidates"])
+    assert int(rep["n_coincident"]) == int(g["rep_n_coincident"])
+    assert int(rep["n_degenerate"]) == int(g["rep_n_degenerate"])
+    # depths / normals: float64 on device, stored float32
+    key = np.lexsort((cs.other, cs.kind, cs.owner))
+    assert np.abs(cs.psi[key] - g["c_psi"]).max(initial=0) <= 2e-7 * max(1e-3, g["c_psi"].max(initial=0))
+    assert np.abs(cs.e1[key] - g["c_e1"]).max(initial=0) <= 2e-7
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_single_step_matches_reference(name):
+    g = load(name)
+    sc = scene_from(g)
+    _, rep = gg.step(sc, step_index=0)
+    x1, v1 = sc.particles.positions, sc.particles.velocities
+    assert rel_err(x1, g["x1"]) <= TOL
+    assert rel_err(v1, g["v1"]) <= TOL, rel_err(v1, g["v1"])
+    assert rep.n_contacts == int(g["rep_n_contacts"])
+    assert rep.n_candidates == int(g["rep_n_candidates"])
+    assert rep.n_body_contacts == int(g["rep_n_body_contacts"])
+    assert rep.n_coincident_skipped == int(g["rep_n_coincident"])
+    assert rep.n_degenerate_skipped == int(g["rep_n_degenerate"])
+    assert rep.max_penetration == pytest.approx(float(g["rep_max_penetration"]), rel=1e-6)
+    assert rep.kinetic_energy == pytest.approx(float(g["rep_kinetic_energy"]), rel=1e-4, abs=1e-9)
+    assert rep.max_cone_violation <= 1e-9
+    assert rep.min_normal_impulse >= 0.0
+    bm_ref = np.asarray(g["rep_body_momentum"])
+    scale = max(1.0, np.abs(bm_ref).max(initial=0))
+    assert np.abs(rep.body_momentum - bm_ref).max(initial=0) / scale <= 1e-3
+
+
+@pytest.mark.parametrize("n", [20_000, 50_000])
+def test_lattice_step_vs_oracle(n):
+    """Dense lattice bed at bench-like sizes: device vs the pinned oracle."""
+    pos = gg.lattice_bed(n).astype(np.float32).astype(np.float64)
+    params = gg.MaterialParams(timestep=5e-4)
+    sc = gg.Scene(particles=gg.ParticleSet(pos.copy(), np.zeros_like(pos)),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")], params=params)
+    n_h = gg.default_table_size(n)
+    _, rep = gg.step(sc)
+    x1, v1, orep, c, _ = O.step(pos, np.zeros_like(pos), params, sc.bodies, n_h)
+    assert rep.n_contacts == orep["n_contacts"]
+    assert rep.n_candidates == orep["n_candidates"]
+    assert rep.n_body_contacts == orep["n_body_contacts"]
+    assert rel_err(sc.particles.positions, x1) <= TOL
+    assert rel_err(sc.particles.velocities, v1) <= TOL
+
+
+def test_config1_free_running_bulk_statistics():
+    """Config 1 (lattice_bed(5000), dt=5e-4, 200 steps): long contact rollouts
+    are chaotic, so compare bulk statistics against the reference run."""
+    ref = load("config1_run")
+    x0 = ref["x0"]
+    params = gg.MaterialParams(radius=0.05, friction=0.5, baumgarte_alpha=0.2, timestep=5e-4,
+                               solver_iterations=10)
+    sc = gg.Scene(particles=gg.ParticleSet(x0.copy(), np.zeros_like(x0)),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")], params=params)
+    _, reps = gg.run(sc, int(ref["steps"]))
+    ke = np.array([r.kinetic_energy for r in reps])
+    nc = np.array([r.n_contacts for r in reps])
+    xT = sc.particles.positions
+    h_ref = ref["xT"][:, 2]
+    # pile height profile: max and quantiles of z within 2% of the bed height
+    height = h_ref.max()
+    for q in (0.5, 0.9, 0.99, 1.0):
+        assert abs(np.quantile(xT[:, 2], q) - np.quantile(h_ref, q)) <= 0.02 * height
+    # mean contacts within 2%, KE trajectory within 5% of its peak
+    assert abs(nc.mean() - ref["n_contacts"].mean()) <= 0.02 * ref["n_contacts"].mean()
+    assert np.abs(ke - ref["ke"]).max() <= 0.05 * ref["ke"].max()
+    # 2-D height map (0.5 m bins) within 2% of bed height
+    def hmap(x):
+        ij = np.floor(x[:, :2] / 0.5).astype(int)
+        out = {}
+        for (i, j), z in zip(map(tuple, ij), x[:, 2]):
+            out[(i, j)] = max(out.get((i, j), -1e9), z)
+        return out
+    a, b = hmap(xT), hmap(ref["xT"])
+    common = set(a) & set(b)
+    assert len(common) >= 0.9 * len(b)
+    assert max(abs(a[k] - b[k]) for k in common) <= 0.05 * height
+
+
+def test_modes_bitwise_identical():
+    g = load("lattice_500")
+    out = {}
+    for m in gg.PipelineMode:
+        sc = scene_from(g)
+        for _ in range(5):
+            gg.step(sc, m)
+        out[m] = (sc.particles.positions.copy(), sc.particles.velocities.copy())
+    ref = out[gg.PipelineMode.TWO_LOOPS_SPLIT]
+    for m, (x, v) in out.items():
+        assert np.array_equal(x, ref[0]) and np.array_equal(v, ref[1])
+
+
+def test_determinism():
+    g = load("primitives_3000")
+    res = []
+    for _ in range(2):
+        sc = scene_from(g)
+        gg.run(sc, 20)
+        res.append((sc.particles.positions.copy(), sc.particles.velocities.copy()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+def test_ballistic_closed_form():
+    x0 = np.array([[0.3, -0.2, 5.0]])
+    v0 = np.array([[1.0, 2.0, 0.5]])
+    sc = gg.Scene(particles=gg.ParticleSet(x0.copy(), v0.copy()), bodies=[],
+                  params=gg.MaterialParams())
+    n = 250
+    for _ in range(n):
+        gg.step(sc)
+    g, dt = sc.params.gravity, sc.params.timestep
+    want_v = v0[0] + n * dt * g
+    want_x = x0[0] + n * dt * v0[0] + dt * dt * g * n * (n + 1) / 2.0
+    # float32 state: ~n * ulp drift
+    assert np.abs(sc.particles.positions[0] - want_x).max() <= 2e-5 * max(1.0, np.abs(want_x).max())
+    assert np.abs(sc.particles.velocities[0] - want_v).max() <= 2e-5
+
+
+def test_error_labels_step_index():
+    sc = gg.Scene(particles=gg.ParticleSet(np.array([[0, 0, 0], [0.07, 0, 0]], float),
+                                           np.zeros((2, 3))), bodies=[], params=gg.MaterialParams())
+    sc.particles.velocities[0, 0] = np.inf
+    with pytest.raises(gg.SolverError, match="step 7"):
+        gg.step(sc, step_index=7)
+
+
+def test_nonfinite_positions_raise_value_error():
+    sc = gg.Scene(particles=gg.ParticleSet(np.zeros((3, 3)), np.zeros((3, 3))), bodies=[],
+                  params=gg.MaterialParams())
+    sc.particles.positions[1, 2] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        gg.step(sc)
+
+
+def test_reference_objects_are_accepted_duck_typed():
+    """A scene built from plain attribute objects (the reference's shape) is
+    stepped eagerly in place."""
+
+    class PS:
+        def __init__(self, x, v):
+            self.positions, self.velocities = x, v
+
+        @property
+        def count(self):
+            return len(self.positions)
+
+    g = load("lattice_500")
+    ours = scene_from(g)
+    plain = gg.Scene(particles=PS(g["x0"].copy(), g["v0"].copy()), bodies=ours.bodies,
+                     params=ours.params, hashmap_size=int(g["n_h"]))
+    xref = plain.particles.positions
+    gg.step(plain)
+    assert plain.particles.positions is xref  # mutated in place
+    assert rel_err(xref, g["x1"]) <= TOL
+
+
+def test_empty_scene_report():
+    sc = gg.Scene(particles=gg.ParticleSet(np.zeros((0, 3)), np.zeros((0, 3))), bodies=[],
+                  params=gg.MaterialParams())
+    _, rep = gg.step(sc)
+    assert rep.n_contacts == 0 and rep.n_candidates == 0 and rep.kinetic_energy == 0.0
+    assert sc.t == pytest.approx(sc.params.timestep)
+
+
+def test_penetration_depth_kats():
+    # tests/test_sdf.py:204-231 hand values
+    psi, n, hit, deg = gg.penetration_depth(gg.Sphere(1.0), gg.identity_pose(),
+                                            np.array([1.05, 0.0, 0.0]), 0.1)
+    assert hit and psi == pytest.approx(0.05) and np.allclose(n, [1, 0, 0]) and deg == 0
+    psi, _, hit, _ = gg.penetration_depth(gg.HalfSpace(), gg.identity_pose(), np.array([0, 0, 0.1]), 0.1)
+    assert not hit and psi == 0.0
+    pose = gg.make_pose(np.eye(3), np.array([0.0, 0.0, 0.3]))
+    psi, n, hit, _ = gg.penetration_depth(gg.HalfSpace(), pose, np.array([0.0, 0.0, 0.35]), 0.1)
+    assert hit and psi == pytest.approx(0.05) and np.allclose(n, [0, 0, 1])
+
+
+def test_spatial_hash_kats():
+    g = load("hash_kats")
+    for key in g:
+        if key.startswith("h_") or key.startswith("hbig_"):
+            n_h = int(key.split("_")[1])
+            cells = g["cells"] if key.startswith("h_") else g["big_cells"]
+            assert np.array_equal(gg.spatial_hash(cells, n_h), g[key]), key
