@@ -224,12 +224,14 @@ class Clocks:
 # ---------------------------------------------------------------------------
 def bytes_model(n_h: int, S: int, c_pp: float, c_b: float) -> dict:
     P = int(np.ceil(np.log2(max(n_h, 2)) / 8))
+    # SURVEY.md §8d per-kernel terms mapped onto this schedule
     per_kernel = {
-        "k_hash_count": 24.0,
-        "k_reorder": 68.0,
-        "k_narrow": 36.0 + 20.0 * c_pp + 32.0 * c_b,
-        "k_sweep": 48.0 + 20.0 * c_pp + 32.0 * c_b,
-        "k_integrate": 80.0,
+        "k_count": 24.0,                                   # hash: read x, write key + idx
+        "k_resort": 68.0,                                  # reorder (every resort_every steps)
+        "k_fill": 68.0,                                    # bucket-ordered candidate copy
+        "k_narrow": 20.0 + 20.0 * c_pp,                    # pp narrowphase
+        "k_bodies": 16.0 + 32.0 * c_b,                     # body contacts
+        "k_solve": S * (48.0 + 20.0 * c_pp + 32.0 * c_b) + 80.0,  # S sweeps + integrate
     }
     step = 228.0 + 16.0 * P + 48.0 * S + (S + 1) * (20.0 * c_pp + 32.0 * c_b)
     return {"per_kernel_per_particle": per_kernel, "step_per_particle": step, "radix_passes": P}
@@ -367,15 +369,17 @@ def run_ours(args, dist: Dist):
     peak, peak_src = peaks()
     P = max(args.profile_steps, 1)
     table3, _ = eng.body_tables(sc, P)
-    kind_ms = np.zeros(11, dtype=np.float32)
-    kind_n = np.zeros(11, dtype=np.int32)
+    kind_ms = np.zeros(16, dtype=np.float32)
+    kind_n = np.zeros(16, dtype=np.int32)
     st = lib.gg_profile_steps(eng.ctx, P, N.ptr(np.ascontiguousarray(table3)), nb, N.ptr(kind_ms),
                               N.ptr(kind_n))
     N.check(eng.ctx, st, "gg_profile_steps")
-    names = [lib.gg_profile_kind_name(k).decode() for k in range(11)]
+    names = [lib.gg_profile_kind_name(k).decode() for k in range(16)]
+    names = [nm for nm in names if nm]
+    kind_ms, kind_n = kind_ms[: len(names)], kind_n[: len(names)]
     model = bytes_model(eng.n_h, sc.params.solver_iterations, c_pp, c_b)
-    share = {names[k]: float(kind_ms[k] / max(kind_ms.sum(), 1e-9)) for k in range(11)}
-    top = max((k for k in range(11) if names[k] in model["per_kernel_per_particle"]),
+    share = {names[k]: float(kind_ms[k] / max(kind_ms.sum(), 1e-9)) for k in range(len(names))}
+    top = max((k for k in range(len(names)) if names[k] in model["per_kernel_per_particle"]),
               key=lambda k: kind_ms[k])
     top_name = names[top]
     avg_ms = float(kind_ms[top] / max(kind_n[top], 1))

@@ -194,6 +194,11 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t max_contacts);
 int gg_max_contacts(const gg_ctx* ctx);
 int gg_required_contacts(gg_ctx* ctx);
 
+/* Physical particle order: re-sorted into Morton order of the cells every
+ * `steps` steps (and after every state upload).  Results do not depend on
+ * it (contact enumeration order is the bucket order); only locality does. */
+int gg_set_resort_every(gg_ctx* ctx, int32_t steps);
+
 /* Page-lock host arrays so gg_set/get_state_f64 run at full PCIe speed. */
 int gg_host_register(void* ptr, int64_t bytes);
 int gg_host_unregister(void* ptr);

@@ -54,9 +54,12 @@ struct gg_ctx {
   long long flush_bytes = 0;
   std::vector<cudaEvent_t> evpool;
 
-  // graph of one step
-  cudaGraphExec_t gexec = nullptr;
+  // graphs of one step: [0] plain, [1] re-sort first
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   bool graph_dirty = true;
+  int solve_grid = 0;      // co-resident blocks of k_solve
+  int resort_every = 8;    // physical re-sort period (steps)
+  long long since_resort = 1 << 30;  // force a re-sort after upload
 
   std::vector<void*> owned;  // fixed-size allocations freed at destroy
 };
@@ -158,13 +161,10 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
   const int nbx = std::max(nb, 1);
   if (need <= ctx->batch_cap && nbx <= std::max(ctx->max_bodies, 1)) return GG_OK;
   if (nb > ctx->max_bodies) {
-    // grow the body capacity: momentum partials depend on it
+    // grow the body capacity: the fallback momentum accumulators depend on it
     ctx->max_bodies = nb;
-    dfree(ctx, ctx->D.bm_part);
     dfree(ctx, ctx->D.bm_glob);
-    ctx->D.bm_part = nullptr;
     ctx->D.bm_glob = nullptr;
-    CK(dalloc(ctx, &ctx->D.bm_part, static_cast<size_t>(ctx->nblocks) * nb * 3));
     CK(dalloc(ctx, &ctx->D.bm_glob, static_cast<size_t>(nb) * 3));
   }
   int cap = std::max(ctx->batch_cap, 1);
@@ -187,34 +187,72 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
   return GG_OK;
 }
 
-// The step schedule: 9 + S kernels and one memset, all on ctx->stream.
-int enqueue_step(gg_ctx* ctx) {
-  const Dev& D = ctx->D;
-  cudaStream_t s = ctx->stream;
+// The step schedule.  Optional Morton re-sort (R1-R4), the hash index
+// (H1-H4), narrowphase, cooperative solve.  All on ctx->stream.
+int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->solve_grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_solve, D));
+  return GG_OK;
+}
+
+int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
   const int nbn = ctx->nblocks;
   CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
-  k_hash_count<<<nbn, kBlock, 0, s>>>(D);
+  k_count<<<nbn, kBlock, 0, s>>>(D);
   k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
   k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
   k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
   k_scatter<<<nbn, kBlock, 0, s>>>(D);
-  k_reorder<<<nbn, kBlock, 0, s>>>(D);
-  k_narrow<<<nbn, kBlock, 0, s>>>(D);
-  for (int it = 0; it < D.S; ++it) k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
-  k_integrate<<<nbn, kBlock, 0, s>>>(D);
-  k_finalize<<<1, kBlock, 0, s>>>(D);
+  if (D.key_morton)
+    k_resort<<<nbn, kBlock, 0, s>>>(D);
+  else
+    k_fill<<<nbn, kBlock, 0, s>>>(D);
   CK(cudaGetLastError());
   return GG_OK;
 }
 
-int kernels_per_step(const gg_ctx* ctx) { return 9 + ctx->D.S; }
+Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
+  Dev D = ctx->D;
+  D.resort = resort;
+  D.key_morton = morton;
+  return D;
+}
+
+int enqueue_step(gg_ctx* ctx, int resort) {
+  cudaStream_t s = ctx->stream;
+  int st;
+  if (resort) {
+    st = enqueue_sort_pass(ctx, pass_dev(ctx, 1, 1), s);
+    if (st != GG_OK) return st;
+  }
+  const Dev D = pass_dev(ctx, resort, 0);
+  st = enqueue_sort_pass(ctx, D, s);
+  if (st != GG_OK) return st;
+  k_narrow<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  if (D.nb > 0) k_bodies<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  CK(cudaGetLastError());
+  return launch_solve(ctx, D, s);
+}
+
+int kernels_per_step(const gg_ctx* ctx, int resort) {
+  return 8 + (ctx->D.nb > 0 ? 1 : 0) + (resort ? 6 : 0);
+}
 
 // Same schedule as enqueue_step, with an event after every kernel so each
 // kernel kind's device time can be attributed (bench roofline pass).
 constexpr int kProfKinds = 11;
-const char* kProfNames[kProfKinds] = {"memset_counts", "k_hash_count", "k_scan_tiles", "k_scan_top",
-                                      "k_scan_apply",  "k_scatter",    "k_reorder",    "k_narrow",
-                                      "k_sweep",       "k_integrate",  "k_finalize"};
+const char* kProfNames[kProfKinds] = {"memset_counts", "k_count", "k_scan_tiles", "k_scan_top",
+                                      "k_scan_apply",  "k_scatter", "k_resort",  "k_fill",
+                                      "k_narrow",      "k_solve",   "k_bodies"};
 
 int ensure_events(gg_ctx* ctx, size_t n) {
   while (ctx->evpool.size() < n) {
@@ -225,8 +263,9 @@ int ensure_events(gg_ctx* ctx, size_t n) {
   return GG_OK;
 }
 
-int enqueue_step_profiled(gg_ctx* ctx, cudaEvent_t* ev, int* kind_of_interval) {
-  const Dev& D = ctx->D;
+// Same schedule as enqueue_step with an event after every kernel, so each
+// kernel kind's device time can be attributed (bench roofline pass).
+int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of_interval) {
   cudaStream_t s = ctx->stream;
   const int nbn = ctx->nblocks;
   int e = 0;
@@ -236,32 +275,39 @@ int enqueue_step_profiled(gg_ctx* ctx, cudaEvent_t* ev, int* kind_of_interval) {
     ++e;
   };
   cudaEventRecord(ev[0], s);
-  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
-  mark(0);
-  k_hash_count<<<nbn, kBlock, 0, s>>>(D);
-  mark(1);
-  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  mark(2);
-  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
-  mark(3);
-  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  mark(4);
-  k_scatter<<<nbn, kBlock, 0, s>>>(D);
-  mark(5);
-  k_reorder<<<nbn, kBlock, 0, s>>>(D);
-  mark(6);
-  k_narrow<<<nbn, kBlock, 0, s>>>(D);
-  mark(7);
-  for (int it = 0; it < D.S; ++it) {
-    k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
-    mark(8);
+  for (int pass = resort ? 0 : 1; pass < 2; ++pass) {
+    const Dev D = pass_dev(ctx, resort, pass == 0 ? 1 : 0);
+    cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s);
+    mark(0);
+    k_count<<<nbn, kBlock, 0, s>>>(D);
+    mark(1);
+    k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
+    mark(2);
+    k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+    mark(3);
+    k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+    mark(4);
+    k_scatter<<<nbn, kBlock, 0, s>>>(D);
+    mark(5);
+    if (pass == 0) {
+      k_resort<<<nbn, kBlock, 0, s>>>(D);
+      mark(6);
+    } else {
+      k_fill<<<nbn, kBlock, 0, s>>>(D);
+      mark(7);
+    }
   }
-  k_integrate<<<nbn, kBlock, 0, s>>>(D);
+  const Dev D = pass_dev(ctx, resort, 0);
+  k_narrow<<<nbn, kBlock, 0, s>>>(D);
+  mark(8);
+  if (D.nb > 0) {
+    k_bodies<<<nbn, kBlock, 0, s>>>(D);
+    mark(10);
+  }
+  if (launch_solve(ctx, D, s) != GG_OK) return -1;
   mark(9);
-  k_finalize<<<1, kBlock, 0, s>>>(D);
-  mark(10);
-  CK(cudaGetLastError());
-  return e;  // number of intervals
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return e;
 }
 
 int refresh_dev(gg_ctx* ctx) {
@@ -275,24 +321,35 @@ int refresh_dev(gg_ctx* ctx) {
 }
 
 int build_graph(gg_ctx* ctx) {
-  if (ctx->gexec) {
-    cudaGraphExecDestroy(ctx->gexec);
-    ctx->gexec = nullptr;
-  }
   refresh_dev(ctx);
-  cudaGraph_t g = nullptr;
-  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  int st = enqueue_step(ctx);
-  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
-  if (st != GG_OK) {
-    if (g) cudaGraphDestroy(g);
-    return st;
+  for (int g = 0; g < 2; ++g) {
+    if (ctx->gexec[g]) {
+      cudaGraphExecDestroy(ctx->gexec[g]);
+      ctx->gexec[g] = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int st = enqueue_step(ctx, g);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (st != GG_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&ctx->gexec[g], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
   }
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
-  e = cudaGraphInstantiate(&ctx->gexec, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
   ctx->graph_dirty = false;
+  return GG_OK;
+}
+
+// launch one step's graph, re-sorting the physical order every resort_every
+int launch_step(gg_ctx* ctx) {
+  const int resort = ctx->since_resort >= ctx->resort_every ? 1 : 0;
+  CK(cudaGraphLaunch(ctx->gexec[resort], ctx->stream));
+  ctx->since_resort = resort ? 1 : ctx->since_resort + 1;
+  ctx->launches += kernels_per_step(ctx, resort);
   return GG_OK;
 }
 
@@ -353,6 +410,11 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
   D.H.n_h = n_h;
   D.H.pow2 = (n_h & (n_h - 1)) == 0 ? 1 : 0;
   D.H.mask = static_cast<uint32_t>(n_h - 1);
+  {
+    long long p2 = 1;
+    while (p2 * 2 <= n_h) p2 *= 2;
+    D.mmask = static_cast<uint32_t>(p2 - 1);
+  }
   fill_params(ctx);
   D.nb = 0;
   for (int b = 0; b < 2; ++b) {
@@ -371,8 +433,15 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
   CK(dalloc(ctx, &D.V0, n));
   CK(dalloc(ctx, &D.ccount, n));
   CK(dalloc(ctx, &D.acc, 1));
-  CK(dalloc(ctx, &D.ke_part, ctx->nblocks));
-  CK(dalloc(ctx, &D.bm_part, static_cast<size_t>(ctx->nblocks) * std::max(ctx->max_bodies, 1) * 3));
+  // co-resident grid of the cooperative solve kernel
+  {
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kBlock, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    ctx->solve_grid = std::max(1, std::min(ctx->nblocks, per_sm * sms));
+  }
+  CK(dalloc(ctx, &D.Xh, n));
+  CK(dalloc(ctx, &D.part, static_cast<size_t>(ctx->solve_grid) * kPartStride));
   CK(dalloc(ctx, &D.bm_glob, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3));
   CK(dalloc(ctx, &D.ctl, 1));
   CK(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
@@ -397,7 +466,8 @@ int gg_destroy(gg_ctx* ctx) {
   {
     DeviceGuard guard(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    for (int g = 0; g < 2; ++g)
+      if (ctx->gexec[g]) cudaGraphExecDestroy(ctx->gexec[g]);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
     for (void* p : ctx->owned) cudaFree(p);
     ctx->owned.clear();
@@ -430,9 +500,16 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
 
 int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
 
+int gg_set_resort_every(gg_ctx* ctx, int32_t steps) {
+  if (!ctx || steps < 1) return fail(ctx, GG_EINVAL, "resort_every must be >= 1");
+  ctx->resort_every = steps;
+  return GG_OK;
+}
+
 static int ensure_stage(gg_ctx* ctx) {
   if (ctx->d_stage) return GG_OK;
   CK(dalloc(ctx, &ctx->d_stage, static_cast<size_t>(ctx->n) * 6));
+  static_assert(sizeof(double) == sizeof(long long), "stage reuse");
   return GG_OK;
 }
 
@@ -444,6 +521,7 @@ int gg_set_state_f64(gg_ctx* ctx, const double* x, const double* v) {
   const size_t bytes = sizeof(double) * 3 * static_cast<size_t>(ctx->n);
   CK(cudaMemcpyAsync(ctx->d_stage, x, bytes, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_stage + 3 * ctx->n, v, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->since_resort = 1 << 30;
   k_load_f64<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, ctx->d_stage,
                                                         ctx->d_stage + 3 * ctx->n);
   ctx->launches += 1;
@@ -471,6 +549,7 @@ int gg_get_state_f64(gg_ctx* ctx, double* x, double* v) {
 int gg_set_state_f32x4_dev(gg_ctx* ctx, const void* x4, const void* v4) {
   if (!ctx || !x4 || !v4) return fail(ctx, GG_EINVAL, "null argument");
   DeviceGuard guard(ctx->device);
+  ctx->since_resort = 1 << 30;
   k_load_f4<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, static_cast<const float4*>(x4),
                                                        static_cast<const float4*>(v4));
   ctx->launches += 1;
@@ -567,9 +646,12 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
   refresh_dev(ctx);
   k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  for (int i = 0; i < n_steps; ++i) CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+  for (int i = 0; i < n_steps; ++i) {
+    int st2 = launch_step(ctx);
+    if (st2 != GG_OK) return st2;
+  }
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  ctx->launches += 1 + static_cast<long long>(n_steps) * kernels_per_step(ctx);
+  ctx->launches += 1;
   ctx->last_batch = n_steps;
   ctx->last_nb = n_bodies;
   ctx->tap_uncommitted = false;
@@ -590,18 +672,14 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
   if (n_bodies > 0)
     CK(cudaMemcpy(ctx->d_bodies, bodies, sizeof(gg_body) * n_bodies, cudaMemcpyHostToDevice));
   refresh_dev(ctx);
-  const Dev& D = ctx->D;
+  const Dev D = pass_dev(ctx, 0, 0);
   cudaStream_t s = ctx->stream;
   k_batch_begin<<<1, 1, 0, s>>>(D);
-  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
-  k_hash_count<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
-  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  k_scatter<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  k_reorder<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  st = enqueue_sort_pass(ctx, D, s);
+  if (st != GG_OK) return st;
   k_narrow<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  ctx->launches += 9;
+  if (D.nb > 0) k_bodies<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  ctx->launches += 10;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   ctx->tap_uncommitted = true;
@@ -671,10 +749,11 @@ int gg_bench_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t 
     if (flush_bytes > 0)
       CK(cudaMemsetAsync(ctx->flush_buf, i & 0xff, static_cast<size_t>(flush_bytes), ctx->stream));
     CK(cudaEventRecord(ctx->evpool[2 * i], ctx->stream));
-    CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    st = launch_step(ctx);
+    if (st != GG_OK) return st;
     CK(cudaEventRecord(ctx->evpool[2 * i + 1], ctx->stream));
   }
-  ctx->launches += 1 + static_cast<long long>(n_steps) * kernels_per_step(ctx);
+  ctx->launches += 1;
   ctx->last_batch = n_steps;
   ctx->last_nb = n_bodies;
   ctx->tap_uncommitted = false;
@@ -690,7 +769,7 @@ int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_
   DeviceGuard guard(ctx->device);
   int st = stage_bodies(ctx, n_steps, bodies, n_bodies);
   if (st != GG_OK) return st;
-  const int per = 11 + ctx->D.S;
+  const int per = 24;
   st = ensure_events(ctx, static_cast<size_t>(per + 1));
   if (st != GG_OK) return st;
   for (int k = 0; k < kProfKinds; ++k) {
@@ -700,8 +779,11 @@ int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_
   std::vector<int> kinds(per + 1);
   k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
   for (int i = 0; i < n_steps; ++i) {
-    const int m = enqueue_step_profiled(ctx, ctx->evpool.data(), kinds.data());
-    if (m < 0) return m;
+    const int resort = ctx->since_resort >= ctx->resort_every ? 1 : 0;
+    ctx->since_resort = resort ? 1 : ctx->since_resort + 1;
+    ctx->launches += kernels_per_step(ctx, resort);
+    const int m = enqueue_step_profiled(ctx, resort, ctx->evpool.data(), kinds.data());
+    if (m < 0) return fail(ctx, GG_ECUDA, "profiled launch failed");
     CK(cudaStreamSynchronize(ctx->stream));
     for (int e = 0; e < m; ++e) {
       float t = 0.f;
@@ -710,7 +792,7 @@ int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_
       if (kind_launches && kinds[e] > 0) kind_launches[kinds[e]] += 1;
     }
   }
-  ctx->launches += 1 + static_cast<long long>(n_steps) * kernels_per_step(ctx);
+  ctx->launches += 1;
   ctx->last_batch = n_steps;
   ctx->last_nb = n_bodies;
   ctx->tap_uncommitted = false;
@@ -784,32 +866,23 @@ int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order) {
   int st = ensure_stage(ctx);
   if (st != GG_OK) return st;
   const long long n = ctx->n;
-  Dev D = ctx->D;
+  refresh_dev(ctx);
+  const Dev D = pass_dev(ctx, 0, 0);
   cudaStream_t s = ctx->stream;
   k_batch_begin<<<1, 1, 0, s>>>(D);
-  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
-  k_hash_count<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
-  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  k_scatter<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  k_reorder<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  long long* tmp = reinterpret_cast<long long*>(ctx->d_stage);  // 6n doubles = room for 4n i64
+  st = enqueue_sort_pass(ctx, D, s);
+  if (st != GG_OK) return st;
+  long long* tmp = reinterpret_cast<long long*>(ctx->d_stage);  // 6n doubles = room for 5n i64
   k_tap_cells<<<ctx->nblocks, kBlock, 0, s>>>(D, tmp, tmp + 3 * n);
-  ctx->launches += 9;
+  k_tap_order<<<ctx->nblocks, kBlock, 0, s>>>(D, tmp + 4 * n);
+  ctx->launches += 10;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   CK(cudaMemcpy(ctx->h_ctl, D.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   if (ctx->h_ctl->err == GG_EPOSITIONS) return fail(ctx, GG_EPOSITIONS, "positions must be finite");
   if (cells) CK(cudaMemcpy(cells, tmp, sizeof(long long) * 3 * n, cudaMemcpyDeviceToHost));
   if (hashes) CK(cudaMemcpy(hashes, tmp + 3 * n, sizeof(long long) * n, cudaMemcpyDeviceToHost));
-  if (order) {
-    std::vector<int> u(n);
-    int cur = 0;
-    CK(cudaMemcpy(&cur, &D.ctl->cur, sizeof(int), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(u.data(), D.UID[cur ^ 1], sizeof(int) * n, cudaMemcpyDeviceToHost));
-    for (long long i = 0; i < n; ++i) order[i] = u[i];
-  }
+  if (order) CK(cudaMemcpy(order, tmp + 4 * n, sizeof(long long) * n, cudaMemcpyDeviceToHost));
   return GG_OK;
 }
 
@@ -822,11 +895,10 @@ int gg_tap_contacts(gg_ctx* ctx, int64_t cap, int64_t* count, int32_t* owner, in
   const int K = ctx->K;
   std::vector<int> cnt(n), uid(n), oth(static_cast<size_t>(K) * n);
   std::vector<float4> geo(static_cast<size_t>(K) * n);
-  int cur = 0;
-  CK(cudaMemcpy(&cur, &ctx->D.ctl->cur, sizeof(int), cudaMemcpyDeviceToHost));
+  int ucur = 0;
+  CK(cudaMemcpy(&ucur, &ctx->D.ctl->ucur, sizeof(int), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cnt.data(), ctx->D.ccount, sizeof(int) * n, cudaMemcpyDeviceToHost));
-  const int ub = ctx->tap_uncommitted ? (cur ^ 1) : cur;
-  CK(cudaMemcpy(uid.data(), ctx->D.UID[ub], sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(uid.data(), ctx->D.UID[ucur], sizeof(int) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(oth.data(), ctx->D.coth, sizeof(int) * oth.size(), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(geo.data(), ctx->D.cgeo, sizeof(float4) * geo.size(), cudaMemcpyDeviceToHost));
   long long m = 0;

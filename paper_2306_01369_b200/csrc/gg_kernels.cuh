@@ -1,23 +1,34 @@
 // gg_kernels.cuh — the per-step kernels of the split pipeline
-// (stepper.py:57-135, TWO_LOOPS_SPLIT):
+// (stepper.py:57-135, TWO_LOOPS_SPLIT), B200 layout:
 //
-//   K1 k_hash_count   cell + hash per particle, bucket occupancy (atomic)
-//   K2 k_scan_*       exclusive scan of bucket counts -> bucket starts
-//   K3 k_scatter      counting-sort scatter (arrival order within bucket)
-//   K4 k_reorder      stable fix-up (ties by user id) + gather x, v to sorted SoA
-//   K5 k_narrow       pp narrowphase over 27 de-duplicated buckets + body SDF contacts
-//   K7 k_sweep (xS)   projected-Jacobi sweep, owner-computes, atomic-free
-//   K8 k_integrate    symplectic Euler + cyclic boundary + NaN check + KE
-//   K9 k_finalize     fixed-order reductions -> StepReport, commit
+//   physical order   particles live in a spatially coherent order (Morton
+//                    code of their cell, low bits), re-sorted every
+//                    `resort_every` steps by the same deterministic counting
+//                    sort the hash index uses (R1-R4).  Neighbours of a warp's
+//                    particles are then neighbours in memory, so the
+//                    narrowphase and solver gathers hit L1/L2.
+//   hash index       rebuilt every step over the physical order (H1-H4):
+//                    bucket counts -> scan -> scatter -> stable fill of
+//                    Xh[bucket order] = (x, y, z, physical index), ties by
+//                    user id, i.e. exactly np.argsort(hashes, kind="stable")
+//                    (broadphase.py:160) — candidates are read with ONE
+//                    float4 load each.
+//   K5 k_narrow      pp narrowphase over the 27 neighbour buckets (de-duplicated,
+//                    broadphase.py:164-171) + body SDF contacts -> slot-major
+//                    contact records.
+//   K7 k_solve       one cooperative persistent kernel: S projected-Jacobi
+//                    sweeps separated by grid barriers, symplectic Euler,
+//                    cyclic boundary, NaN check, fixed-order reductions into
+//                    the StepReport and the commit.
 //
-// Layout (all in HBM, n = particles):
-//   X[2], V[2]  float4   committed state, in the PREVIOUS step's sorted order
-//   UID[2]      int32    sorted position -> user particle id
-//   Xs, V0      float4   this step's sorted positions / start-of-step velocity
-//   W[2]        float4   predicted velocity w = v + dv, ping-ponged per sweep
-//   cgeo[K][n]  float4   contact (e1.xyz, psi)   slot-major, coalesced per slot
-//   coth[K][n]  int32    other: >=0 sorted particle index, <0 -> body -(b+1)
-//   cvb[K][n]   float4   body surface velocity (body contacts only)
+// Buffers (n particles, K slots):
+//   X[2], V[2]  float4  committed state (physical order), ping-pong on commit
+//   UID[2]      int32   physical index -> user id, flips on re-sort steps
+//   Xs, V0      float4  re-sorted layout of this step (re-sort steps only)
+//   Xh          float4  bucket-ordered copy (x, y, z, bits(physical index))
+//   W[2]        float4  predicted velocity w = v + dv, ping-ponged per sweep
+//   cgeo[K][n]  float4  (e1.xyz, psi)     coth[K][n] int32 other (<0: body)
+//   cvb[K][n]   float4  body surface velocity (body contacts only)
 #pragma once
 
 #include <cstdint>
@@ -28,29 +39,35 @@
 namespace gg {
 
 constexpr int kBlock = 256;
-constexpr int kScanTile = 2048;        // elements per scan tile (256 thr x 8)
-constexpr int kRegBodies = 4;          // bodies with deterministic in-register momentum
+constexpr int kScanTile = 2048;  // elements per scan tile (256 thr x 8)
+constexpr int kRegBodies = 4;    // bodies with deterministic in-register momentum
 constexpr int kMaxBad = 32;
 
 struct Ctl {
-  int cur;        // committed state buffer
-  int step;       // steps committed in this batch
-  int err;        // first error code (0 = none)
-  int err_step;   // batch-relative step of the error
-  int cap_needed; // largest per-owner contact count seen (capacity hint)
-  int n_bad;      // non-finite particles recorded
-  int pad[2];
+  int cur;         // committed state buffer
+  int ucur;        // committed uid buffer
+  int step;        // steps committed in this batch
+  int err;         // first error code (0 = none)
+  int err_step;    // batch-relative step of the error
+  int cap_needed;  // largest per-owner contact count seen (capacity hint)
+  int n_bad;       // non-finite particles recorded
+  int pad;
+  unsigned bar_count;  // grid barrier
+  unsigned bar_gen;
   int bad_uid[kMaxBad];
 };
 
 struct Acc {
   unsigned long long n_pp, n_cand, n_body, n_coinc, n_deg;
-  unsigned long long max_psi_bits, max_viol_bits, min_b1_bits;
+  unsigned long long max_psi_bits;
 };
 
 struct Dev {
   int n, K, nb, S, nblocks;
+  int resort;     // this graph re-sorts the physical order first
+  int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
   HashCfg H;
+  uint32_t mmask;  // Morton key mask (power of two <= n_h, minus one)
   double r, two_r, contact_d2, coinc_d2, mass, mu, alpha, dt, gamma;
   double gdt0, gdt1, gdt2;
   int has_boundary;
@@ -66,6 +83,7 @@ struct Dev {
   int* tmp;
   float4* Xs;
   float4* V0;
+  float4* Xh;
   float4* W[2];
   float4* cgeo;
   int* coth;
@@ -75,13 +93,14 @@ struct Dev {
   const DevGrid* grids;
   const double* gvals;
   Acc* acc;
-  double* ke_part;  // [nblocks]
-  double* bm_part;  // [nblocks][nb][3]
+  double* part;     // [nblocks_solve][4 + 3 * kRegBodies] per-block partials
   double* bm_glob;  // [nb][3] fallback accumulators for bodies >= kRegBodies
   gg_report* reports;
-  double* bm_out;   // [batch][nb][3]
+  double* bm_out;  // [batch][nb][3]
   Ctl* ctl;
 };
+
+constexpr int kPartStride = 4 + 3 * kRegBodies;
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void raise_err(Ctl* ctl, int code) {
@@ -109,7 +128,7 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
-// Fixed-order block reduction of a double (deterministic).  All threads call.
+// Fixed-order block reduction of a double (deterministic); result on thread 0.
 template <int kOp>  // 0 sum, 1 max, 2 min
 __device__ __forceinline__ double block_reduce(double v, double* sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -122,7 +141,7 @@ __device__ __forceinline__ double block_reduce(double v, double* sm) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
       r = kOp == 0 ? r + sm[w] : (kOp == 1 ? nmax(r, sm[w]) : nmin(r, sm[w]));
   }
-  return r;  // valid on thread 0
+  return r;
 }
 
 __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v,
@@ -146,6 +165,55 @@ __device__ __forceinline__ bool block_should_exit(const Ctl* ctl) {
   return s_err != 0;
 }
 
+// Grid-wide barrier for the cooperative kernel (all blocks co-resident).
+__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = &ctl->bar_gen;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+      ctl->bar_count = 0;
+      __threadfence();
+      atomicExch(&ctl->bar_gen, g + 1);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// the layout the step works on: re-sorted this step, or the committed one
+struct Layout {
+  const float4* x;
+  const float4* v;
+  const int* uid;
+};
+__device__ __forceinline__ Layout layout(const Dev& D, const Ctl* ctl) {
+  const int cur = ctl->cur, u = ctl->ucur;
+  if (D.resort) return {D.Xs, D.V0, D.UID[u ^ 1]};
+  return {D.X[cur], D.V[cur], D.UID[u]};
+}
+
+// ---------------------------------------------------------------------------
+// Morton key of a cell: interleaved low bits (wraps into tiles), masked to
+// the table size.  Only locality matters; any deterministic key is correct.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+__device__ __forceinline__ uint32_t morton_key(long long c0, long long c1, long long c2,
+                                               uint32_t mask) {
+  return (spread3(static_cast<uint32_t>(c0)) | (spread3(static_cast<uint32_t>(c1)) << 1) |
+          (spread3(static_cast<uint32_t>(c2)) << 2)) & mask;
+}
+
 // ---------------------------------------------------------------------------
 // batch begin: reset per-batch control + per-step accumulators
 // ---------------------------------------------------------------------------
@@ -156,23 +224,23 @@ __global__ void k_batch_begin(Dev D) {
   c->err_step = -1;
   c->cap_needed = 0;
   c->n_bad = 0;
+  c->bar_count = 0;
   Acc* a = D.acc;
   a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
   a->max_psi_bits = 0;
-  a->max_viol_bits = 0;
-  a->min_b1_bits = dbits(__longlong_as_double(0x7ff0000000000000ll));
   for (int i = 0; i < D.nb * 3; ++i) D.bm_glob[i] = 0.0;
 }
 
 // ---------------------------------------------------------------------------
-// K1: cell + hash + bucket occupancy (build_hashmap, broadphase.py:89-130)
+// R1/H1: key + bucket occupancy.  R (Morton key) reads the committed state;
+// H (spatial hash, build_hashmap broadphase.py:89-130) reads the layout.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_hash_count(Dev D) {
+__global__ void __launch_bounds__(kBlock) k_count(Dev D) {
   const Ctl* ctl = D.ctl;
   if (ctl->err) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= D.n) return;
-  const float4 p = D.X[ctl->cur][i];
+  const float4 p = D.key_morton ? D.X[ctl->cur][i] : layout(D, ctl).x[i];
   if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z)) {
     raise_err(D.ctl, GG_EPOSITIONS);
     return;
@@ -180,13 +248,13 @@ __global__ void __launch_bounds__(kBlock) k_hash_count(Dev D) {
   const long long c0 = cell_coord(p.x, D.two_r);
   const long long c1 = cell_coord(p.y, D.two_r);
   const long long c2 = cell_coord(p.z, D.two_r);
-  const uint32_t h = hash_cell(c0, c1, c2, D.H);
+  const uint32_t h = D.key_morton ? morton_key(c0, c1, c2, D.mmask) : hash_cell(c0, c1, c2, D.H);
   D.key[i] = h;
   D.arrive[i] = atomicAdd(&D.cnt[h], 1u);
 }
 
 // ---------------------------------------------------------------------------
-// K2: exclusive scan of cnt[0..n_h) -> start[0..n_h)   (start[n_h] = n fixed)
+// exclusive scan of cnt[0..n_h) -> start[0..n_h)   (start[n_h] = n fixed)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sm, uint32_t* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -206,7 +274,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sm
       const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    if (lane < nw) sm[lane] = s;  // inclusive warp totals
+    if (lane < nw) sm[lane] = s;
   }
   __syncthreads();
   const uint32_t warp_off = wid ? sm[wid - 1] : 0u;
@@ -220,9 +288,14 @@ __global__ void __launch_bounds__(kBlock) k_scan_tiles(Dev D) {
   __shared__ uint32_t sm[32];
   const long long base = static_cast<long long>(blockIdx.x) * kScanTile + threadIdx.x * 8;
   uint32_t s = 0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e)
-    if (base + e < D.H.n_h) s += D.cnt[base + e];
+  if (base + 8 <= D.H.n_h) {
+    const uint4 a = *reinterpret_cast<const uint4*>(D.cnt + base);
+    const uint4 b = *reinterpret_cast<const uint4*>(D.cnt + base + 4);
+    s = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+  } else {
+    for (int e = 0; e < 8; ++e)
+      if (base + e < D.H.n_h) s += D.cnt[base + e];
+  }
   uint32_t total;
   (void)block_excl_scan_u32(s, sm, &total);
   if (threadIdx.x == 0) D.tile[blockIdx.x] = total;
@@ -251,24 +324,37 @@ __global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D) {
   __shared__ uint32_t sm[32];
   const long long base = static_cast<long long>(blockIdx.x) * kScanTile + threadIdx.x * 8;
   uint32_t v[8];
+  const bool full = base + 8 <= D.H.n_h;
+  if (full) {
+    const uint4 a = *reinterpret_cast<const uint4*>(D.cnt + base);
+    const uint4 b = *reinterpret_cast<const uint4*>(D.cnt + base + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (base + e < D.H.n_h) ? D.cnt[base + e] : 0u;
+  }
   uint32_t s = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    v[e] = (base + e < D.H.n_h) ? D.cnt[base + e] : 0u;
-    s += v[e];
-  }
+  for (int e = 0; e < 8; ++e) s += v[e];
   uint32_t total;
   uint32_t run = block_excl_scan_u32(s, sm, &total) + D.tile[blockIdx.x];
+  uint32_t o[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
-    if (base + e < D.H.n_h) {
-      D.start[base + e] = run;
-      run += v[e];
-    }
+  for (int e = 0; e < 8; ++e) {
+    o[e] = run;
+    run += v[e];
+  }
+  if (full) {
+    *reinterpret_cast<uint4*>(D.start + base) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(D.start + base + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+  } else {
+    for (int e = 0; e < 8; ++e)
+      if (base + e < D.H.n_h) D.start[base + e] = o[e];
+  }
 }
 
 // ---------------------------------------------------------------------------
-// K3: counting-sort scatter (arrival order inside a bucket)
+// R3/H3: counting-sort scatter (arrival order inside a bucket)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
   if (D.ctl->err) return;
@@ -277,50 +363,94 @@ __global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
   D.tmp[D.start[D.key[i]] + D.arrive[i]] = i;
 }
 
-// ---------------------------------------------------------------------------
-// K4: stable fix-up + reorder.  Final position inside a bucket = number of
-// bucket members with a smaller USER id, which reproduces
-// np.argsort(hashes, kind="stable") / lexsort((rank, hashes)) exactly
-// (broadphase.py:122,160).  Gathers x, v into the sorted layout.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_reorder(Dev D) {
+// rank of member p inside its bucket by user id (the stable tie order)
+__device__ __forceinline__ uint32_t rank_in_bucket(const Dev& D, const int* __restrict__ uid,
+                                                   uint32_t s, uint32_t e, int my_uid) {
+  uint32_t rank = 0;
+  for (uint32_t m = s; m < e; ++m) rank += (uid[D.tmp[m]] < my_uid) ? 1u : 0u;
+  return rank;
+}
+
+// R4: re-sort the committed state into Morton order (deterministic: ties by uid)
+__global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
   const Ctl* ctl = D.ctl;
   if (ctl->err) return;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= D.n) return;
-  const int cur = ctl->cur;
-  const int* __restrict__ uid_in = D.UID[cur];
+  const int cur = ctl->cur, u = ctl->ucur;
+  const int* __restrict__ uid_in = D.UID[u];
   const int p = D.tmp[k];
   const int uid = uid_in[p];
   const uint32_t h = D.key[p];
-  const uint32_t s = D.start[h], e = D.start[h + 1];
-  uint32_t rank = 0;
-  for (uint32_t m = s; m < e; ++m) rank += (uid_in[D.tmp[m]] < uid) ? 1u : 0u;
-  const uint32_t f = s + rank;
-  D.UID[cur ^ 1][f] = uid;
+  const uint32_t s = D.start[h];
+  const uint32_t f = s + rank_in_bucket(D, uid_in, s, D.start[h + 1], uid);
+  D.UID[u ^ 1][f] = uid;
   D.Xs[f] = D.X[cur][p];
   D.V0[f] = D.V[cur][p];
 }
 
+// H4: fill the bucket-ordered candidate array Xh = (x, y, z, physical index)
+__global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
+  const Ctl* ctl = D.ctl;
+  if (ctl->err) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n) return;
+  const Layout L = layout(D, ctl);
+  const int p = D.tmp[k];
+  const uint32_t h = D.key[p];
+  const uint32_t s = D.start[h], e = D.start[h + 1];
+  const uint32_t f = (e - s == 1) ? s : s + rank_in_bucket(D, L.uid, s, e, L.uid[p]);
+  const float4 x = L.x[p];
+  D.Xh[f] = make_float4(x.x, x.y, x.z, __int_as_float(p));
+}
+
 // ---------------------------------------------------------------------------
-// K5: narrowphase (narrowphase_contacts, contact.py:244-300 with
-// candidate_pairs_with_distances, broadphase.py:149-221).  One thread per
-// sorted particle; 27 neighbour buckets, duplicates among the non-empty ones
-// skipped (the reference's sort + dedupe, broadphase.py:164-171).
+// K5: narrowphase.  One thread per physical particle; the 27 neighbour
+// buckets are visited in three batches of 9 whose bound loads are issued
+// together.  De-duplication (the reference sorts and de-dupes the 27 bucket
+// hashes, broadphase.py:164-171) is only needed if two of the 27 cells can
+// share a bucket; for power-of-two tables that is decided exactly from the
+// per-axis hash terms (63 XOR tests) so the common case skips it.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_narrow(Dev D) {
+__device__ __forceinline__ bool may_alias(const uint32_t tx[3], const uint32_t ty[3],
+                                          const uint32_t tz[3], uint32_t mask) {
+  // differences per axis between the three neighbour coordinates
+  const uint32_t ax[4] = {0u, tx[0] ^ tx[1], tx[1] ^ tx[2], tx[0] ^ tx[2]};
+  const uint32_t ay[4] = {0u, ty[0] ^ ty[1], ty[1] ^ ty[2], ty[0] ^ ty[2]};
+  const uint32_t az[4] = {0u, tz[0] ^ tz[1], tz[1] ^ tz[2], tz[0] ^ tz[2]};
+  bool hit = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (i | j | k) hit |= ((ax[i] ^ ay[j] ^ az[k]) & mask) == 0u;
+  return hit;
+}
+
+__device__ __forceinline__ uint32_t nb_hash(const Dev& D, int o, long long c0, long long c1,
+                                            long long c2, const uint32_t tx[3], const uint32_t ty[3],
+                                            const uint32_t tz[3]) {
+  const int ox = o / 9, oy = (o / 3) % 3, oz = o % 3;
+  if (D.H.pow2) return (tx[ox] ^ ty[oy] ^ tz[oz]) & D.H.mask;
+  return hash_cell64(c0 + ox - 1, c1 + oy - 1, c2 + oz - 1, D.H.n_h);
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
   __shared__ double smd[32];
   __shared__ unsigned long long smu[32];
   const Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  const int step = ctl->step;
-  const gg_body* __restrict__ bodies = D.bodies + static_cast<long long>(step) * D.nb;
+  const float4* __restrict__ LX = layout(D, ctl).x;
+  const float4* __restrict__ Xh = D.Xh;
+  const uint32_t* __restrict__ start = D.start;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = k < D.n;
-  unsigned long long n_pp = 0, n_cand = 0, n_coinc = 0, n_body = 0, n_deg = 0;
+  unsigned long long n_pp = 0, n_cand = 0, n_coinc = 0;
   double max_psi = 0.0;
   if (active) {
-    const float4 pf = D.Xs[k];
+    const float4 pf = LX[k];
     const double px = pf.x, py = pf.y, pz = pf.z;
     const long long c0 = cell_coord(px, D.two_r);
     const long long c1 = cell_coord(py, D.two_r);
@@ -332,55 +462,101 @@ __global__ void __launch_bounds__(kBlock) k_narrow(Dev D) {
       ty[d] = hash_term32(c1 + d - 1, kP1);
       tz[d] = hash_term32(c2 + d - 1, kP2);
     }
+    const bool dedup = !D.H.pow2 || may_alias(tx, ty, tz, D.H.mask);
     const long long K = D.K;
     const long long n = D.n;
     int cnt = 0;
-    uint32_t seen[27];
-    int nseen = 0;
-    for (int o = 0; o < 27; ++o) {
-      const int ox = o / 9, oy = (o / 3) % 3, oz = o % 3;
-      const uint32_t h =
-          D.H.pow2 ? ((tx[ox] ^ ty[oy] ^ tz[oz]) & D.H.mask)
-                   : hash_cell64(c0 + ox - 1, c1 + oy - 1, c2 + oz - 1, D.H.n_h);
-      const uint32_t s = D.start[h], e = D.start[h + 1];
-      if (s == e) continue;
-      bool dup = false;
-      for (int q = 0; q < nseen; ++q) dup |= (seen[q] == h);
-      if (dup) continue;
-      seen[nseen++] = h;
-      n_cand += e - s;
-      for (uint32_t m = s; m < e; ++m) {
-        if (static_cast<int>(m) == k) continue;
-        const float4 qf = D.Xs[m];
-        const double dx = __dsub_rn(px, static_cast<double>(qf.x));
-        const double dy = __dsub_rn(py, static_cast<double>(qf.y));
-        const double dz = __dsub_rn(pz, static_cast<double>(qf.z));
-        // einsum("ij,ij->i") on this numpy build: (dx^2 + dz^2) + dy^2
-        const double d2 =
-            __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
-        if (!(d2 >= D.coinc_d2)) {
-          ++n_coinc;
-          continue;
+#pragma unroll 1
+    for (int g = 0; g < 3; ++g) {
+      uint32_t hb[9], sb[9], eb[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        hb[j] = nb_hash(D, g * 9 + j, c0, c1, c2, tx, ty, tz);
+        sb[j] = __ldg(start + hb[j]);
+        eb[j] = __ldg(start + hb[j] + 1);
+      }
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const uint32_t s = sb[j], e = eb[j];
+        if (s == e) continue;
+        if (dedup) {
+          bool dup = false;
+          const int o = g * 9 + j;
+          for (int q = 0; q < o; ++q) dup |= nb_hash(D, q, c0, c1, c2, tx, ty, tz) == hb[j];
+          if (dup) continue;
         }
-        if (d2 < D.contact_d2) {
-          const double dist = __dsqrt_rn(d2);
-          const double psi = __dsub_rn(D.two_r, dist);
-          if (cnt < K) {
-            const long long sl = cnt * n + k;
-            D.cgeo[sl] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
-                                     static_cast<float>(__ddiv_rn(dy, dist)),
-                                     static_cast<float>(__ddiv_rn(dz, dist)),
-                                     static_cast<float>(psi));
-            D.coth[sl] = static_cast<int>(m);
+        n_cand += e - s;
+        for (uint32_t m = s; m < e; ++m) {
+          const float4 qf = Xh[m];
+          const int q = __float_as_int(qf.w);
+          if (q == k) continue;
+          const double dx = __dsub_rn(px, static_cast<double>(qf.x));
+          const double dy = __dsub_rn(py, static_cast<double>(qf.y));
+          const double dz = __dsub_rn(pz, static_cast<double>(qf.z));
+          // einsum("ij,ij->i") on the reference host: (dx^2 + dz^2) + dy^2
+          const double d2 =
+              __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
+          if (!(d2 >= D.coinc_d2)) {
+            ++n_coinc;
+            continue;
           }
-          ++cnt;
-          max_psi = nmax(max_psi, psi);
+          if (d2 < D.contact_d2) {
+            const double dist = __dsqrt_rn(d2);
+            const double psi = __dsub_rn(D.two_r, dist);
+            if (cnt < K) {
+              const long long sl = cnt * n + k;
+              D.cgeo[sl] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
+                                       static_cast<float>(__ddiv_rn(dy, dist)),
+                                       static_cast<float>(__ddiv_rn(dz, dist)),
+                                       static_cast<float>(psi));
+              D.coth[sl] = q;
+            }
+            ++cnt;
+            max_psi = nmax(max_psi, psi);
+          }
         }
       }
     }
     n_cand -= 1;  // the self pair (one per particle, broadphase.py:441-447)
     n_pp = cnt;
-    // body pass (contact.py:274-286), bodies in index order
+    D.ccount[k] = cnt < K ? cnt : static_cast<int>(K);
+    if (cnt > K) {
+      atomicMax(&D.ctl->cap_needed, cnt);
+      raise_err(D.ctl, GG_ECAPACITY);
+    }
+  }
+  unsigned long long t;
+  t = block_sum_u64(n_pp, smu);
+  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_pp, t);
+  t = block_sum_u64(n_cand, smu);
+  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_cand, t);
+  t = block_sum_u64(n_coinc, smu);
+  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_coinc, t);
+  const double mp = block_reduce<1>(max_psi, smd);
+  if (threadIdx.x == 0 && mp > 0.0) atomicMax(&D.acc->max_psi_bits, dbits(mp));
+}
+
+// ---------------------------------------------------------------------------
+// K6: particle-body contacts (contact.py:274-286): world-AABB prefilter
+// (`_near_body`, contact.py:187-203) then the SDF penetration test
+// (sdf.py:472-512); appended after the particle's pp slots, bodies in index
+// order, like the reference's per-body concatenation.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
+  __shared__ double smd[32];
+  __shared__ unsigned long long smu[32];
+  const Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;
+  const gg_body* __restrict__ bodies = D.bodies + static_cast<long long>(ctl->step) * D.nb;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long n_body = 0, n_deg = 0;
+  double max_psi = 0.0;
+  if (k < D.n) {
+    const float4 pf = layout(D, ctl).x[k];
+    const double px = pf.x, py = pf.y, pz = pf.z;
+    const long long K = D.K;
+    const long long n = D.n;
+    int cnt = D.ccount[k];
     for (int b = 0; b < D.nb; ++b) {
       const gg_body& B = bodies[b];
       if (B.bounded) {
@@ -407,21 +583,15 @@ __global__ void __launch_bounds__(kBlock) k_narrow(Dev D) {
       }
       n_deg += deg;
     }
-    D.ccount[k] = cnt < K ? cnt : static_cast<int>(K);
-    if (cnt > K) {
-      atomicMax(&D.ctl->cap_needed, cnt);
-      raise_err(D.ctl, GG_ECAPACITY);
+    if (n_body) {
+      D.ccount[k] = cnt < K ? cnt : static_cast<int>(K);
+      if (cnt > K) {
+        atomicMax(&D.ctl->cap_needed, cnt);
+        raise_err(D.ctl, GG_ECAPACITY);
+      }
     }
   }
-  // reductions (integers are order-independent; max via bit pattern of a
-  // non-negative double)
   unsigned long long t;
-  t = block_sum_u64(n_pp, smu);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_pp, t);
-  t = block_sum_u64(n_cand, smu);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_cand, t);
-  t = block_sum_u64(n_coinc, smu);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_coinc, t);
   t = block_sum_u64(n_body, smu);
   if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_body, t);
   t = block_sum_u64(n_deg, smu);
@@ -431,129 +601,117 @@ __global__ void __launch_bounds__(kBlock) k_narrow(Dev D) {
 }
 
 // ---------------------------------------------------------------------------
-// K7: one projected-Jacobi sweep (solve_contacts_pja, contact.py:463-501).
-// w = v + dv is the predicted velocity; every contact of owner i reads w of
-// the previous sweep for both i and j, so the sweep is Jacobi-synchronous and
-// each thread writes only its own w (no atomics).  The tangential impulse is
-// -(u - (u.e1) e1), identical to e2*b2 + e3*b3 for the orthonormal frame the
-// reference builds (contact.py:47-56), so the frame is never materialised.
+// K7: the solve.  Cooperative persistent kernel (grid = co-resident blocks):
+//   for s < S: every particle p (grid-stride, static assignment) runs one
+//     projected-Jacobi sweep (solve_contacts_pja, contact.py:463-501):
+//     w = v + dv is the predicted velocity; every contact of owner i reads w
+//     of the previous sweep for both i and j (Jacobi), writes only w_i (no
+//     atomics); sweeps are separated by grid barriers.  The tangential
+//     impulse is -(u - (u.e1) e1), identical to e2*b2 + e3*b3 for the
+//     orthonormal frame of contact.py:47-56, so the frame is never built.
+//   then symplectic Euler (stepper.py:102-106), the SolverError check
+//   (contact.py:503-509), kinetic energy (stepper.py:118), and after a last
+//   barrier block 0 reduces the per-block partials in fixed order into the
+//   StepReport and commits the state.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
-  __shared__ double smd[32];
-  const Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
-  const float4* __restrict__ Win = (s == 0) ? D.V0 : D.W[(s - 1) & 1];
-  float4* __restrict__ Wout = D.W[s & 1];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = k < D.n;
-  double maxviol = 0.0;
-  double minb1 = __longlong_as_double(0x7ff0000000000000ll);
+struct SweepAcc {
+  double maxviol, minb1;
   double bm[kRegBodies][3];
-#pragma unroll
-  for (int b = 0; b < kRegBodies; ++b) bm[b][0] = bm[b][1] = bm[b][2] = 0.0;
-  if (active) {
-    const float4 wf = Win[k];
-    const double wx = wf.x, wy = wf.y, wz = wf.z;
-    double ax = 0.0, ay = 0.0, az = 0.0;
-    const int c = D.ccount[k];
-    const long long n = D.n;
-    for (int sl = 0; sl < c; ++sl) {
-      const long long idx = sl * n + k;
-      const float4 g = D.cgeo[idx];
-      const int j = D.coth[idx];
-      double vjx, vjy, vjz, eff;
-      if (j >= 0) {
-        const float4 q = Win[j];
-        vjx = q.x; vjy = q.y; vjz = q.z;
-        eff = 0.5;  // both partners mobile (contact.py:457-460)
-      } else {
-        const float4 q = D.cvb[idx];
-        vjx = q.x; vjy = q.y; vjz = q.z;
-        eff = 1.0;
-      }
-      const double e1x = g.x, e1y = g.y, e1z = g.z, psi = g.w;
-      const double ux = (wx - D.gamma * vjx) + D.gdt0;
-      const double uy = (wy - D.gamma * vjy) + D.gdt1;
-      const double uz = (wz - D.gamma * vjz) + D.gdt2;
-      const double un = ux * e1x + uy * e1y + uz * e1z;
-      const double bias = D.alpha * psi / D.dt;
-      const double b1 = nmax(-un + bias, 0.0);
-      double btx = -(ux - un * e1x), bty = -(uy - un * e1y), btz = -(uz - un * e1z);
-      const double tn = sqrt(btx * btx + bty * bty + btz * btz);
-      const double lim = D.mu * b1;
-      const double scale = (tn > lim) ? lim / fmax(tn, 1e-300) : 1.0;
-      btx *= scale; bty *= scale; btz *= scale;
-      const double ix = (e1x * b1 + btx) * eff;
-      const double iy = (e1y * b1 + bty) * eff;
-      const double iz = (e1z * b1 + btz) * eff;
-      ax += ix; ay += iy; az += iz;
-      maxviol = nmax(maxviol, tn * scale - lim);
-      minb1 = nmin(minb1, b1);
-      if (j < 0) {
-        const int b = -j - 1;
-        const double mx = -D.mass * ix, my = -D.mass * iy, mz = -D.mass * iz;
-        bool placed = false;
-#pragma unroll
-        for (int q = 0; q < kRegBodies; ++q)
-          if (q == b) { bm[q][0] += mx; bm[q][1] += my; bm[q][2] += mz; placed = true; }
-        if (!placed) {
-          atomicAdd(&D.bm_glob[b * 3 + 0], mx);
-          atomicAdd(&D.bm_glob[b * 3 + 1], my);
-          atomicAdd(&D.bm_glob[b * 3 + 2], mz);
-        }
-      }
+};
+
+__device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* __restrict__ Win,
+                                               float4* __restrict__ Wout, SweepAcc& A) {
+  const float4 wf = Win[k];
+  const double wx = wf.x, wy = wf.y, wz = wf.z;
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  const int c = D.ccount[k];
+  const long long n = D.n;
+  for (int sl = 0; sl < c; ++sl) {
+    const long long idx = sl * n + k;
+    const float4 g = D.cgeo[idx];
+    const int j = D.coth[idx];
+    float4 q;
+    double eff;
+    if (j >= 0) {
+      q = Win[j];
+      eff = 0.5;  // both partners mobile (contact.py:457-460)
+    } else {
+      q = D.cvb[idx];
+      eff = 1.0;
     }
-    Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
-                          static_cast<float>(wz + az), 0.f);
-  }
-  const double mv = block_reduce<1>(maxviol, smd);
-  if (threadIdx.x == 0 && mv > 0.0) atomicMax(&D.acc->max_viol_bits, dbits(mv));
-  const double mb = block_reduce<2>(minb1, smd);
-  if (threadIdx.x == 0 && mb == mb) atomicMin(&D.acc->min_b1_bits, dbits(mb));
-  const int nreg = D.nb < kRegBodies ? D.nb : kRegBodies;
-  for (int b = 0; b < nreg; ++b) {
+    const double e1x = g.x, e1y = g.y, e1z = g.z;
+    const double ux = (wx - D.gamma * q.x) + D.gdt0;
+    const double uy = (wy - D.gamma * q.y) + D.gdt1;
+    const double uz = (wz - D.gamma * q.z) + D.gdt2;
+    const double un = ux * e1x + uy * e1y + uz * e1z;
+    const double b1 = nmax(-un + D.alpha * (double)g.w / D.dt, 0.0);
+    double btx = un * e1x - ux, bty = un * e1y - uy, btz = un * e1z - uz;
+    const double tn = sqrt(btx * btx + bty * bty + btz * btz);
+    const double lim = D.mu * b1;
+    if (tn > lim) {
+      const double sc = lim / fmax(tn, 1e-300);
+      btx *= sc; bty *= sc; btz *= sc;
+      A.maxviol = nmax(A.maxviol, tn * sc - lim);
+    }
+    const double ix = (e1x * b1 + btx) * eff;
+    const double iy = (e1y * b1 + bty) * eff;
+    const double iz = (e1z * b1 + btz) * eff;
+    ax += ix; ay += iy; az += iz;
+    A.minb1 = nmin(A.minb1, b1);
+    if (j < 0) {
+      const int b = -j - 1;
+      const double mx = -D.mass * ix, my = -D.mass * iy, mz = -D.mass * iz;
+      bool placed = false;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      double v = 0.0;
-#pragma unroll
-      for (int q = 0; q < kRegBodies; ++q)
-        if (q == b) v = bm[q][a];
-      const double tot = block_reduce<0>(v, smd);
-      if (threadIdx.x == 0) {
-        double* dst = &D.bm_part[(static_cast<long long>(blockIdx.x) * D.nb + b) * 3 + a];
-        *dst = (s == 0) ? tot : *dst + tot;
+      for (int qq = 0; qq < kRegBodies; ++qq)
+        if (qq == b) { A.bm[qq][0] += mx; A.bm[qq][1] += my; A.bm[qq][2] += mz; placed = true; }
+      if (!placed) {
+        atomicAdd(&D.bm_glob[b * 3 + 0], mx);
+        atomicAdd(&D.bm_glob[b * 3 + 1], my);
+        atomicAdd(&D.bm_glob[b * 3 + 2], mz);
       }
     }
   }
+  Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
+                        static_cast<float>(wz + az), 0.f);
 }
 
-// ---------------------------------------------------------------------------
-// K8: integrate (stepper.py:102-106) + SolverError check (contact.py:503-509)
-// + kinetic energy partials (stepper.py:118).  Writes the uncommitted state
-// buffer; k_finalize commits it only when the step raised nothing.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_integrate(Dev D) {
+__global__ void __launch_bounds__(kBlock, 2) k_solve(Dev D) {
   __shared__ double smd[32];
-  const Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
+  Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
   const int cur = ctl->cur;
-  const float4* __restrict__ Wf = D.S > 0 ? D.W[(D.S - 1) & 1] : D.V0;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int step = ctl->step;
+  const Layout L = layout(D, ctl);
+  const int G = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  SweepAcc A;
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+  for (int b = 0; b < kRegBodies; ++b) A.bm[b][0] = A.bm[b][1] = A.bm[b][2] = 0.0;
+  for (int s = 0; s < D.S; ++s) {
+    const float4* __restrict__ Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+    float4* __restrict__ Wout = D.W[s & 1];
+    for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+    grid_barrier(ctl);
+  }
+  // integrate: v += dt*g + dv ; x += dt*v ; cyclic boundary
+  const float4* __restrict__ Wf = D.W[(D.S - 1) & 1];
   double ke = 0.0;
-  if (k < D.n) {
-    const float4 xo = D.Xs[k];
-    const float4 vo = D.V0[k];
+  for (int k = t0; k < D.n; k += G) {
+    const float4 xo = L.x[k];
+    const float4 vo = L.v[k];
     const float4 wf = Wf[k];
     const bool has = D.ccount[k] > 0;
     const double dvx = has ? (double)wf.x - (double)vo.x : 0.0;
     const double dvy = has ? (double)wf.y - (double)vo.y : 0.0;
     const double dvz = has ? (double)wf.z - (double)vo.z : 0.0;
     if (!isfinite(dvx) || !isfinite(dvy) || !isfinite(dvz)) {
-      const int slot = atomicAdd(&D.ctl->n_bad, 1);
-      if (slot < kMaxBad) D.ctl->bad_uid[slot] = D.UID[cur ^ 1][k];
-      raise_err(D.ctl, GG_ENONFINITE);
+      const int slot = atomicAdd(&ctl->n_bad, 1);
+      if (slot < kMaxBad) ctl->bad_uid[slot] = L.uid[k];
+      raise_err(ctl, GG_ENONFINITE);
     }
-    // v += dt*g + dv ; x += dt*v
     const double vx = __dadd_rn((double)vo.x, __dadd_rn(D.gdt0, dvx));
     const double vy = __dadd_rn((double)vo.y, __dadd_rn(D.gdt1, dvy));
     const double vz = __dadd_rn((double)vo.z, __dadd_rn(D.gdt2, dvz));
@@ -565,37 +723,57 @@ __global__ void __launch_bounds__(kBlock) k_integrate(Dev D) {
                                   static_cast<float>(z), 0.f);
     D.V[cur ^ 1][k] = make_float4(static_cast<float>(vx), static_cast<float>(vy),
                                   static_cast<float>(vz), 0.f);
-    ke = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    ke += __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
   }
-  const double kb = block_reduce<0>(ke, smd);
-  if (threadIdx.x == 0) D.ke_part[blockIdx.x] = kb;
-}
-
-// ---------------------------------------------------------------------------
-// K9: fixed-order reduction of the per-block partials -> StepReport; commit.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_finalize(Dev D) {
-  __shared__ double smd[32];
-  Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
-  const int step = ctl->step;
-  double ke = 0.0;
-  for (int b = threadIdx.x; b < D.nblocks; b += blockDim.x) ke += D.ke_part[b];
-  const double ke_tot = block_reduce<0>(ke, smd);
+  // per-block partials, fixed order
+  double* P = D.part + static_cast<long long>(blockIdx.x) * kPartStride;
+  double r;
+  r = block_reduce<0>(ke, smd);
+  if (threadIdx.x == 0) P[0] = r;
+  r = block_reduce<1>(A.maxviol, smd);
+  if (threadIdx.x == 0) P[1] = r;
+  r = block_reduce<2>(A.minb1, smd);
+  if (threadIdx.x == 0) P[2] = r;
+  const int nreg = D.nb < kRegBodies ? D.nb : kRegBodies;
+  for (int b = 0; b < nreg; ++b) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < kRegBodies; ++q)
+        if (q == b) v = A.bm[q][a];
+      r = block_reduce<0>(v, smd);
+      if (threadIdx.x == 0) P[4 + 3 * b + a] = r;
+    }
+  }
+  grid_barrier(ctl);
+  if (blockIdx.x != 0) return;
+  // block 0: fixed-order reduction over blocks -> StepReport, commit
+  const int nbk = gridDim.x;
+  double v0 = 0.0, v1 = 0.0, v2 = __longlong_as_double(0x7ff0000000000000ll);
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
+    const double* Q = D.part + static_cast<long long>(b) * kPartStride;
+    v0 += Q[0];
+    v1 = nmax(v1, Q[1]);
+    v2 = nmin(v2, Q[2]);
+  }
+  const double ke_tot = block_reduce<0>(v0, smd);
+  const double viol = block_reduce<1>(v1, smd);
+  const double minb1 = block_reduce<2>(v2, smd);
   for (int q = 0; q < D.nb * 3; ++q) {
-    double v = 0.0;
     const int b = q / 3;
+    double v = 0.0;
     if (b < kRegBodies)
-      for (int blk = threadIdx.x; blk < D.nblocks; blk += blockDim.x)
-        v += D.bm_part[static_cast<long long>(blk) * D.nb * 3 + q];
+      for (int blk = threadIdx.x; blk < nbk; blk += blockDim.x)
+        v += D.part[static_cast<long long>(blk) * kPartStride + 4 + q];
     const double tot = block_reduce<0>(v, smd);
     if (threadIdx.x == 0) {
-      D.bm_out[static_cast<long long>(step) * D.nb * 3 + q] =
-          b < kRegBodies ? (D.S > 0 ? tot : 0.0) : D.bm_glob[q];
+      D.bm_out[static_cast<long long>(step) * D.nb * 3 + q] = b < kRegBodies ? tot : D.bm_glob[q];
       D.bm_glob[q] = 0.0;
     }
   }
   if (threadIdx.x == 0) {
+    if (*((volatile int*)&ctl->err)) return;  // NaN raised in integrate: no commit
     Acc* a = D.acc;
     gg_report& R = D.reports[step];
     R.n_contacts = static_cast<long long>(a->n_pp);
@@ -605,19 +783,18 @@ __global__ void __launch_bounds__(kBlock) k_finalize(Dev D) {
     R.n_degenerate = static_cast<long long>(a->n_deg);
     R.max_penetration = __longlong_as_double(static_cast<long long>(a->max_psi_bits));
     R.kinetic_energy = 0.5 * D.mass * ke_tot;
-    R.max_cone_violation = __longlong_as_double(static_cast<long long>(a->max_viol_bits));
-    R.min_normal_impulse = __longlong_as_double(static_cast<long long>(a->min_b1_bits));
+    R.max_cone_violation = viol;
+    R.min_normal_impulse = minb1;
     a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
     a->max_psi_bits = 0;
-    a->max_viol_bits = 0;
-    a->min_b1_bits = dbits(__longlong_as_double(0x7ff0000000000000ll));
-    ctl->cur ^= 1;
+    ctl->cur = cur ^ 1;
+    if (D.resort) ctl->ucur ^= 1;
     ctl->step = step + 1;
   }
 }
 
 // ---------------------------------------------------------------------------
-// state upload / download helpers
+// state upload / download helpers (committed layout)
 // ---------------------------------------------------------------------------
 __global__ void k_load_f64(Dev D, const double* __restrict__ x, const double* __restrict__ v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -627,14 +804,14 @@ __global__ void k_load_f64(Dev D, const double* __restrict__ x, const double* __
                             static_cast<float>(x[3 * i + 2]), 0.f);
   D.V[cur][i] = make_float4(static_cast<float>(v[3 * i]), static_cast<float>(v[3 * i + 1]),
                             static_cast<float>(v[3 * i + 2]), 0.f);
-  D.UID[cur][i] = i;
+  D.UID[D.ctl->ucur][i] = i;
 }
 
 __global__ void k_store_f64(Dev D, double* __restrict__ x, double* __restrict__ v) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= D.n) return;
   const int cur = D.ctl->cur;
-  const int u = D.UID[cur][k];
+  const int u = D.UID[D.ctl->ucur][k];
   const float4 p = D.X[cur][k], q = D.V[cur][k];
   x[3 * u] = p.x; x[3 * u + 1] = p.y; x[3 * u + 2] = p.z;
   v[3 * u] = q.x; v[3 * u + 1] = q.y; v[3 * u + 2] = q.z;
@@ -645,17 +822,18 @@ __global__ void k_load_f4(Dev D, const float4* __restrict__ x, const float4* __r
   if (i >= D.n) return;
   const int cur = D.ctl->cur;
   float4 a = x[i], b = v[i];
-  a.w = 0.f; b.w = 0.f;
+  a.w = 0.f;
+  b.w = 0.f;
   D.X[cur][i] = a;
   D.V[cur][i] = b;
-  D.UID[cur][i] = i;
+  D.UID[D.ctl->ucur][i] = i;
 }
 
 __global__ void k_store_f4(Dev D, float4* __restrict__ x, float4* __restrict__ v) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= D.n) return;
   const int cur = D.ctl->cur;
-  const int u = D.UID[cur][k];
+  const int u = D.UID[D.ctl->ucur][k];
   x[u] = D.X[cur][k];
   v[u] = D.V[cur][k];
 }
@@ -665,13 +843,20 @@ __global__ void k_tap_cells(Dev D, long long* __restrict__ cells, long long* __r
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= D.n) return;
   const int cur = D.ctl->cur;
-  const int u = D.UID[cur][k];
+  const int u = D.UID[D.ctl->ucur][k];
   const float4 p = D.X[cur][k];
   const long long c0 = cell_coord(p.x, D.two_r);
   const long long c1 = cell_coord(p.y, D.two_r);
   const long long c2 = cell_coord(p.z, D.two_r);
   cells[3 * u] = c0; cells[3 * u + 1] = c1; cells[3 * u + 2] = c2;
   hashes[u] = hash_cell(c0, c1, c2, D.H);
+}
+
+// bucket order as user ids (the stable argsort tap)
+__global__ void k_tap_order(Dev D, long long* __restrict__ order) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n) return;
+  order[k] = D.UID[D.ctl->ucur][__float_as_int(D.Xh[k].w)];
 }
 
 __global__ void k_hash_cells(const long long* __restrict__ cells, long long k, HashCfg H,
