@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=20)
+    ap.add_argument("--solve-mode", type=int, default=0)
+    ap.add_argument("--resort-every", type=int, default=8)
     return ap.parse_args()
 
 
@@ -233,6 +235,9 @@ def bytes_model(n_h: int, S: int, c_pp: float, c_b: float) -> dict:
         "k_bodies": 16.0 + 32.0 * c_b,                     # body contacts
         "k_solve": S * (48.0 + 20.0 * c_pp + 32.0 * c_b) + 80.0,  # S sweeps + integrate
     }
+    per_kernel["k_step_fused"] = (per_kernel["k_count"] + 16.0 * 1 + 20.0 + per_kernel["k_fill"]
+                                  + per_kernel["k_narrow"] + per_kernel["k_bodies"]
+                                  + per_kernel["k_solve"])  # the whole step in one kernel
     step = 228.0 + 16.0 * P + 48.0 * S + (S + 1) * (20.0 * c_pp + 32.0 * c_b)
     return {"per_kernel_per_particle": per_kernel, "step_per_particle": step, "radix_passes": P}
 
@@ -326,6 +331,8 @@ def run_ours(args, dist: Dist):
     eng = engine_for(sc)
     eng.device = dev
     eng.prepare(sc)
+    N.check(eng.ctx, N.lib().gg_set_solve_mode(eng.ctx, args.solve_mode), "solve mode")
+    N.check(eng.ctx, N.lib().gg_set_resort_every(eng.ctx, args.resort_every), "resort")
     nb = len(sc.bodies)
     K, W = args.steps, args.warmup
     table, _ = eng.body_tables(sc, W + K)
@@ -379,7 +386,8 @@ def run_ours(args, dist: Dist):
     kind_ms, kind_n = kind_ms[: len(names)], kind_n[: len(names)]
     model = bytes_model(eng.n_h, sc.params.solver_iterations, c_pp, c_b)
     share = {names[k]: float(kind_ms[k] / max(kind_ms.sum(), 1e-9)) for k in range(len(names))}
-    top = max((k for k in range(len(names)) if names[k] in model["per_kernel_per_particle"]),
+    top = max((k for k in range(len(names))
+               if names[k] in model["per_kernel_per_particle"] and kind_n[k] > 0),
               key=lambda k: kind_ms[k])
     top_name = names[top]
     avg_ms = float(kind_ms[top] / max(kind_n[top], 1))

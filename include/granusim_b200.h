@@ -199,6 +199,13 @@ int gg_required_contacts(gg_ctx* ctx);
  * it (contact enumeration order is the bucket order); only locality does. */
 int gg_set_resort_every(gg_ctx* ctx, int32_t steps);
 
+/* Launch strategy: 0 auto (the whole step as ONE persistent cooperative
+ * kernel when every particle has its own co-resident thread, else one kernel
+ * per phase and per sweep), 1 per-phase kernels + cooperative persistent
+ * solve, 2 same without the cooperative attribute, 3 per-phase kernels and
+ * one launch per sweep, 4 fused step.  Results are identical in every mode. */
+int gg_set_solve_mode(gg_ctx* ctx, int32_t mode);
+
 /* Page-lock host arrays so gg_set/get_state_f64 run at full PCIe speed. */
 int gg_host_register(void* ptr, int64_t bytes);
 int gg_host_unregister(void* ptr);

@@ -115,6 +115,7 @@ def _bind(lib: C.CDLL) -> None:
         "gg_set_max_contacts": (C.c_int, [P, i32]),
         "gg_max_contacts": (C.c_int, [P]),
         "gg_set_resort_every": (C.c_int, [P, i32]),
+        "gg_set_solve_mode": (C.c_int, [P, i32]),
         "gg_required_contacts": (C.c_int, [P]),
         "gg_host_register": (C.c_int, [P, i64]),
         "gg_host_unregister": (C.c_int, [P]),

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -59,6 +60,8 @@ struct gg_ctx {
   bool graph_dirty = true;
   int solve_grid = 0;      // co-resident blocks of k_solve
   int resort_every = 8;    // physical re-sort period (steps)
+  int solve_mode = 0;      // 0 auto, 1 coop solve, 2 plain persistent solve, 3 per-sweep, 4 fused step
+  int fused_grid = 0;      // co-resident blocks of k_step_fused
   long long since_resort = 1 << 30;  // force a re-sort after upload
 
   std::vector<void*> owned;  // fixed-size allocations freed at destroy
@@ -129,6 +132,14 @@ void fill_params(gg_ctx* ctx) {
   D.alpha = P.baumgarte_alpha;
   D.dt = P.timestep;
   D.gamma = P.gamma;
+  D.bias_coef = P.baumgarte_alpha / P.timestep;
+  {
+    // conservative float32 reject threshold (see k_narrow)
+    const double t = P.contact_d2 * (1.0 + 1e-5);
+    float f = static_cast<float>(t);
+    if (static_cast<double>(f) < t) f = nextafterf(f, INFINITY);
+    D.reject_d2f = f;
+  }
   D.gdt0 = P.gdt[0];
   D.gdt1 = P.gdt[1];
   D.gdt2 = P.gdt[2];
@@ -163,9 +174,10 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
   if (nb > ctx->max_bodies) {
     // grow the body capacity: the fallback momentum accumulators depend on it
     ctx->max_bodies = nb;
-    dfree(ctx, ctx->D.bm_glob);
-    ctx->D.bm_glob = nullptr;
-    CK(dalloc(ctx, &ctx->D.bm_glob, static_cast<size_t>(nb) * 3));
+    dfree(ctx, ctx->D.bm_fix);
+    ctx->D.bm_fix = nullptr;
+    CK(dalloc(ctx, &ctx->D.bm_fix, static_cast<size_t>(nb) * 3));
+    CK(cudaMemset(ctx->D.bm_fix, 0, sizeof(unsigned long long) * nb * 3));
   }
   int cap = std::max(ctx->batch_cap, 1);
   while (cap < need) cap *= 2;
@@ -189,9 +201,22 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
 
 // The step schedule.  Optional Morton re-sort (R1-R4), the hash index
 // (H1-H4), narrowphase, cooperative solve.  All on ctx->stream.
-int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
+bool use_fused_step(const gg_ctx* ctx) {
+  if (ctx->solve_mode == 4) return true;
+  if (ctx->solve_mode != 0) return false;
+  return ctx->n <= static_cast<long long>(ctx->fused_grid) * kBlock;
+}
+
+bool use_persistent_solve(const gg_ctx* ctx) {
+  if (ctx->solve_mode == 3) return false;
+  if (ctx->solve_mode == 0) return false;  // auto: fused for small n, per-sweep otherwise
+  return ctx->n <= static_cast<long long>(ctx->solve_grid) * kBlock;
+}
+
+int launch_coop(gg_ctx* ctx, void (*kern)(Dev), int grid, const Dev& D, cudaStream_t s, bool coop) {
+  CK(cudaMemsetAsync(&D.ctl->bar_count, 0, sizeof(unsigned), s));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ctx->solve_grid);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kBlock);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
@@ -199,9 +224,20 @@ int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_solve, D));
+  cfg.numAttrs = coop ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kern, D));
   return GG_OK;
+}
+
+int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
+  if (!use_persistent_solve(ctx)) {
+    // one thread per particle: S sweep launches + integrate/report
+    for (int it = 0; it < D.S; ++it) k_sweep<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
+    k_finish<<<ctx->nblocks, kBlock, 0, s>>>(D);
+    CK(cudaGetLastError());
+    return GG_OK;
+  }
+  return launch_coop(ctx, k_solve, ctx->solve_grid, D, s, ctx->solve_mode != 2);
 }
 
 int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
@@ -229,6 +265,7 @@ Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
 
 int enqueue_step(gg_ctx* ctx, int resort) {
   cudaStream_t s = ctx->stream;
+  if (use_fused_step(ctx)) return launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s, true);
   int st;
   if (resort) {
     st = enqueue_sort_pass(ctx, pass_dev(ctx, 1, 1), s);
@@ -243,16 +280,21 @@ int enqueue_step(gg_ctx* ctx, int resort) {
   return launch_solve(ctx, D, s);
 }
 
+bool use_persistent_solve(const gg_ctx* ctx);
+bool use_fused_step(const gg_ctx* ctx);
+
 int kernels_per_step(const gg_ctx* ctx, int resort) {
-  return 8 + (ctx->D.nb > 0 ? 1 : 0) + (resort ? 6 : 0);
+  if (use_fused_step(ctx)) return 1;
+  const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 1;
+  return 7 + solve + (ctx->D.nb > 0 ? 1 : 0) + (resort ? 6 : 0);
 }
 
 // Same schedule as enqueue_step, with an event after every kernel so each
 // kernel kind's device time can be attributed (bench roofline pass).
-constexpr int kProfKinds = 11;
+constexpr int kProfKinds = 12;
 const char* kProfNames[kProfKinds] = {"memset_counts", "k_count", "k_scan_tiles", "k_scan_top",
                                       "k_scan_apply",  "k_scatter", "k_resort",  "k_fill",
-                                      "k_narrow",      "k_solve",   "k_bodies"};
+                                      "k_narrow",      "k_solve",   "k_bodies",  "k_step_fused"};
 
 int ensure_events(gg_ctx* ctx, size_t n) {
   while (ctx->evpool.size() < n) {
@@ -275,6 +317,12 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     ++e;
   };
   cudaEventRecord(ev[0], s);
+  if (use_fused_step(ctx)) {
+    if (launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s, true) != GG_OK)
+      return -1;
+    mark(11);
+    return e;
+  }
   for (int pass = resort ? 0 : 1; pass < 2; ++pass) {
     const Dev D = pass_dev(ctx, resort, pass == 0 ? 1 : 0);
     cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s);
@@ -435,14 +483,17 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
   CK(dalloc(ctx, &D.acc, 1));
   // co-resident grid of the cooperative solve kernel
   {
-    int per_sm = 0, sms = 0;
+    int per_sm = 0, sms = 0, per_sm_f = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kBlock, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, k_step_fused, kBlock, 0));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     ctx->solve_grid = std::max(1, std::min(ctx->nblocks, per_sm * sms));
+    ctx->fused_grid = std::max(1, std::min(ctx->nblocks, per_sm_f * sms));
   }
   CK(dalloc(ctx, &D.Xh, n));
-  CK(dalloc(ctx, &D.part, static_cast<size_t>(ctx->solve_grid) * kPartStride));
-  CK(dalloc(ctx, &D.bm_glob, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3));
+  CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks}))));
+  CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3));
+  CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3));
   CK(dalloc(ctx, &D.ctl, 1));
   CK(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
   st = alloc_slots(ctx, max_contacts > 0 ? max_contacts : 16);
@@ -499,6 +550,13 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
 }
 
 int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
+
+int gg_set_solve_mode(gg_ctx* ctx, int32_t mode) {
+  if (!ctx || mode < 0 || mode > 4) return fail(ctx, GG_EINVAL, "solve mode must be 0..4");
+  ctx->solve_mode = mode;
+  ctx->graph_dirty = true;
+  return GG_OK;
+}
 
 int gg_set_resort_every(gg_ctx* ctx, int32_t steps) {
   if (!ctx || steps < 1) return fail(ctx, GG_EINVAL, "resort_every must be >= 1");

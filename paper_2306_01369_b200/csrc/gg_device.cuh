@@ -100,7 +100,7 @@ struct DevGrid {
   long long offset;       // into the concatenated value store
 };
 
-__device__ __forceinline__ double grid_distance(const DevGrid& G, const double* __restrict__ vals,
+__device__ __noinline__ double grid_distance(const DevGrid& G, const double* __restrict__ vals,
                                                 double px, double py, double pz) {
   const double p[3] = {px, py, pz};
   double cl[3], u[3], f[3];
@@ -175,7 +175,7 @@ __device__ __forceinline__ double sdf_distance(const gg_body& B, const DevGrid* 
   }
 }
 
-__device__ __forceinline__ d3 sdf_gradient(const gg_body& B, const DevGrid* __restrict__ grids,
+__device__ __noinline__ d3 sdf_gradient(const gg_body& B, const DevGrid* __restrict__ grids,
                                            const double* __restrict__ gvals, double x, double y,
                                            double z) {
   d3 g{0.0, 0.0, 0.0};

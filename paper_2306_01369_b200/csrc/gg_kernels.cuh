@@ -40,7 +40,6 @@ namespace gg {
 
 constexpr int kBlock = 256;
 constexpr int kScanTile = 2048;  // elements per scan tile (256 thr x 8)
-constexpr int kRegBodies = 4;    // bodies with deterministic in-register momentum
 constexpr int kMaxBad = 32;
 
 struct Ctl {
@@ -52,15 +51,22 @@ struct Ctl {
   int cap_needed;  // largest per-owner contact count seen (capacity hint)
   int n_bad;       // non-finite particles recorded
   int pad;
-  unsigned bar_count;  // grid barrier
-  unsigned bar_gen;
+  unsigned bar_count;  // grid barrier arrivals (monotonic within a launch, reset per launch)
+  unsigned done_count; // last-block-done counter of the solve kernel
   int bad_uid[kMaxBad];
 };
 
 struct Acc {
   unsigned long long n_pp, n_cand, n_body, n_coinc, n_deg;
-  unsigned long long max_psi_bits;
+  unsigned long long max_psi_bits, max_viol_bits, min_b1_bits;
 };
+
+// body reaction momentum is accumulated in 64-bit fixed point so the sum is
+// independent of the order in which contacts add to it (deterministic)
+constexpr double kMomScale = 68719476736.0;  // 2^36
+__device__ __forceinline__ unsigned long long to_fix(double v) {
+  return static_cast<unsigned long long>(__double2ll_rn(v * kMomScale));
+}
 
 struct Dev {
   int n, K, nb, S, nblocks;
@@ -68,7 +74,8 @@ struct Dev {
   int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
   HashCfg H;
   uint32_t mmask;  // Morton key mask (power of two <= n_h, minus one)
-  double r, two_r, contact_d2, coinc_d2, mass, mu, alpha, dt, gamma;
+  double r, two_r, contact_d2, coinc_d2, mass, mu, alpha, dt, gamma, bias_coef;
+  float reject_d2f;  // float32 pre-filter: d2_f32 > this  =>  d2 >= contact_d2 exactly
   double gdt0, gdt1, gdt2;
   int has_boundary;
   double z_min, band;
@@ -93,14 +100,13 @@ struct Dev {
   const DevGrid* grids;
   const double* gvals;
   Acc* acc;
-  double* part;     // [nblocks_solve][4 + 3 * kRegBodies] per-block partials
-  double* bm_glob;  // [nb][3] fallback accumulators for bodies >= kRegBodies
+  double* part;     // [nblocks_solve] per-block kinetic-energy partials
+  unsigned long long* bm_fix;  // [nb][3] fixed-point body momentum of the step
   gg_report* reports;
   double* bm_out;  // [batch][nb][3]
   Ctl* ctl;
 };
 
-constexpr int kPartStride = 4 + 3 * kRegBodies;
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void raise_err(Ctl* ctl, int code) {
@@ -166,19 +172,21 @@ __device__ __forceinline__ bool block_should_exit(const Ctl* ctl) {
 }
 
 // Grid-wide barrier for the cooperative kernel (all blocks co-resident).
-__device__ __forceinline__ void grid_barrier(Ctl* ctl) {
+// One release-add per block on a counter that only grows during a launch
+// (zeroed by a memset node before the launch); blocks wait with acquire loads
+// until it reaches the barrier's target (nblocks x barrier ordinal).
+__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = &ctl->bar_gen;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
-      ctl->bar_count = 0;
-      __threadfence();
-      atomicExch(&ctl->bar_gen, g + 1);
-    } else {
-      while (*gen == g) __nanosleep(32);
+    unsigned v;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
+    v += 1;
+    while (static_cast<int>(v - target) < 0) {
+      __nanosleep(16);
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
     }
+    // gpu-scope fence: invalidates this SM's L1 (CCTL.IVALL) so no block
+    // reads a line cached before other SMs rewrote it in the previous phase
     __threadfence();
   }
   __syncthreads();
@@ -225,37 +233,38 @@ __global__ void k_batch_begin(Dev D) {
   c->cap_needed = 0;
   c->n_bad = 0;
   c->bar_count = 0;
+  c->done_count = 0;
   Acc* a = D.acc;
   a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
-  a->max_psi_bits = 0;
-  for (int i = 0; i < D.nb * 3; ++i) D.bm_glob[i] = 0.0;
+  a->max_psi_bits = a->max_viol_bits = 0;
+  a->min_b1_bits = dbits(__longlong_as_double(0x7ff0000000000000ll));
+  for (int i = 0; i < D.nb * 3; ++i) D.bm_fix[i] = 0ull;
 }
 
-// ---------------------------------------------------------------------------
+// ===========================================================================
+// Phases.  Element-wise phases (ph_count, ph_scatter, ph_resort, ph_fill)
+// handle one index; block phases (ph_scan_*, ph_narrow, ph_bodies) contain
+// __syncthreads and must be called by every thread of the block.  The
+// standalone kernels and the fused small-n kernel are thin drivers.
+// ===========================================================================
+
 // R1/H1: key + bucket occupancy.  R (Morton key) reads the committed state;
 // H (spatial hash, build_hashmap broadphase.py:89-130) reads the layout.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_count(Dev D) {
-  const Ctl* ctl = D.ctl;
-  if (ctl->err) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= D.n) return;
-  const float4 p = D.key_morton ? D.X[ctl->cur][i] : layout(D, ctl).x[i];
+__device__ __forceinline__ void ph_count(const Dev& D, Ctl* ctl, int i, bool morton) {
+  const float4 p = morton ? D.X[ctl->cur][i] : layout(D, ctl).x[i];
   if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z)) {
-    raise_err(D.ctl, GG_EPOSITIONS);
+    raise_err(ctl, GG_EPOSITIONS);
     return;
   }
   const long long c0 = cell_coord(p.x, D.two_r);
   const long long c1 = cell_coord(p.y, D.two_r);
   const long long c2 = cell_coord(p.z, D.two_r);
-  const uint32_t h = D.key_morton ? morton_key(c0, c1, c2, D.mmask) : hash_cell(c0, c1, c2, D.H);
+  const uint32_t h = morton ? morton_key(c0, c1, c2, D.mmask) : hash_cell(c0, c1, c2, D.H);
   D.key[i] = h;
   D.arrive[i] = atomicAdd(&D.cnt[h], 1u);
 }
 
-// ---------------------------------------------------------------------------
 // exclusive scan of cnt[0..n_h) -> start[0..n_h)   (start[n_h] = n fixed)
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sm, uint32_t* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t x = v;
@@ -283,27 +292,28 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sm
   return warp_off + x - v;
 }
 
-__global__ void __launch_bounds__(kBlock) k_scan_tiles(Dev D) {
-  if (D.ctl->err) return;
-  __shared__ uint32_t sm[32];
-  const long long base = static_cast<long long>(blockIdx.x) * kScanTile + threadIdx.x * 8;
-  uint32_t s = 0;
+// 8 consecutive counts of a tile (kScanTile = 8 x kBlock)
+__device__ __forceinline__ void load8(const Dev& D, long long base, uint32_t v[8]) {
   if (base + 8 <= D.H.n_h) {
     const uint4 a = *reinterpret_cast<const uint4*>(D.cnt + base);
     const uint4 b = *reinterpret_cast<const uint4*>(D.cnt + base + 4);
-    s = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
   } else {
-    for (int e = 0; e < 8; ++e)
-      if (base + e < D.H.n_h) s += D.cnt[base + e];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = (base + e < D.H.n_h) ? D.cnt[base + e] : 0u;
   }
-  uint32_t total;
-  (void)block_excl_scan_u32(s, sm, &total);
-  if (threadIdx.x == 0) D.tile[blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_top(Dev D, int ntiles) {
-  if (D.ctl->err) return;
-  __shared__ uint32_t sm[32];
+__device__ __forceinline__ void ph_scan_tile(const Dev& D, int t, uint32_t* sm) {
+  uint32_t v[8];
+  load8(D, static_cast<long long>(t) * kScanTile + threadIdx.x * 8, v);
+  uint32_t s = v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7];
+  uint32_t total;
+  (void)block_excl_scan_u32(s, sm, &total);
+  if (threadIdx.x == 0) D.tile[t] = total;
+}
+
+__device__ __forceinline__ void ph_scan_top(const Dev& D, int ntiles, uint32_t* sm) {
   const int per = (ntiles + blockDim.x - 1) / blockDim.x;
   const int b0 = threadIdx.x * per;
   uint32_t s = 0;
@@ -319,32 +329,20 @@ __global__ void __launch_bounds__(1024) k_scan_top(Dev D, int ntiles) {
     }
 }
 
-__global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D) {
-  if (D.ctl->err) return;
-  __shared__ uint32_t sm[32];
-  const long long base = static_cast<long long>(blockIdx.x) * kScanTile + threadIdx.x * 8;
+__device__ __forceinline__ void ph_scan_apply(const Dev& D, int t, uint32_t* sm) {
+  const long long base = static_cast<long long>(t) * kScanTile + threadIdx.x * 8;
   uint32_t v[8];
-  const bool full = base + 8 <= D.H.n_h;
-  if (full) {
-    const uint4 a = *reinterpret_cast<const uint4*>(D.cnt + base);
-    const uint4 b = *reinterpret_cast<const uint4*>(D.cnt + base + 4);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = (base + e < D.H.n_h) ? D.cnt[base + e] : 0u;
-  }
-  uint32_t s = 0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) s += v[e];
+  load8(D, base, v);
+  const uint32_t s = v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7];
   uint32_t total;
-  uint32_t run = block_excl_scan_u32(s, sm, &total) + D.tile[blockIdx.x];
+  uint32_t run = block_excl_scan_u32(s, sm, &total) + D.tile[t];
   uint32_t o[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     o[e] = run;
     run += v[e];
   }
-  if (full) {
+  if (base + 8 <= D.H.n_h) {
     *reinterpret_cast<uint4*>(D.start + base) = make_uint4(o[0], o[1], o[2], o[3]);
     *reinterpret_cast<uint4*>(D.start + base + 4) = make_uint4(o[4], o[5], o[6], o[7]);
   } else {
@@ -353,18 +351,13 @@ __global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D) {
   }
 }
 
-// ---------------------------------------------------------------------------
 // R3/H3: counting-sort scatter (arrival order inside a bucket)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
-  if (D.ctl->err) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= D.n) return;
+__device__ __forceinline__ void ph_scatter(const Dev& D, int i) {
   D.tmp[D.start[D.key[i]] + D.arrive[i]] = i;
 }
 
-// rank of member p inside its bucket by user id (the stable tie order)
-__device__ __forceinline__ uint32_t rank_in_bucket(const Dev& D, const int* __restrict__ uid,
+// rank of a member inside its bucket by user id (the stable tie order)
+__device__ __forceinline__ uint32_t rank_in_bucket(const Dev& D, const int* uid,
                                                    uint32_t s, uint32_t e, int my_uid) {
   uint32_t rank = 0;
   for (uint32_t m = s; m < e; ++m) rank += (uid[D.tmp[m]] < my_uid) ? 1u : 0u;
@@ -372,13 +365,9 @@ __device__ __forceinline__ uint32_t rank_in_bucket(const Dev& D, const int* __re
 }
 
 // R4: re-sort the committed state into Morton order (deterministic: ties by uid)
-__global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
-  const Ctl* ctl = D.ctl;
-  if (ctl->err) return;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= D.n) return;
+__device__ __forceinline__ void ph_resort(const Dev& D, const Ctl* ctl, int k) {
   const int cur = ctl->cur, u = ctl->ucur;
-  const int* __restrict__ uid_in = D.UID[u];
+  const int* uid_in = D.UID[u];
   const int p = D.tmp[k];
   const int uid = uid_in[p];
   const uint32_t h = D.key[p];
@@ -390,11 +379,7 @@ __global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
 }
 
 // H4: fill the bucket-ordered candidate array Xh = (x, y, z, physical index)
-__global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
-  const Ctl* ctl = D.ctl;
-  if (ctl->err) return;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= D.n) return;
+__device__ __forceinline__ void ph_fill(const Dev& D, const Ctl* ctl, int k) {
   const Layout L = layout(D, ctl);
   const int p = D.tmp[k];
   const uint32_t h = D.key[p];
@@ -405,16 +390,12 @@ __global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
 }
 
 // ---------------------------------------------------------------------------
-// K5: narrowphase.  One thread per physical particle; the 27 neighbour
-// buckets are visited in three batches of 9 whose bound loads are issued
-// together.  De-duplication (the reference sorts and de-dupes the 27 bucket
-// hashes, broadphase.py:164-171) is only needed if two of the 27 cells can
-// share a bucket; for power-of-two tables that is decided exactly from the
-// per-axis hash terms (63 XOR tests) so the common case skips it.
+// K5 narrowphase helpers
 // ---------------------------------------------------------------------------
+// Can two of the 27 neighbour cells share a bucket?  For power-of-two tables
+// decided exactly from the per-axis hash terms (63 XOR tests).
 __device__ __forceinline__ bool may_alias(const uint32_t tx[3], const uint32_t ty[3],
                                           const uint32_t tz[3], uint32_t mask) {
-  // differences per axis between the three neighbour coordinates
   const uint32_t ax[4] = {0u, tx[0] ^ tx[1], tx[1] ^ tx[2], tx[0] ^ tx[2]};
   const uint32_t ay[4] = {0u, ty[0] ^ ty[1], ty[1] ^ ty[2], ty[0] ^ ty[2]};
   const uint32_t az[4] = {0u, tz[0] ^ tz[1], tz[1] ^ tz[2], tz[0] ^ tz[2]};
@@ -437,19 +418,59 @@ __device__ __forceinline__ uint32_t nb_hash(const Dev& D, int o, long long c0, l
   return hash_cell64(c0 + ox - 1, c1 + oy - 1, c2 + oz - 1, D.H.n_h);
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
-  __shared__ double smd[32];
-  __shared__ unsigned long long smu[32];
-  const Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
-  const float4* __restrict__ LX = layout(D, ctl).x;
-  const float4* __restrict__ Xh = D.Xh;
-  const uint32_t* __restrict__ start = D.start;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = k < D.n;
+// The exact pp test on one candidate (contact.py:257-272): float64 from
+// float32-representable inputs in the reference's operation order.
+__device__ __forceinline__ void pp_candidate(const Dev& D, int k, double px, double py, double pz,
+                                             float4 qf, int q, int& cnt, unsigned long long& n_coinc,
+                                             double& max_psi) {
+  const double dx = __dsub_rn(px, static_cast<double>(qf.x));
+  const double dy = __dsub_rn(py, static_cast<double>(qf.y));
+  const double dz = __dsub_rn(pz, static_cast<double>(qf.z));
+  // einsum("ij,ij->i") on the reference host: (dx^2 + dz^2) + dy^2
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
+  if (!(d2 >= D.coinc_d2)) {
+    ++n_coinc;
+    return;
+  }
+  if (d2 < D.contact_d2) {
+    const double dist = __dsqrt_rn(d2);
+    const double psi = __dsub_rn(D.two_r, dist);
+    if (cnt < D.K) {
+      const long long sl = static_cast<long long>(cnt) * D.n + k;
+      D.cgeo[sl] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
+                               static_cast<float>(__ddiv_rn(dy, dist)),
+                               static_cast<float>(__ddiv_rn(dz, dist)), static_cast<float>(psi));
+      D.coth[sl] = q;
+    }
+    ++cnt;
+    max_psi = nmax(max_psi, psi);
+  }
+}
+
+struct NarrowSmem {
+  uint32_t beg[27][kBlock];
+  uint16_t len[27][kBlock];  // bucket sizes are < 2^16
+  double d[32];
+  unsigned long long u[32];
+};
+
+// Particle k = base + threadIdx.x.  Phase 1: the 27 neighbour-bucket bounds,
+// loaded in three batches of 9 independent loads; empty and duplicate buckets
+// are dropped and the rest compacted into a per-thread list in shared memory.
+// Phase 2: ONE flat loop over the concatenated candidates (lanes stay
+// converged; the next candidate is prefetched while the current one is
+// tested), a conservative float32 reject, then the exact float64 test.
+__device__ __forceinline__ void ph_narrow(const Dev& D, Ctl* ctl, int base, NarrowSmem& sm) {
+  // plain (coherent) loads: in the fused kernel these buffers are written
+  // earlier in the same launch, so the read-only (.nc) path is not allowed
+  const float4* LX = layout(D, ctl).x;
+  const float4* Xh = D.Xh;
+  const uint32_t* start = D.start;
+  const int tid = threadIdx.x;
+  const int k = base + tid;
   unsigned long long n_pp = 0, n_cand = 0, n_coinc = 0;
   double max_psi = 0.0;
-  if (active) {
+  if (k < D.n) {
     const float4 pf = LX[k];
     const double px = pf.x, py = pf.y, pz = pf.z;
     const long long c0 = cell_coord(px, D.two_r);
@@ -463,99 +484,88 @@ __global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
       tz[d] = hash_term32(c2 + d - 1, kP2);
     }
     const bool dedup = !D.H.pow2 || may_alias(tx, ty, tz, D.H.mask);
-    const long long K = D.K;
-    const long long n = D.n;
-    int cnt = 0;
-#pragma unroll 1
+    int nb = 0;
+    uint32_t total = 0;
+#pragma unroll
     for (int g = 0; g < 3; ++g) {
       uint32_t hb[9], sb[9], eb[9];
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
         hb[j] = nb_hash(D, g * 9 + j, c0, c1, c2, tx, ty, tz);
-        sb[j] = __ldg(start + hb[j]);
-        eb[j] = __ldg(start + hb[j] + 1);
+        sb[j] = start[hb[j]];
+        eb[j] = start[hb[j] + 1];
       }
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
-        const uint32_t s = sb[j], e = eb[j];
-        if (s == e) continue;
-        if (dedup) {
-          bool dup = false;
-          const int o = g * 9 + j;
-          for (int q = 0; q < o; ++q) dup |= nb_hash(D, q, c0, c1, c2, tx, ty, tz) == hb[j];
-          if (dup) continue;
+        bool keep = eb[j] > sb[j];
+        if (keep && dedup) {
+          for (int q = 0; q < g * 9 + j; ++q) keep &= nb_hash(D, q, c0, c1, c2, tx, ty, tz) != hb[j];
         }
-        n_cand += e - s;
-        for (uint32_t m = s; m < e; ++m) {
-          const float4 qf = Xh[m];
-          const int q = __float_as_int(qf.w);
-          if (q == k) continue;
-          const double dx = __dsub_rn(px, static_cast<double>(qf.x));
-          const double dy = __dsub_rn(py, static_cast<double>(qf.y));
-          const double dz = __dsub_rn(pz, static_cast<double>(qf.z));
-          // einsum("ij,ij->i") on the reference host: (dx^2 + dz^2) + dy^2
-          const double d2 =
-              __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
-          if (!(d2 >= D.coinc_d2)) {
-            ++n_coinc;
-            continue;
-          }
-          if (d2 < D.contact_d2) {
-            const double dist = __dsqrt_rn(d2);
-            const double psi = __dsub_rn(D.two_r, dist);
-            if (cnt < K) {
-              const long long sl = cnt * n + k;
-              D.cgeo[sl] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
-                                       static_cast<float>(__ddiv_rn(dy, dist)),
-                                       static_cast<float>(__ddiv_rn(dz, dist)),
-                                       static_cast<float>(psi));
-              D.coth[sl] = q;
-            }
-            ++cnt;
-            max_psi = nmax(max_psi, psi);
-          }
+        if (keep) {
+          sm.beg[nb][tid] = sb[j];
+          sm.len[nb][tid] = static_cast<uint16_t>(eb[j] - sb[j]);
+          total += eb[j] - sb[j];
+          ++nb;
         }
       }
     }
-    n_cand -= 1;  // the self pair (one per particle, broadphase.py:441-447)
+    n_cand = total - 1;  // minus the self pair (one per particle, broadphase.py:441-447)
+    int cnt = 0;
+    int b = 0;
+    uint32_t m = sm.beg[0][tid];
+    uint32_t left = sm.len[0][tid];
+    float4 qf = Xh[m];
+    for (uint32_t i = 0; i < total; ++i) {
+      // advance to the next candidate and prefetch it
+      ++m;
+      --left;
+      if (left == 0 && i + 1 < total) {
+        ++b;
+        m = sm.beg[b][tid];
+        left = sm.len[b][tid];
+      }
+      const float4 nxt = (i + 1 < total) ? Xh[m] : qf;
+      const int q = __float_as_int(qf.w);
+      if (q != k) {
+        // float32 pre-filter, conservative by a 1e-5 relative margin (the
+        // float32 estimate is within ~4e-7 relative of the exact square)
+        const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
+        if (fx * fx + fy * fy + fz * fz <= D.reject_d2f)
+          pp_candidate(D, k, px, py, pz, qf, q, cnt, n_coinc, max_psi);
+      }
+      qf = nxt;
+    }
     n_pp = cnt;
-    D.ccount[k] = cnt < K ? cnt : static_cast<int>(K);
-    if (cnt > K) {
-      atomicMax(&D.ctl->cap_needed, cnt);
-      raise_err(D.ctl, GG_ECAPACITY);
+    D.ccount[k] = cnt < D.K ? cnt : D.K;
+    if (cnt > D.K) {
+      atomicMax(&ctl->cap_needed, cnt);
+      raise_err(ctl, GG_ECAPACITY);
     }
   }
   unsigned long long t;
-  t = block_sum_u64(n_pp, smu);
+  t = block_sum_u64(n_pp, sm.u);
   if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_pp, t);
-  t = block_sum_u64(n_cand, smu);
+  t = block_sum_u64(n_cand, sm.u);
   if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_cand, t);
-  t = block_sum_u64(n_coinc, smu);
+  t = block_sum_u64(n_coinc, sm.u);
   if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_coinc, t);
-  const double mp = block_reduce<1>(max_psi, smd);
+  const double mp = block_reduce<1>(max_psi, sm.d);
   if (threadIdx.x == 0 && mp > 0.0) atomicMax(&D.acc->max_psi_bits, dbits(mp));
 }
 
-// ---------------------------------------------------------------------------
 // K6: particle-body contacts (contact.py:274-286): world-AABB prefilter
 // (`_near_body`, contact.py:187-203) then the SDF penetration test
 // (sdf.py:472-512); appended after the particle's pp slots, bodies in index
 // order, like the reference's per-body concatenation.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
-  __shared__ double smd[32];
-  __shared__ unsigned long long smu[32];
-  const Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
-  const gg_body* __restrict__ bodies = D.bodies + static_cast<long long>(ctl->step) * D.nb;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void ph_bodies(const Dev& D, Ctl* ctl, int base, double* smd,
+                                          unsigned long long* smu) {
+  const gg_body* bodies = D.bodies + static_cast<long long>(ctl->step) * D.nb;
+  const int k = base + threadIdx.x;
   unsigned long long n_body = 0, n_deg = 0;
   double max_psi = 0.0;
   if (k < D.n) {
     const float4 pf = layout(D, ctl).x[k];
     const double px = pf.x, py = pf.y, pz = pf.z;
-    const long long K = D.K;
-    const long long n = D.n;
     int cnt = D.ccount[k];
     for (int b = 0; b < D.nb; ++b) {
       const gg_body& B = bodies[b];
@@ -568,8 +578,8 @@ __global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
       d3 nrm;
       int deg;
       if (penetrate(B, D.grids, D.gvals, px, py, pz, D.r, &psi, &nrm, &deg)) {
-        if (cnt < K) {
-          const long long sl = cnt * n + k;
+        if (cnt < D.K) {
+          const long long sl = static_cast<long long>(cnt) * D.n + k;
           const d3 vb = body_surface_velocity(B, px, py, pz, nrm, D.r, psi);
           D.cgeo[sl] = make_float4(static_cast<float>(nrm.x), static_cast<float>(nrm.y),
                                    static_cast<float>(nrm.z), static_cast<float>(psi));
@@ -584,10 +594,10 @@ __global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
       n_deg += deg;
     }
     if (n_body) {
-      D.ccount[k] = cnt < K ? cnt : static_cast<int>(K);
-      if (cnt > K) {
-        atomicMax(&D.ctl->cap_needed, cnt);
-        raise_err(D.ctl, GG_ECAPACITY);
+      D.ccount[k] = cnt < D.K ? cnt : D.K;
+      if (cnt > D.K) {
+        atomicMax(&ctl->cap_needed, cnt);
+        raise_err(ctl, GG_ECAPACITY);
       }
     }
   }
@@ -601,103 +611,98 @@ __global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
 }
 
 // ---------------------------------------------------------------------------
-// K7: the solve.  Cooperative persistent kernel (grid = co-resident blocks):
-//   for s < S: every particle p (grid-stride, static assignment) runs one
-//     projected-Jacobi sweep (solve_contacts_pja, contact.py:463-501):
-//     w = v + dv is the predicted velocity; every contact of owner i reads w
-//     of the previous sweep for both i and j (Jacobi), writes only w_i (no
-//     atomics); sweeps are separated by grid barriers.  The tangential
-//     impulse is -(u - (u.e1) e1), identical to e2*b2 + e3*b3 for the
-//     orthonormal frame of contact.py:47-56, so the frame is never built.
-//   then symplectic Euler (stepper.py:102-106), the SolverError check
-//   (contact.py:503-509), kinetic energy (stepper.py:118), and after a last
-//   barrier block 0 reduces the per-block partials in fixed order into the
-//   StepReport and commits the state.
+// K7: projected-Jacobi sweep (solve_contacts_pja, contact.py:463-501).
+// w = v + dv is the predicted velocity; every contact of owner i reads w of
+// the previous sweep for both i and j (Jacobi), writes only w_i (no atomics).
+// The tangential impulse is -(u - (u.e1) e1), identical to e2*b2 + e3*b3 for
+// the orthonormal frame of contact.py:47-56, so the frame is never built.
 // ---------------------------------------------------------------------------
 struct SweepAcc {
   double maxviol, minb1;
-  double bm[kRegBodies][3];
 };
 
-__device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* __restrict__ Win,
-                                               float4* __restrict__ Wout, SweepAcc& A) {
+__device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
+                                                float4 g, int j, float4 q, double& ax, double& ay,
+                                                double& az, SweepAcc& A) {
+  const double eff = (j >= 0) ? 0.5 : 1.0;  // both partners mobile (contact.py:457-460)
+  const double e1x = g.x, e1y = g.y, e1z = g.z;
+  const double ux = (wx - D.gamma * q.x) + D.gdt0;
+  const double uy = (wy - D.gamma * q.y) + D.gdt1;
+  const double uz = (wz - D.gamma * q.z) + D.gdt2;
+  const double un = ux * e1x + uy * e1y + uz * e1z;
+  const double b1 = nmax(D.bias_coef * (double)g.w - un, 0.0);
+  double btx = un * e1x - ux, bty = un * e1y - uy, btz = un * e1z - uz;
+  const double tn2 = btx * btx + bty * bty + btz * btz;
+  const double lim = D.mu * b1;
+  if (tn2 > lim * lim) {  // sliding: project onto the Coulomb cone
+    const double tn = sqrt(tn2);
+    const double sc = lim / fmax(tn, 1e-300);
+    btx *= sc;
+    bty *= sc;
+    btz *= sc;
+    A.maxviol = nmax(A.maxviol, tn * sc - lim);
+  }
+  const double ix = (e1x * b1 + btx) * eff;
+  const double iy = (e1y * b1 + bty) * eff;
+  const double iz = (e1z * b1 + btz) * eff;
+  ax += ix;
+  ay += iy;
+  az += iz;
+  A.minb1 = nmin(A.minb1, b1);
+  if (j < 0) {  // reaction momentum on the body (contact.py:489-495)
+    unsigned long long* bm = D.bm_fix + 3 * (-j - 1);
+    atomicAdd(bm + 0, to_fix(-D.mass * ix));
+    atomicAdd(bm + 1, to_fix(-D.mass * iy));
+    atomicAdd(bm + 2, to_fix(-D.mass * iz));
+  }
+}
+
+__device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* Win, float4* Wout,
+                                               SweepAcc& A) {
+  // slot 0 is fetched together with the count and w_k (one round trip)
+  const int c = D.ccount[k];
   const float4 wf = Win[k];
+  const float4 g0 = D.cgeo[k];
+  const int j0 = D.coth[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  const int c = D.ccount[k];
-  const long long n = D.n;
-  for (int sl = 0; sl < c; ++sl) {
-    const long long idx = sl * n + k;
-    const float4 g = D.cgeo[idx];
-    const int j = D.coth[idx];
-    float4 q;
-    double eff;
-    if (j >= 0) {
-      q = Win[j];
-      eff = 0.5;  // both partners mobile (contact.py:457-460)
-    } else {
-      q = D.cvb[idx];
-      eff = 1.0;
-    }
-    const double e1x = g.x, e1y = g.y, e1z = g.z;
-    const double ux = (wx - D.gamma * q.x) + D.gdt0;
-    const double uy = (wy - D.gamma * q.y) + D.gdt1;
-    const double uz = (wz - D.gamma * q.z) + D.gdt2;
-    const double un = ux * e1x + uy * e1y + uz * e1z;
-    const double b1 = nmax(-un + D.alpha * (double)g.w / D.dt, 0.0);
-    double btx = un * e1x - ux, bty = un * e1y - uy, btz = un * e1z - uz;
-    const double tn = sqrt(btx * btx + bty * bty + btz * btz);
-    const double lim = D.mu * b1;
-    if (tn > lim) {
-      const double sc = lim / fmax(tn, 1e-300);
-      btx *= sc; bty *= sc; btz *= sc;
-      A.maxviol = nmax(A.maxviol, tn * sc - lim);
-    }
-    const double ix = (e1x * b1 + btx) * eff;
-    const double iy = (e1y * b1 + bty) * eff;
-    const double iz = (e1z * b1 + btz) * eff;
-    ax += ix; ay += iy; az += iz;
-    A.minb1 = nmin(A.minb1, b1);
-    if (j < 0) {
-      const int b = -j - 1;
-      const double mx = -D.mass * ix, my = -D.mass * iy, mz = -D.mass * iz;
-      bool placed = false;
-#pragma unroll
-      for (int qq = 0; qq < kRegBodies; ++qq)
-        if (qq == b) { A.bm[qq][0] += mx; A.bm[qq][1] += my; A.bm[qq][2] += mz; placed = true; }
-      if (!placed) {
-        atomicAdd(&D.bm_glob[b * 3 + 0], mx);
-        atomicAdd(&D.bm_glob[b * 3 + 1], my);
-        atomicAdd(&D.bm_glob[b * 3 + 2], mz);
-      }
+  if (c > 0) {
+    const float4 q0 = (j0 >= 0) ? Win[j0] : D.cvb[k];
+    contact_impulse(D, wx, wy, wz, g0, j0, q0, ax, ay, az, A);
+    const int n = D.n;
+    for (int sl = 1; sl < c; ++sl) {
+      const int idx = sl * n + k;
+      const float4 g = D.cgeo[idx];
+      const int j = D.coth[idx];
+      const float4 q = (j >= 0) ? Win[j] : D.cvb[idx];
+      contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
     }
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
                         static_cast<float>(wz + az), 0.f);
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_solve(Dev D) {
-  __shared__ double smd[32];
-  Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
+// warp-level reduction of the sweep diagnostics into the step accumulators
+__device__ __forceinline__ void flush_diag(const Dev& D, const SweepAcc& A) {
+  const double mv = warp_max(A.maxviol);
+  const double mb = warp_min(A.minb1);
+  if ((threadIdx.x & 31) == 0) {
+    if (mv > 0.0) atomicMax(&D.acc->max_viol_bits, dbits(mv));
+    if (mb == mb && mb < __longlong_as_double(0x7ff0000000000000ll))
+      atomicMin(&D.acc->min_b1_bits, dbits(mb));
+  }
+}
+
+// Symplectic Euler (stepper.py:102-106), SolverError check
+// (contact.py:503-509), kinetic energy (stepper.py:118); the last block to
+// finish reduces the per-block partials in fixed order into the StepReport
+// and commits the new state.  Called by every thread of every block.
+__device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int t0, int G,
+                                                     double* smd, int* s_last) {
   const int cur = ctl->cur;
   const int step = ctl->step;
   const Layout L = layout(D, ctl);
-  const int G = gridDim.x * blockDim.x;
-  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
-  SweepAcc A;
-  A.maxviol = 0.0;
-  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
-#pragma unroll
-  for (int b = 0; b < kRegBodies; ++b) A.bm[b][0] = A.bm[b][1] = A.bm[b][2] = 0.0;
-  for (int s = 0; s < D.S; ++s) {
-    const float4* __restrict__ Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
-    float4* __restrict__ Wout = D.W[s & 1];
-    for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
-    grid_barrier(ctl);
-  }
-  // integrate: v += dt*g + dv ; x += dt*v ; cyclic boundary
-  const float4* __restrict__ Wf = D.W[(D.S - 1) & 1];
+  const float4* Wf = D.W[(D.S - 1) & 1];
   double ke = 0.0;
   for (int k = t0; k < D.n; k += G) {
     const float4 xo = L.x[k];
@@ -712,6 +717,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_solve(Dev D) {
       if (slot < kMaxBad) ctl->bad_uid[slot] = L.uid[k];
       raise_err(ctl, GG_ENONFINITE);
     }
+    // v += dt*g + dv ; x += dt*v
     const double vx = __dadd_rn((double)vo.x, __dadd_rn(D.gdt0, dvx));
     const double vy = __dadd_rn((double)vo.y, __dadd_rn(D.gdt1, dvy));
     const double vz = __dadd_rn((double)vo.z, __dadd_rn(D.gdt2, dvz));
@@ -725,55 +731,27 @@ __global__ void __launch_bounds__(kBlock, 2) k_solve(Dev D) {
                                   static_cast<float>(vz), 0.f);
     ke += __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
   }
-  // per-block partials, fixed order
-  double* P = D.part + static_cast<long long>(blockIdx.x) * kPartStride;
-  double r;
-  r = block_reduce<0>(ke, smd);
-  if (threadIdx.x == 0) P[0] = r;
-  r = block_reduce<1>(A.maxviol, smd);
-  if (threadIdx.x == 0) P[1] = r;
-  r = block_reduce<2>(A.minb1, smd);
-  if (threadIdx.x == 0) P[2] = r;
-  const int nreg = D.nb < kRegBodies ? D.nb : kRegBodies;
-  for (int b = 0; b < nreg; ++b) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      double v = 0.0;
-#pragma unroll
-      for (int q = 0; q < kRegBodies; ++q)
-        if (q == b) v = A.bm[q][a];
-      r = block_reduce<0>(v, smd);
-      if (threadIdx.x == 0) P[4 + 3 * b + a] = r;
-    }
+  const double r = block_reduce<0>(ke, smd);
+  if (threadIdx.x == 0) {
+    D.part[blockIdx.x] = r;
+    __threadfence();
+    *s_last = atomicAdd(&ctl->done_count, 1u) == gridDim.x - 1;
   }
-  grid_barrier(ctl);
-  if (blockIdx.x != 0) return;
-  // block 0: fixed-order reduction over blocks -> StepReport, commit
-  const int nbk = gridDim.x;
-  double v0 = 0.0, v1 = 0.0, v2 = __longlong_as_double(0x7ff0000000000000ll);
-  for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
-    const double* Q = D.part + static_cast<long long>(b) * kPartStride;
-    v0 += Q[0];
-    v1 = nmax(v1, Q[1]);
-    v2 = nmin(v2, Q[2]);
-  }
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();
+  double v0 = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v0 += *((volatile double*)&D.part[b]);
   const double ke_tot = block_reduce<0>(v0, smd);
-  const double viol = block_reduce<1>(v1, smd);
-  const double minb1 = block_reduce<2>(v2, smd);
-  for (int q = 0; q < D.nb * 3; ++q) {
-    const int b = q / 3;
-    double v = 0.0;
-    if (b < kRegBodies)
-      for (int blk = threadIdx.x; blk < nbk; blk += blockDim.x)
-        v += D.part[static_cast<long long>(blk) * kPartStride + 4 + q];
-    const double tot = block_reduce<0>(v, smd);
-    if (threadIdx.x == 0) {
-      D.bm_out[static_cast<long long>(step) * D.nb * 3 + q] = b < kRegBodies ? tot : D.bm_glob[q];
-      D.bm_glob[q] = 0.0;
-    }
+  if (threadIdx.x < D.nb * 3) {
+    const long long f =
+        static_cast<long long>(*((volatile unsigned long long*)&D.bm_fix[threadIdx.x]));
+    D.bm_out[static_cast<long long>(step) * D.nb * 3 + threadIdx.x] = static_cast<double>(f) / kMomScale;
+    D.bm_fix[threadIdx.x] = 0ull;
   }
   if (threadIdx.x == 0) {
-    if (*((volatile int*)&ctl->err)) return;  // NaN raised in integrate: no commit
+    ctl->done_count = 0;
+    if (*((volatile int*)&ctl->err)) return;  // an error was raised this step: no commit
     Acc* a = D.acc;
     gg_report& R = D.reports[step];
     R.n_contacts = static_cast<long long>(a->n_pp);
@@ -783,14 +761,204 @@ __global__ void __launch_bounds__(kBlock, 2) k_solve(Dev D) {
     R.n_degenerate = static_cast<long long>(a->n_deg);
     R.max_penetration = __longlong_as_double(static_cast<long long>(a->max_psi_bits));
     R.kinetic_energy = 0.5 * D.mass * ke_tot;
-    R.max_cone_violation = viol;
-    R.min_normal_impulse = minb1;
+    R.max_cone_violation = __longlong_as_double(static_cast<long long>(a->max_viol_bits));
+    R.min_normal_impulse = __longlong_as_double(static_cast<long long>(a->min_b1_bits));
     a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
-    a->max_psi_bits = 0;
+    a->max_psi_bits = a->max_viol_bits = 0;
+    a->min_b1_bits = dbits(__longlong_as_double(0x7ff0000000000000ll));
     ctl->cur = cur ^ 1;
     if (D.resort) ctl->ucur ^= 1;
     ctl->step = step + 1;
   }
+}
+
+// ===========================================================================
+// Large-n drivers: one kernel per phase, one thread per element.
+// ===========================================================================
+__global__ void __launch_bounds__(kBlock) k_count(Dev D) {
+  Ctl* ctl = D.ctl;
+  if (ctl->err) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < D.n) ph_count(D, ctl, i, D.key_morton != 0);
+}
+
+__global__ void __launch_bounds__(kBlock) k_scan_tiles(Dev D) {
+  __shared__ uint32_t sm[32];
+  if (D.ctl->err) return;
+  ph_scan_tile(D, blockIdx.x, sm);
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(Dev D, int ntiles) {
+  __shared__ uint32_t sm[32];
+  if (D.ctl->err) return;
+  ph_scan_top(D, ntiles, sm);
+}
+
+__global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D) {
+  __shared__ uint32_t sm[32];
+  if (D.ctl->err) return;
+  ph_scan_apply(D, blockIdx.x, sm);
+}
+
+__global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
+  if (D.ctl->err) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < D.n) ph_scatter(D, i);
+}
+
+__global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
+  if (D.ctl->err) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < D.n) ph_resort(D, D.ctl, k);
+}
+
+__global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
+  if (D.ctl->err) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < D.n) ph_fill(D, D.ctl, k);
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
+  __shared__ NarrowSmem sm;
+  Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;
+  ph_narrow(D, ctl, blockIdx.x * blockDim.x, sm);
+}
+
+__global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
+  __shared__ double smd[32];
+  __shared__ unsigned long long smu[32];
+  Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;
+  ph_bodies(D, ctl, blockIdx.x * blockDim.x, smd, smu);
+}
+
+__global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
+  const Ctl* ctl = D.ctl;
+  if (ctl->err) return;
+  const Layout L = layout(D, ctl);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  SweepAcc A;
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  if (k < D.n) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+  flush_diag(D, A);
+}
+
+__global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
+  __shared__ double smd[32];
+  __shared__ int s_last;
+  Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;
+  integrate_and_finish(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, smd,
+                       &s_last);
+}
+
+// ===========================================================================
+// Small-n driver: the WHOLE step in one persistent kernel (grid = co-resident
+// blocks, cooperative launch), grid barriers between phases instead of
+// kernel launches.  Blocks never leave early: after every barrier each block
+// re-reads the error flag (all errors raised before a barrier are visible
+// after it) and skips work, so every block reaches every barrier.
+// ===========================================================================
+__device__ __forceinline__ bool barrier_ok(Ctl* ctl, unsigned& target, int* s_flag) {
+  target += gridDim.x;
+  grid_barrier(ctl, target);
+  if (threadIdx.x == 0) *s_flag = *((volatile int*)&ctl->err);
+  __syncthreads();
+  return *s_flag == 0;
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
+  __shared__ NarrowSmem sm;
+  __shared__ uint32_t smu[32];
+  __shared__ int s_flag;
+  __shared__ int s_last;
+  Ctl* ctl = D.ctl;
+  if (threadIdx.x == 0) s_flag = *((volatile int*)&ctl->err);
+  __syncthreads();
+  bool ok = s_flag == 0;
+  unsigned target = 0;
+  const int G = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ntiles = static_cast<int>((D.H.n_h + kScanTile - 1) / kScanTile);
+  for (int pass = D.resort ? 0 : 1; pass < 2; ++pass) {
+    const bool morton = pass == 0;
+    if (ok) {
+      uint4* c4 = reinterpret_cast<uint4*>(D.cnt);
+      const long long n4 = D.H.n_h / 4;
+      for (long long i = t0; i < n4; i += G) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      for (long long i = 4 * n4 + t0; i < D.H.n_h; i += G) D.cnt[i] = 0u;
+    }
+    ok = barrier_ok(ctl, target, &s_flag);
+    if (ok)
+      for (int i = t0; i < D.n; i += G) ph_count(D, ctl, i, morton);
+    ok = barrier_ok(ctl, target, &s_flag);
+    if (ok)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ph_scan_tile(D, t, smu);
+    ok = barrier_ok(ctl, target, &s_flag);
+    if (ok && blockIdx.x == 0) ph_scan_top(D, ntiles, smu);
+    ok = barrier_ok(ctl, target, &s_flag);
+    if (ok)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ph_scan_apply(D, t, smu);
+    ok = barrier_ok(ctl, target, &s_flag);
+    if (ok)
+      for (int i = t0; i < D.n; i += G) ph_scatter(D, i);
+    ok = barrier_ok(ctl, target, &s_flag);
+    if (ok) {
+      for (int k = t0; k < D.n; k += G) {
+        if (morton)
+          ph_resort(D, ctl, k);
+        else
+          ph_fill(D, ctl, k);
+      }
+    }
+    ok = barrier_ok(ctl, target, &s_flag);
+  }
+  // narrowphase + bodies; the sweeps below use the same particle -> thread
+  // map, so a particle's contacts are read by the thread that wrote them
+  if (ok) {
+    for (int base = blockIdx.x * blockDim.x; base < D.n; base += G) {
+      ph_narrow(D, ctl, base, sm);
+      if (D.nb > 0) ph_bodies(D, ctl, base, sm.d, sm.u);
+    }
+  }
+  const Layout L = layout(D, ctl);
+  SweepAcc A;
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  for (int s = 0; s < D.S; ++s) {
+    if (s > 0) ok = barrier_ok(ctl, target, &s_flag) && ok;
+    if (ok) {
+      const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+      float4* Wout = D.W[s & 1];
+      for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+    }
+  }
+  flush_diag(D, A);
+  integrate_and_finish(D, ctl, t0, G, sm.d, &s_last);
+}
+
+// Small-n solve only (cooperative): S sweeps with grid barriers + finish.
+__global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
+  __shared__ double smd[32];
+  __shared__ int s_last;
+  Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
+  const Layout L = layout(D, ctl);
+  const int G = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  SweepAcc A;
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  for (int s = 0; s < D.S; ++s) {
+    if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
+    const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+    float4* Wout = D.W[s & 1];
+    for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+  }
+  flush_diag(D, A);
+  integrate_and_finish(D, ctl, t0, G, smd, &s_last);
 }
 
 // ---------------------------------------------------------------------------

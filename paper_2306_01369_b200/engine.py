@@ -237,7 +237,11 @@ class Engine:
 
     def body_tables(self, scene, n_steps: int):
         """Advance scene.t / body poses step by step (stepper.py:65-67) and
-        pack one gg_body row per body per step.  Returns (table, ts)."""
+        pack one gg_body row per body per step.  Returns (table, ts).
+
+        Drivers that can evaluate a whole batch of times (``pose_batch``)
+        are packed with array operations; any other driver (e.g. the
+        reference's own objects) is evaluated step by step."""
         dt = scene.params.timestep
         r = float(scene.params.radius)
         nb = len(scene.bodies)
@@ -247,22 +251,51 @@ class Engine:
         for k in range(n_steps):
             t += dt
             ts[k] = t
-        batchable = nb > 0 and all(hasattr(b.driver, "pose_batch") for b in scene.bodies)
-        if batchable and n_steps > 1:
-            for bi, body in enumerate(scene.bodies):
+        for bi, body in enumerate(scene.bodies):
+            col = table[:, bi]
+            if n_steps > 1 and hasattr(body.driver, "pose_batch"):
                 poses, omegas, vels = body.driver.pose_batch(ts)
+                self._fill_column(body, r, col, poses, omegas, vels)
+            else:
                 for k in range(n_steps):
-                    body.pose, body.omega, body.v_origin = poses[k], omegas[k], vels[k]
-                    self.body_row(body, r, table[k, bi])
-            for body in scene.bodies:
-                body.update(ts[-1])
-        else:
-            for k in range(n_steps):
-                for bi, body in enumerate(scene.bodies):
                     body.update(ts[k])
-                    self.body_row(body, r, table[k, bi])
+                    self.body_row(body, r, col[k])
+        if n_steps > 1:
+            for body in scene.bodies:
+                if hasattr(body.driver, "pose_batch"):
+                    body.update(ts[-1])
         scene.t = t
         return table, ts
+
+    def _fill_column(self, body, r: float, col, poses, omegas, vels) -> None:
+        """Vectorised body_row for T poses of one body."""
+        geom = body.geometry
+        kind = geometry_kind(geom)
+        T = len(col)
+        poses = np.broadcast_to(np.asarray(poses, dtype=np.float64), (T, 4, 4))
+        col["kind"] = kind
+        col["shape"] = geometry_shape(geom)
+        col["grid_id"] = self.grid_id(geom) if kind == N.GEOM_GRID else -1
+        R = poses[:, :3, :3]
+        tr = poses[:, :3, 3]
+        col["rot"] = R.reshape(T, 9)
+        col["trans"] = tr
+        col["omega"] = np.broadcast_to(np.asarray(omegas, dtype=np.float64), (T, 3))
+        col["v_origin"] = np.broadcast_to(np.asarray(vels, dtype=np.float64), (T, 3))
+        bounds = geom.contact_bounds(r)
+        if bounds is None:
+            col["bounded"] = 0
+            return
+        lo, hi = bounds
+        corners = np.array(
+            [[x, y, z] for x in (lo[0], hi[0]) for y in (lo[1], hi[1]) for z in (lo[2], hi[2])]
+        )
+        # corners @ R^T + t per step; the box is conservative by r, so the
+        # last-bit rounding of its faces cannot decide a contact (d < r strict)
+        world = np.matmul(corners[None, :, :], np.transpose(R, (0, 2, 1))) + tr[:, None, :]
+        col["bounded"] = 1
+        col["aabb_lo"] = world.min(axis=1)
+        col["aabb_hi"] = world.max(axis=1)
 
     # -- batches ---------------------------------------------------------------
     def run_batch(self, table: np.ndarray, nb: int, mode: int):

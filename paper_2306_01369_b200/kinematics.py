@@ -77,6 +77,10 @@ class StaticDriver(MotionDriver):
     def twist_at(self, t):
         return np.zeros(3), np.zeros(3)
 
+    def pose_batch(self, ts):
+        T = len(ts)
+        return np.broadcast_to(np.asarray(self.pose, dtype=np.float64), (T, 4, 4)), np.zeros((T, 3)), np.zeros((T, 3))
+
 
 @dataclass
 class SpinDriver(MotionDriver):
@@ -100,6 +104,23 @@ class SpinDriver(MotionDriver):
     def twist_at(self, t):
         omega = self.axis * self.rate
         return omega, np.cross(omega, self.pose_at(t)[:3, 3] - self.center)
+
+    def pose_batch(self, ts):
+        ts = np.asarray(ts, dtype=np.float64)
+        th = self.rate * ts + self.phase
+        K = skew(self.axis)
+        K2 = K @ K
+        R = np.eye(3) + np.sin(th)[:, None, None] * K + (1.0 - np.cos(th))[:, None, None] * K2
+        small = np.abs(th) < 1e-12
+        if small.any():
+            R[small] = np.eye(3) + th[small, None, None] * K
+        spin = np.zeros((len(ts), 4, 4))
+        spin[:, :3, :3] = R
+        spin[:, :3, 3] = self.center - R @ self.center
+        spin[:, 3, 3] = 1.0
+        P = spin @ self.base_pose
+        omega = self.axis * self.rate
+        return P, np.broadcast_to(omega, (len(ts), 3)), np.cross(omega, P[:, :3, 3] - self.center)
 
 
 @dataclass
@@ -188,6 +209,14 @@ class ChainLinkDriver(MotionDriver):
 
     def twist_at(self, t):
         return self.chain.fk()[1][self.link_index]
+
+    def pose_batch(self, ts):
+        # the chain does not move inside one batch (nothing advances it)
+        poses, twists = self.chain.fk()
+        w, v = twists[self.link_index]
+        T = len(ts)
+        return (np.broadcast_to(poses[self.link_index], (T, 4, 4)), np.broadcast_to(w, (T, 3)),
+                np.broadcast_to(v, (T, 3)))
 
 
 @dataclass

@@ -170,6 +170,32 @@ def test_physical_order_does_not_change_results():
         assert np.array_equal(x, out[0][0]) and np.array_equal(v, out[0][1])
 
 
+@pytest.mark.parametrize("name", ["grid_tool", "primitives_3000", "lattice_5000", "cyl_slope_cyclic"])
+def test_launch_modes_bitwise_identical(name):
+    """Fused single-kernel step, per-phase kernels with a cooperative solve,
+    and one launch per sweep must give identical states (race detector for
+    the grid barriers: run the fused mode twice)."""
+    from paper_2306_01369_b200 import _native as N
+    from paper_2306_01369_b200.engine import engine_for
+
+    g = load(name)
+    out = {}
+    for mode in (4, 4, 1, 3):
+        sc = scene_from(g)
+        eng = engine_for(sc)
+        eng.max_contacts = 64
+        eng.prepare(sc)
+        N.lib().gg_set_solve_mode(eng.ctx, mode)
+        N.lib().gg_set_resort_every(eng.ctx, 3)
+        gg.run(sc, 7)
+        xv = (sc.particles.positions.copy(), sc.particles.velocities.copy())
+        if mode in out:
+            assert np.array_equal(xv[0], out[mode][0]) and np.array_equal(xv[1], out[mode][1])
+        out[mode] = xv
+    for m in (1, 3):
+        assert np.array_equal(out[m][0], out[4][0]) and np.array_equal(out[m][1], out[4][1]), m
+
+
 def test_ballistic_closed_form():
     x0 = np.array([[0.3, -0.2, 5.0]])
     v0 = np.array([[1.0, 2.0, 0.5]])

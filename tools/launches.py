@@ -1,0 +1,18 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list."""
+import collections
+import csv
+import sys
+
+for f in sys.argv[1:]:
+    rows = [r for r in csv.reader(open(f)) if len(r) > 10]
+    hdr, data = rows[0], rows[1:]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(list)
+    for r in data:
+        v = float(r[vi].replace(",", ""))
+        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        agg[r[ki].split("(")[0].replace("gg::", "")].append(v)
+    tot = sum(sum(v) for v in agg.values())
+    print(f)
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        print(f"  {k:16s} n={len(v):3d} avg={sum(v)/len(v):9.2f} us  share={sum(v)/tot:6.1%}")
