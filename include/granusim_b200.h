@@ -206,6 +206,11 @@ int gg_set_resort_every(gg_ctx* ctx, int32_t steps);
  * one launch per sweep, 4 fused step.  Results are identical in every mode. */
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode);
 
+/* Phase timer of the fused single-kernel step (bench breakdown): on != 0
+ * makes the kernel record %globaltimer after every phase; `stamps` (if not
+ * NULL) receives the last step's stamps (up to 64, ns). */
+int gg_phase_timer(gg_ctx* ctx, int32_t on, uint64_t* stamps, int32_t cap);
+
 /* Page-lock host arrays so gg_set/get_state_f64 run at full PCIe speed. */
 int gg_host_register(void* ptr, int64_t bytes);
 int gg_host_unregister(void* ptr);

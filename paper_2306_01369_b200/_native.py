@@ -116,6 +116,7 @@ def _bind(lib: C.CDLL) -> None:
         "gg_max_contacts": (C.c_int, [P]),
         "gg_set_resort_every": (C.c_int, [P, i32]),
         "gg_set_solve_mode": (C.c_int, [P, i32]),
+        "gg_phase_timer": (C.c_int, [P, i32, P, i32]),
         "gg_required_contacts": (C.c_int, [P]),
         "gg_host_register": (C.c_int, [P, i64]),
         "gg_host_unregister": (C.c_int, [P]),

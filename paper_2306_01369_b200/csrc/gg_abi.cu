@@ -201,8 +201,19 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
 
 // The step schedule.  Optional Morton re-sort (R1-R4), the hash index
 // (H1-H4), narrowphase, cooperative solve.  All on ctx->stream.
+// every entry point starts with zeroed bucket/tile counts (a failed step may
+// leave them dirty; within a batch each scatter re-zeroes them)
+int begin_batch(gg_ctx* ctx, cudaStream_t s) {
+  CK(cudaMemsetAsync(ctx->D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  CK(cudaMemsetAsync(ctx->D.tile, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->ntiles), s));
+  CK(cudaMemsetAsync(ctx->D.bflags, 0, sizeof(unsigned) * std::max(ctx->fused_grid, 1), s));
+  k_batch_begin<<<1, 1, 0, s>>>(ctx->D);
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
 bool use_fused_step(const gg_ctx* ctx) {
-  if (ctx->solve_mode == 4) return true;
+  if (ctx->solve_mode == 4 || ctx->solve_mode == 5) return true;
   if (ctx->solve_mode != 0) return false;
   return ctx->n <= static_cast<long long>(ctx->fused_grid) * kBlock;
 }
@@ -214,7 +225,9 @@ bool use_persistent_solve(const gg_ctx* ctx) {
 }
 
 int launch_coop(gg_ctx* ctx, void (*kern)(Dev), int grid, const Dev& D, cudaStream_t s, bool coop) {
-  CK(cudaMemsetAsync(&D.ctl->bar_count, 0, sizeof(unsigned), s));
+  // bar_count, done_count, bar_gen are contiguous in Ctl
+  // barrier words and sweep flags are zero on entry: begin_batch zeroes them
+  // and the last block of every cooperative launch resets them
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kBlock);
@@ -242,7 +255,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
 
 int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
   const int nbn = ctx->nblocks;
-  CK(cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  // bucket/tile counts are zero on entry: the previous scatter zeroed them
   k_count<<<nbn, kBlock, 0, s>>>(D);
   k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
   k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
@@ -265,7 +278,10 @@ Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
 
 int enqueue_step(gg_ctx* ctx, int resort) {
   cudaStream_t s = ctx->stream;
-  if (use_fused_step(ctx)) return launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s, true);
+  if (use_fused_step(ctx)) {
+    return launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s,
+                       ctx->solve_mode != 5);
+  }
   int st;
   if (resort) {
     st = enqueue_sort_pass(ctx, pass_dev(ctx, 1, 1), s);
@@ -292,7 +308,7 @@ int kernels_per_step(const gg_ctx* ctx, int resort) {
 // Same schedule as enqueue_step, with an event after every kernel so each
 // kernel kind's device time can be attributed (bench roofline pass).
 constexpr int kProfKinds = 12;
-const char* kProfNames[kProfKinds] = {"memset_counts", "k_count", "k_scan_tiles", "k_scan_top",
+const char* kProfNames[kProfKinds] = {"(unused)", "k_count", "k_scan_tiles", "k_scan_top",
                                       "k_scan_apply",  "k_scatter", "k_resort",  "k_fill",
                                       "k_narrow",      "k_solve",   "k_bodies",  "k_step_fused"};
 
@@ -318,15 +334,14 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
   };
   cudaEventRecord(ev[0], s);
   if (use_fused_step(ctx)) {
-    if (launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s, true) != GG_OK)
+    if (launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s,
+                    ctx->solve_mode != 5) != GG_OK)
       return -1;
     mark(11);
     return e;
   }
   for (int pass = resort ? 0 : 1; pass < 2; ++pass) {
     const Dev D = pass_dev(ctx, resort, pass == 0 ? 1 : 0);
-    cudaMemsetAsync(D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s);
-    mark(0);
     k_count<<<nbn, kBlock, 0, s>>>(D);
     mark(1);
     k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
@@ -491,6 +506,7 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
     ctx->fused_grid = std::max(1, std::min(ctx->nblocks, per_sm_f * sms));
   }
   CK(dalloc(ctx, &D.Xh, n));
+  CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks}))));
   CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3));
   CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3));
@@ -552,9 +568,30 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
 int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
 
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode) {
-  if (!ctx || mode < 0 || mode > 4) return fail(ctx, GG_EINVAL, "solve mode must be 0..4");
+  if (!ctx || mode < 0 || mode > 5) return fail(ctx, GG_EINVAL, "solve mode must be 0..5");
   ctx->solve_mode = mode;
   ctx->graph_dirty = true;
+  return GG_OK;
+}
+
+int gg_phase_timer(gg_ctx* ctx, int32_t on, uint64_t* stamps, int32_t cap) {
+  if (!ctx) return GG_EINVAL;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (stamps && ctx->D.tstamp && cap > 0)
+    CK(cudaMemcpy(stamps, ctx->D.tstamp, sizeof(uint64_t) * std::min(cap, 64),
+                  cudaMemcpyDeviceToHost));
+  if (on && !ctx->D.tstamp) {
+    unsigned long long* t = nullptr;
+    CK(dalloc(ctx, &t, 64));
+    CK(cudaMemset(t, 0, sizeof(unsigned long long) * 64));
+    ctx->D.tstamp = t;
+    ctx->graph_dirty = true;
+  } else if (!on && ctx->D.tstamp) {
+    dfree(ctx, ctx->D.tstamp);
+    ctx->D.tstamp = nullptr;
+    ctx->graph_dirty = true;
+  }
   return GG_OK;
 }
 
@@ -702,7 +739,8 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
     if (st != GG_OK) return st;
   }
   refresh_dev(ctx);
-  k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
+  st = begin_batch(ctx, ctx->stream);
+  if (st != GG_OK) return st;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   for (int i = 0; i < n_steps; ++i) {
     int st2 = launch_step(ctx);
@@ -732,7 +770,8 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
   refresh_dev(ctx);
   const Dev D = pass_dev(ctx, 0, 0);
   cudaStream_t s = ctx->stream;
-  k_batch_begin<<<1, 1, 0, s>>>(D);
+  st = begin_batch(ctx, s);
+  if (st != GG_OK) return st;
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
   k_narrow<<<ctx->nblocks, kBlock, 0, s>>>(D);
@@ -802,7 +841,8 @@ int gg_bench_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t 
   }
   st = ensure_events(ctx, 2 * static_cast<size_t>(n_steps));
   if (st != GG_OK) return st;
-  k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
+  st = begin_batch(ctx, ctx->stream);
+  if (st != GG_OK) return st;
   for (int i = 0; i < n_steps; ++i) {
     if (flush_bytes > 0)
       CK(cudaMemsetAsync(ctx->flush_buf, i & 0xff, static_cast<size_t>(flush_bytes), ctx->stream));
@@ -835,7 +875,8 @@ int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_
     if (kind_launches) kind_launches[k] = 0;
   }
   std::vector<int> kinds(per + 1);
-  k_batch_begin<<<1, 1, 0, ctx->stream>>>(ctx->D);
+  st = begin_batch(ctx, ctx->stream);
+  if (st != GG_OK) return st;
   for (int i = 0; i < n_steps; ++i) {
     const int resort = ctx->since_resort >= ctx->resort_every ? 1 : 0;
     ctx->since_resort = resort ? 1 : ctx->since_resort + 1;
@@ -927,7 +968,8 @@ int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order) {
   refresh_dev(ctx);
   const Dev D = pass_dev(ctx, 0, 0);
   cudaStream_t s = ctx->stream;
-  k_batch_begin<<<1, 1, 0, s>>>(D);
+  st = begin_batch(ctx, s);
+  if (st != GG_OK) return st;
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
   long long* tmp = reinterpret_cast<long long*>(ctx->d_stage);  // 6n doubles = room for 5n i64

@@ -41,6 +41,7 @@ namespace gg {
 constexpr int kBlock = 256;
 constexpr int kScanTile = 2048;  // elements per scan tile (256 thr x 8)
 constexpr int kMaxBad = 32;
+constexpr int kMaxFusedBlocks = 1024;  // neighbour-flag sweeps: block-set bitmask size
 
 struct Ctl {
   int cur;         // committed state buffer
@@ -53,6 +54,8 @@ struct Ctl {
   int pad;
   unsigned bar_count;  // grid barrier arrivals (monotonic within a launch, reset per launch)
   unsigned done_count; // last-block-done counter of the solve kernel
+  unsigned bar_gen;    // last completed barrier target (reset with bar_count)
+  unsigned pad2;
   int bad_uid[kMaxBad];
 };
 
@@ -100,6 +103,8 @@ struct Dev {
   const DevGrid* grids;
   const double* gvals;
   Acc* acc;
+  unsigned long long* tstamp;  // optional phase timestamps of the fused kernel (64)
+  unsigned* bflags;  // [fused grid] per-block sweep progress (fused kernel)
   double* part;     // [nblocks_solve] per-block kinetic-energy partials
   unsigned long long* bm_fix;  // [nb][3] fixed-point body momentum of the step
   gg_report* reports;
@@ -178,12 +183,17 @@ __device__ __forceinline__ bool block_should_exit(const Ctl* ctl) {
 __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    // arrive on the counter; the last arriver publishes the barrier ordinal
+    // on a separate generation word, which is all the waiters poll (they
+    // never contend with the arrival atomics)
     unsigned v;
     asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
-    v += 1;
-    while (static_cast<int>(v - target) < 0) {
-      __nanosleep(16);
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
+    if (v + 1 == target) {
+      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&ctl->bar_gen), "r"(target) : "memory");
+    } else {
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&ctl->bar_gen) : "memory");
+      } while (static_cast<int>(v - target) < 0);
     }
     // gpu-scope fence: invalidates this SM's L1 (CCTL.IVALL) so no block
     // reads a line cached before other SMs rewrote it in the previous phase
@@ -234,6 +244,7 @@ __global__ void k_batch_begin(Dev D) {
   c->n_bad = 0;
   c->bar_count = 0;
   c->done_count = 0;
+  c->bar_gen = 0;
   Acc* a = D.acc;
   a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
   a->max_psi_bits = a->max_viol_bits = 0;
@@ -329,13 +340,26 @@ __device__ __forceinline__ void ph_scan_top(const Dev& D, int ntiles, uint32_t* 
     }
 }
 
-__device__ __forceinline__ void ph_scan_apply(const Dev& D, int t, uint32_t* sm) {
+// Tile t's exclusive bucket offsets.  `tile_counts`: tile[] still holds the
+// per-tile totals (few tiles: each block sums its predecessors); otherwise
+// k_scan_top has already turned tile[] into exclusive offsets.
+__device__ __forceinline__ void ph_scan_apply(const Dev& D, int t, uint32_t* sm, bool tile_counts) {
   const long long base = static_cast<long long>(t) * kScanTile + threadIdx.x * 8;
+  uint32_t prefix;
+  if (tile_counts) {
+    uint32_t part = 0;
+    for (int q = threadIdx.x; q < t; q += blockDim.x) part += D.tile[q];
+    uint32_t total;
+    (void)block_excl_scan_u32(part, sm, &total);
+    prefix = total;
+  } else {
+    prefix = D.tile[t];
+  }
   uint32_t v[8];
   load8(D, base, v);
   const uint32_t s = v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7];
   uint32_t total;
-  uint32_t run = block_excl_scan_u32(s, sm, &total) + D.tile[t];
+  uint32_t run = block_excl_scan_u32(s, sm, &total) + prefix;
   uint32_t o[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
@@ -354,6 +378,17 @@ __device__ __forceinline__ void ph_scan_apply(const Dev& D, int t, uint32_t* sm)
 // R3/H3: counting-sort scatter (arrival order inside a bucket)
 __device__ __forceinline__ void ph_scatter(const Dev& D, int i) {
   D.tmp[D.start[D.key[i]] + D.arrive[i]] = i;
+}
+
+// Once the scan has consumed them, bucket and tile counts are zeroed in the
+// scatter phase, so the next pass starts from zero without its own pass.
+__device__ __forceinline__ void ph_zero_counts(const Dev& D, long long t0, long long G) {
+  uint4* c4 = reinterpret_cast<uint4*>(D.cnt);
+  const long long n4 = D.H.n_h / 4;
+  for (long long i = t0; i < n4; i += G) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (long long i = 4 * n4 + t0; i < D.H.n_h; i += G) D.cnt[i] = 0u;
+  const long long nt = (D.H.n_h + kScanTile - 1) / kScanTile;
+  for (long long i = t0; i < nt; i += G) D.tile[i] = 0u;
 }
 
 // rank of a member inside its bucket by user id (the stable tie order)
@@ -514,26 +549,37 @@ __device__ __forceinline__ void ph_narrow(const Dev& D, Ctl* ctl, int base, Narr
     int b = 0;
     uint32_t m = sm.beg[0][tid];
     uint32_t left = sm.len[0][tid];
-    float4 qf = Xh[m];
-    for (uint32_t i = 0; i < total; ++i) {
-      // advance to the next candidate and prefetch it
-      ++m;
-      --left;
-      if (left == 0 && i + 1 < total) {
-        ++b;
-        m = sm.beg[b][tid];
-        left = sm.len[b][tid];
+    constexpr int kDepth = 4;  // candidates in flight per thread
+    for (uint32_t i = 0; i < total; i += kDepth) {
+      uint32_t mi[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        mi[u] = m;
+        if (i + u + 1 < total) {  // advance the cursor to the next candidate
+          ++m;
+          if (--left == 0) {
+            ++b;
+            m = sm.beg[b][tid];
+            left = sm.len[b][tid];
+          }
+        }
       }
-      const float4 nxt = (i + 1 < total) ? Xh[m] : qf;
-      const int q = __float_as_int(qf.w);
-      if (q != k) {
+      float4 qv[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u)
+        if (i + u < total) qv[u] = Xh[mi[u]];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        if (i + u >= total) break;
+        const float4 qf = qv[u];
+        const int q = __float_as_int(qf.w);
+        if (q == k) continue;
         // float32 pre-filter, conservative by a 1e-5 relative margin (the
         // float32 estimate is within ~4e-7 relative of the exact square)
         const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
         if (fx * fx + fy * fy + fz * fz <= D.reject_d2f)
           pp_candidate(D, k, px, py, pz, qf, q, cnt, n_coinc, max_psi);
       }
-      qf = nxt;
     }
     n_pp = cnt;
     D.ccount[k] = cnt < D.K ? cnt : D.K;
@@ -617,9 +663,39 @@ __device__ __forceinline__ void ph_bodies(const Dev& D, Ctl* ctl, int base, doub
 // The tangential impulse is -(u - (u.e1) e1), identical to e2*b2 + e3*b3 for
 // the orthonormal frame of contact.py:47-56, so the frame is never built.
 // ---------------------------------------------------------------------------
+// Body reaction momentum is summed per block in shared memory (exact int64
+// fixed-point adds: order-independent) and flushed to the global per-body
+// accumulators once per block per kernel — a per-contact global atomic on
+// the same three addresses per body serialises every body contact of the
+// floor at the L2 and sits on the critical path of every sweep.
+constexpr int kSmemBodies = 16;
+
 struct SweepAcc {
   double maxviol, minb1;
+  unsigned long long* sbm;  // shared [kSmemBodies][3]
 };
+
+__device__ __forceinline__ void sweep_acc_init(SweepAcc& A, unsigned long long* sbm) {
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  A.sbm = sbm;
+  for (int i = threadIdx.x; i < kSmemBodies * 3; i += blockDim.x) sbm[i] = 0ull;
+  __syncthreads();
+}
+
+// per block: diagnostics (block max/min, one atomic each) + body momentum
+// (one atomic per non-zero component).  Called by every thread.
+__device__ __forceinline__ void sweep_acc_flush(const Dev& D, const SweepAcc& A, double* smd) {
+  const double mv = block_reduce<1>(A.maxviol, smd);
+  if (threadIdx.x == 0 && mv > 0.0) atomicMax(&D.acc->max_viol_bits, dbits(mv));
+  const double mb = block_reduce<2>(A.minb1, smd);
+  if (threadIdx.x == 0 && mb == mb && mb < __longlong_as_double(0x7ff0000000000000ll))
+    atomicMin(&D.acc->min_b1_bits, dbits(mb));
+  __syncthreads();
+  const int m = (D.nb < kSmemBodies ? D.nb : kSmemBodies) * 3;
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    if (A.sbm[i]) atomicAdd(&D.bm_fix[i], A.sbm[i]);
+}
 
 __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
                                                 float4 g, int j, float4 q, double& ax, double& ay,
@@ -650,7 +726,8 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   az += iz;
   A.minb1 = nmin(A.minb1, b1);
   if (j < 0) {  // reaction momentum on the body (contact.py:489-495)
-    unsigned long long* bm = D.bm_fix + 3 * (-j - 1);
+    const int b = -j - 1;
+    unsigned long long* bm = (b < kSmemBodies) ? A.sbm + 3 * b : D.bm_fix + 3 * b;
     atomicAdd(bm + 0, to_fix(-D.mass * ix));
     atomicAdd(bm + 1, to_fix(-D.mass * iy));
     atomicAdd(bm + 2, to_fix(-D.mass * iz));
@@ -682,16 +759,61 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
                         static_cast<float>(wz + az), 0.f);
 }
 
-// warp-level reduction of the sweep diagnostics into the step accumulators
-__device__ __forceinline__ void flush_diag(const Dev& D, const SweepAcc& A) {
-  const double mv = warp_max(A.maxviol);
-  const double mb = warp_min(A.minb1);
-  if ((threadIdx.x & 31) == 0) {
-    if (mv > 0.0) atomicMax(&D.acc->max_viol_bits, dbits(mv));
-    if (mb == mb && mb < __longlong_as_double(0x7ff0000000000000ll))
-      atomicMin(&D.acc->min_b1_bits, dbits(mb));
+// Register-resident variant for the fused kernel (one particle per thread):
+// the first kRegSlots contacts and the particle's own w are loaded once and
+// kept across all sweeps; each sweep issues its neighbour gathers together.
+// Arithmetic and accumulation order are exactly those of sweep_particle.
+constexpr int kRegSlots = 4;
+struct RegContacts {
+  int c;
+  float4 g[kRegSlots];
+  int j[kRegSlots];
+  float4 qb[kRegSlots];
+  float wx, wy, wz;
+
+  __device__ __forceinline__ void load(const Dev& D, int k, float4 w0) {
+    c = D.ccount[k];
+    const int n = D.n;
+#pragma unroll
+    for (int s = 0; s < kRegSlots; ++s) {
+      j[s] = 0;
+      if (s < c) {
+        g[s] = D.cgeo[s * n + k];
+        j[s] = D.coth[s * n + k];
+        if (j[s] < 0) qb[s] = D.cvb[s * n + k];
+      }
+    }
+    wx = w0.x;
+    wy = w0.y;
+    wz = w0.z;
   }
-}
+
+  __device__ __forceinline__ void sweep(const Dev& D, int k, const float4* Win, float4* Wout,
+                                        SweepAcc& A) {
+    float4 q[kRegSlots];
+#pragma unroll
+    for (int s = 0; s < kRegSlots; ++s)
+      if (s < c) q[s] = (j[s] >= 0) ? Win[j[s]] : qb[s];
+    double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+    for (int s = 0; s < kRegSlots; ++s)
+      if (s < c) contact_impulse(D, wx, wy, wz, g[s], j[s], q[s], ax, ay, az, A);
+    const int n = D.n;
+    for (int s = kRegSlots; s < c; ++s) {
+      const int idx = s * n + k;
+      const float4 gg = D.cgeo[idx];
+      const int jj = D.coth[idx];
+      const float4 qq = (jj >= 0) ? Win[jj] : D.cvb[idx];
+      contact_impulse(D, wx, wy, wz, gg, jj, qq, ax, ay, az, A);
+    }
+    const float4 out = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
+                                   static_cast<float>(wz + az), 0.f);
+    Wout[k] = out;
+    wx = out.x;
+    wy = out.y;
+    wz = out.z;
+  }
+};
 
 // Symplectic Euler (stepper.py:102-106), SolverError check
 // (contact.py:503-509), kinetic energy (stepper.py:118); the last block to
@@ -749,8 +871,14 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
     D.bm_out[static_cast<long long>(step) * D.nb * 3 + threadIdx.x] = static_cast<double>(f) / kMomScale;
     D.bm_fix[threadIdx.x] = 0ull;
   }
+  // every other block has finished (it incremented done_count last), so the
+  // barrier words and sweep flags can be reset here for the next launch
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+    if (D.bflags) D.bflags[b] = 0u;
   if (threadIdx.x == 0) {
     ctl->done_count = 0;
+    ctl->bar_count = 0;
+    ctl->bar_gen = 0;
     if (*((volatile int*)&ctl->err)) return;  // an error was raised this step: no commit
     Acc* a = D.acc;
     gg_report& R = D.reports[step];
@@ -797,13 +925,14 @@ __global__ void __launch_bounds__(1024) k_scan_top(Dev D, int ntiles) {
 __global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D) {
   __shared__ uint32_t sm[32];
   if (D.ctl->err) return;
-  ph_scan_apply(D, blockIdx.x, sm);
+  ph_scan_apply(D, blockIdx.x, sm, false);
 }
 
 __global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
   if (D.ctl->err) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < D.n) ph_scatter(D, i);
+  ph_zero_counts(D, i, static_cast<long long>(gridDim.x) * blockDim.x);
 }
 
 __global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
@@ -834,15 +963,16 @@ __global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
 }
 
 __global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
+  __shared__ unsigned long long sbm[kSmemBodies * 3];
+  __shared__ double smd[32];
   const Ctl* ctl = D.ctl;
-  if (ctl->err) return;
+  if (block_should_exit(ctl)) return;
   const Layout L = layout(D, ctl);
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   SweepAcc A;
-  A.maxviol = 0.0;
-  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  sweep_acc_init(A, sbm);
   if (k < D.n) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
-  flush_diag(D, A);
+  sweep_acc_flush(D, A, smd);
 }
 
 __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
@@ -861,11 +991,23 @@ __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
 // re-reads the error flag (all errors raised before a barrier are visible
 // after it) and skips work, so every block reaches every barrier.
 // ===========================================================================
-__device__ __forceinline__ bool barrier_ok(Ctl* ctl, unsigned& target, int* s_flag) {
+// optional phase timestamps (block 0, %globaltimer) for the bench breakdown
+__device__ __forceinline__ void stamp(const Dev& D, int& idx) {
+  if (D.tstamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    D.tstamp[idx] = t;
+  }
+  ++idx;
+}
+
+__device__ __forceinline__ bool barrier_ok(const Dev& D, Ctl* ctl, unsigned& target, int* s_flag,
+                                           int& ts) {
   target += gridDim.x;
   grid_barrier(ctl, target);
   if (threadIdx.x == 0) *s_flag = *((volatile int*)&ctl->err);
   __syncthreads();
+  stamp(D, ts);
   return *s_flag == 0;
 }
 
@@ -875,6 +1017,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   __shared__ int s_flag;
   __shared__ int s_last;
   Ctl* ctl = D.ctl;
+  int ts = 0;
+  stamp(D, ts);
   if (threadIdx.x == 0) s_flag = *((volatile int*)&ctl->err);
   __syncthreads();
   bool ok = s_flag == 0;
@@ -882,29 +1026,23 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   const int G = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
   const int ntiles = static_cast<int>((D.H.n_h + kScanTile - 1) / kScanTile);
+  // bucket/tile counts are zero on entry (zeroed by the previous scatter)
   for (int pass = D.resort ? 0 : 1; pass < 2; ++pass) {
     const bool morton = pass == 0;
-    if (ok) {
-      uint4* c4 = reinterpret_cast<uint4*>(D.cnt);
-      const long long n4 = D.H.n_h / 4;
-      for (long long i = t0; i < n4; i += G) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-      for (long long i = 4 * n4 + t0; i < D.H.n_h; i += G) D.cnt[i] = 0u;
-    }
-    ok = barrier_ok(ctl, target, &s_flag);
     if (ok)
       for (int i = t0; i < D.n; i += G) ph_count(D, ctl, i, morton);
-    ok = barrier_ok(ctl, target, &s_flag);
+    ok = barrier_ok(D, ctl, target, &s_flag, ts);
     if (ok)
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ph_scan_tile(D, t, smu);
-    ok = barrier_ok(ctl, target, &s_flag);
-    if (ok && blockIdx.x == 0) ph_scan_top(D, ntiles, smu);
-    ok = barrier_ok(ctl, target, &s_flag);
+    ok = barrier_ok(D, ctl, target, &s_flag, ts);
     if (ok)
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ph_scan_apply(D, t, smu);
-    ok = barrier_ok(ctl, target, &s_flag);
-    if (ok)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ph_scan_apply(D, t, smu, true);
+    ok = barrier_ok(D, ctl, target, &s_flag, ts);
+    if (ok) {
       for (int i = t0; i < D.n; i += G) ph_scatter(D, i);
-    ok = barrier_ok(ctl, target, &s_flag);
+      ph_zero_counts(D, t0, G);
+    }
+    ok = barrier_ok(D, ctl, target, &s_flag, ts);
     if (ok) {
       for (int k = t0; k < D.n; k += G) {
         if (morton)
@@ -913,7 +1051,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
           ph_fill(D, ctl, k);
       }
     }
-    ok = barrier_ok(ctl, target, &s_flag);
+    ok = barrier_ok(D, ctl, target, &s_flag, ts);
   }
   // narrowphase + bodies; the sweeps below use the same particle -> thread
   // map, so a particle's contacts are read by the thread that wrote them
@@ -923,20 +1061,87 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
       if (D.nb > 0) ph_bodies(D, ctl, base, sm.d, sm.u);
     }
   }
+  stamp(D, ts);
   const Layout L = layout(D, ctl);
+  __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
-  A.maxviol = 0.0;
-  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
-  for (int s = 0; s < D.S; ++s) {
-    if (s > 0) ok = barrier_ok(ctl, target, &s_flag) && ok;
-    if (ok) {
-      const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
-      float4* Wout = D.W[s & 1];
-      for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+  sweep_acc_init(A, sbm);
+  if (G >= D.n && gridDim.x <= kMaxFusedBlocks) {
+    // One particle per thread: its contacts (first kRegSlots) and its own w
+    // stay in registers for all sweeps.  Jacobi sweep s of a block only needs
+    // sweep s-1 of the blocks that own its particles' contact partners, and
+    // (contacts being symmetric) those are also the only blocks that read its
+    // w — so instead of a grid barrier a block waits on its neighbour blocks'
+    // progress flags (release/acquire), then publishes its own.
+    __shared__ unsigned s_nbmask[kMaxFusedBlocks / 32];
+    __shared__ int s_nblist[kMaxFusedBlocks];
+    __shared__ int s_nnb;
+    RegContacts RC;
+    RC.c = 0;
+    if (ok && t0 < D.n) RC.load(D, t0, L.v[t0]);
+    for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
+    __syncthreads();
+    {
+      const int n = D.n;
+      const int c = RC.c < D.K ? RC.c : D.K;
+      for (int sl = 0; sl < c; ++sl) {
+        const int j = sl < kRegSlots ? RC.j[sl] : D.coth[sl * n + t0];
+        if (j >= 0) {
+          const int b = j / blockDim.x;
+          if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int m = 0;
+      for (int w = 0; w < (int)((gridDim.x + 31) / 32); ++w) {
+        unsigned bits = s_nbmask[w];
+        while (bits) {
+          const int bit = __ffs(bits) - 1;
+          bits &= bits - 1;
+          s_nblist[m++] = w * 32 + bit;
+        }
+      }
+      s_nnb = m;
+    }
+    __syncthreads();
+    unsigned* flags = D.bflags;
+    for (int s = 0; s < D.S; ++s) {
+      if (s > 0) {
+        for (int q = threadIdx.x; q < s_nnb; q += blockDim.x) {
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flags + s_nblist[q]) : "memory");
+          } while (static_cast<int>(v - static_cast<unsigned>(s)) < 0);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) __threadfence();  // invalidate stale L1 lines (CCTL.IVALL)
+        __syncthreads();
+        if (threadIdx.x == 0) s_flag = *((volatile int*)&ctl->err);
+        __syncthreads();
+        ok = ok && s_flag == 0;
+        stamp(D, ts);
+      }
+      if (ok && t0 < D.n) RC.sweep(D, t0, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+      __syncthreads();
+      if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(s + 1) : "memory");
+    }
+  } else {
+    for (int s = 0; s < D.S; ++s) {
+      if (s > 0) ok = barrier_ok(D, ctl, target, &s_flag, ts) && ok;
+      if (ok) {
+        const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+        float4* Wout = D.W[s & 1];
+        for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+      }
     }
   }
-  flush_diag(D, A);
+  stamp(D, ts);
+  sweep_acc_flush(D, A, sm.d);
   integrate_and_finish(D, ctl, t0, G, sm.d, &s_last);
+  stamp(D, ts);
 }
 
 // Small-n solve only (cooperative): S sweeps with grid barriers + finish.
@@ -948,16 +1153,16 @@ __global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
   const Layout L = layout(D, ctl);
   const int G = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
-  A.maxviol = 0.0;
-  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  sweep_acc_init(A, sbm);
   for (int s = 0; s < D.S; ++s) {
     if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
     const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
     float4* Wout = D.W[s & 1];
     for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
   }
-  flush_diag(D, A);
+  sweep_acc_flush(D, A, smd);
   integrate_and_finish(D, ctl, t0, G, smd, &s_last);
 }
 
