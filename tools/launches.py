@@ -10,7 +10,7 @@ for f in sys.argv[1:]:
     agg = collections.defaultdict(list)
     for r in data:
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         agg[r[ki].split("(")[0].replace("gg::", "")].append(v)
     tot = sum(sum(v) for v in agg.values())
     print(f)
