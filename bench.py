@@ -10,6 +10,10 @@ Workloads (BASELINE.json configs):
            dt = 5e-4, 10 PJA sweeps.  Initial state: bench_data/hero50k_settled.npz
            (settled once on the GPU, shared by both arms), else settled at start.
   bed1m    config 4 scale: lattice_bed(1e6) on a floor with a spinning grid SDF tool.
+  envs     config 3: 4096 BulldozerEnv scenes x 2000 particles (r = 0.025), ground
+           + blade on TrackSteering drivers with fixed random actions, physics
+           substeps only; env e runs on rank e mod N (no communication), so the
+           total work is fixed as N grows ("scaling": "strong").
 
 One JSON line on rank 0.  ``value`` is device time (CUDA events per step, L2
 flushed by a 512 MB write before every step); ``e2e`` is wall time through
@@ -49,7 +53,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="hero50k", choices=["hero50k", "bed1m"])
+    ap.add_argument("--workload", default="hero50k", choices=["hero50k", "bed1m", "envs"])
+    ap.add_argument("--envs", type=int, default=4096, help="envs workload: total envs")
+    ap.add_argument("--env-particles", type=int, default=2000)
     ap.add_argument("--settle", type=int, default=3000)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -231,12 +237,12 @@ def bytes_model(n_h: int, S: int, c_pp: float, c_b: float) -> dict:
         "k_count": 24.0,                                   # hash: read x, write key + idx
         "k_resort": 68.0,                                  # reorder (every resort_every steps)
         "k_fill": 68.0,                                    # bucket-ordered candidate copy
-        "k_narrow": 20.0 + 20.0 * c_pp,                    # pp narrowphase
-        "k_bodies": 16.0 + 32.0 * c_b,                     # body contacts
+        # pp narrowphase + body contacts (one kernel: K5 + K6)
+        "k_narrow": 20.0 + 20.0 * c_pp + 16.0 + 32.0 * c_b,
         "k_solve": S * (48.0 + 20.0 * c_pp + 32.0 * c_b) + 80.0,  # S sweeps + integrate
     }
     per_kernel["k_step_fused"] = (per_kernel["k_count"] + 16.0 * 1 + 20.0 + per_kernel["k_fill"]
-                                  + per_kernel["k_narrow"] + per_kernel["k_bodies"]
+                                  + per_kernel["k_narrow"]
                                   + per_kernel["k_solve"])  # the whole step in one kernel
     step = 228.0 + 16.0 * P + 48.0 * S + (S + 1) * (20.0 * c_pp + 32.0 * c_b)
     return {"per_kernel_per_particle": per_kernel, "step_per_particle": step, "radix_passes": P}
@@ -301,6 +307,20 @@ def run_reference(args, dist: Dist):
     the reference is Python) on the host, rank 0 only."""
     if dist.rank != 0:
         return
+    if args.workload == "envs":
+        budget = min(args.cpu_seconds, 60.0)
+        cb = envs_cpu_baseline(args, budget)
+        n_total = args.envs * args.env_particles
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000.0 * n_total / cb["value"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "envs", "n_envs": args.envs,
+                           "n_particles": n_total}, "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     sc, desc = make_scene(args, with_gpu=False)
     x = np.asarray(sc.particles._x, float).copy()
     v = np.asarray(sc.particles._v, float).copy()
@@ -317,6 +337,165 @@ def run_reference(args, dist: Dist):
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def envs_setup(args, dist: Dist, device: int):
+    from paper_2306_01369_b200.batch import shard_envs
+    from paper_2306_01369_b200.envs import BatchedBulldozerEnv, BulldozerEnvConfig
+
+    mine = shard_envs(args.envs, dist.rank, dist.world)
+    cfg = BulldozerEnvConfig(n_particles=args.env_particles, radius=0.025)
+    env = BatchedBulldozerEnv(len(mine), cfg, device=device)
+    env.reset(mine)  # seed = env id
+    acts = np.stack([np.random.default_rng(int(e)).uniform(-1, 1, 2) for e in mine])
+    acts[:, 0] = np.abs(acts[:, 0])  # drive forward into the bed
+    env.driver.command(acts)
+    desc = {"workload": "envs", "config": "BASELINE configs[2]: batched bulldozer envs "
+            f"{args.envs} x {args.env_particles} particles, sharded env e -> rank e mod N",
+            "n_envs": args.envs, "envs_per_rank": len(mine), "n_particles": args.envs * env.batch.n,
+            "dt": cfg.timestep, "solver_iterations": 10, "bodies": "ground + Box blade per env"}
+    return env, acts, desc
+
+
+def envs_cpu_baseline(args, budget_s: float) -> dict:
+    """Reference algorithm (oracle port) on one env at a time, 1 host core."""
+    from oracle import granular_oracle as O
+    from paper_2306_01369_b200.envs import BulldozerEnvConfig, bulldozer_scene
+
+    cfg = BulldozerEnvConfig(n_particles=args.env_particles, radius=0.025)
+    sc = bulldozer_scene(0, cfg)
+    x = sc.particles.positions.astype(np.float32).astype(np.float64)
+    v = np.zeros_like(x)
+    drv = sc.bodies[1].driver
+    drv.command(np.array([0.8, 0.1]))
+    steps, t = 0, 0.0
+    t0 = time.perf_counter()
+    while True:
+        t += cfg.timestep
+        drv.advance(cfg.timestep)
+        bodies = []
+        for b in sc.bodies:
+            om, vo = b.driver.twist_at(t)
+            bodies.append(_BodyAt(b.geometry, np.asarray(b.driver.pose_at(t), float), om, vo))
+        x, v, _, _, _ = O.step(x, v, sc.params, bodies, O.table_size(len(x)))
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= 2000:
+            break
+    n = len(x)
+    return {"value": n * steps / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{steps} oracle steps of env 0 ({n} particles) from its seeded bed, "
+                      f"{el:.1f}s, numpy single thread; per-env work is independent, so the "
+                      f"{args.envs}-env batch scales with host cores at best"}
+
+
+def run_envs(args, dist: Dist):
+    from paper_2306_01369_b200 import _native as N
+
+    dev = dist.local
+    env, acts, desc = envs_setup(args, dist, dev)
+    batch = env.batch
+    lib = N.lib()
+    # settle: the seeded bed falls onto the floor before the blade arrives
+    batch.run_raw(100)
+    K, W = args.steps, args.warmup
+    if W:
+        batch.run_raw(W)
+    chunk = 25
+    step_ms = np.zeros(K, dtype=np.float32)
+    l0 = batch.kernel_launches()
+    clocks = Clocks(dev)
+    clocks.start()
+    dist.barrier()
+    done = 0
+    reps_all = []
+    while done < K:
+        m = min(chunk, K - done)
+        table = batch.body_tables(m)
+        st = lib.gg_bench_steps(batch.ctx, m, N.ptr(np.ascontiguousarray(table)), batch.nb,
+                                args.flush_mb << 20, N.ptr(step_ms[done:]))
+        N.check(batch.ctx, st, "gg_bench_steps")
+        rbuf = np.zeros((m, batch.E), dtype=N.REPORT_DTYPE)
+        bbuf = np.zeros((m, batch.E, batch.nb, 3))
+        nd, es = ctypes.c_int32(0), ctypes.c_int32(-1)
+        st = lib.gg_sync(batch.ctx, N.ptr(rbuf), N.ptr(bbuf), m, ctypes.byref(nd), ctypes.byref(es))
+        if st != N.GG_OK or nd.value != m:
+            raise RuntimeError(f"envs bench failed: {st} {N.last_error(batch.ctx)}")
+        reps_all.append(rbuf)
+        done += m
+    dist.barrier()
+    clk = clocks.stop()
+    launches = batch.kernel_launches() - l0
+    t_ms = dist.max(float(step_ms.sum()))
+    n_total = args.envs * batch.n
+    value = n_total * K / (t_ms / 1000.0)
+    reps = np.concatenate(reps_all)
+    n_local = batch.E * batch.n
+    c_pp = float(reps["n_contacts"].sum(axis=1).mean()) / n_local
+    c_b = float(reps["n_body_contacts"].sum(axis=1).mean()) / n_local
+
+    # per-kernel roofline pass
+    peak, peak_src = peaks()
+    P = max(min(args.profile_steps, 10), 1)
+    table3 = batch.body_tables(P)
+    kind_ms = np.zeros(16, dtype=np.float32)
+    kind_n = np.zeros(16, dtype=np.int32)
+    st = lib.gg_profile_steps(batch.ctx, P, N.ptr(np.ascontiguousarray(table3)), batch.nb,
+                              N.ptr(kind_ms), N.ptr(kind_n))
+    N.check(batch.ctx, st, "gg_profile_steps")
+    names = [lib.gg_profile_kind_name(k).decode() for k in range(16)]
+    names = [nm for nm in names if nm]
+    model = bytes_model(batch.n_h, 10, c_pp, c_b)
+    share = {names[k]: float(kind_ms[k] / max(kind_ms[: len(names)].sum(), 1e-9))
+             for k in range(len(names)) if kind_n[k] > 0}
+    top = max((k for k in range(len(names))
+               if names[k] in model["per_kernel_per_particle"] and kind_n[k] > 0),
+              key=lambda k: kind_ms[k])
+    avg_ms = float(kind_ms[top] / max(kind_n[top], 1))
+    bytes_launch = model["per_kernel_per_particle"][names[top]] * n_local
+    achieved = bytes_launch / (avg_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": names[top], "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(names[top], "envs"),
+                "algorithmic_bytes_per_launch": bytes_launch, "avg_launch_ms": avg_ms,
+                "peak_source": peak_src, "kernel_time_share": share,
+                "step_bytes_per_particle": model["step_per_particle"],
+                "step_frac": (value / dist.world) * model["step_per_particle"] / (peak * 1e9)}
+
+    # e2e through the public env API: actions in, rewards out, frame_skip substeps per call
+    fs = env.config.frame_skip
+    n_ctrl = max(K // fs, 1)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(n_ctrl):
+        _, rew, _, info = env.step(acts)
+        _ = float(rew.sum())
+    t_e2e = dist.max(time.perf_counter() - t0)
+    e2e = {"value": n_total * n_ctrl * fs / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": batch.E * batch.nb * N.BODY_DTYPE.itemsize,
+           "d2h_bytes_per_step": batch.E * N.REPORT_DTYPE.itemsize
+           + (batch.E * (8 + 8) + batch.E * batch.nb * 24) / fs,
+           "api": "BatchedBulldozerEnv.step(actions): per-env blade kinematics, body tables "
+                  "uploaded, frame_skip substeps, per-env StepReports and on-device rewards read back",
+           "wall_s": t_e2e}
+    cb = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cb = envs_cpu_baseline(args, args.cpu_seconds)
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
+            "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
+            "data": "synthetic (seeded bulldozer beds, settled 100 substeps)",
+            "config": {**desc, "parallelism": f"env shards x{dist.world}",
+                       "l2": f"flushed before every timed step ({args.flush_mb} MB write); "
+                             "state (~0.5 GB) exceeds L2 anyway",
+                       "c_pp": c_pp, "c_b": c_b, "n_h_per_env": batch.n_h},
+            "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    env.close()
 
 
 def run_ours(args, dist: Dist):
@@ -453,6 +632,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif args.workload == "envs":
+            run_envs(args, dist)
         else:
             run_ours(args, dist)
     finally:

@@ -111,6 +111,29 @@ typedef struct gg_ctx gg_ctx;
  * max_contacts = per-owner contact slots (grown on GG_ECAPACITY). */
 int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h,
               int32_t max_bodies, int32_t max_contacts, gg_ctx** out);
+
+/* Batched independent environments (the RL env
+ * batch, BulldozerEnv/ExcavationEnv scenes, envs.py:102-348).  One context
+ * steps n_envs scenes of n_per_env particles each, all with the same params
+ * and per-env table size n_h; each env keeps its own hash table (buckets
+ * [e*n_h, (e+1)*n_h)) and its own bodies, so every env evolves exactly as it
+ * would in a context of its own (bitwise).  Layout conventions with E envs:
+ *   state arrays        (E * n_per_env, 3) env-major (env e = rows e*n_per_env..)
+ *   gg_step bodies      [n_steps][E][n_bodies]
+ *   gg_sync reports     [n_steps][E];  body_momentum [n_steps][E][n_bodies][3]
+ *   gg_detect out       [E]
+ *   taps                global particle ids (env e owns ids e*n_per_env..)
+ * gg_create(...) == gg_create_batched(device, params, 1, n, n_h, ...). */
+int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64_t n_per_env,
+                      int64_t n_h, int32_t max_bodies, int32_t max_contacts, gg_ctx** out);
+int gg_num_envs(const gg_ctx* ctx);
+/* Per-env goal-box statistics of the current state: reward[e] =
+ * bulldozer_reward(positions of env e, GoalBox(lo, hi)) (envs.py:61-70:
+ * +100/n inside the box, boundary inclusive, -d/n outside) and inside[e] =
+ * particles of env e in the box (the transported-mass statistic).  Either
+ * output may be NULL; both hold n_envs entries. */
+int gg_env_box_stats(gg_ctx* ctx, const double lo[3], const double hi[3], double* reward,
+                     int64_t* inside);
 int gg_destroy(gg_ctx* ctx);
 const char* gg_last_error(const gg_ctx* ctx);
 int gg_set_params(gg_ctx* ctx, const gg_params* params);

@@ -43,10 +43,21 @@ from .stepper import (
     step,
 )
 from .beds import column_scene, hero_scene, lattice_bed, make_column_scene
+from .batch import SceneBatch, StaticBatch, TrackSteeringBatch, shard_envs
+from .envs import BatchedBulldozerEnv, BulldozerEnvConfig, GoalBox, bulldozer_reward, bulldozer_scene
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "BatchedBulldozerEnv",
+    "BulldozerEnvConfig",
+    "GoalBox",
+    "SceneBatch",
+    "StaticBatch",
+    "TrackSteeringBatch",
+    "bulldozer_reward",
+    "bulldozer_scene",
+    "shard_envs",
     "Box",
     "BoxRegion",
     "ChainLink",

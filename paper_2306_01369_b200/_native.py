@@ -93,6 +93,10 @@ def _bind(lib: C.CDLL) -> None:
     i32, i64, dbl = C.c_int32, C.c_int64, C.c_double
     sig = {
         "gg_create": (C.c_int, [C.c_int, C.POINTER(GGParams), i64, i64, i32, i32, C.POINTER(P)]),
+        "gg_create_batched": (C.c_int, [C.c_int, C.POINTER(GGParams), i32, i64, i64, i32, i32,
+                                        C.POINTER(P)]),
+        "gg_num_envs": (C.c_int, [P]),
+        "gg_env_box_stats": (C.c_int, [P, P, P, P, P]),
         "gg_destroy": (C.c_int, [P]),
         "gg_last_error": (C.c_char_p, [P]),
         "gg_set_params": (C.c_int, [P, C.POINTER(GGParams)]),

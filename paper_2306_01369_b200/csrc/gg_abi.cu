@@ -17,7 +17,9 @@ struct gg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   gg_params P{};
-  long long n = 0, n_h = 0;
+  long long n = 0, n_h = 0;  // n = E * ne particles; n_h buckets per env
+  int E = 1;                 // independent environments (segments)
+  long long ne = 0;          // particles per env
   int K = 16;
   int max_bodies = 0;
   int nblocks = 0;
@@ -157,12 +159,15 @@ int alloc_slots(gg_ctx* ctx, int K) {
   D.cgeo = nullptr;
   D.coth = nullptr;
   D.cvb = nullptr;
+  // K records per particle on average: the warp allocator hands out
+  // [0, K * n) (per-owner counts are not limited by K)
   const size_t slots = static_cast<size_t>(K) * static_cast<size_t>(std::max<long long>(ctx->n, 1));
   CK(dalloc(ctx, &D.cgeo, slots));
   CK(dalloc(ctx, &D.coth, slots));
   CK(dalloc(ctx, &D.cvb, slots));
   ctx->K = K;
   D.K = K;
+  D.cap_tot = static_cast<long long>(slots);
   ctx->graph_dirty = true;
   return GG_OK;
 }
@@ -176,8 +181,8 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
     ctx->max_bodies = nb;
     dfree(ctx, ctx->D.bm_fix);
     ctx->D.bm_fix = nullptr;
-    CK(dalloc(ctx, &ctx->D.bm_fix, static_cast<size_t>(nb) * 3));
-    CK(cudaMemset(ctx->D.bm_fix, 0, sizeof(unsigned long long) * nb * 3));
+    CK(dalloc(ctx, &ctx->D.bm_fix, static_cast<size_t>(nb) * 3 * ctx->E));
+    CK(cudaMemset(ctx->D.bm_fix, 0, sizeof(unsigned long long) * nb * 3 * ctx->E));
   }
   int cap = std::max(ctx->batch_cap, 1);
   while (cap < need) cap *= 2;
@@ -189,9 +194,9 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
   ctx->d_reports = nullptr;
   ctx->d_bm = nullptr;
   ctx->h_bodies = nullptr;
-  const int mb = std::max(ctx->max_bodies, 1);
+  const size_t mb = static_cast<size_t>(std::max(ctx->max_bodies, 1)) * ctx->E;  // per step
   CK(dalloc(ctx, &ctx->d_bodies, static_cast<size_t>(cap) * mb));
-  CK(dalloc(ctx, &ctx->d_reports, static_cast<size_t>(cap)));
+  CK(dalloc(ctx, &ctx->d_reports, static_cast<size_t>(cap) * ctx->E));
   CK(dalloc(ctx, &ctx->d_bm, static_cast<size_t>(cap) * mb * 3));
   CK(cudaMallocHost(&ctx->h_bodies, sizeof(gg_body) * static_cast<size_t>(cap) * mb));
   ctx->batch_cap = cap;
@@ -207,7 +212,8 @@ int begin_batch(gg_ctx* ctx, cudaStream_t s) {
   CK(cudaMemsetAsync(ctx->D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
   CK(cudaMemsetAsync(ctx->D.tile, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->ntiles), s));
   CK(cudaMemsetAsync(ctx->D.bflags, 0, sizeof(unsigned) * std::max(ctx->fused_grid, 1), s));
-  k_batch_begin<<<1, 1, 0, s>>>(ctx->D);
+  const long long work = std::max<long long>(ctx->E, static_cast<long long>(ctx->E) * std::max(ctx->max_bodies, 1) * 3);
+  k_batch_begin<<<static_cast<int>(std::min<long long>(148, (work + 255) / 256)), 256, 0, s>>>(ctx->D);
   CK(cudaGetLastError());
   return GG_OK;
 }
@@ -224,14 +230,15 @@ bool use_persistent_solve(const gg_ctx* ctx) {
   return ctx->n <= static_cast<long long>(ctx->solve_grid) * kBlock;
 }
 
-int launch_coop(gg_ctx* ctx, void (*kern)(Dev), int grid, const Dev& D, cudaStream_t s, bool coop) {
+int launch_coop(gg_ctx* ctx, void (*kern)(Dev), int grid, const Dev& D, cudaStream_t s, bool coop,
+                size_t smem = 0) {
   // bar_count, done_count, bar_gen are contiguous in Ctl
   // barrier words and sweep flags are zero on entry: begin_batch zeroes them
   // and the last block of every cooperative launch resets them
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kBlock);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -280,7 +287,7 @@ int enqueue_step(gg_ctx* ctx, int resort) {
   cudaStream_t s = ctx->stream;
   if (use_fused_step(ctx)) {
     return launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s,
-                       ctx->solve_mode != 5);
+                       ctx->solve_mode != 5, sizeof(NarrowSmem));
   }
   int st;
   if (resort) {
@@ -290,8 +297,7 @@ int enqueue_step(gg_ctx* ctx, int resort) {
   const Dev D = pass_dev(ctx, resort, 0);
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
-  k_narrow<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  if (D.nb > 0) k_bodies<<<ctx->nblocks, kBlock, 0, s>>>(D);
+  k_narrow<<<ctx->nblocks, kBlock, sizeof(NarrowSmem), s>>>(D);
   CK(cudaGetLastError());
   return launch_solve(ctx, D, s);
 }
@@ -302,7 +308,7 @@ bool use_fused_step(const gg_ctx* ctx);
 int kernels_per_step(const gg_ctx* ctx, int resort) {
   if (use_fused_step(ctx)) return 1;
   const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 1;
-  return 7 + solve + (ctx->D.nb > 0 ? 1 : 0) + (resort ? 6 : 0);
+  return 7 + solve + (resort ? 6 : 0);
 }
 
 // Same schedule as enqueue_step, with an event after every kernel so each
@@ -310,7 +316,7 @@ int kernels_per_step(const gg_ctx* ctx, int resort) {
 constexpr int kProfKinds = 12;
 const char* kProfNames[kProfKinds] = {"(unused)", "k_count", "k_scan_tiles", "k_scan_top",
                                       "k_scan_apply",  "k_scatter", "k_resort",  "k_fill",
-                                      "k_narrow",      "k_solve",   "k_bodies",  "k_step_fused"};
+                                      "k_narrow",      "k_solve",   "(unused)",  "k_step_fused"};
 
 int ensure_events(gg_ctx* ctx, size_t n) {
   while (ctx->evpool.size() < n) {
@@ -335,7 +341,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
   cudaEventRecord(ev[0], s);
   if (use_fused_step(ctx)) {
     if (launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s,
-                    ctx->solve_mode != 5) != GG_OK)
+                    ctx->solve_mode != 5, sizeof(NarrowSmem)) != GG_OK)
       return -1;
     mark(11);
     return e;
@@ -361,12 +367,8 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     }
   }
   const Dev D = pass_dev(ctx, resort, 0);
-  k_narrow<<<nbn, kBlock, 0, s>>>(D);
+  k_narrow<<<nbn, kBlock, sizeof(NarrowSmem), s>>>(D);
   mark(8);
-  if (D.nb > 0) {
-    k_bodies<<<nbn, kBlock, 0, s>>>(D);
-    mark(10);
-  }
   if (launch_solve(ctx, D, s) != GG_OK) return -1;
   mark(9);
   if (cudaGetLastError() != cudaSuccess) return -1;
@@ -441,6 +443,11 @@ const char* gg_last_error(const gg_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 
 int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32_t max_bodies,
               int32_t max_contacts, gg_ctx** out) {
+  return gg_create_batched(device, params, 1, n, n_h, max_bodies, max_contacts, out);
+}
+
+int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64_t n_per_env,
+                      int64_t n_h, int32_t max_bodies, int32_t max_contacts, gg_ctx** out) {
   if (!out) return GG_EINVAL;
   *out = nullptr;
   gg_ctx* ctx = new gg_ctx();
@@ -450,9 +457,13 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
     *out = ctx;
     return st;
   }
-  if (n < 1 || n >= (1ll << 31) || n_h < 1 || n_h >= (1ll << 31)) {
+  const long long E = n_envs;
+  const long long n = E * n_per_env;
+  if (E < 1 || n_per_env < 1 || n >= (1ll << 31) || n_h < 1 || E * n_h >= (1ll << 31)) {
     *out = ctx;
-    return fail(ctx, GG_EINVAL, "need 1 <= n < 2^31 and 1 <= n_h < 2^31");
+    return fail(ctx, GG_EINVAL,
+                "need n_envs >= 1, n_per_env >= 1, n_envs * n_per_env < 2^31 and "
+                "1 <= n_envs * n_h < 2^31");
   }
   *out = ctx;
   ctx->device = device;
@@ -464,11 +475,16 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
   ctx->P = *params;
   ctx->n = n;
   ctx->n_h = n_h;
+  ctx->E = static_cast<int>(E);
+  ctx->ne = n_per_env;
   ctx->max_bodies = std::max(max_bodies, 0);
   ctx->nblocks = blocks_for(n);
-  ctx->ntiles = static_cast<int>((n_h + kScanTile - 1) / kScanTile);
+  ctx->ntiles = static_cast<int>((E * n_h + kScanTile - 1) / kScanTile);
   Dev& D = ctx->D;
   D.n = static_cast<int>(n);
+  D.E = static_cast<int>(E);
+  D.ne = static_cast<int>(n_per_env);
+  D.nh_tot = E * n_h;
   D.nblocks = ctx->nblocks;
   D.H.n_h = n_h;
   D.H.pow2 = (n_h & (n_h - 1)) == 0 ? 1 : 0;
@@ -477,6 +493,7 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
     long long p2 = 1;
     while (p2 * 2 <= n_h) p2 *= 2;
     D.mmask = static_cast<uint32_t>(p2 - 1);
+    D.mspan = static_cast<uint32_t>(p2);
   }
   fill_params(ctx);
   D.nb = 0;
@@ -489,18 +506,29 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
   CK(dalloc(ctx, &D.key, n));
   CK(dalloc(ctx, &D.arrive, n));
   CK(dalloc(ctx, &D.tmp, n));
-  CK(dalloc(ctx, &D.cnt, n_h));
-  CK(dalloc(ctx, &D.start, n_h + 1));
+  CK(dalloc(ctx, &D.cnt, E * n_h));
+  CK(dalloc(ctx, &D.start, E * n_h + 1));
   CK(dalloc(ctx, &D.tile, ctx->ntiles));
   CK(dalloc(ctx, &D.Xs, n));
   CK(dalloc(ctx, &D.V0, n));
-  CK(dalloc(ctx, &D.ccount, n));
-  CK(dalloc(ctx, &D.acc, 1));
+  CK(dalloc(ctx, &D.cinfo, n));
+  CK(cudaMemset(D.cinfo, 0, sizeof(int2) * n));
+  CK(cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(sizeof(NarrowSmem))));
+  CK(cudaFuncSetAttribute(k_step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(sizeof(NarrowSmem))));
+  CK(dalloc(ctx, &D.acc, E));
+  D.ke_fix = nullptr;
+  if (E > 1) {
+    CK(dalloc(ctx, &D.ke_fix, E));
+    CK(cudaMemset(D.ke_fix, 0, sizeof(unsigned long long) * E));
+  }
   // co-resident grid of the cooperative solve kernel
   {
     int per_sm = 0, sms = 0, per_sm_f = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kBlock, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, k_step_fused, kBlock, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, k_step_fused, kBlock,
+                                                     sizeof(NarrowSmem)));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     ctx->solve_grid = std::max(1, std::min(ctx->nblocks, per_sm * sms));
     ctx->fused_grid = std::max(1, std::min(ctx->nblocks, per_sm_f * sms));
@@ -508,15 +536,15 @@ int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32
   CK(dalloc(ctx, &D.Xh, n));
   CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks}))));
-  CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3));
-  CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3));
+  CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3 * E));
+  CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3 * E));
   CK(dalloc(ctx, &D.ctl, 1));
   CK(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
   st = alloc_slots(ctx, max_contacts > 0 ? max_contacts : 16);
   if (st != GG_OK) return st;
-  // start[n_h] = n never changes for a context
+  // start[E * n_h] = n never changes for a context
   const uint32_t nn = static_cast<uint32_t>(n);
-  CK(cudaMemcpy(D.start + n_h, &nn, sizeof(uint32_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(D.start + E * n_h, &nn, sizeof(uint32_t), cudaMemcpyHostToDevice));
   CK(cudaMemset(D.ctl, 0, sizeof(Ctl)));
   CK(cudaMemset(D.UID[0], 0, sizeof(int) * n));
   st = ensure_batch(ctx, 1, ctx->max_bodies);
@@ -713,7 +741,7 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
   if (n_steps < 0) return fail(ctx, GG_EINVAL, "n_steps must be >= 0");
   if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
   if (mode < 0 || mode > 2) return fail(ctx, GG_EINVAL, "unknown pipeline mode");
-  for (long long i = 0; i < static_cast<long long>(n_steps) * n_bodies; ++i) {
+  for (long long i = 0; i < static_cast<long long>(n_steps) * ctx->E * n_bodies; ++i) {
     const gg_body& b = bodies[i];
     if (b.kind < GG_GEOM_SPHERE || b.kind > GG_GEOM_GRID)
       return fail(ctx, GG_EINVAL, "unknown geometry kind");
@@ -730,7 +758,7 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
     ctx->graph_dirty = true;
   }
   if (n_bodies > 0) {
-    const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * n_bodies;
+    const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * ctx->E * n_bodies;
     std::memcpy(ctx->h_bodies, bodies, bytes);
     CK(cudaMemcpyAsync(ctx->d_bodies, ctx->h_bodies, bytes, cudaMemcpyHostToDevice, ctx->stream));
   }
@@ -766,7 +794,8 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
     ctx->graph_dirty = true;
   }
   if (n_bodies > 0)
-    CK(cudaMemcpy(ctx->d_bodies, bodies, sizeof(gg_body) * n_bodies, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bodies, bodies, sizeof(gg_body) * n_bodies * ctx->E,
+                  cudaMemcpyHostToDevice));
   refresh_dev(ctx);
   const Dev D = pass_dev(ctx, 0, 0);
   cudaStream_t s = ctx->stream;
@@ -774,9 +803,8 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
   if (st != GG_OK) return st;
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
-  k_narrow<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  if (D.nb > 0) k_bodies<<<ctx->nblocks, kBlock, 0, s>>>(D);
-  ctx->launches += 10;
+  k_narrow<<<ctx->nblocks, kBlock, sizeof(NarrowSmem), s>>>(D);
+  ctx->launches += 9;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   ctx->tap_uncommitted = true;
@@ -789,17 +817,21 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
     return fail(ctx, GG_ECAPACITY, buf);
   }
   if (out) {
-    Acc a;
-    CK(cudaMemcpy(&a, D.acc, sizeof(Acc), cudaMemcpyDeviceToHost));
-    std::memset(out, 0, sizeof(gg_report));
-    out->n_contacts = static_cast<int64_t>(a.n_pp);
-    out->n_candidates = static_cast<int64_t>(a.n_cand);
-    out->n_body_contacts = static_cast<int64_t>(a.n_body);
-    out->n_coincident = static_cast<int64_t>(a.n_coinc);
-    out->n_degenerate = static_cast<int64_t>(a.n_deg);
-    double mp;
-    std::memcpy(&mp, &a.max_psi_bits, sizeof(double));
-    out->max_penetration = mp;
+    std::vector<Acc> acc(ctx->E);
+    CK(cudaMemcpy(acc.data(), D.acc, sizeof(Acc) * ctx->E, cudaMemcpyDeviceToHost));
+    for (int e = 0; e < ctx->E; ++e) {
+      const Acc& a = acc[e];
+      gg_report* o = out + e;
+      std::memset(o, 0, sizeof(gg_report));
+      o->n_contacts = static_cast<int64_t>(a.n_pp);
+      o->n_candidates = static_cast<int64_t>(a.n_cand);
+      o->n_body_contacts = static_cast<int64_t>(a.n_body);
+      o->n_coincident = static_cast<int64_t>(a.n_coinc);
+      o->n_degenerate = static_cast<int64_t>(a.n_deg);
+      double mp;
+      std::memcpy(&mp, &a.max_psi_bits, sizeof(double));
+      o->max_penetration = mp;
+    }
   }
   return GG_OK;
 }
@@ -813,7 +845,7 @@ static int stage_bodies(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int
     ctx->graph_dirty = true;
   }
   if (n_bodies > 0) {
-    const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * n_bodies;
+    const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * ctx->E * n_bodies;
     std::memcpy(ctx->h_bodies, bodies, bytes);
     CK(cudaMemcpyAsync(ctx->d_bodies, ctx->h_bodies, bytes, cudaMemcpyHostToDevice, ctx->stream));
   }
@@ -922,9 +954,10 @@ int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
   if (err_step) *err_step = c.err ? c.err_step : -1;
   const int ncopy = std::min(done, cap);
   if (reports && ncopy > 0)
-    CK(cudaMemcpy(reports, ctx->d_reports, sizeof(gg_report) * ncopy, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(reports, ctx->d_reports, sizeof(gg_report) * ncopy * ctx->E,
+                  cudaMemcpyDeviceToHost));
   if (body_momentum && ncopy > 0 && ctx->last_nb > 0)
-    CK(cudaMemcpy(body_momentum, ctx->d_bm, sizeof(double) * 3 * ctx->last_nb * ncopy,
+    CK(cudaMemcpy(body_momentum, ctx->d_bm, sizeof(double) * 3 * ctx->last_nb * ctx->E * ncopy,
                   cudaMemcpyDeviceToHost));
   if (!c.err) return GG_OK;
   char buf[512];
@@ -986,26 +1019,27 @@ int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order) {
   return GG_OK;
 }
 
-int gg_tap_contacts(gg_ctx* ctx, int64_t cap, int64_t* count, int32_t* owner, int32_t* other,
+int gg_tap_contacts(gg_ctx* ctx, int64_t cap_out, int64_t* count, int32_t* owner, int32_t* other,
                     int32_t* kind, double* psi, double* e1) {
   if (!ctx || !count) return GG_EINVAL;
   DeviceGuard guard(ctx->device);
   CK(cudaStreamSynchronize(ctx->stream));
   const long long n = ctx->n;
-  const int K = ctx->K;
-  std::vector<int> cnt(n), uid(n), oth(static_cast<size_t>(K) * n);
-  std::vector<float4> geo(static_cast<size_t>(K) * n);
+  const long long cap = ctx->D.cap_tot;
+  std::vector<int2> ci(n);
+  std::vector<int> uid(n), oth(cap);
+  std::vector<float4> geo(cap);
   int ucur = 0;
   CK(cudaMemcpy(&ucur, &ctx->D.ctl->ucur, sizeof(int), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(cnt.data(), ctx->D.ccount, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ci.data(), ctx->D.cinfo, sizeof(int2) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(uid.data(), ctx->D.UID[ucur], sizeof(int) * n, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(oth.data(), ctx->D.coth, sizeof(int) * oth.size(), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(geo.data(), ctx->D.cgeo, sizeof(float4) * geo.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(oth.data(), ctx->D.coth, sizeof(int) * cap, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(geo.data(), ctx->D.cgeo, sizeof(float4) * cap, cudaMemcpyDeviceToHost));
   long long m = 0;
   for (long long k = 0; k < n; ++k) {
-    for (int s = 0; s < cnt[k]; ++s, ++m) {
-      if (m >= cap) continue;
-      const size_t idx = static_cast<size_t>(s) * n + k;
+    for (int s = 0; s < ci[k].y; ++s, ++m) {
+      if (m >= cap_out) continue;
+      const size_t idx = static_cast<size_t>(ci[k].x) + s;
       const int j = oth[idx];
       if (owner) owner[m] = uid[k];
       if (other) other[m] = j >= 0 ? uid[j] : -(j + 1);
@@ -1092,5 +1126,28 @@ int gg_host_unregister(void* ptr) {
 }
 
 void* gg_stream(gg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int gg_num_envs(const gg_ctx* ctx) { return ctx ? ctx->E : 0; }
+
+int gg_env_box_stats(gg_ctx* ctx, const double lo[3], const double hi[3], double* reward,
+                     int64_t* inside) {
+  if (!ctx || !lo || !hi) return fail(ctx, GG_EINVAL, "null argument");
+  for (int a = 0; a < 3; ++a)
+    if (!(lo[a] < hi[a])) return fail(ctx, GG_EINVAL, "goal box requires min < max componentwise");
+  DeviceGuard guard(ctx->device);
+  const int E = ctx->E;
+  double* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(double) * 2 * E));
+  long long* di = reinterpret_cast<long long*>(d + E);
+  k_env_box<<<E, kBlock, 0, ctx->stream>>>(ctx->D, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], d, di);
+  ctx->launches += 1;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess && reward) e = cudaMemcpy(reward, d, sizeof(double) * E, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && inside) e = cudaMemcpy(inside, di, sizeof(long long) * E, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gg_env_box_stats");
+  return GG_OK;
+}
 
 }  // extern "C"

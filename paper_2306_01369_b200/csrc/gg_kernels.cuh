@@ -31,6 +31,7 @@
 //   cvb[K][n]   float4  body surface velocity (body contacts only)
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -56,6 +57,7 @@ struct Ctl {
   unsigned done_count; // last-block-done counter of the solve kernel
   unsigned bar_gen;    // last completed barrier target (reset with bar_count)
   unsigned pad2;
+  unsigned long long ccursor;  // contact records allocated this step (warp allocator)
   int bad_uid[kMaxBad];
 };
 
@@ -75,8 +77,17 @@ struct Dev {
   int n, K, nb, S, nblocks;
   int resort;     // this graph re-sorts the physical order first
   int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
-  HashCfg H;
+  // Independent environments (segments).  E == 1 is a single bed.  With
+  // E > 1 env e owns particles [e*ne, (e+1)*ne) of the physical order and
+  // buckets [e*n_h, (e+1)*n_h) of the index (its own table, the reference's
+  // per-scene hash): every sort key is env-major, so the physical order stays
+  // env-contiguous and no candidate ever crosses an env boundary.
+  int E, ne;
+  long long nh_tot;  // E * n_h: length of cnt / start
+  HashCfg H;         // the per-env table (n_h buckets)
   uint32_t mmask;  // Morton key mask (power of two <= n_h, minus one)
+  uint32_t mspan;  // mmask + 1: Morton key range per env
+  unsigned long long* ke_fix;  // [E] fixed-point sum |v|^2 (E > 1)
   double r, two_r, contact_d2, coinc_d2, mass, mu, alpha, dt, gamma, bias_coef;
   float reject_d2f;  // float32 pre-filter: d2_f32 > this  =>  d2 >= contact_d2 exactly
   double gdt0, gdt1, gdt2;
@@ -95,10 +106,11 @@ struct Dev {
   float4* V0;
   float4* Xh;
   float4* W[2];
-  float4* cgeo;
-  int* coth;
-  float4* cvb;
-  int* ccount;
+  float4* cgeo;     // contact records [cap_tot]: (e1.xyz, psi)
+  int* coth;        // partner: physical index, or -(body + 1)
+  float4* cvb;      // body surface velocity (body records)
+  int2* cinfo;      // per particle {first record, record count} (warp-contiguous CSR)
+  long long cap_tot;  // record capacity
   const gg_body* bodies;  // [batch][nb]
   const DevGrid* grids;
   const double* gvals;
@@ -168,6 +180,78 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Per-env accumulation.  E == 1: fixed-order block reduction, one atomic per
+// block (the single-bed path).  E > 1: a warp whose lanes all belong to one
+// env reduces and issues one atomic; a warp straddling an env boundary (at
+// most one per env) issues per-lane atomics.  Integer adds and max/min on
+// the bit patterns of non-negative doubles are order-independent, so the
+// result is deterministic either way.  Called by every thread of the block.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int env_of(const Dev& D, int k) {
+  if (D.E == 1) return 0;
+  const int e = k / D.ne;
+  return e < D.E ? e : D.E - 1;
+}
+
+__device__ __forceinline__ bool warp_env_uniform(int env, int* e0) {
+  *e0 = __shfl_sync(0xffffffffu, env, 0);
+  return __all_sync(0xffffffffu, env == *e0);
+}
+
+// field: byte offset of an unsigned long long member of Acc
+__device__ __forceinline__ unsigned long long* acc_field(const Dev& D, int env, size_t off) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(D.acc + env) + off);
+}
+
+__device__ __forceinline__ void acc_add(const Dev& D, int env, unsigned long long v, size_t off,
+                                        unsigned long long* smu) {
+  if (D.E == 1) {
+    const unsigned long long t = block_sum_u64(v, smu);
+    if (threadIdx.x == 0 && t) atomicAdd(acc_field(D, 0, off), t);
+    return;
+  }
+  int e0;
+  if (warp_env_uniform(env, &e0)) {
+    const unsigned long long t = warp_sum(v);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(acc_field(D, e0, off), t);
+  } else if (v) {
+    atomicAdd(acc_field(D, env, off), v);
+  }
+}
+
+// kOp 1: max of non-negative doubles, 2: min (NaN and +inf are ignored)
+template <int kOp>
+__device__ __forceinline__ void acc_ext(const Dev& D, int env, double v, size_t off, double* smd) {
+  double t;
+  int tgt;
+  bool issue;
+  if (D.E == 1) {
+    t = block_reduce<kOp>(v, smd);
+    tgt = 0;
+    issue = threadIdx.x == 0;
+  } else {
+    int e0;
+    if (warp_env_uniform(env, &e0)) {
+      t = kOp == 1 ? warp_max(v) : warp_min(v);
+      tgt = e0;
+      issue = (threadIdx.x & 31) == 0;
+    } else {
+      t = v;
+      tgt = env;
+      issue = true;
+    }
+  }
+  if (!issue) return;
+  if (kOp == 1) {
+    if (t > 0.0) atomicMax(acc_field(D, tgt, off), dbits(t));
+  } else {
+    if (t == t && t < __longlong_as_double(0x7ff0000000000000ll)) atomicMin(acc_field(D, tgt, off), dbits(t));
+  }
+}
+
+#define GG_ACC(f) offsetof(Acc, f)
+
 // block-uniform early exit: every kernel that syncs reads err through smem
 __device__ __forceinline__ bool block_should_exit(const Ctl* ctl) {
   __shared__ int s_err;
@@ -235,26 +319,37 @@ __device__ __forceinline__ uint32_t morton_key(long long c0, long long c1, long 
 // ---------------------------------------------------------------------------
 // batch begin: reset per-batch control + per-step accumulators
 // ---------------------------------------------------------------------------
-__global__ void k_batch_begin(Dev D) {
-  Ctl* c = D.ctl;
-  c->step = 0;
-  c->err = 0;
-  c->err_step = -1;
-  c->cap_needed = 0;
-  c->n_bad = 0;
-  c->bar_count = 0;
-  c->done_count = 0;
-  c->bar_gen = 0;
-  Acc* a = D.acc;
+__device__ __forceinline__ void acc_reset(Acc* a) {
   a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
   a->max_psi_bits = a->max_viol_bits = 0;
   a->min_b1_bits = dbits(__longlong_as_double(0x7ff0000000000000ll));
-  for (int i = 0; i < D.nb * 3; ++i) D.bm_fix[i] = 0ull;
+}
+
+__global__ void k_batch_begin(Dev D) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int G = gridDim.x * blockDim.x;
+  if (t == 0) {
+    Ctl* c = D.ctl;
+    c->step = 0;
+    c->err = 0;
+    c->err_step = -1;
+    c->cap_needed = 0;
+    c->n_bad = 0;
+    c->bar_count = 0;
+    c->done_count = 0;
+    c->bar_gen = 0;
+    c->ccursor = 0ull;
+  }
+  for (int e = t; e < D.E; e += G) {
+    acc_reset(D.acc + e);
+    if (D.ke_fix) D.ke_fix[e] = 0ull;
+  }
+  for (int i = t; i < D.E * D.nb * 3; i += G) D.bm_fix[i] = 0ull;
 }
 
 // ===========================================================================
 // Phases.  Element-wise phases (ph_count, ph_scatter, ph_resort, ph_fill)
-// handle one index; block phases (ph_scan_*, ph_narrow, ph_bodies) contain
+// handle one index; block phases (ph_scan_*, ph_contacts) contain
 // __syncthreads and must be called by every thread of the block.  The
 // standalone kernels and the fused small-n kernel are thin drivers.
 // ===========================================================================
@@ -270,7 +365,9 @@ __device__ __forceinline__ void ph_count(const Dev& D, Ctl* ctl, int i, bool mor
   const long long c0 = cell_coord(p.x, D.two_r);
   const long long c1 = cell_coord(p.y, D.two_r);
   const long long c2 = cell_coord(p.z, D.two_r);
-  const uint32_t h = morton ? morton_key(c0, c1, c2, D.mmask) : hash_cell(c0, c1, c2, D.H);
+  const uint32_t env = static_cast<uint32_t>(env_of(D, i));
+  const uint32_t h = morton ? env * D.mspan + morton_key(c0, c1, c2, D.mmask)
+                            : env * static_cast<uint32_t>(D.H.n_h) + hash_cell(c0, c1, c2, D.H);
   D.key[i] = h;
   D.arrive[i] = atomicAdd(&D.cnt[h], 1u);
 }
@@ -305,13 +402,13 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sm
 
 // 8 consecutive counts of a tile (kScanTile = 8 x kBlock)
 __device__ __forceinline__ void load8(const Dev& D, long long base, uint32_t v[8]) {
-  if (base + 8 <= D.H.n_h) {
+  if (base + 8 <= D.nh_tot) {
     const uint4 a = *reinterpret_cast<const uint4*>(D.cnt + base);
     const uint4 b = *reinterpret_cast<const uint4*>(D.cnt + base + 4);
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
   } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = (base + e < D.H.n_h) ? D.cnt[base + e] : 0u;
+    for (int e = 0; e < 8; ++e) v[e] = (base + e < D.nh_tot) ? D.cnt[base + e] : 0u;
   }
 }
 
@@ -366,12 +463,12 @@ __device__ __forceinline__ void ph_scan_apply(const Dev& D, int t, uint32_t* sm,
     o[e] = run;
     run += v[e];
   }
-  if (base + 8 <= D.H.n_h) {
+  if (base + 8 <= D.nh_tot) {
     *reinterpret_cast<uint4*>(D.start + base) = make_uint4(o[0], o[1], o[2], o[3]);
     *reinterpret_cast<uint4*>(D.start + base + 4) = make_uint4(o[4], o[5], o[6], o[7]);
   } else {
     for (int e = 0; e < 8; ++e)
-      if (base + e < D.H.n_h) D.start[base + e] = o[e];
+      if (base + e < D.nh_tot) D.start[base + e] = o[e];
   }
 }
 
@@ -384,10 +481,10 @@ __device__ __forceinline__ void ph_scatter(const Dev& D, int i) {
 // scatter phase, so the next pass starts from zero without its own pass.
 __device__ __forceinline__ void ph_zero_counts(const Dev& D, long long t0, long long G) {
   uint4* c4 = reinterpret_cast<uint4*>(D.cnt);
-  const long long n4 = D.H.n_h / 4;
+  const long long n4 = D.nh_tot / 4;
   for (long long i = t0; i < n4; i += G) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-  for (long long i = 4 * n4 + t0; i < D.H.n_h; i += G) D.cnt[i] = 0u;
-  const long long nt = (D.H.n_h + kScanTile - 1) / kScanTile;
+  for (long long i = 4 * n4 + t0; i < D.nh_tot; i += G) D.cnt[i] = 0u;
+  const long long nt = (D.nh_tot + kScanTile - 1) / kScanTile;
   for (long long i = t0; i < nt; i += G) D.tile[i] = 0u;
 }
 
@@ -453,60 +550,191 @@ __device__ __forceinline__ uint32_t nb_hash(const Dev& D, int o, long long c0, l
   return hash_cell64(c0 + ox - 1, c1 + oy - 1, c2 + oz - 1, D.H.n_h);
 }
 
-// The exact pp test on one candidate (contact.py:257-272): float64 from
-// float32-representable inputs in the reference's operation order.
-__device__ __forceinline__ void pp_candidate(const Dev& D, int k, double px, double py, double pz,
-                                             float4 qf, int q, int& cnt, unsigned long long& n_coinc,
-                                             double& max_psi) {
-  const double dx = __dsub_rn(px, static_cast<double>(qf.x));
-  const double dy = __dsub_rn(py, static_cast<double>(qf.y));
-  const double dz = __dsub_rn(pz, static_cast<double>(qf.z));
-  // einsum("ij,ij->i") on the reference host: (dx^2 + dz^2) + dy^2
-  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
-  if (!(d2 >= D.coinc_d2)) {
-    ++n_coinc;
-    return;
-  }
-  if (d2 < D.contact_d2) {
-    const double dist = __dsqrt_rn(d2);
-    const double psi = __dsub_rn(D.two_r, dist);
-    if (cnt < D.K) {
-      const long long sl = static_cast<long long>(cnt) * D.n + k;
-      D.cgeo[sl] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
-                               static_cast<float>(__ddiv_rn(dy, dist)),
-                               static_cast<float>(__ddiv_rn(dz, dist)), static_cast<float>(psi));
-      D.coth[sl] = q;
-    }
-    ++cnt;
-    max_psi = nmax(max_psi, psi);
-  }
+// The exact pp distance (contact.py:257-262): float64 from float32-representable
+// inputs in the reference's operation order.  einsum("ij,ij->i") on the
+// reference host sums (dx^2 + dz^2) + dy^2.
+__device__ __forceinline__ double pp_d2(double px, double py, double pz, float4 qf, double& dx,
+                                        double& dy, double& dz) {
+  dx = __dsub_rn(px, static_cast<double>(qf.x));
+  dy = __dsub_rn(py, static_cast<double>(qf.y));
+  dz = __dsub_rn(pz, static_cast<double>(qf.z));
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
 }
+
+// One pp contact record (contact.py:264-272): e1 = d / |d| (j -> i),
+// psi = 2r - |d|, partner q (physical index).  Returns psi.
+__device__ __forceinline__ double pp_write(const Dev& D, long long dst, double dx, double dy,
+                                           double dz, double d2, int q) {
+  const double dist = __dsqrt_rn(d2);
+  const double psi = __dsub_rn(D.two_r, dist);
+  D.cgeo[dst] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
+                            static_cast<float>(__ddiv_rn(dy, dist)),
+                            static_cast<float>(__ddiv_rn(dz, dist)), static_cast<float>(psi));
+  D.coth[dst] = q;
+  return psi;
+}
+
+constexpr int kPassCap = 16;  // prefilter passes queued per owner (more: exact inline path)
+constexpr int kWarps = kBlock / 32;
 
 struct NarrowSmem {
   uint32_t beg[27][kBlock];
-  uint16_t len[27][kBlock];  // bucket sizes are < 2^16
+  uint16_t len[27][kBlock];        // bucket sizes are < 2^16
+  uint32_t pass[kPassCap][kBlock]; // Xh index of every prefilter pass, per owner, in order
+  float4 pos[kBlock];              // owner positions
+  uint32_t off[kWarps][32];        // per-warp exclusive offsets of the owners' queue segments
+  uint32_t hit[kWarps][kPassCap];  // per-warp queue bits: exact contact
+  uint32_t coi[kWarps][kPassCap];  // per-warp queue bits: coincident
   double d[32];
   unsigned long long u[32];
 };
 
-// Particle k = base + threadIdx.x.  Phase 1: the 27 neighbour-bucket bounds,
-// loaded in three batches of 9 independent loads; empty and duplicate buckets
-// are dropped and the rest compacted into a per-thread list in shared memory.
-// Phase 2: ONE flat loop over the concatenated candidates (lanes stay
-// converged; the next candidate is prefetched while the current one is
-// tested), a conservative float32 reject, then the exact float64 test.
-__device__ __forceinline__ void ph_narrow(const Dev& D, Ctl* ctl, int base, NarrowSmem& sm) {
+// bits [s, s+len) of a bit array, len <= 32
+__device__ __forceinline__ uint32_t popc_range(const uint32_t* w, uint32_t s, uint32_t len) {
+  if (len == 0) return 0u;
+  const uint32_t e = s + len;
+  const uint32_t ws = s >> 5, we = (e - 1) >> 5;
+  const uint32_t lo = ~0u << (s & 31);
+  const uint32_t hi = (e & 31) ? ((1u << (e & 31)) - 1u) : ~0u;
+  if (ws == we) return __popc(w[ws] & lo & hi);
+  return __popc(w[ws] & lo) + __popc(w[we] & hi);
+}
+
+// the owner lane of queue entry idx: the largest o with off[o] <= idx
+__device__ __forceinline__ int queue_owner(const uint32_t* off, uint32_t idx) {
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1)  // o + step <= 31 throughout
+    if (off[o + step] <= idx) o += step;
+  return o;
+}
+
+// Iterate over a thread's concatenated candidate list (its compacted
+// neighbour buckets) — the cursor of the flat candidate loop.
+struct CandCursor {
+  int b;
+  uint32_t m, left;
+  __device__ __forceinline__ void init(const NarrowSmem& sm, int tid) {
+    b = 0;
+    m = sm.beg[0][tid];
+    left = sm.len[0][tid];
+  }
+  __device__ __forceinline__ uint32_t next(const NarrowSmem& sm, int tid, bool more) {
+    const uint32_t cur = m;
+    if (more) {
+      ++m;
+      if (--left == 0) {
+        ++b;
+        m = sm.beg[b][tid];
+        left = sm.len[b][tid];
+      }
+    }
+    return cur;
+  }
+};
+
+// Exact inline pass over ALL candidates of one owner (owners with more than
+// kPassCap prefilter passes): counts (write == false) or writes records from
+// dst on (write == true), in candidate order — the same order the queue gives.
+__device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, int tid, int k,
+                                           float4 pf, uint32_t total, bool write, long long dst,
+                                           int& c_pp, unsigned long long& n_coinc,
+                                           double& max_psi) {
+  const double px = pf.x, py = pf.y, pz = pf.z;
+  CandCursor cur;
+  cur.init(sm, tid);
+  c_pp = 0;
+  n_coinc = 0;
+  for (uint32_t i = 0; i < total; ++i) {
+    const uint32_t mi = cur.next(sm, tid, i + 1 < total);
+    const float4 qf = D.Xh[mi];
+    const int q = __float_as_int(qf.w);
+    if (q == k) continue;
+    const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
+    if (!(fx * fx + fy * fy + fz * fz <= D.reject_d2f)) continue;
+    double dx, dy, dz;
+    const double d2 = pp_d2(px, py, pz, qf, dx, dy, dz);
+    if (!(d2 >= D.coinc_d2)) {
+      ++n_coinc;
+      continue;
+    }
+    if (d2 < D.contact_d2) {
+      if (write) max_psi = nmax(max_psi, pp_write(D, dst + c_pp, dx, dy, dz, d2, q));
+      ++c_pp;
+    }
+  }
+}
+
+// K6: particle-body contacts of one particle (contact.py:274-286): world-AABB
+// prefilter (`_near_body`, contact.py:187-203), then the SDF penetration test
+// (sdf.py:472-512); bodies in index order after the particle's pp records,
+// like the reference's per-body concatenation.  write == false only counts.
+__device__ __forceinline__ int body_contacts(const Dev& D, const gg_body* bodies, float4 pf,
+                                             bool write, long long dst,
+                                             unsigned long long& n_deg, double& max_psi) {
+  const double px = pf.x, py = pf.y, pz = pf.z;
+  int c = 0;
+  n_deg = 0;
+  for (int b = 0; b < D.nb; ++b) {
+    const gg_body& B = bodies[b];
+    if (B.bounded) {
+      if (!(px >= B.aabb_lo[0] && px <= B.aabb_hi[0] && py >= B.aabb_lo[1] &&
+            py <= B.aabb_hi[1] && pz >= B.aabb_lo[2] && pz <= B.aabb_hi[2]))
+        continue;
+    }
+    double psi;
+    d3 nrm;
+    int deg;
+    if (penetrate(B, D.grids, D.gvals, px, py, pz, D.r, &psi, &nrm, &deg)) {
+      if (write) {
+        const long long sl = dst + c;
+        const d3 vb = body_surface_velocity(B, px, py, pz, nrm, D.r, psi);
+        D.cgeo[sl] = make_float4(static_cast<float>(nrm.x), static_cast<float>(nrm.y),
+                                 static_cast<float>(nrm.z), static_cast<float>(psi));
+        D.coth[sl] = -(b + 1);
+        D.cvb[sl] = make_float4(static_cast<float>(vb.x), static_cast<float>(vb.y),
+                                static_cast<float>(vb.z), 0.f);
+        max_psi = nmax(max_psi, psi);
+      }
+      ++c;
+    }
+    n_deg += deg;
+  }
+  return c;
+}
+
+// K5+K6: all contacts of particles base .. base+blockDim (contact.py:244-300).
+//
+// Phase A (per thread): the 27 neighbour-bucket bounds (three batches of 9
+//   independent loads; empty and duplicate buckets dropped) compacted into a
+//   per-thread list in shared memory, then ONE flat loop over the candidates
+//   with a conservative float32 reject; survivors are queued (shared memory).
+// Phase B (per warp): the warp's queued candidates are laid end to end and
+//   tested exactly in float64 by all 32 lanes (no lane idles on a
+//   neighbour's contact); ballots give each owner its contacts in candidate
+//   order.  Bodies are counted per thread, the warp allocates its records
+//   with ONE atomic (warp-contiguous CSR: cinfo[k] = {offset, count}), and
+//   the records are written in a second cooperative pass.  Records of one
+//   owner stay in candidate order, then bodies in index order, so results
+//   do not depend on where the allocator put them.
+__device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, NarrowSmem& sm) {
   // plain (coherent) loads: in the fused kernel these buffers are written
   // earlier in the same launch, so the read-only (.nc) path is not allowed
   const float4* LX = layout(D, ctl).x;
   const float4* Xh = D.Xh;
-  const uint32_t* start = D.start;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5, wb = w * 32;
   const int k = base + tid;
-  unsigned long long n_pp = 0, n_cand = 0, n_coinc = 0;
-  double max_psi = 0.0;
-  if (k < D.n) {
-    const float4 pf = LX[k];
+  const bool live = k < D.n;
+  const int env = env_of(D, live ? k : D.n - 1);
+  unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
+  uint32_t total = 0, npass = 0;
+  float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
+  // ---- phase A ------------------------------------------------------------
+  if (live) {
+    // this env's table: buckets [env*n_h, (env+1)*n_h)
+    const uint32_t* start = D.start + static_cast<long long>(env) * D.H.n_h;
+    pf = LX[k];
     const double px = pf.x, py = pf.y, pz = pf.z;
     const long long c0 = cell_coord(px, D.two_r);
     const long long c1 = cell_coord(py, D.two_r);
@@ -520,7 +748,6 @@ __device__ __forceinline__ void ph_narrow(const Dev& D, Ctl* ctl, int base, Narr
     }
     const bool dedup = !D.H.pow2 || may_alias(tx, ty, tz, D.H.mask);
     int nb = 0;
-    uint32_t total = 0;
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
       uint32_t hb[9], sb[9], eb[9];
@@ -545,25 +772,13 @@ __device__ __forceinline__ void ph_narrow(const Dev& D, Ctl* ctl, int base, Narr
       }
     }
     n_cand = total - 1;  // minus the self pair (one per particle, broadphase.py:441-447)
-    int cnt = 0;
-    int b = 0;
-    uint32_t m = sm.beg[0][tid];
-    uint32_t left = sm.len[0][tid];
+    CandCursor cur;
+    cur.init(sm, tid);
     constexpr int kDepth = 4;  // candidates in flight per thread
     for (uint32_t i = 0; i < total; i += kDepth) {
       uint32_t mi[kDepth];
 #pragma unroll
-      for (int u = 0; u < kDepth; ++u) {
-        mi[u] = m;
-        if (i + u + 1 < total) {  // advance the cursor to the next candidate
-          ++m;
-          if (--left == 0) {
-            ++b;
-            m = sm.beg[b][tid];
-            left = sm.len[b][tid];
-          }
-        }
-      }
+      for (int u = 0; u < kDepth; ++u) mi[u] = cur.next(sm, tid, i + u + 1 < total);
       float4 qv[kDepth];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u)
@@ -572,88 +787,117 @@ __device__ __forceinline__ void ph_narrow(const Dev& D, Ctl* ctl, int base, Narr
       for (int u = 0; u < kDepth; ++u) {
         if (i + u >= total) break;
         const float4 qf = qv[u];
-        const int q = __float_as_int(qf.w);
-        if (q == k) continue;
+        if (__float_as_int(qf.w) == k) continue;
         // float32 pre-filter, conservative by a 1e-5 relative margin (the
         // float32 estimate is within ~4e-7 relative of the exact square)
         const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
-        if (fx * fx + fy * fy + fz * fz <= D.reject_d2f)
-          pp_candidate(D, k, px, py, pz, qf, q, cnt, n_coinc, max_psi);
+        if (fx * fx + fy * fy + fz * fz <= D.reject_d2f) {
+          if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
+          ++npass;
+        }
       }
     }
-    n_pp = cnt;
-    D.ccount[k] = cnt < D.K ? cnt : D.K;
-    if (cnt > D.K) {
-      atomicMax(&ctl->cap_needed, cnt);
+  }
+  sm.pos[tid] = pf;
+  // ---- phase B: warp-cooperative exact test ---------------------------------
+  const uint32_t np = npass < kPassCap ? npass : kPassCap;
+  const bool ovf = npass > kPassCap;
+  uint32_t incl = np;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t excl = incl - np;
+  const uint32_t Tw = __shfl_sync(0xffffffffu, incl, 31);
+  sm.off[w][lane] = excl;
+  __syncwarp();
+  const uint32_t* offw = sm.off[w];
+  for (uint32_t r = 0; r * 32 < Tw; ++r) {
+    const uint32_t idx = r * 32 + lane;
+    bool hit = false, coi = false;
+    if (idx < Tw) {
+      const int o = queue_owner(offw, idx);
+      const float4 qf = Xh[sm.pass[idx - offw[o]][wb + o]];
+      const float4 of = sm.pos[wb + o];
+      double dx, dy, dz;
+      const double d2 = pp_d2(of.x, of.y, of.z, qf, dx, dy, dz);
+      coi = !(d2 >= D.coinc_d2);
+      hit = !coi && d2 < D.contact_d2;
+    }
+    const uint32_t bh = __ballot_sync(0xffffffffu, hit);
+    const uint32_t bc = __ballot_sync(0xffffffffu, coi);
+    if (lane == 0) {
+      sm.hit[w][r] = bh;
+      sm.coi[w][r] = bc;
+    }
+  }
+  __syncwarp();
+  int c_pp = static_cast<int>(popc_range(sm.hit[w], excl, np));
+  n_coinc = popc_range(sm.coi[w], excl, np);
+  double max_psi = 0.0;
+  if (ovf) {  // more prefilter passes than the queue holds: exact inline count
+    scan_exact(D, sm, tid, k, pf, total, false, 0, c_pp, n_coinc, max_psi);
+  }
+  // this env's bodies at this step: bodies[step][env][nb]
+  const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
+  const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, 0, n_deg, max_psi) : 0;
+  // ---- allocation: one atomic per warp ---------------------------------------
+  const int tot = c_pp + c_b;
+  int wincl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+    if (lane >= o) wincl += y;
+  }
+  const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
+  unsigned long long wbase = 0;
+  if (lane == 0 && wtot > 0) wbase = atomicAdd(&ctl->ccursor, static_cast<unsigned long long>(wtot));
+  wbase = __shfl_sync(0xffffffffu, wbase, 0);
+  const long long my_off = static_cast<long long>(wbase) + (wincl - tot);
+  const bool fits = static_cast<long long>(wbase) + wtot <= D.cap_tot;
+  if (!fits) {
+    if (lane == 0) {
+      const long long need = (static_cast<long long>(wbase) + wtot + D.n - 1) / D.n + 1;
+      atomicMax(&ctl->cap_needed, static_cast<int>(need < (1 << 30) ? need : (1 << 30)));
       raise_err(ctl, GG_ECAPACITY);
     }
-  }
-  unsigned long long t;
-  t = block_sum_u64(n_pp, sm.u);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_pp, t);
-  t = block_sum_u64(n_cand, sm.u);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_cand, t);
-  t = block_sum_u64(n_coinc, sm.u);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_coinc, t);
-  const double mp = block_reduce<1>(max_psi, sm.d);
-  if (threadIdx.x == 0 && mp > 0.0) atomicMax(&D.acc->max_psi_bits, dbits(mp));
-}
-
-// K6: particle-body contacts (contact.py:274-286): world-AABB prefilter
-// (`_near_body`, contact.py:187-203) then the SDF penetration test
-// (sdf.py:472-512); appended after the particle's pp slots, bodies in index
-// order, like the reference's per-body concatenation.
-__device__ __forceinline__ void ph_bodies(const Dev& D, Ctl* ctl, int base, double* smd,
-                                          unsigned long long* smu) {
-  const gg_body* bodies = D.bodies + static_cast<long long>(ctl->step) * D.nb;
-  const int k = base + threadIdx.x;
-  unsigned long long n_body = 0, n_deg = 0;
-  double max_psi = 0.0;
-  if (k < D.n) {
-    const float4 pf = layout(D, ctl).x[k];
-    const double px = pf.x, py = pf.y, pz = pf.z;
-    int cnt = D.ccount[k];
-    for (int b = 0; b < D.nb; ++b) {
-      const gg_body& B = bodies[b];
-      if (B.bounded) {
-        if (!(px >= B.aabb_lo[0] && px <= B.aabb_hi[0] && py >= B.aabb_lo[1] &&
-              py <= B.aabb_hi[1] && pz >= B.aabb_lo[2] && pz <= B.aabb_hi[2]))
-          continue;
-      }
-      double psi;
-      d3 nrm;
-      int deg;
-      if (penetrate(B, D.grids, D.gvals, px, py, pz, D.r, &psi, &nrm, &deg)) {
-        if (cnt < D.K) {
-          const long long sl = static_cast<long long>(cnt) * D.n + k;
-          const d3 vb = body_surface_velocity(B, px, py, pz, nrm, D.r, psi);
-          D.cgeo[sl] = make_float4(static_cast<float>(nrm.x), static_cast<float>(nrm.y),
-                                   static_cast<float>(nrm.z), static_cast<float>(psi));
-          D.coth[sl] = -(b + 1);
-          D.cvb[sl] = make_float4(static_cast<float>(vb.x), static_cast<float>(vb.y),
-                                  static_cast<float>(vb.z), 0.f);
+  } else {
+    // pp records, cooperatively in queue order; each goes to its owner's
+    // offset + its rank among the owner's hits
+    const bool uni = (D.E == 1) || __all_sync(0xffffffffu, env == __shfl_sync(0xffffffffu, env, 0));
+    for (uint32_t r = 0; r * 32 < Tw; ++r) {
+      const uint32_t idx = r * 32 + lane;
+      const int o = idx < Tw ? queue_owner(offw, idx) : 0;
+      const long long oo = __shfl_sync(0xffffffffu, my_off, o);
+      const bool oovf = __shfl_sync(0xffffffffu, ovf, o);
+      if (idx < Tw && !oovf && ((sm.hit[w][r] >> lane) & 1u)) {
+        const uint32_t s = offw[o];
+        const float4 qf = Xh[sm.pass[idx - s][wb + o]];
+        const int q = __float_as_int(qf.w);
+        const float4 of = sm.pos[wb + o];
+        double dx, dy, dz;
+        const double d2 = pp_d2(of.x, of.y, of.z, qf, dx, dy, dz);
+        const double psi = pp_write(D, oo + popc_range(sm.hit[w], s, idx - s), dx, dy, dz, d2, q);
+        if (uni) {
+          max_psi = nmax(max_psi, psi);
+        } else if (psi > 0.0) {  // warp straddles two envs (rare): owner's env directly
+          atomicMax(&D.acc[env_of(D, base + wb + o)].max_psi_bits, dbits(psi));
         }
-        ++cnt;
-        ++n_body;
-        max_psi = nmax(max_psi, psi);
       }
-      n_deg += deg;
     }
-    if (n_body) {
-      D.ccount[k] = cnt < D.K ? cnt : D.K;
-      if (cnt > D.K) {
-        atomicMax(&ctl->cap_needed, cnt);
-        raise_err(ctl, GG_ECAPACITY);
-      }
+    if (live) {
+      if (ovf) scan_exact(D, sm, tid, k, pf, total, true, my_off, c_pp, n_coinc, max_psi);
+      if (c_b > 0) body_contacts(D, bodies, pf, true, my_off + c_pp, n_deg, max_psi);
+      D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
     }
   }
-  unsigned long long t;
-  t = block_sum_u64(n_body, smu);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_body, t);
-  t = block_sum_u64(n_deg, smu);
-  if (threadIdx.x == 0 && t) atomicAdd(&D.acc->n_deg, t);
-  const double mp = block_reduce<1>(max_psi, smd);
-  if (threadIdx.x == 0 && mp > 0.0) atomicMax(&D.acc->max_psi_bits, dbits(mp));
+  acc_add(D, env, static_cast<unsigned long long>(c_pp), GG_ACC(n_pp), sm.u);
+  acc_add(D, env, n_cand, GG_ACC(n_cand), sm.u);
+  acc_add(D, env, n_coinc, GG_ACC(n_coinc), sm.u);
+  acc_add(D, env, static_cast<unsigned long long>(c_b), GG_ACC(n_body), sm.u);
+  acc_add(D, env, n_deg, GG_ACC(n_deg), sm.u);
+  acc_ext<1>(D, env, max_psi, GG_ACC(max_psi_bits), sm.d);
 }
 
 // ---------------------------------------------------------------------------
@@ -672,29 +916,48 @@ constexpr int kSmemBodies = 16;
 
 struct SweepAcc {
   double maxviol, minb1;
+  int env;                  // env of the particle being swept (E > 1)
+  int gb_lo;                // first global body slot (env * nb + b) held in sbm
   unsigned long long* sbm;  // shared [kSmemBodies][3]
 };
 
-__device__ __forceinline__ void sweep_acc_init(SweepAcc& A, unsigned long long* sbm) {
+// k0: the first particle this thread sweeps (its env seeds A.env)
+__device__ __forceinline__ void sweep_acc_init(const Dev& D, SweepAcc& A, unsigned long long* sbm,
+                                               int k0) {
   A.maxviol = 0.0;
   A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
   A.sbm = sbm;
+  A.env = env_of(D, k0 < D.n ? k0 : D.n - 1);
+  const int kb = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x);
+  A.gb_lo = env_of(D, kb < D.n ? kb : D.n - 1) * D.nb;
   for (int i = threadIdx.x; i < kSmemBodies * 3; i += blockDim.x) sbm[i] = 0ull;
   __syncthreads();
+}
+
+// Strided loops (persistent kernels) may hand a thread particles of several
+// envs: diagnostics gathered for the previous env are flushed lane-wise
+// before the next particle's are accumulated.
+__device__ __forceinline__ void sweep_acc_env(const Dev& D, SweepAcc& A, int k) {
+  if (D.E == 1) return;
+  const int e = env_of(D, k);
+  if (e == A.env) return;
+  Acc* a = D.acc + A.env;
+  if (A.maxviol > 0.0) atomicMax(&a->max_viol_bits, dbits(A.maxviol));
+  if (A.minb1 == A.minb1 && A.minb1 < __longlong_as_double(0x7ff0000000000000ll))
+    atomicMin(&a->min_b1_bits, dbits(A.minb1));
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
+  A.env = e;
 }
 
 // per block: diagnostics (block max/min, one atomic each) + body momentum
 // (one atomic per non-zero component).  Called by every thread.
 __device__ __forceinline__ void sweep_acc_flush(const Dev& D, const SweepAcc& A, double* smd) {
-  const double mv = block_reduce<1>(A.maxviol, smd);
-  if (threadIdx.x == 0 && mv > 0.0) atomicMax(&D.acc->max_viol_bits, dbits(mv));
-  const double mb = block_reduce<2>(A.minb1, smd);
-  if (threadIdx.x == 0 && mb == mb && mb < __longlong_as_double(0x7ff0000000000000ll))
-    atomicMin(&D.acc->min_b1_bits, dbits(mb));
+  acc_ext<1>(D, A.env, A.maxviol, GG_ACC(max_viol_bits), smd);
+  acc_ext<2>(D, A.env, A.minb1, GG_ACC(min_b1_bits), smd);
   __syncthreads();
-  const int m = (D.nb < kSmemBodies ? D.nb : kSmemBodies) * 3;
-  for (int i = threadIdx.x; i < m; i += blockDim.x)
-    if (A.sbm[i]) atomicAdd(&D.bm_fix[i], A.sbm[i]);
+  for (int i = threadIdx.x; i < kSmemBodies * 3; i += blockDim.x)
+    if (A.sbm[i]) atomicAdd(&D.bm_fix[A.gb_lo * 3 + i], A.sbm[i]);
 }
 
 __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
@@ -726,8 +989,9 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   az += iz;
   A.minb1 = nmin(A.minb1, b1);
   if (j < 0) {  // reaction momentum on the body (contact.py:489-495)
-    const int b = -j - 1;
-    unsigned long long* bm = (b < kSmemBodies) ? A.sbm + 3 * b : D.bm_fix + 3 * b;
+    const int gb = A.env * D.nb + (-j - 1);  // global body slot
+    const int sl = gb - A.gb_lo;
+    unsigned long long* bm = (sl >= 0 && sl < kSmemBodies) ? A.sbm + 3 * sl : D.bm_fix + 3 * gb;
     atomicAdd(bm + 0, to_fix(-D.mass * ix));
     atomicAdd(bm + 1, to_fix(-D.mass * iy));
     atomicAdd(bm + 2, to_fix(-D.mass * iz));
@@ -736,24 +1000,17 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
 
 __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* Win, float4* Wout,
                                                SweepAcc& A) {
-  // slot 0 is fetched together with the count and w_k (one round trip)
-  const int c = D.ccount[k];
+  sweep_acc_env(D, A, k);
+  const int2 ci = D.cinfo[k];
   const float4 wf = Win[k];
-  const float4 g0 = D.cgeo[k];
-  const int j0 = D.coth[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  if (c > 0) {
-    const float4 q0 = (j0 >= 0) ? Win[j0] : D.cvb[k];
-    contact_impulse(D, wx, wy, wz, g0, j0, q0, ax, ay, az, A);
-    const int n = D.n;
-    for (int sl = 1; sl < c; ++sl) {
-      const int idx = sl * n + k;
-      const float4 g = D.cgeo[idx];
-      const int j = D.coth[idx];
-      const float4 q = (j >= 0) ? Win[j] : D.cvb[idx];
-      contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
-    }
+  for (int sl = 0; sl < ci.y; ++sl) {
+    const long long idx = static_cast<long long>(ci.x) + sl;
+    const float4 g = D.cgeo[idx];
+    const int j = D.coth[idx];
+    const float4 q = (j >= 0) ? Win[j] : D.cvb[idx];
+    contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
                         static_cast<float>(wz + az), 0.f);
@@ -771,16 +1028,18 @@ struct RegContacts {
   float4 qb[kRegSlots];
   float wx, wy, wz;
 
+  int off;
   __device__ __forceinline__ void load(const Dev& D, int k, float4 w0) {
-    c = D.ccount[k];
-    const int n = D.n;
+    const int2 ci = D.cinfo[k];
+    c = ci.y;
+    off = ci.x;
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s) {
       j[s] = 0;
       if (s < c) {
-        g[s] = D.cgeo[s * n + k];
-        j[s] = D.coth[s * n + k];
-        if (j[s] < 0) qb[s] = D.cvb[s * n + k];
+        g[s] = D.cgeo[off + s];
+        j[s] = D.coth[off + s];
+        if (j[s] < 0) qb[s] = D.cvb[off + s];
       }
     }
     wx = w0.x;
@@ -798,9 +1057,8 @@ struct RegContacts {
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s)
       if (s < c) contact_impulse(D, wx, wy, wz, g[s], j[s], q[s], ax, ay, az, A);
-    const int n = D.n;
     for (int s = kRegSlots; s < c; ++s) {
-      const int idx = s * n + k;
+      const long long idx = static_cast<long long>(off) + s;
       const float4 gg = D.cgeo[idx];
       const int jj = D.coth[idx];
       const float4 qq = (jj >= 0) ? Win[jj] : D.cvb[idx];
@@ -815,10 +1073,42 @@ struct RegContacts {
   }
 };
 
+// per-env kinetic energy (E > 1): sum |v|^2 in 64-bit fixed point (2^-32),
+// exact and order-independent like the body momentum
+constexpr double kKeScale = 4294967296.0;  // 2^32
+__device__ __forceinline__ unsigned long long to_ke_fix(double v2) {
+  return static_cast<unsigned long long>(__double2ll_rn(v2 * kKeScale));
+}
+
+__device__ __forceinline__ void env_add_arr(const Dev& D, int env, unsigned long long v,
+                                            unsigned long long* arr) {
+  int e0;
+  if (warp_env_uniform(env, &e0)) {
+    const unsigned long long t = warp_sum(v);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(arr + e0, t);
+  } else if (v) {
+    atomicAdd(arr + env, v);
+  }
+}
+
+__device__ __forceinline__ void write_report(const Dev& D, gg_report& R, const Acc* a, double ke_sum) {
+  const volatile Acc* va = a;
+  R.n_contacts = static_cast<long long>(va->n_pp);
+  R.n_candidates = static_cast<long long>(va->n_cand);
+  R.n_body_contacts = static_cast<long long>(va->n_body);
+  R.n_coincident = static_cast<long long>(va->n_coinc);
+  R.n_degenerate = static_cast<long long>(va->n_deg);
+  R.max_penetration = __longlong_as_double(static_cast<long long>(va->max_psi_bits));
+  R.kinetic_energy = 0.5 * D.mass * ke_sum;
+  R.max_cone_violation = __longlong_as_double(static_cast<long long>(va->max_viol_bits));
+  R.min_normal_impulse = __longlong_as_double(static_cast<long long>(va->min_b1_bits));
+}
+
 // Symplectic Euler (stepper.py:102-106), SolverError check
 // (contact.py:503-509), kinetic energy (stepper.py:118); the last block to
-// finish reduces the per-block partials in fixed order into the StepReport
-// and commits the new state.  Called by every thread of every block.
+// finish reduces the per-block partials in fixed order into the StepReport(s)
+// — one per env — and commits the new state.  Called by every thread of
+// every block.
 __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int t0, int G,
                                                      double* smd, int* s_last) {
   const int cur = ctl->cur;
@@ -826,11 +1116,13 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
   const Layout L = layout(D, ctl);
   const float4* Wf = D.W[(D.S - 1) & 1];
   double ke = 0.0;
+  unsigned long long kef = 0;  // E > 1: this thread's fixed-point sum for env kenv
+  int kenv = env_of(D, t0 < D.n ? t0 : D.n - 1);
   for (int k = t0; k < D.n; k += G) {
     const float4 xo = L.x[k];
     const float4 vo = L.v[k];
     const float4 wf = Wf[k];
-    const bool has = D.ccount[k] > 0;
+    const bool has = D.cinfo[k].y > 0;
     const double dvx = has ? (double)wf.x - (double)vo.x : 0.0;
     const double dvy = has ? (double)wf.y - (double)vo.y : 0.0;
     const double dvz = has ? (double)wf.z - (double)vo.z : 0.0;
@@ -851,9 +1143,24 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
                                   static_cast<float>(z), 0.f);
     D.V[cur ^ 1][k] = make_float4(static_cast<float>(vx), static_cast<float>(vy),
                                   static_cast<float>(vz), 0.f);
-    ke += __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    if (D.E == 1) {
+      ke += v2;
+    } else {
+      const int e = env_of(D, k);
+      if (e != kenv) {  // strided loops only
+        if (kef) atomicAdd(D.ke_fix + kenv, kef);
+        kef = 0;
+        kenv = e;
+      }
+      kef += to_ke_fix(v2);
+    }
   }
-  const double r = block_reduce<0>(ke, smd);
+  double r = 0.0;
+  if (D.E == 1)
+    r = block_reduce<0>(ke, smd);
+  else
+    env_add_arr(D, kenv, kef, D.ke_fix);
   if (threadIdx.x == 0) {
     D.part[blockIdx.x] = r;
     __threadfence();
@@ -862,38 +1169,44 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
   __syncthreads();
   if (!*s_last) return;
   __threadfence();
-  double v0 = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v0 += *((volatile double*)&D.part[b]);
-  const double ke_tot = block_reduce<0>(v0, smd);
-  if (threadIdx.x < D.nb * 3) {
-    const long long f =
-        static_cast<long long>(*((volatile unsigned long long*)&D.bm_fix[threadIdx.x]));
-    D.bm_out[static_cast<long long>(step) * D.nb * 3 + threadIdx.x] = static_cast<double>(f) / kMomScale;
-    D.bm_fix[threadIdx.x] = 0ull;
+  double ke_tot = 0.0;
+  if (D.E == 1) {
+    double v0 = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v0 += *((volatile double*)&D.part[b]);
+    ke_tot = block_reduce<0>(v0, smd);
+  }
+  __shared__ int s_err;
+  if (threadIdx.x == 0) s_err = *((volatile int*)&ctl->err);
+  __syncthreads();
+  const long long nbm = static_cast<long long>(D.E) * D.nb * 3;
+  for (long long i = threadIdx.x; i < nbm; i += blockDim.x) {
+    const long long f = static_cast<long long>(*((volatile unsigned long long*)&D.bm_fix[i]));
+    if (!s_err) D.bm_out[static_cast<long long>(step) * nbm + i] = static_cast<double>(f) / kMomScale;
+    D.bm_fix[i] = 0ull;
   }
   // every other block has finished (it incremented done_count last), so the
   // barrier words and sweep flags can be reset here for the next launch
   for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
     if (D.bflags) D.bflags[b] = 0u;
+  if (D.E > 1 && !s_err) {
+    for (int e = threadIdx.x; e < D.E; e += blockDim.x) {
+      volatile unsigned long long* kf = D.ke_fix + e;
+      write_report(D, D.reports[static_cast<long long>(step) * D.E + e], D.acc + e,
+                   static_cast<double>(static_cast<long long>(*kf)) / kKeScale);
+      *kf = 0ull;
+      acc_reset(D.acc + e);
+    }
+  }
   if (threadIdx.x == 0) {
     ctl->done_count = 0;
     ctl->bar_count = 0;
     ctl->bar_gen = 0;
-    if (*((volatile int*)&ctl->err)) return;  // an error was raised this step: no commit
-    Acc* a = D.acc;
-    gg_report& R = D.reports[step];
-    R.n_contacts = static_cast<long long>(a->n_pp);
-    R.n_candidates = static_cast<long long>(a->n_cand);
-    R.n_body_contacts = static_cast<long long>(a->n_body);
-    R.n_coincident = static_cast<long long>(a->n_coinc);
-    R.n_degenerate = static_cast<long long>(a->n_deg);
-    R.max_penetration = __longlong_as_double(static_cast<long long>(a->max_psi_bits));
-    R.kinetic_energy = 0.5 * D.mass * ke_tot;
-    R.max_cone_violation = __longlong_as_double(static_cast<long long>(a->max_viol_bits));
-    R.min_normal_impulse = __longlong_as_double(static_cast<long long>(a->min_b1_bits));
-    a->n_pp = a->n_cand = a->n_body = a->n_coinc = a->n_deg = 0;
-    a->max_psi_bits = a->max_viol_bits = 0;
-    a->min_b1_bits = dbits(__longlong_as_double(0x7ff0000000000000ll));
+    ctl->ccursor = 0ull;
+    if (s_err) return;  // an error was raised this step: no commit
+    if (D.E == 1) {
+      write_report(D, D.reports[step], D.acc, ke_tot);
+      acc_reset(D.acc);
+    }
     ctl->cur = cur ^ 1;
     if (D.resort) ctl->ucur ^= 1;
     ctl->step = step + 1;
@@ -947,19 +1260,14 @@ __global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
   if (k < D.n) ph_fill(D, D.ctl, k);
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
-  __shared__ NarrowSmem sm;
-  Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
-  ph_narrow(D, ctl, blockIdx.x * blockDim.x, sm);
-}
+// NarrowSmem (> 48 KB) is dynamic shared memory: launch with sizeof(NarrowSmem)
+extern __shared__ __align__(16) unsigned char g_dsmem[];
 
-__global__ void __launch_bounds__(kBlock) k_bodies(Dev D) {
-  __shared__ double smd[32];
-  __shared__ unsigned long long smu[32];
+__global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
+  NarrowSmem& sm = *reinterpret_cast<NarrowSmem*>(g_dsmem);
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  ph_bodies(D, ctl, blockIdx.x * blockDim.x, smd, smu);
+  ph_contacts(D, ctl, blockIdx.x * blockDim.x, sm);
 }
 
 __global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
@@ -970,7 +1278,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
   const Layout L = layout(D, ctl);
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   SweepAcc A;
-  sweep_acc_init(A, sbm);
+  sweep_acc_init(D, A, sbm, k);
   if (k < D.n) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
   sweep_acc_flush(D, A, smd);
 }
@@ -1012,7 +1320,7 @@ __device__ __forceinline__ bool barrier_ok(const Dev& D, Ctl* ctl, unsigned& tar
 }
 
 __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
-  __shared__ NarrowSmem sm;
+  NarrowSmem& sm = *reinterpret_cast<NarrowSmem*>(g_dsmem);
   __shared__ uint32_t smu[32];
   __shared__ int s_flag;
   __shared__ int s_last;
@@ -1025,7 +1333,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   unsigned target = 0;
   const int G = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ntiles = static_cast<int>((D.H.n_h + kScanTile - 1) / kScanTile);
+  const int ntiles = static_cast<int>((D.nh_tot + kScanTile - 1) / kScanTile);
   // bucket/tile counts are zero on entry (zeroed by the previous scatter)
   for (int pass = D.resort ? 0 : 1; pass < 2; ++pass) {
     const bool morton = pass == 0;
@@ -1053,19 +1361,17 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     }
     ok = barrier_ok(D, ctl, target, &s_flag, ts);
   }
-  // narrowphase + bodies; the sweeps below use the same particle -> thread
-  // map, so a particle's contacts are read by the thread that wrote them
+  // narrowphase + bodies; the sweeps below use the same particle -> block
+  // map, so a particle's records were written by its own block (visible
+  // after the __syncthreads in sweep_acc_init)
   if (ok) {
-    for (int base = blockIdx.x * blockDim.x; base < D.n; base += G) {
-      ph_narrow(D, ctl, base, sm);
-      if (D.nb > 0) ph_bodies(D, ctl, base, sm.d, sm.u);
-    }
+    for (int base = blockIdx.x * blockDim.x; base < D.n; base += G) ph_contacts(D, ctl, base, sm);
   }
   stamp(D, ts);
   const Layout L = layout(D, ctl);
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
-  sweep_acc_init(A, sbm);
+  sweep_acc_init(D, A, sbm, t0);
   if (G >= D.n && gridDim.x <= kMaxFusedBlocks) {
     // One particle per thread: its contacts (first kRegSlots) and its own w
     // stay in registers for all sweeps.  Jacobi sweep s of a block only needs
@@ -1082,10 +1388,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
     __syncthreads();
     {
-      const int n = D.n;
-      const int c = RC.c < D.K ? RC.c : D.K;
-      for (int sl = 0; sl < c; ++sl) {
-        const int j = sl < kRegSlots ? RC.j[sl] : D.coth[sl * n + t0];
+      for (int sl = 0; sl < RC.c; ++sl) {
+        const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl];
         if (j >= 0) {
           const int b = j / blockDim.x;
           if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
@@ -1155,7 +1459,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
-  sweep_acc_init(A, sbm);
+  sweep_acc_init(D, A, sbm, t0);
   for (int s = 0; s < D.S; ++s) {
     if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
     const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
@@ -1209,6 +1513,43 @@ __global__ void k_store_f4(Dev D, float4* __restrict__ x, float4* __restrict__ v
   const int u = D.UID[D.ctl->ucur][k];
   x[u] = D.X[cur][k];
   v[u] = D.V[cur][k];
+}
+
+// Goal-box statistics per env on the committed state (bulldozer_reward,
+// GoalBox.contains / .distance, envs.py:39-70): one block per env, fixed-order
+// reduction.  reward = sum(inside ? 100/n : -d/n); inside = particles in the box.
+__global__ void __launch_bounds__(kBlock) k_env_box(Dev D, double lx, double ly, double lz,
+                                                    double hx, double hy, double hz,
+                                                    double* __restrict__ reward,
+                                                    long long* __restrict__ inside) {
+  __shared__ double smd[32];
+  __shared__ unsigned long long smu[32];
+  const int env = blockIdx.x;
+  const float4* X = D.X[D.ctl->cur];
+  const double inv_n = 100.0 / static_cast<double>(D.ne);
+  const double dn = static_cast<double>(D.ne);
+  double acc = 0.0;
+  unsigned long long cnt = 0;
+  for (int q = threadIdx.x; q < D.ne; q += blockDim.x) {
+    const float4 p = X[static_cast<long long>(env) * D.ne + q];
+    const double px = p.x, py = p.y, pz = p.z;
+    const bool in = px >= lx && py >= ly && pz >= lz && px <= hx && py <= hy && pz <= hz;
+    if (in) {
+      acc += inv_n;
+      ++cnt;
+    } else {
+      const double dx = nmax(nmax(__dsub_rn(lx, px), __dsub_rn(px, hx)), 0.0);
+      const double dy = nmax(nmax(__dsub_rn(ly, py), __dsub_rn(py, hy)), 0.0);
+      const double dz = nmax(nmax(__dsub_rn(lz, pz), __dsub_rn(pz, hz)), 0.0);
+      acc += -__ddiv_rn(norm3(dx, dy, dz), dn);
+    }
+  }
+  const double r = block_reduce<0>(acc, smd);
+  const unsigned long long c = block_sum_u64(cnt, smu);
+  if (threadIdx.x == 0) {
+    if (reward) reward[env] = r;
+    if (inside) inside[env] = static_cast<long long>(c);
+  }
 }
 
 // cells + hashes of the committed state, user order (parity tap)

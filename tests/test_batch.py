@@ -1,0 +1,285 @@
+"""Batched independent environments.
+
+CPU: the env builder and the array drivers against the reference's own
+outputs (tests/golden/bulldozer_env.npz, made by make_golden_envs.py), batch
+validation and env sharding.
+GPU: a batch of E envs evolves exactly as E single-scene contexts (bitwise
+state, exact counters), each env matches the reference / oracle, and the
+on-device reward equals the host reward.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import rel_err
+
+import paper_2306_01369_b200 as gg
+from paper_2306_01369_b200.batch import SceneBatch, StaticBatch, TrackSteeringBatch, shard_envs
+from paper_2306_01369_b200.beds import lattice_scene
+from paper_2306_01369_b200.envs import (
+    BatchedBulldozerEnv,
+    BulldozerEnvConfig,
+    GoalBox,
+    blade_base_pose,
+    bulldozer_reward,
+    bulldozer_scene,
+)
+from oracle import granular_oracle as O
+
+from helpers import GOLDEN
+
+TOL = 1e-5
+
+
+def golden():
+    with np.load(GOLDEN / "bulldozer_env.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+# ---------------------------------------------------------------------------
+# CPU
+# ---------------------------------------------------------------------------
+def test_bulldozer_scene_matches_reference_seeding():
+    g = golden()
+    cfg = BulldozerEnvConfig(n_particles=400)
+    for e, seed in enumerate(g["seeds"]):
+        sc = bulldozer_scene(int(seed), cfg)
+        assert np.array_equal(sc.particles.positions, g["x0"][e])
+        assert [type(b.geometry).__name__ for b in sc.bodies] == ["HalfSpace", "Box"]
+
+
+def test_track_steering_batch_matches_reference_driver():
+    g = golden()
+    cfg = BulldozerEnvConfig(n_particles=400)
+    E = len(g["seeds"])
+    drv = TrackSteeringBatch(np.full(E, -2.0), np.zeros(E), np.zeros(E), z=0.0,
+                             base_pose=blade_base_pose(cfg))
+    drv.command(g["actions"])
+    P, W, V = drv.rollout(int(g["frame_skip"]), cfg.timestep, None)
+    np.testing.assert_allclose(np.transpose(P, (1, 0, 2, 3)), g["blade_pose"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(np.transpose(W, (1, 0, 2)), g["blade_omega"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(np.transpose(V, (1, 0, 2)), g["blade_v"], rtol=0, atol=1e-14)
+
+
+def test_track_steering_batch_equals_single_driver():
+    from paper_2306_01369_b200.kinematics import TrackSteeringDriver, TrackSteeringState
+
+    rng = np.random.default_rng(3)
+    E = 5
+    x, y, th = rng.normal(size=E), rng.normal(size=E), rng.normal(size=E)
+    base = gg.make_pose(gg.so3_exp(np.array([0.1, 0.2, 0.3])), np.array([0.4, -0.1, 0.2]))
+    acts = rng.uniform(-1.5, 1.5, size=(E, 2))
+    b = TrackSteeringBatch(x, y, th, z=0.3, scale_v=1.3, scale_omega=0.7, base_pose=base)
+    b.command(acts)
+    P, W, V = b.rollout(4, 2e-3, None)
+    for e in range(E):
+        d = TrackSteeringDriver(state=TrackSteeringState(x[e], y[e], th[e]), z=0.3, scale_v=1.3,
+                                scale_omega=0.7, base_pose=base)
+        d.command(acts[e])
+        for k in range(4):
+            d.advance(2e-3)
+            np.testing.assert_allclose(P[k, e], d.pose_at(0.0), rtol=0, atol=1e-13)
+            om, vo = d.twist_at(0.0)
+            np.testing.assert_allclose(W[k, e], om, rtol=0, atol=1e-13)
+            np.testing.assert_allclose(V[k, e], vo, rtol=0, atol=1e-13)
+
+
+def test_host_reward_matches_reference_formula():
+    g = golden()
+    goal = GoalBox(BulldozerEnvConfig().goal_min, BulldozerEnvConfig().goal_max)
+    for e in range(len(g["seeds"])):
+        assert bulldozer_reward(g["xT"][e], goal) == pytest.approx(g["reward"][e], rel=0, abs=1e-12)
+    with pytest.raises(ValueError):
+        bulldozer_reward(np.zeros((0, 3)), goal)
+    with pytest.raises(ValueError):
+        GoalBox([0, 0, 0], [1, 0, 1])
+
+
+def test_shard_envs_partitions():
+    for world in (1, 2, 3, 8):
+        parts = [shard_envs(4096, r, world) for r in range(world)]
+        allv = np.sort(np.concatenate(parts))
+        assert np.array_equal(allv, np.arange(4096))
+        assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+
+
+def test_scene_batch_validation_before_device():
+    a = lattice_scene(100)
+    b = lattice_scene(120)
+    with pytest.raises(ValueError, match="particles"):
+        SceneBatch([a, b])
+    c = lattice_scene(100, friction=0.3)
+    with pytest.raises(ValueError, match="params"):
+        SceneBatch([a, c])
+    d = lattice_scene(100)
+    d.hashmap_size = 64
+    with pytest.raises(ValueError, match="hash table"):
+        SceneBatch([a, d])
+    with pytest.raises(ValueError):
+        SceneBatch([])
+    with pytest.raises(ValueError, match="envs"):
+        SceneBatch([a, lattice_scene(100)], body_drivers={0: StaticBatch(3)})
+
+
+# ---------------------------------------------------------------------------
+# GPU
+# ---------------------------------------------------------------------------
+def _mixed_scenes(E, n=700):
+    """E different beds of n particles: lattices of different seeds and
+    densities, with a floor and a moving box."""
+    out = []
+    for e in range(E):
+        sc = lattice_scene(n, seed=e, timestep=5e-4)
+        sc.particles.positions = sc.particles.positions + np.array([0.013 * e, -0.007 * e, 0.0])
+        sc.particles.velocities = np.random.default_rng(e).normal(scale=0.2, size=(n, 3))
+        drv = gg.SpinDriver(axis=np.array([0.0, 0.0, 1.0]), rate=2.0 + e,
+                            center=np.array([0.3, 0.3, 0.0]),
+                            base_pose=gg.make_pose(np.eye(3), np.array([0.45, 0.3, 0.2])))
+        sc.bodies.append(gg.RigidBody(gg.Box(np.array([0.15, 0.1, 0.04])), driver=drv, name="tool"))
+        out.append(sc)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 3])
+def test_batch_equals_single_contexts_bitwise(mode):
+    from paper_2306_01369_b200 import _native as N
+
+    E, T = 6, 12
+    scenes = _mixed_scenes(E)
+    singles = _mixed_scenes(E)
+    batch = SceneBatch(scenes)
+    N.check(batch.ctx, N.lib().gg_set_solve_mode(batch.ctx, mode), "mode")
+    reps, bm = batch.run_raw(T)
+    xb, vb = batch.state()
+    for e in range(E):
+        sc = singles[e]
+        _, rs = gg.run(sc, T)
+        assert np.array_equal(sc.particles.positions, xb[e]), e
+        assert np.array_equal(sc.particles.velocities, vb[e]), e
+        for k in (0, T - 1):
+            r = rs[k]
+            assert reps[k, e]["n_contacts"] == r.n_contacts
+            assert reps[k, e]["n_candidates"] == r.n_candidates
+            assert reps[k, e]["n_body_contacts"] == r.n_body_contacts
+            assert reps[k, e]["max_penetration"] == r.max_penetration
+            assert reps[k, e]["max_cone_violation"] == r.max_cone_violation
+            assert reps[k, e]["kinetic_energy"] == pytest.approx(r.kinetic_energy, rel=1e-9)
+            np.testing.assert_allclose(bm[k, e], r.body_momentum, rtol=0, atol=1e-9)
+    assert reps["n_contacts"].min() > 0
+    batch.close()
+
+
+@pytest.mark.gpu
+def test_batch_single_step_matches_oracle_per_env():
+    E = 4
+    scenes = _mixed_scenes(E, n=1500)
+    x0 = [np.asarray(sc.particles.positions, np.float32).astype(np.float64) for sc in scenes]
+    v0 = [np.asarray(sc.particles.velocities, np.float32).astype(np.float64) for sc in scenes]
+    batch = SceneBatch(scenes)
+    reps, _ = batch.run_raw(1)
+    xb, vb = batch.state()
+    for e in range(E):
+        sc = scenes[e]
+        bodies = []
+        for b in sc.bodies:
+            b.update(sc.params.timestep)
+            bodies.append(b)
+        x1, v1, orep, _, _ = O.step(x0[e], v0[e], sc.params, bodies, gg.default_table_size(1500))
+        assert int(reps[0, e]["n_contacts"]) == orep["n_contacts"]
+        assert int(reps[0, e]["n_candidates"]) == orep["n_candidates"]
+        assert int(reps[0, e]["n_body_contacts"]) == orep["n_body_contacts"]
+        assert rel_err(xb[e], x1) <= TOL and rel_err(vb[e], v1) <= TOL
+
+
+@pytest.mark.gpu
+def test_batched_bulldozer_env_matches_reference():
+    """One control step (frame_skip substeps) of 3 envs vs the reference:
+    first substep teacher-forced to 1e-5; the whole control step and the
+    reward as bulk statistics."""
+    g = golden()
+    cfg = BulldozerEnvConfig(n_particles=400)
+    env = BatchedBulldozerEnv(len(g["seeds"]), cfg)
+    env.reset(g["seeds"])
+    env.driver.command(g["actions"])
+    reps, _ = env.batch.run_raw(1)
+    xb, vb = env.batch.state()
+    for e in range(len(g["seeds"])):
+        assert rel_err(xb[e], g["x1"][e]) <= TOL
+        assert rel_err(vb[e], g["v1"][e]) <= TOL
+        assert int(reps[0, e]["n_contacts"]) == int(g["n_contacts"][e, 0])
+    # remaining substeps of the control step
+    reps, _ = env.batch.run_raw(int(g["frame_skip"]) - 1)
+    xb, _ = env.batch.state()
+    rew, ins = env.goal_stats()
+    for e in range(len(g["seeds"])):
+        assert rel_err(xb[e], g["xT"][e]) <= 1e-3
+        assert rew[e] == pytest.approx(bulldozer_reward(xb[e], env.goal), rel=1e-12, abs=1e-12)
+        assert abs(rew[e] - g["reward"][e]) <= 1e-3 * abs(g["reward"][e])
+    assert ins.shape == (3,)
+    env.close()
+
+
+@pytest.mark.gpu
+def test_batched_bulldozer_env_api():
+    env = BatchedBulldozerEnv(8, BulldozerEnvConfig(n_particles=300))
+    obs = env.reset()
+    assert obs.shape == (8, 3)
+    obs, rew, done, info = env.step(np.tile([1.0, 0.0], (8, 1)))
+    assert obs.shape == (8, 3) and rew.shape == (8,) and done.shape == (8,)
+    assert np.all(obs[:, 0] > -2.0)  # vehicles drove forward
+    assert np.all(info["t"] == pytest.approx(10 * 2e-3))
+    with pytest.raises(ValueError):
+        env.step(np.zeros((8, 3)))
+    with pytest.raises(ValueError):
+        env.step(np.full((8, 2), np.nan))
+    env.close()
+
+
+class _Replay(gg.StaticDriver):
+    """Replays recorded per-step poses/twists (step k at t = (k+1) dt)."""
+
+    def __init__(self, P, W, V, dt):
+        super().__init__()
+        self.P, self.W, self.V, self.dt = P, W, V, dt
+
+    def _k(self, t):
+        return int(round(t / self.dt)) - 1
+
+    def pose_at(self, t):
+        return self.P[self._k(t)]
+
+    def twist_at(self, t):
+        k = self._k(t)
+        return self.W[k].copy(), self.V[k].copy()
+
+
+@pytest.mark.gpu
+def test_large_batch_sampled_envs_match_singles():
+    """256 envs x 2000 particles (the config-3 env size) in one context:
+    sampled envs' counters and states equal single-context runs fed the same
+    blade poses."""
+    cfg = BulldozerEnvConfig(n_particles=2000, radius=0.025)
+    E, T = 256, 80  # the bed reaches the floor after ~60 substeps
+    env = BatchedBulldozerEnv(E, cfg)
+    env.reset(np.arange(E))
+    acts = np.random.default_rng(0).uniform(-1, 1, size=(E, 2))
+    env.driver.command(acts)
+    twin = TrackSteeringBatch(np.full(E, -2.0), np.zeros(E), np.zeros(E), z=0.0,
+                              base_pose=blade_base_pose(cfg))
+    twin.command(acts)
+    P, W, V = twin.rollout(T, cfg.timestep, None)
+    reps, _ = env.batch.run_raw(T)
+    xb, vb = env.batch.state()
+    assert reps["n_contacts"][-1].min() > 0 and reps["n_body_contacts"][-1].min() > 0
+    for e in (0, 77, 255):
+        sc = bulldozer_scene(e, cfg)
+        sc.bodies[1].driver = _Replay(P[:, e], W[:, e], V[:, e], cfg.timestep)
+        for k in range(T):
+            _, r = gg.step(sc)
+            assert int(reps[k, e]["n_contacts"]) == r.n_contacts
+            assert int(reps[k, e]["n_body_contacts"]) == r.n_body_contacts
+        assert np.array_equal(sc.particles.positions, xb[e])
+        assert np.array_equal(sc.particles.velocities, vb[e])
+    assert env.batch.kernel_launches() > 0
+    env.close()
