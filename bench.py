@@ -10,6 +10,9 @@ Workloads (BASELINE.json configs):
            dt = 5e-4, 10 PJA sweeps.  Initial state: bench_data/hero50k_settled.npz
            (settled once on the GPU, shared by both arms), else settled at start.
   bed1m    config 4 scale: lattice_bed(1e6) on a floor with a spinning grid SDF tool.
+  slab     config 5: lattice_bed(8e6) on a floor, slab-decomposed along x over the
+           N ranks (SlabBed: migration + ghost halo + per-sweep w halo, NCCL P2P);
+           total work fixed as N grows ("scaling": "strong").
   envs     config 3: 4096 BulldozerEnv scenes x 2000 particles (r = 0.025), ground
            + blade on TrackSteering drivers with fixed random actions, physics
            substeps only; env e runs on rank e mod N (no communication), so the
@@ -53,7 +56,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="hero50k", choices=["hero50k", "bed1m", "envs"])
+    ap.add_argument("--workload", default="hero50k", choices=["hero50k", "bed1m", "envs", "slab"])
+    ap.add_argument("--slab-particles", type=int, default=8_000_000)
     ap.add_argument("--envs", type=int, default=4096, help="envs workload: total envs")
     ap.add_argument("--env-particles", type=int, default=2000)
     ap.add_argument("--settle", type=int, default=3000)
@@ -230,7 +234,7 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # byte model and roofline
 # ---------------------------------------------------------------------------
-def bytes_model(n_h: int, S: int, c_pp: float, c_b: float) -> dict:
+def bytes_model(n_h: int, S: int, c_pp: float, c_b: float, fused_split: bool = False) -> dict:
     P = int(np.ceil(np.log2(max(n_h, 2)) / 8))
     # SURVEY.md §8d per-kernel terms mapped onto this schedule
     per_kernel = {
@@ -241,11 +245,39 @@ def bytes_model(n_h: int, S: int, c_pp: float, c_b: float) -> dict:
         "k_narrow": 20.0 + 20.0 * c_pp + 16.0 + 32.0 * c_b,
         "k_solve": S * (48.0 + 20.0 * c_pp + 32.0 * c_b) + 80.0,  # S sweeps + integrate
     }
+    # the small-n schedule: sort + contacts in one persistent kernel, and the
+    # solve either in the same kernel or (split) on the 16-CTA cluster
     per_kernel["k_step_fused"] = (per_kernel["k_count"] + 16.0 * 1 + 20.0 + per_kernel["k_fill"]
                                   + per_kernel["k_narrow"]
-                                  + per_kernel["k_solve"])  # the whole step in one kernel
+                                  + (0.0 if fused_split else per_kernel["k_solve"]))
     step = 228.0 + 16.0 * P + 48.0 * S + (S + 1) * (20.0 * c_pp + 32.0 * c_b)
     return {"per_kernel_per_particle": per_kernel, "step_per_particle": step, "radix_passes": P}
+
+
+def merge_solve_kinds(lib, kind_ms, kind_n):
+    """Per-kernel-kind times of gg_profile_steps; the per-sweep launches
+    (k_sweep x S + k_finish) are also reported as one logical k_solve per step
+    (the byte model's unit), the parts kept for the breakdown."""
+    names = [lib.gg_profile_kind_name(k).decode() for k in range(16)]
+    ms = {nm: 0.0 for nm in names if nm}
+    cnt = {nm: 0 for nm in names if nm}
+    for k, nm in enumerate(names):
+        if nm:
+            ms[nm] += float(kind_ms[k])
+            cnt[nm] += int(kind_n[k])
+    if cnt.get("k_finish", 0) > 0:
+        ms["k_solve"] = ms.get("k_solve", 0.0) + ms["k_sweep"] + ms["k_finish"]
+        cnt["k_solve"] = cnt.get("k_solve", 0) + cnt["k_finish"]
+    out = [nm for nm in ms if nm != "(unused)"]
+    return out, np.array([ms[nm] for nm in out]), np.array([cnt[nm] for nm in out])
+
+
+def time_shares(names, kind_ms, kind_n) -> dict:
+    """Share of the step per kernel kind (k_solve, when it is the sum of the
+    per-sweep parts, is reported but not double counted)."""
+    parts = "k_finish" in names and kind_n[names.index("k_finish")] > 0
+    total = sum(float(kind_ms[k]) for k, nm in enumerate(names) if not (parts and nm == "k_solve"))
+    return {nm: float(kind_ms[k]) / max(total, 1e-9) for k, nm in enumerate(names) if kind_n[k] > 0}
 
 
 def peaks():
@@ -443,11 +475,9 @@ def run_envs(args, dist: Dist):
     st = lib.gg_profile_steps(batch.ctx, P, N.ptr(np.ascontiguousarray(table3)), batch.nb,
                               N.ptr(kind_ms), N.ptr(kind_n))
     N.check(batch.ctx, st, "gg_profile_steps")
-    names = [lib.gg_profile_kind_name(k).decode() for k in range(16)]
-    names = [nm for nm in names if nm]
+    names, kind_ms, kind_n = merge_solve_kinds(lib, kind_ms, kind_n)
     model = bytes_model(batch.n_h, 10, c_pp, c_b)
-    share = {names[k]: float(kind_ms[k] / max(kind_ms[: len(names)].sum(), 1e-9))
-             for k in range(len(names)) if kind_n[k] > 0}
+    share = time_shares(names, kind_ms, kind_n)
     top = max((k for k in range(len(names))
                if names[k] in model["per_kernel_per_particle"] and kind_n[k] > 0),
               key=lambda k: kind_ms[k])
@@ -496,6 +526,73 @@ def run_envs(args, dist: Dist):
         }
         print(json.dumps(line), flush=True)
     env.close()
+
+
+def run_slab(args, dist: Dist):
+    import paper_2306_01369_b200 as gg
+    from paper_2306_01369_b200 import _native as N
+    from paper_2306_01369_b200.slab import SlabBed
+
+    import torch
+
+    dev = dist.local
+    n = args.slab_particles
+    x = gg.lattice_bed(n).astype(np.float32).astype(np.float64)
+    sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
+                  params=gg.MaterialParams(timestep=5e-4))
+    bed = SlabBed(sc, rank=dist.rank, world=dist.world, device=dev,
+                  backend="nccl" if dist.world > 1 else None)
+    lib = N.lib()
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        bed.step()
+    stream = torch.cuda.ExternalStream(lib.gg_stream(bed.ctx), device=torch.device("cuda", dev))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = int(lib.gg_kernel_launches(bed.ctx))
+    clocks = Clocks(dev)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    reps = [bed.step() for _ in range(K)]
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clk = clocks.stop()
+    t_ms = dist.max(float(e0.elapsed_time(e1)))
+    value = n * K / (t_ms / 1000.0)
+    c_pp = float(np.mean([r.n_contacts for r in reps])) / n
+    c_b = float(np.mean([r.n_body_contacts for r in reps])) / n
+    peak, peak_src = peaks()
+    model = bytes_model(bed.n_h, 10, c_pp, c_b)
+    owned = dist.max(float(bed.n_owned))
+    roofline = {"bound": "hbm", "kernel": "step (slab)", "achieved": (value / dist.world) *
+                model["step_per_particle"] / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": (value / dist.world) * model["step_per_particle"] / (peak * 1e9),
+                "traffic": None, "peak_source": peak_src,
+                "step_bytes_per_particle": model["step_per_particle"],
+                "note": "whole-step byte model per GPU (SURVEY.md §8d); per-kernel fractions "
+                        "are those of bed1m/envs (same kernels)"}
+    if dist.rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
+                "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 state / f64 contact geometry", "data": "synthetic (lattice bed)",
+                "config": {"workload": "slab", "config": "BASELINE configs[4]: 8M bed, slab "
+                           "decomposition over N GPUs", "n_particles": n, "dt": 5e-4,
+                           "solver_iterations": 10, "parallelism": f"slabs x{dist.world}",
+                           "n_h": bed.n_h, "c_pp": c_pp, "c_b": c_b, "max_owned": owned,
+                           "l2": "state (>1 GB) exceeds L2"},
+                "roofline": roofline, "cpu_baseline": None,
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 240,
+                        "d2h_bytes_per_step": 72,
+                        "api": "SlabBed.step(): the public slab API (host orchestrated; the "
+                               "state stays resident)"},
+                "clocks": clk, "gpu_launches": int(lib.gg_kernel_launches(bed.ctx)) - l0}
+        print(json.dumps(line), flush=True)
+    bed.close()
 
 
 def run_ours(args, dist: Dist):
@@ -560,11 +657,10 @@ def run_ours(args, dist: Dist):
     st = lib.gg_profile_steps(eng.ctx, P, N.ptr(np.ascontiguousarray(table3)), nb, N.ptr(kind_ms),
                               N.ptr(kind_n))
     N.check(eng.ctx, st, "gg_profile_steps")
-    names = [lib.gg_profile_kind_name(k).decode() for k in range(16)]
-    names = [nm for nm in names if nm]
-    kind_ms, kind_n = kind_ms[: len(names)], kind_n[: len(names)]
-    model = bytes_model(eng.n_h, sc.params.solver_iterations, c_pp, c_b)
-    share = {names[k]: float(kind_ms[k] / max(kind_ms.sum(), 1e-9)) for k in range(len(names))}
+    names, kind_ms, kind_n = merge_solve_kinds(lib, kind_ms, kind_n)
+    split = "k_step_fused" in names and "k_solve" in names and kind_n[names.index("k_solve")] > 0
+    model = bytes_model(eng.n_h, sc.params.solver_iterations, c_pp, c_b, fused_split=split)
+    share = time_shares(names, kind_ms, kind_n)
     top = max((k for k in range(len(names))
                if names[k] in model["per_kernel_per_particle"] and kind_n[k] > 0),
               key=lambda k: kind_ms[k])
@@ -634,6 +730,8 @@ def main():
             run_reference(args, dist)
         elif args.workload == "envs":
             run_envs(args, dist)
+        elif args.workload == "slab":
+            run_slab(args, dist)
         else:
             run_ours(args, dist)
     finally:

@@ -222,11 +222,13 @@ int gg_required_contacts(gg_ctx* ctx);
  * it (contact enumeration order is the bucket order); only locality does. */
 int gg_set_resort_every(gg_ctx* ctx, int32_t steps);
 
-/* Launch strategy: 0 auto (the whole step as ONE persistent cooperative
- * kernel when every particle has its own co-resident thread, else one kernel
- * per phase and per sweep), 1 per-phase kernels + cooperative persistent
+/* Launch strategy: 0 auto (small n: mode 4; large n: mode 3), 1 per-phase kernels + cooperative persistent
  * solve, 2 same without the cooperative attribute, 3 per-phase kernels and
- * one launch per sweep, 4 fused step.  Results are identical in every mode. */
+ * one launch per sweep, 4 the whole step as ONE persistent cooperative
+ * kernel (grid barriers between phases), 5 mode 4 without the cooperative
+ * attribute, 6 sort + contacts as one persistent kernel, then the sweeps and
+ * the commit on one 16-CTA thread-block cluster (hardware cluster barriers).
+ * Results are identical in every mode. */
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode);
 
 /* Phase timer of the fused single-kernel step (bench breakdown): on != 0
@@ -245,6 +247,41 @@ void* gg_stream(gg_ctx* ctx);
  * this context (the bench's gpu_launches evidence). */
 const char* gg_build_info(void);
 int64_t gg_kernel_launches(const gg_ctx* ctx);
+
+/* ---- slab domain decomposition -----------------
+ * One bed over several GPUs, one context per rank (single-bed context whose
+ * n is the rank's particle CAPACITY: owned + ghosts).  The bed is cut along x
+ * at cell boundaries (cell = round(x / 2r), broadphase.py:33-41); the rank
+ * owns cells [cell_lo, cell_hi) (unbounded below / above when has_lo / has_hi
+ * is 0).  n_h must be the GLOBAL table size so bucket order is the one-GPU
+ * order.  Per step, with the host moving buffers between neighbours
+ * (NCCL / gloo / P2P — the library only packs and unpacks):
+ *   gg_slab_migrate_pack   -> exchange -> gg_slab_migrate_unpack
+ *   [gg_slab_resort every few steps: Morton order of the owned particles]
+ *   gg_slab_ghost_pack     -> exchange -> gg_slab_ghost_unpack
+ *   gg_slab_detect(bodies)
+ *   for s in 0..S-1: gg_slab_sweep(s); if s < S-1:
+ *       gg_slab_halo_pack(s) -> exchange -> gg_slab_halo_unpack(s)
+ *   gg_slab_finish(report)   (report of the owned particles; sum over ranks)
+ * Particle records are 32 B: float4 (x, y, z, bits(global id)), float4 (v, 0);
+ * halo records are float4 w.  *_pack return the counts for each side and
+ * fail with GG_ECAPACITY if a buffer of `cap` records is too small. */
+int gg_slab_setup(gg_ctx* ctx, int64_t cell_lo, int64_t cell_hi, int32_t has_lo, int32_t has_hi);
+int gg_slab_load(gg_ctx* ctx, const double* x, const double* v, const int32_t* gid, int64_t n_own);
+int gg_slab_migrate_pack(gg_ctx* ctx, void* send_lo, void* send_hi, int64_t cap, int64_t counts[2]);
+int gg_slab_migrate_unpack(gg_ctx* ctx, const void* recv_lo, int64_t n_lo, const void* recv_hi,
+                           int64_t n_hi);
+int gg_slab_resort(gg_ctx* ctx);
+int gg_slab_ghost_pack(gg_ctx* ctx, void* send_lo, void* send_hi, int64_t cap, int64_t counts[2]);
+int gg_slab_ghost_unpack(gg_ctx* ctx, const void* recv_lo, int64_t n_lo, const void* recv_hi,
+                         int64_t n_hi);
+int gg_slab_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies);
+int gg_slab_sweep(gg_ctx* ctx, int32_t sweep);
+int gg_slab_halo_pack(gg_ctx* ctx, int32_t sweep, void* out_lo, void* out_hi);
+int gg_slab_halo_unpack(gg_ctx* ctx, int32_t sweep, const void* in_lo, const void* in_hi);
+int gg_slab_finish(gg_ctx* ctx, gg_report* report, double* body_momentum);
+int64_t gg_slab_owned(const gg_ctx* ctx);
+int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, int64_t* n_own);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ import numpy as np
 from .errors import SolverError
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libgranusim_b200.so"
+LIB_PATH = Path(os.environ.get("GG_LIB", str(_PKG / "_lib" / "libgranusim_b200.so")))  # GG_LIB: A/B experiments
 
 GG_OK = 0
 GG_EINVAL = 1
@@ -97,6 +97,20 @@ def _bind(lib: C.CDLL) -> None:
                                         C.POINTER(P)]),
         "gg_num_envs": (C.c_int, [P]),
         "gg_env_box_stats": (C.c_int, [P, P, P, P, P]),
+        "gg_slab_setup": (C.c_int, [P, i64, i64, i32, i32]),
+        "gg_slab_load": (C.c_int, [P, P, P, P, i64]),
+        "gg_slab_migrate_pack": (C.c_int, [P, P, P, i64, P]),
+        "gg_slab_migrate_unpack": (C.c_int, [P, P, i64, P, i64]),
+        "gg_slab_resort": (C.c_int, [P]),
+        "gg_slab_ghost_pack": (C.c_int, [P, P, P, i64, P]),
+        "gg_slab_ghost_unpack": (C.c_int, [P, P, i64, P, i64]),
+        "gg_slab_detect": (C.c_int, [P, P, i32]),
+        "gg_slab_sweep": (C.c_int, [P, i32]),
+        "gg_slab_halo_pack": (C.c_int, [P, i32, P, P]),
+        "gg_slab_halo_unpack": (C.c_int, [P, i32, P, P]),
+        "gg_slab_finish": (C.c_int, [P, P, P]),
+        "gg_slab_owned": (i64, [P]),
+        "gg_slab_get": (C.c_int, [P, P, P, P, i64, P]),
         "gg_destroy": (C.c_int, [P]),
         "gg_last_error": (C.c_char_p, [P]),
         "gg_set_params": (C.c_int, [P, C.POINTER(GGParams)]),

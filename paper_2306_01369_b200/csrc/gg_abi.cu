@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "gg_kernels.cuh"
+#include "gg_slab.cuh"
 
 using namespace gg;
 
@@ -64,9 +65,22 @@ struct gg_ctx {
   int resort_every = 8;    // physical re-sort period (steps)
   int solve_mode = 0;      // 0 auto, 1 coop solve, 2 plain persistent solve, 3 per-sweep, 4 fused step
   int fused_grid = 0;      // co-resident blocks of k_step_fused
+  bool cluster_ok = false; // a 16-CTA cluster of k_solve_cluster can be resident
   long long since_resort = 1 << 30;  // force a re-sort after upload
 
   std::vector<void*> owned;  // fixed-size allocations freed at destroy
+
+  // slab mode (gg_slab_*): owned particles [0, n_own), ghosts [n_own, n_cur)
+  bool slab_on = false;
+  SlabCfg slab{};
+  long long n_own = 0, n_cur = 0;
+  long long ghost_in[2] = {0, 0};   // ghosts received from lo / hi
+  long long ghost_out[2] = {0, 0};  // boundary particles sent to lo / hi
+  unsigned long long* d_scnt = nullptr;  // [4] slab counters
+  unsigned long long* h_scnt = nullptr;  // pinned mirror
+  int* d_holes = nullptr;
+  int* d_movers = nullptr;
+  int* d_map[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -219,9 +233,15 @@ int begin_batch(gg_ctx* ctx, cudaStream_t s) {
 }
 
 bool use_fused_step(const gg_ctx* ctx) {
-  if (ctx->solve_mode == 4 || ctx->solve_mode == 5) return true;
+  if (ctx->solve_mode == 4 || ctx->solve_mode == 5 || ctx->solve_mode == 6) return true;
   if (ctx->solve_mode != 0) return false;
   return ctx->n <= static_cast<long long>(ctx->fused_grid) * kBlock;
+}
+
+// fused prep (sort + contacts, grid-wide) + cluster solve: auto for small n
+bool use_cluster_solve(const gg_ctx* ctx) {
+  if (!use_fused_step(ctx) || !ctx->cluster_ok) return false;
+  return ctx->solve_mode == 6;
 }
 
 bool use_persistent_solve(const gg_ctx* ctx) {
@@ -246,6 +266,22 @@ int launch_coop(gg_ctx* ctx, void (*kern)(Dev), int grid, const Dev& D, cudaStre
   cfg.attrs = attr;
   cfg.numAttrs = coop ? 1 : 0;
   CK(cudaLaunchKernelEx(&cfg, kern, D));
+  return GG_OK;
+}
+
+int launch_cluster_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterCTAs);
+  cfg.blockDim = dim3(kClusterBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kClusterCTAs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_solve_cluster, D));
   return GG_OK;
 }
 
@@ -280,15 +316,27 @@ Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
   Dev D = ctx->D;
   D.resort = resort;
   D.key_morton = morton;
+  D.fused_stop = 0;
   return D;
+}
+
+bool use_cluster_solve(const gg_ctx* ctx);
+
+// the small-n schedule: k_step_fused, then (split mode) k_solve_cluster
+int launch_fused(gg_ctx* ctx, int resort, cudaStream_t s) {
+  Dev D = pass_dev(ctx, resort, 0);
+  const bool split = use_cluster_solve(ctx);
+  D.fused_stop = split ? 1 : 0;
+  int st = launch_coop(ctx, k_step_fused, ctx->fused_grid, D, s, ctx->solve_mode != 5,
+                       sizeof(NarrowSmem));
+  if (st != GG_OK || !split) return st;
+  D.fused_stop = 0;
+  return launch_cluster_solve(ctx, D, s);
 }
 
 int enqueue_step(gg_ctx* ctx, int resort) {
   cudaStream_t s = ctx->stream;
-  if (use_fused_step(ctx)) {
-    return launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s,
-                       ctx->solve_mode != 5, sizeof(NarrowSmem));
-  }
+  if (use_fused_step(ctx)) return launch_fused(ctx, resort, s);
   int st;
   if (resort) {
     st = enqueue_sort_pass(ctx, pass_dev(ctx, 1, 1), s);
@@ -306,17 +354,18 @@ bool use_persistent_solve(const gg_ctx* ctx);
 bool use_fused_step(const gg_ctx* ctx);
 
 int kernels_per_step(const gg_ctx* ctx, int resort) {
-  if (use_fused_step(ctx)) return 1;
+  if (use_fused_step(ctx)) return use_cluster_solve(ctx) ? 2 : 1;
   const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 1;
   return 7 + solve + (resort ? 6 : 0);
 }
 
 // Same schedule as enqueue_step, with an event after every kernel so each
 // kernel kind's device time can be attributed (bench roofline pass).
-constexpr int kProfKinds = 12;
+constexpr int kProfKinds = 14;
 const char* kProfNames[kProfKinds] = {"(unused)", "k_count", "k_scan_tiles", "k_scan_top",
                                       "k_scan_apply",  "k_scatter", "k_resort",  "k_fill",
-                                      "k_narrow",      "k_solve",   "(unused)",  "k_step_fused"};
+                                      "k_narrow",      "k_solve",   "(unused)",  "k_step_fused",
+                                      "k_sweep",       "k_finish"};
 
 int ensure_events(gg_ctx* ctx, size_t n) {
   while (ctx->evpool.size() < n) {
@@ -340,10 +389,18 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
   };
   cudaEventRecord(ev[0], s);
   if (use_fused_step(ctx)) {
-    if (launch_coop(ctx, k_step_fused, ctx->fused_grid, pass_dev(ctx, resort, 0), s,
-                    ctx->solve_mode != 5, sizeof(NarrowSmem)) != GG_OK)
+    Dev D = pass_dev(ctx, resort, 0);
+    const bool split = use_cluster_solve(ctx);
+    D.fused_stop = split ? 1 : 0;
+    if (launch_coop(ctx, k_step_fused, ctx->fused_grid, D, s, ctx->solve_mode != 5,
+                    sizeof(NarrowSmem)) != GG_OK)
       return -1;
     mark(11);
+    if (split) {
+      D.fused_stop = 0;
+      if (launch_cluster_solve(ctx, D, s) != GG_OK) return -1;
+      mark(9);
+    }
     return e;
   }
   for (int pass = resort ? 0 : 1; pass < 2; ++pass) {
@@ -369,8 +426,17 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
   const Dev D = pass_dev(ctx, resort, 0);
   k_narrow<<<nbn, kBlock, sizeof(NarrowSmem), s>>>(D);
   mark(8);
-  if (launch_solve(ctx, D, s) != GG_OK) return -1;
-  mark(9);
+  if (use_persistent_solve(ctx)) {
+    if (launch_solve(ctx, D, s) != GG_OK) return -1;
+    mark(9);
+  } else {
+    for (int it = 0; it < D.S; ++it) {
+      k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
+      mark(12);
+    }
+    k_finish<<<nbn, kBlock, 0, s>>>(D);
+    mark(13);
+  }
   if (cudaGetLastError() != cudaSuccess) return -1;
   return e;
 }
@@ -482,6 +548,7 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   ctx->ntiles = static_cast<int>((E * n_h + kScanTile - 1) / kScanTile);
   Dev& D = ctx->D;
   D.n = static_cast<int>(n);
+  D.n_own = static_cast<int>(n);
   D.E = static_cast<int>(E);
   D.ne = static_cast<int>(n_per_env);
   D.nh_tot = E * n_h;
@@ -532,10 +599,29 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     ctx->solve_grid = std::max(1, std::min(ctx->nblocks, per_sm * sms));
     ctx->fused_grid = std::max(1, std::min(ctx->nblocks, per_sm_f * sms));
+    // can one 16-CTA cluster of k_solve_cluster be resident?
+    if (cudaFuncSetAttribute(k_solve_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kClusterCTAs);
+      cfg.blockDim = dim3(kClusterBlock);
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kClusterCTAs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      ctx->cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, k_solve_cluster, &cfg) == cudaSuccess &&
+                        nclusters >= 1;
+    }
+    cudaGetLastError();  // a refused query only disables the cluster path
   }
   CK(dalloc(ctx, &D.Xh, n));
   CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
-  CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks}))));
+  CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks,
+                                                          kClusterCTAs}))));
   CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3 * E));
   CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3 * E));
   CK(dalloc(ctx, &D.ctl, 1));
@@ -568,6 +654,7 @@ int gg_destroy(gg_ctx* ctx) {
     ctx->owned.clear();
     if (ctx->h_bodies) cudaFreeHost(ctx->h_bodies);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+    if (ctx->h_scnt) cudaFreeHost(ctx->h_scnt);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -596,7 +683,7 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
 int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
 
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode) {
-  if (!ctx || mode < 0 || mode > 5) return fail(ctx, GG_EINVAL, "solve mode must be 0..5");
+  if (!ctx || mode < 0 || mode > 6) return fail(ctx, GG_EINVAL, "solve mode must be 0..6");
   ctx->solve_mode = mode;
   ctx->graph_dirty = true;
   return GG_OK;
@@ -899,7 +986,7 @@ int gg_profile_steps(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_
   DeviceGuard guard(ctx->device);
   int st = stage_bodies(ctx, n_steps, bodies, n_bodies);
   if (st != GG_OK) return st;
-  const int per = 24;
+  const int per = 40;
   st = ensure_events(ctx, static_cast<size_t>(per + 1));
   if (st != GG_OK) return st;
   for (int k = 0; k < kProfKinds; ++k) {
@@ -1147,6 +1234,322 @@ int gg_env_box_stats(gg_ctx* ctx, const double lo[3], const double hi[3], double
   if (e == cudaSuccess && inside) e = cudaMemcpy(inside, di, sizeof(long long) * E, cudaMemcpyDeviceToHost);
   cudaFree(d);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gg_env_box_stats");
+  return GG_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Slab domain decomposition (gg_slab.cuh).  All calls are on the context
+// stream; *_pack calls synchronise (the host needs the counts to size the
+// exchange), the others are asynchronous until gg_slab_finish.
+// ===========================================================================
+namespace {
+
+Dev slab_dev(const gg_ctx* ctx) {
+  Dev D = ctx->D;
+  D.n = static_cast<int>(ctx->n_cur);
+  D.n_own = static_cast<int>(ctx->n_own);
+  D.resort = 0;
+  D.key_morton = 0;
+  return D;
+}
+
+int slab_check(gg_ctx* ctx) {
+  if (!ctx) return GG_EINVAL;
+  if (!ctx->slab_on) return fail(ctx, GG_EINVAL, "gg_slab_setup has not been called");
+  return GG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gg_slab_setup(gg_ctx* ctx, int64_t cell_lo, int64_t cell_hi, int32_t has_lo, int32_t has_hi) {
+  if (!ctx) return GG_EINVAL;
+  if (ctx->E != 1) return fail(ctx, GG_EINVAL, "slab mode needs a single-bed context");
+  if (has_lo && has_hi && !(cell_lo < cell_hi)) return fail(ctx, GG_EINVAL, "empty slab");
+  DeviceGuard guard(ctx->device);
+  if (!ctx->d_scnt) {
+    CK(dalloc(ctx, &ctx->d_scnt, 4));
+    CK(cudaMallocHost(&ctx->h_scnt, sizeof(unsigned long long) * 4));
+    CK(dalloc(ctx, &ctx->d_holes, ctx->n));
+    CK(dalloc(ctx, &ctx->d_movers, ctx->n));
+    CK(dalloc(ctx, &ctx->d_map[0], ctx->n));
+    CK(dalloc(ctx, &ctx->d_map[1], ctx->n));
+  }
+  ctx->slab = SlabCfg{cell_lo, cell_hi, has_lo ? 1 : 0, has_hi ? 1 : 0};
+  ctx->slab_on = true;
+  int st = ensure_batch(ctx, 1, std::max(ctx->max_bodies, 1));
+  if (st != GG_OK) return st;
+  refresh_dev(ctx);
+  ctx->n_cur = ctx->n_own;
+  return begin_batch(ctx, ctx->stream);  // zero bucket/tile counts once
+}
+
+int gg_slab_load(gg_ctx* ctx, const double* x, const double* v, const int32_t* gid, int64_t n_own) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (n_own < 0 || n_own > ctx->n || (n_own > 0 && (!x || !v || !gid)))
+    return fail(ctx, GG_EINVAL, "bad slab state (n_own exceeds the context capacity?)");
+  DeviceGuard guard(ctx->device);
+  st = ensure_stage(ctx);
+  if (st != GG_OK) return st;
+  ctx->n_own = ctx->n_cur = n_own;
+  ctx->ghost_in[0] = ctx->ghost_in[1] = 0;
+  if (n_own == 0) return GG_OK;
+  const size_t b = sizeof(double) * 3 * static_cast<size_t>(n_own);
+  CK(cudaMemcpyAsync(ctx->d_stage, x, b, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_stage + 3 * ctx->n, v, b, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_holes, gid, sizeof(int) * n_own, cudaMemcpyHostToDevice, ctx->stream));
+  k_slab_load<<<blocks_for(n_own), kBlock, 0, ctx->stream>>>(slab_dev(ctx), ctx->d_stage,
+                                                              ctx->d_stage + 3 * ctx->n, ctx->d_holes);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GG_OK;
+}
+
+int gg_slab_migrate_pack(gg_ctx* ctx, void* send_lo, void* send_hi, int64_t cap, int64_t counts[2]) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (!counts) return fail(ctx, GG_EINVAL, "null counts");
+  DeviceGuard guard(ctx->device);
+  ctx->n_cur = ctx->n_own;  // ghosts of the previous step are dropped
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemsetAsync(ctx->d_scnt, 0, sizeof(unsigned long long) * 4, s));
+  const Dev D = slab_dev(ctx);
+  if (ctx->n_own > 0)
+    k_slab_emigrate<<<blocks_for(ctx->n_own), kBlock, 0, s>>>(
+        D, ctx->slab, static_cast<SlabRec*>(send_lo), static_cast<SlabRec*>(send_hi), cap, ctx->d_scnt);
+  CK(cudaMemcpyAsync(ctx->h_scnt, ctx->d_scnt, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  counts[0] = static_cast<int64_t>(ctx->h_scnt[0]);
+  counts[1] = static_cast<int64_t>(ctx->h_scnt[1]);
+  if (counts[0] > cap || counts[1] > cap)
+    return fail(ctx, GG_ECAPACITY, "slab migration buffer too small");
+  const long long n_em = counts[0] + counts[1];
+  ctx->launches += 1;
+  if (n_em > 0) {
+    const int n_stay = static_cast<int>(ctx->n_own - n_em);
+    k_slab_holes<<<blocks_for(ctx->n_own), kBlock, 0, s>>>(D, n_stay, ctx->d_holes, ctx->d_movers,
+                                                            ctx->d_scnt);
+    CK(cudaMemcpyAsync(ctx->h_scnt, ctx->d_scnt, sizeof(unsigned long long) * 4,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int m = static_cast<int>(ctx->h_scnt[2]);
+    if (m > 0) k_slab_fill<<<blocks_for(m), kBlock, 0, s>>>(D, ctx->d_holes, ctx->d_movers, m);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    ctx->n_own = ctx->n_cur = n_stay;
+  }
+  return GG_OK;
+}
+
+static int slab_append(gg_ctx* ctx, const void* rec, int64_t m, long long at) {
+  if (m <= 0) return GG_OK;
+  if (!rec) return fail(ctx, GG_EINVAL, "null receive buffer");
+  k_slab_append<<<blocks_for(m), kBlock, 0, ctx->stream>>>(slab_dev(ctx), static_cast<const SlabRec*>(rec),
+                                                           static_cast<int>(m), static_cast<int>(at));
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_slab_migrate_unpack(gg_ctx* ctx, const void* recv_lo, int64_t n_lo, const void* recv_hi,
+                           int64_t n_hi) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (n_lo < 0 || n_hi < 0 || ctx->n_own + n_lo + n_hi > ctx->n)
+    return fail(ctx, GG_ECAPACITY, "slab particle capacity exceeded by immigrants");
+  DeviceGuard guard(ctx->device);
+  st = slab_append(ctx, recv_lo, n_lo, ctx->n_own);
+  if (st == GG_OK) st = slab_append(ctx, recv_hi, n_hi, ctx->n_own + n_lo);
+  if (st != GG_OK) return st;
+  ctx->n_own += n_lo + n_hi;
+  ctx->n_cur = ctx->n_own;
+  return GG_OK;
+}
+
+int gg_slab_resort(gg_ctx* ctx) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (ctx->n_own == 0) return GG_OK;
+  DeviceGuard guard(ctx->device);
+  ctx->n_cur = ctx->n_own;
+  Dev D = slab_dev(ctx);
+  D.resort = 1;
+  D.key_morton = 1;
+  cudaStream_t s = ctx->stream;
+  k_slab_set_n<<<1, 1, 0, s>>>(D);
+  const int nb_save = ctx->nblocks;
+  ctx->nblocks = blocks_for(ctx->n_own);
+  st = enqueue_sort_pass(ctx, D, s);
+  ctx->nblocks = nb_save;
+  if (st != GG_OK) return st;
+  k_slab_commit_sorted<<<blocks_for(ctx->n_own), kBlock, 0, s>>>(D);
+  ctx->launches += 8;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_slab_ghost_pack(gg_ctx* ctx, void* send_lo, void* send_hi, int64_t cap, int64_t counts[2]) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (!counts) return fail(ctx, GG_EINVAL, "null counts");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  ctx->n_cur = ctx->n_own;
+  CK(cudaMemsetAsync(ctx->d_scnt, 0, sizeof(unsigned long long) * 4, s));
+  if (ctx->n_own > 0)
+    k_slab_ghosts<<<blocks_for(ctx->n_own), kBlock, 0, s>>>(
+        slab_dev(ctx), ctx->slab, static_cast<SlabRec*>(send_lo), static_cast<SlabRec*>(send_hi),
+        ctx->d_map[0], ctx->d_map[1], std::min<long long>(cap, ctx->n), ctx->d_scnt);
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(ctx->h_scnt, ctx->d_scnt, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  counts[0] = static_cast<int64_t>(ctx->h_scnt[0]);
+  counts[1] = static_cast<int64_t>(ctx->h_scnt[1]);
+  if (counts[0] > cap || counts[1] > cap) return fail(ctx, GG_ECAPACITY, "slab ghost buffer too small");
+  ctx->ghost_out[0] = counts[0];
+  ctx->ghost_out[1] = counts[1];
+  return GG_OK;
+}
+
+int gg_slab_ghost_unpack(gg_ctx* ctx, const void* recv_lo, int64_t n_lo, const void* recv_hi,
+                         int64_t n_hi) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (n_lo < 0 || n_hi < 0 || ctx->n_own + n_lo + n_hi > ctx->n)
+    return fail(ctx, GG_ECAPACITY, "slab particle capacity exceeded by ghosts");
+  DeviceGuard guard(ctx->device);
+  st = slab_append(ctx, recv_lo, n_lo, ctx->n_own);
+  if (st == GG_OK) st = slab_append(ctx, recv_hi, n_hi, ctx->n_own + n_lo);
+  if (st != GG_OK) return st;
+  ctx->ghost_in[0] = n_lo;
+  ctx->ghost_in[1] = n_hi;
+  ctx->n_cur = ctx->n_own + n_lo + n_hi;
+  return GG_OK;
+}
+
+int gg_slab_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
+  for (int b = 0; b < n_bodies; ++b)
+    if (bodies[b].kind < GG_GEOM_SPHERE || bodies[b].kind > GG_GEOM_GRID ||
+        (bodies[b].kind == GG_GEOM_GRID && (bodies[b].grid_id < 0 || bodies[b].grid_id >= (int)ctx->grids.size())))
+      return fail(ctx, GG_EINVAL, "bad body");
+  DeviceGuard guard(ctx->device);
+  st = stage_bodies(ctx, 1, bodies, n_bodies);
+  if (st != GG_OK) return st;
+  cudaStream_t s = ctx->stream;
+  const Dev D = slab_dev(ctx);
+  k_batch_begin<<<1, 256, 0, s>>>(D);  // step / error / accumulators (bucket counts stay zero)
+  k_slab_set_n<<<1, 1, 0, s>>>(D);
+  if (ctx->n_cur > 0) {
+    const int nb_save = ctx->nblocks;
+    ctx->nblocks = blocks_for(ctx->n_cur);
+    st = enqueue_sort_pass(ctx, D, s);
+    ctx->nblocks = nb_save;
+    if (st != GG_OK) return st;
+    k_narrow<<<blocks_for(ctx->n_cur), kBlock, sizeof(NarrowSmem), s>>>(D);
+  }
+  ctx->launches += 9;
+  ctx->last_batch = 1;
+  ctx->last_nb = n_bodies;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_slab_sweep(gg_ctx* ctx, int32_t sweep) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (sweep < 0 || sweep >= ctx->D.S) return fail(ctx, GG_EINVAL, "sweep index out of range");
+  DeviceGuard guard(ctx->device);
+  if (ctx->n_own > 0)
+    k_sweep<<<blocks_for(ctx->n_own), kBlock, 0, ctx->stream>>>(slab_dev(ctx), sweep);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_slab_halo_pack(gg_ctx* ctx, int32_t sweep, void* out_lo, void* out_hi) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  DeviceGuard guard(ctx->device);
+  const Dev D = slab_dev(ctx);
+  for (int side = 0; side < 2; ++side) {
+    const long long m = ctx->ghost_out[side];
+    void* out = side ? out_hi : out_lo;
+    if (m <= 0) continue;
+    if (!out) return fail(ctx, GG_EINVAL, "null halo buffer");
+    k_slab_halo_pack<<<blocks_for(m), kBlock, 0, ctx->stream>>>(D, sweep, ctx->d_map[side],
+                                                                 static_cast<int>(m), static_cast<float4*>(out));
+    ctx->launches += 1;
+  }
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_slab_halo_unpack(gg_ctx* ctx, int32_t sweep, const void* in_lo, const void* in_hi) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  DeviceGuard guard(ctx->device);
+  const Dev D = slab_dev(ctx);
+  long long at = ctx->n_own;
+  for (int side = 0; side < 2; ++side) {
+    const long long m = ctx->ghost_in[side];
+    const void* in = side ? in_hi : in_lo;
+    if (m > 0) {
+      if (!in) return fail(ctx, GG_EINVAL, "null halo buffer");
+      k_slab_halo_unpack<<<blocks_for(m), kBlock, 0, ctx->stream>>>(
+          D, sweep, static_cast<const float4*>(in), static_cast<int>(m), static_cast<int>(at));
+      ctx->launches += 1;
+    }
+    at += m;
+  }
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_slab_finish(gg_ctx* ctx, gg_report* report, double* body_momentum) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  k_finish<<<blocks_for(std::max<long long>(ctx->n_own, 1)), kBlock, 0, s>>>(slab_dev(ctx));
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  int32_t nd = 0, es = -1;
+  st = gg_sync(ctx, report, body_momentum, 1, &nd, &es);
+  ctx->n_cur = ctx->n_own;  // ghosts are dropped after the commit
+  ctx->ghost_in[0] = ctx->ghost_in[1] = 0;
+  if (st == GG_OK && nd != 1) return fail(ctx, GG_ECUDA, "slab step did not commit");
+  return st;
+}
+
+int64_t gg_slab_owned(const gg_ctx* ctx) { return ctx ? ctx->n_own : 0; }
+
+int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, int64_t* n_own) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (!n_own) return fail(ctx, GG_EINVAL, "null n_own");
+  *n_own = ctx->n_own;
+  if (cap < ctx->n_own) return fail(ctx, GG_EINVAL, "output capacity below the owned count");
+  if (ctx->n_own == 0) return GG_OK;
+  DeviceGuard guard(ctx->device);
+  st = ensure_stage(ctx);
+  if (st != GG_OK) return st;
+  cudaStream_t s = ctx->stream;
+  k_slab_store<<<blocks_for(ctx->n_own), kBlock, 0, s>>>(slab_dev(ctx), ctx->d_stage,
+                                                          ctx->d_stage + 3 * ctx->n, ctx->d_holes);
+  ctx->launches += 1;
+  const size_t b = sizeof(double) * 3 * static_cast<size_t>(ctx->n_own);
+  if (x) CK(cudaMemcpyAsync(x, ctx->d_stage, b, cudaMemcpyDeviceToHost, s));
+  if (v) CK(cudaMemcpyAsync(v, ctx->d_stage + 3 * ctx->n, b, cudaMemcpyDeviceToHost, s));
+  if (gid) CK(cudaMemcpyAsync(gid, ctx->d_holes, sizeof(int) * ctx->n_own, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return GG_OK;
 }
 

@@ -76,6 +76,7 @@ __device__ __forceinline__ unsigned long long to_fix(double v) {
 struct Dev {
   int n, K, nb, S, nblocks;
   int resort;     // this graph re-sorts the physical order first
+  int fused_stop; // k_step_fused ends after the contacts (the cluster kernel solves)
   int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
   // Independent environments (segments).  E == 1 is a single bed.  With
   // E > 1 env e owns particles [e*ne, (e+1)*ne) of the physical order and
@@ -83,6 +84,12 @@ struct Dev {
   // per-scene hash): every sort key is env-major, so the physical order stays
   // env-contiguous and no candidate ever crosses an env boundary.
   int E, ne;
+  // Slab mode (one bed over several GPUs): particles
+  // [0, n_own) are owned, [n_own, n) are ghosts received from the
+  // neighbouring slabs — candidates for the owned particles, but they own no
+  // contacts, are not swept (their w arrives by halo exchange) and are not
+  // integrated.  n_own == n otherwise.
+  int n_own;
   long long nh_tot;  // E * n_h: length of cnt / start
   HashCfg H;         // the per-env table (n_h buckets)
   uint32_t mmask;  // Morton key mask (power of two <= n_h, minus one)
@@ -585,6 +592,7 @@ struct NarrowSmem {
   uint32_t off[kWarps][32];        // per-warp exclusive offsets of the owners' queue segments
   uint32_t hit[kWarps][kPassCap];  // per-warp queue bits: exact contact
   uint32_t coi[kWarps][kPassCap];  // per-warp queue bits: coincident
+  unsigned long long wrec[kWarps]; // per-warp record totals -> bases (block allocation)
   double d[32];
   unsigned long long u[32];
 };
@@ -725,7 +733,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5, wb = w * 32;
   const int k = base + tid;
-  const bool live = k < D.n;
+  const bool live = k < D.n_own;
   const int env = env_of(D, live ? k : D.n - 1);
   unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
   uint32_t total = 0, npass = 0;
@@ -842,7 +850,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
   // this env's bodies at this step: bodies[step][env][nb]
   const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
   const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, 0, n_deg, max_psi) : 0;
-  // ---- allocation: one atomic per warp ---------------------------------------
+  // ---- allocation: one atomic per block ----------------------------------------
   const int tot = c_pp + c_b;
   int wincl = tot;
 #pragma unroll
@@ -850,19 +858,29 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
     const int y = __shfl_up_sync(0xffffffffu, wincl, o);
     if (lane >= o) wincl += y;
   }
-  const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
-  unsigned long long wbase = 0;
-  if (lane == 0 && wtot > 0) wbase = atomicAdd(&ctl->ccursor, static_cast<unsigned long long>(wtot));
-  wbase = __shfl_sync(0xffffffffu, wbase, 0);
-  const long long my_off = static_cast<long long>(wbase) + (wincl - tot);
-  const bool fits = static_cast<long long>(wbase) + wtot <= D.cap_tot;
-  if (!fits) {
-    if (lane == 0) {
-      const long long need = (static_cast<long long>(wbase) + wtot + D.n - 1) / D.n + 1;
+  if (lane == 31) sm.wrec[w] = static_cast<unsigned long long>(wincl);
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long run = 0;
+    for (int q = 0; q < kWarps; ++q) {
+      const unsigned long long t = sm.wrec[q];
+      sm.wrec[q] = run;
+      run += t;
+    }
+    const unsigned long long b0 = run ? atomicAdd(&ctl->ccursor, run) : 0ull;
+    for (int q = 0; q < kWarps; ++q) sm.wrec[q] += b0;
+    if (static_cast<long long>(b0 + run) > D.cap_tot) {
+      const long long need = (static_cast<long long>(b0 + run) + D.n - 1) / D.n + 1;
       atomicMax(&ctl->cap_needed, static_cast<int>(need < (1 << 30) ? need : (1 << 30)));
       raise_err(ctl, GG_ECAPACITY);
     }
-  } else {
+  }
+  __syncthreads();
+  const unsigned long long wbase = sm.wrec[w];
+  const long long my_off = static_cast<long long>(wbase) + (wincl - tot);
+  const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
+  const bool fits = static_cast<long long>(wbase) + wtot <= D.cap_tot;
+  if (fits) {
     // pp records, cooperatively in queue order; each goes to its owner's
     // offset + its rank among the owner's hits
     const bool uni = (D.E == 1) || __all_sync(0xffffffffu, env == __shfl_sync(0xffffffffu, env, 0));
@@ -914,11 +932,18 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
 // floor at the L2 and sits on the critical path of every sweep.
 constexpr int kSmemBodies = 16;
 
+// Body reaction momentum of the first kRegBodies bodies is summed per thread
+// in registers (exact fixed-point adds), reduced across the warp with
+// shuffles and only then added to shared memory: 64-bit shared atomics are
+// CAS loops, and the floor contacts of a warp all hit the same three words.
+constexpr int kRegBodies = 1;
+
 struct SweepAcc {
   double maxviol, minb1;
   int env;                  // env of the particle being swept (E > 1)
   int gb_lo;                // first global body slot (env * nb + b) held in sbm
   unsigned long long* sbm;  // shared [kSmemBodies][3]
+  unsigned long long rb[kRegBodies][3];  // this thread's momentum of bodies 0..kRegBodies-1
 };
 
 // k0: the first particle this thread sweeps (its env seeds A.env)
@@ -930,8 +955,21 @@ __device__ __forceinline__ void sweep_acc_init(const Dev& D, SweepAcc& A, unsign
   A.env = env_of(D, k0 < D.n ? k0 : D.n - 1);
   const int kb = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x);
   A.gb_lo = env_of(D, kb < D.n ? kb : D.n - 1) * D.nb;
+#pragma unroll
+  for (int b = 0; b < kRegBodies; ++b) A.rb[b][0] = A.rb[b][1] = A.rb[b][2] = 0ull;
   for (int i = threadIdx.x; i < kSmemBodies * 3; i += blockDim.x) sbm[i] = 0ull;
   __syncthreads();
+}
+
+// this thread's register momentum straight to the global accumulators of env
+__device__ __forceinline__ void sweep_acc_rb_global(const Dev& D, SweepAcc& A) {
+#pragma unroll
+  for (int b = 0; b < kRegBodies; ++b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (A.rb[b][c]) atomicAdd(&D.bm_fix[(A.env * D.nb + b) * 3 + c], A.rb[b][c]);
+      A.rb[b][c] = 0ull;
+    }
 }
 
 // Strided loops (persistent kernels) may hand a thread particles of several
@@ -942,6 +980,7 @@ __device__ __forceinline__ void sweep_acc_env(const Dev& D, SweepAcc& A, int k) 
   const int e = env_of(D, k);
   if (e == A.env) return;
   Acc* a = D.acc + A.env;
+  sweep_acc_rb_global(D, A);
   if (A.maxviol > 0.0) atomicMax(&a->max_viol_bits, dbits(A.maxviol));
   if (A.minb1 == A.minb1 && A.minb1 < __longlong_as_double(0x7ff0000000000000ll))
     atomicMin(&a->min_b1_bits, dbits(A.minb1));
@@ -952,9 +991,28 @@ __device__ __forceinline__ void sweep_acc_env(const Dev& D, SweepAcc& A, int k) 
 
 // per block: diagnostics (block max/min, one atomic each) + body momentum
 // (one atomic per non-zero component).  Called by every thread.
-__device__ __forceinline__ void sweep_acc_flush(const Dev& D, const SweepAcc& A, double* smd) {
+__device__ __forceinline__ void sweep_acc_flush(const Dev& D, SweepAcc& A, double* smd) {
   acc_ext<1>(D, A.env, A.maxviol, GG_ACC(max_viol_bits), smd);
   acc_ext<2>(D, A.env, A.minb1, GG_ACC(min_b1_bits), smd);
+  // register momentum: warp sum, then one shared-memory add per warp
+  int e0 = A.env;
+  const bool uni = D.E == 1 || warp_env_uniform(A.env, &e0);
+  if (uni) {
+#pragma unroll
+    for (int b = 0; b < kRegBodies; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned long long t = warp_sum(A.rb[b][c]);
+        if ((threadIdx.x & 31) == 0 && t && b < D.nb) {
+          const int gb = e0 * D.nb + b;
+          const int sl = gb - A.gb_lo;
+          atomicAdd((sl >= 0 && sl < kSmemBodies) ? A.sbm + 3 * sl + c : D.bm_fix + 3 * gb + c, t);
+        }
+        A.rb[b][c] = 0ull;
+      }
+  } else {
+    sweep_acc_rb_global(D, A);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < kSmemBodies * 3; i += blockDim.x)
     if (A.sbm[i]) atomicAdd(&D.bm_fix[A.gb_lo * 3 + i], A.sbm[i]);
@@ -989,12 +1047,25 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   az += iz;
   A.minb1 = nmin(A.minb1, b1);
   if (j < 0) {  // reaction momentum on the body (contact.py:489-495)
-    const int gb = A.env * D.nb + (-j - 1);  // global body slot
-    const int sl = gb - A.gb_lo;
-    unsigned long long* bm = (sl >= 0 && sl < kSmemBodies) ? A.sbm + 3 * sl : D.bm_fix + 3 * gb;
-    atomicAdd(bm + 0, to_fix(-D.mass * ix));
-    atomicAdd(bm + 1, to_fix(-D.mass * iy));
-    atomicAdd(bm + 2, to_fix(-D.mass * iz));
+    const int b = -j - 1;
+    const unsigned long long fx = to_fix(-D.mass * ix), fy = to_fix(-D.mass * iy),
+                             fz = to_fix(-D.mass * iz);
+    if (b < kRegBodies) {
+#pragma unroll
+      for (int q = 0; q < kRegBodies; ++q)
+        if (q == b) {
+          A.rb[q][0] += fx;
+          A.rb[q][1] += fy;
+          A.rb[q][2] += fz;
+        }
+    } else {
+      const int gb = A.env * D.nb + b;  // global body slot
+      const int sl = gb - A.gb_lo;
+      unsigned long long* bm = (sl >= 0 && sl < kSmemBodies) ? A.sbm + 3 * sl : D.bm_fix + 3 * gb;
+      atomicAdd(bm + 0, fx);
+      atomicAdd(bm + 1, fy);
+      atomicAdd(bm + 2, fz);
+    }
   }
 }
 
@@ -1118,7 +1189,7 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
   double ke = 0.0;
   unsigned long long kef = 0;  // E > 1: this thread's fixed-point sum for env kenv
   int kenv = env_of(D, t0 < D.n ? t0 : D.n - 1);
-  for (int k = t0; k < D.n; k += G) {
+  for (int k = t0; k < D.n_own; k += G) {
     const float4 xo = L.x[k];
     const float4 vo = L.v[k];
     const float4 wf = Wf[k];
@@ -1270,7 +1341,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
   ph_contacts(D, ctl, blockIdx.x * blockDim.x, sm);
 }
 
-__global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
+__global__ void __launch_bounds__(kBlock, 4) k_sweep(Dev D, int s) {
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   __shared__ double smd[32];
   const Ctl* ctl = D.ctl;
@@ -1279,7 +1350,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep(Dev D, int s) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   SweepAcc A;
   sweep_acc_init(D, A, sbm, k);
-  if (k < D.n) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+  if (k < D.n_own) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
   sweep_acc_flush(D, A, smd);
 }
 
@@ -1368,6 +1439,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     for (int base = blockIdx.x * blockDim.x; base < D.n; base += G) ph_contacts(D, ctl, base, sm);
   }
   stamp(D, ts);
+  // split schedule: k_solve_cluster runs the sweeps and the commit (and
+  // resets the barrier words this launch used)
+  if (D.fused_stop) return;
   const Layout L = layout(D, ctl);
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
@@ -1384,7 +1458,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     __shared__ int s_nnb;
     RegContacts RC;
     RC.c = 0;
-    if (ok && t0 < D.n) RC.load(D, t0, L.v[t0]);
+    if (ok && t0 < D.n_own) RC.load(D, t0, L.v[t0]);
     for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
     __syncthreads();
     {
@@ -1427,7 +1501,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
         ok = ok && s_flag == 0;
         stamp(D, ts);
       }
-      if (ok && t0 < D.n) RC.sweep(D, t0, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+      if (ok && t0 < D.n_own) RC.sweep(D, t0, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
       __syncthreads();
       if (threadIdx.x == 0)
         asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(s + 1) : "memory");
@@ -1438,7 +1512,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
       if (ok) {
         const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
         float4* Wout = D.W[s & 1];
-        for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+        for (int k = t0; k < D.n_own; k += G) sweep_particle(D, k, Win, Wout, A);
       }
     }
   }
@@ -1464,7 +1538,47 @@ __global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
     if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
     const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
     float4* Wout = D.W[s & 1];
-    for (int k = t0; k < D.n; k += G) sweep_particle(D, k, Win, Wout, A);
+    for (int k = t0; k < D.n_own; k += G) sweep_particle(D, k, Win, Wout, A);
+  }
+  sweep_acc_flush(D, A, smd);
+  integrate_and_finish(D, ctl, t0, G, smd, &s_last);
+}
+
+// ---------------------------------------------------------------------------
+// Small-n solve on ONE thread-block cluster (16 CTAs x 1024 threads, one CTA
+// per SM): the S Jacobi sweeps are separated by the hardware cluster barrier
+// (barrier.cluster arrive.release / wait.acquire, ~0.2 us, invalidates L1)
+// instead of a grid barrier through L2 atomics (~4 us).  The sweep work of a
+// small bed (tens of thousands of contacts) fits 16 SMs easily; the
+// synchronisation was the cost.  Then integrate + StepReport + commit.
+// ---------------------------------------------------------------------------
+constexpr int kClusterCTAs = 16;
+constexpr int kClusterBlock = 1024;
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kClusterBlock, 1) k_solve_cluster(Dev D) {
+  __shared__ double smd[32];
+  __shared__ int s_last;
+  __shared__ unsigned long long sbm[kSmemBodies * 3];
+  Ctl* ctl = D.ctl;
+  // an error raised by the contact phase (uniform over the cluster: set by an
+  // earlier kernel) skips the sweeps; the finish still runs so the barrier
+  // words of k_step_fused are reset and nothing is committed
+  const bool ok = !block_should_exit(ctl);
+  const Layout L = layout(D, ctl);
+  const int G = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  SweepAcc A;
+  sweep_acc_init(D, A, sbm, t0);
+  for (int s = 0; ok && s < D.S; ++s) {
+    if (s > 0) cluster_barrier();
+    const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+    float4* Wout = D.W[s & 1];
+    for (int k = t0; k < D.n_own; k += G) sweep_particle(D, k, Win, Wout, A);
   }
   sweep_acc_flush(D, A, smd);
   integrate_and_finish(D, ctl, t0, G, smd, &s_last);

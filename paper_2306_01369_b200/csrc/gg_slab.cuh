@@ -1,0 +1,177 @@
+// gg_slab.cuh — slab domain decomposition of one bed over several GPUs
+// (SURVEY.md §8e "single large bed", config 5).  The reference has no
+// multi-GPU path; parity is "same answer as one GPU".
+//
+// The bed is cut along x at cell boundaries (cells are round(x / 2r),
+// broadphase.py:33-41, so every contact partner lies within +-1 cell).  A
+// rank owns the particles whose cell index cx is in [lo, hi) and, each step,
+//   M  migrates owned particles whose cell left [lo, hi) to the neighbour
+//      (|v dt| < 2r: at most one cell per step, so only neighbours),
+//   G  receives the neighbours' boundary-cell particles (cx == lo - 1 and
+//      cx == hi) as ghosts, appended after the owned ones,
+//   H  exchanges the ghosts' predicted velocity w after every Jacobi sweep
+//      (contact.py:470-472 reads w_j of the previous sweep).
+// Ghosts carry their global id as user id, so the stable bucket order, the
+// candidate order and therefore every owned particle's contact sequence are
+// exactly those of the one-GPU run: the slab step is bitwise identical to it.
+//
+// Transfer records: SlabRec = (x.xyz, bits(global id)), (v.xyz, 0).
+#pragma once
+
+#include "gg_kernels.cuh"
+
+namespace gg {
+
+struct SlabRec {
+  float4 x;  // .w = __int_as_float(global id)
+  float4 v;
+};
+
+struct SlabCfg {
+  long long lo, hi;  // owned cell range [lo, hi) along x
+  int has_lo, has_hi;  // a neighbour exists below / above
+};
+
+// M1: pack emigrants (their slot becomes a hole: UID = -1).  cnt[0] lo,
+// cnt[1] hi (atomic slots: the order of the records does not matter — the
+// stable sort orders particles by global id).
+__global__ void k_slab_emigrate(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
+                                SlabRec* __restrict__ send_hi, long long cap,
+                                unsigned long long* __restrict__ cnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n_own) return;
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  const float4 x = D.X[cur][k];
+  const long long cx = cell_coord(x.x, D.two_r);
+  int side = -1;
+  if (C.has_lo && cx < C.lo) side = 0;
+  if (C.has_hi && cx >= C.hi) side = 1;
+  if (side < 0) return;
+  const unsigned long long slot = atomicAdd(cnt + side, 1ull);
+  if (static_cast<long long>(slot) < cap) {
+    SlabRec r;
+    r.x = make_float4(x.x, x.y, x.z, __int_as_float(D.UID[u][k]));
+    r.v = D.V[cur][k];
+    (side ? send_hi : send_lo)[slot] = r;
+  }
+  D.UID[u][k] = -1;
+}
+
+// M2: holes below the new owned count are refilled from the survivors above
+// it (O(migrants) work): list the holes below n_stay and the survivors at or
+// above it; pair them by slot.  cnt[2] holes, cnt[3] movers.
+__global__ void k_slab_holes(Dev D, int n_stay, int* __restrict__ holes, int* __restrict__ movers,
+                             unsigned long long* __restrict__ cnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n_own) return;
+  const int uid = D.UID[D.ctl->ucur][k];
+  if (k < n_stay && uid < 0) holes[atomicAdd(cnt + 2, 1ull)] = k;
+  if (k >= n_stay && uid >= 0) movers[atomicAdd(cnt + 3, 1ull)] = k;
+}
+
+__global__ void k_slab_fill(Dev D, const int* __restrict__ holes, const int* __restrict__ movers,
+                            int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  const int h = holes[i], s = movers[i];
+  D.X[cur][h] = D.X[cur][s];
+  D.V[cur][h] = D.V[cur][s];
+  D.UID[u][h] = D.UID[u][s];
+}
+
+// Append records at [at, at + m): immigrants (owned) or ghosts.
+__global__ void k_slab_append(Dev D, const SlabRec* __restrict__ in, int m, int at) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  const SlabRec r = in[i];
+  D.X[cur][at + i] = make_float4(r.x.x, r.x.y, r.x.z, 0.f);
+  D.V[cur][at + i] = make_float4(r.v.x, r.v.y, r.v.z, 0.f);
+  D.UID[u][at + i] = __float_as_int(r.x.w);
+}
+
+// G1: the owned particles in the boundary cells, packed for the neighbours;
+// map_* keeps their physical index for the per-sweep halo (no re-sort
+// happens inside a slab step, so the map stays valid for the whole step).
+__global__ void k_slab_ghosts(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
+                              SlabRec* __restrict__ send_hi, int* __restrict__ map_lo,
+                              int* __restrict__ map_hi, long long cap,
+                              unsigned long long* __restrict__ cnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n_own) return;
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  const float4 x = D.X[cur][k];
+  const long long cx = cell_coord(x.x, D.two_r);
+  const bool to_lo = C.has_lo && cx == C.lo;
+  const bool to_hi = C.has_hi && cx == C.hi - 1;
+  if (!to_lo && !to_hi) return;
+  SlabRec r;
+  r.x = make_float4(x.x, x.y, x.z, __int_as_float(D.UID[u][k]));
+  r.v = D.V[cur][k];
+  if (to_lo) {
+    const unsigned long long s = atomicAdd(cnt + 0, 1ull);
+    if (static_cast<long long>(s) < cap) {
+      send_lo[s] = r;
+      map_lo[s] = k;
+    }
+  }
+  if (to_hi) {
+    const unsigned long long s = atomicAdd(cnt + 1, 1ull);
+    if (static_cast<long long>(s) < cap) {
+      send_hi[s] = r;
+      map_hi[s] = k;
+    }
+  }
+}
+
+// H: w of sweep s for the mapped boundary particles -> out; in -> ghosts.
+__global__ void k_slab_halo_pack(Dev D, int s, const int* __restrict__ map, int m,
+                                 float4* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = D.W[s & 1][map[i]];
+}
+
+__global__ void k_slab_halo_unpack(Dev D, int s, const float4* __restrict__ in, int m, int at) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) D.W[s & 1][at + i] = in[i];
+}
+
+// start[E * n_h] = n for the current particle count (n varies per step)
+__global__ void k_slab_set_n(Dev D) { D.start[D.nh_tot] = static_cast<uint32_t>(D.n); }
+
+// copy a Morton-re-sorted owned set (Xs, V0, UID[u^1]) back to the committed buffers
+__global__ void k_slab_commit_sorted(Dev D) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n) return;
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  D.X[cur][k] = D.Xs[k];
+  D.V[cur][k] = D.V0[k];
+  D.UID[u][k] = D.UID[u ^ 1][k];
+}
+
+// owned state in physical order (f64 rows + global ids)
+__global__ void k_slab_store(Dev D, double* __restrict__ x, double* __restrict__ v,
+                             int* __restrict__ gid) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n_own) return;
+  const int cur = D.ctl->cur;
+  const float4 p = D.X[cur][k], q = D.V[cur][k];
+  x[3 * k] = p.x; x[3 * k + 1] = p.y; x[3 * k + 2] = p.z;
+  v[3 * k] = q.x; v[3 * k + 1] = q.y; v[3 * k + 2] = q.z;
+  gid[k] = D.UID[D.ctl->ucur][k];
+}
+
+__global__ void k_slab_load(Dev D, const double* __restrict__ x, const double* __restrict__ v,
+                            const int* __restrict__ gid) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n_own) return;
+  const int cur = D.ctl->cur;
+  D.X[cur][k] = make_float4(static_cast<float>(x[3 * k]), static_cast<float>(x[3 * k + 1]),
+                            static_cast<float>(x[3 * k + 2]), 0.f);
+  D.V[cur][k] = make_float4(static_cast<float>(v[3 * k]), static_cast<float>(v[3 * k + 1]),
+                            static_cast<float>(v[3 * k + 2]), 0.f);
+  D.UID[D.ctl->ucur][k] = gid[k];
+}
+
+}  // namespace gg

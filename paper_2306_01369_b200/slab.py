@@ -1,0 +1,356 @@
+"""One bed over several GPUs: slab domain decomposition.
+
+The reference runs a scene on one CPU core and has no multi-GPU path
+(PAPER.md:524-526); the contract is "same answer as one GPU".  ``SlabBed``
+cuts the bed along x at cell boundaries (cell = round(x / 2r),
+broadphase.py:33-41) into one slab per rank (one process per GPU).  Each
+step a rank
+  1. migrates particles whose cell left its slab to the neighbour,
+  2. receives the neighbours' boundary-cell particles as ghosts,
+  3. runs the step kernels on owned + ghost particles (ghosts are candidates
+     only), exchanging the ghosts' predicted velocity after every Jacobi sweep,
+  4. reduces the StepReport over ranks.
+Ghosts carry their global id, which the device uses as the stable-sort tie
+key, so every owned particle sees the same candidates in the same order as
+on one GPU: states are bitwise identical to the one-GPU run
+(tests/test_slab.py).  The library only packs and unpacks device buffers
+(gg_slab_* in include/granusim_b200.h); this module moves them with
+torch.distributed point-to-point operations — NCCL on device buffers over
+NVLink in production, or gloo staged through host memory (tests, and several
+ranks sharing one GPU).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native as N
+from .engine import _params_struct, default_table_size
+from .stepper import StepReport
+
+REC_FLOATS = 8    # particle record: (x, y, z, bits(gid)), (vx, vy, vz, 0)
+HALO_FLOATS = 4   # halo record: w (float4)
+
+
+def cell_x(x: np.ndarray, radius: float) -> np.ndarray:
+    """round_half_away(x / 2r) along x (broadphase.py:33-41), float64."""
+    q = np.asarray(x, dtype=np.float64) / (2.0 * radius)
+    return (np.copysign(np.floor(np.abs(q) + 0.5), q)).astype(np.int64)
+
+
+def slab_cuts(cx: np.ndarray, world: int) -> np.ndarray:
+    """Cell cuts c_1 < ... < c_{world-1} splitting the particles into slabs of
+    about equal count (rank r owns cells [c_r, c_{r+1}), c_0 = -inf,
+    c_world = +inf).  Each slab keeps at least two cells so a particle never
+    crosses more than one boundary in a step."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if world == 1:
+        return np.zeros(0, dtype=np.int64)
+    cs = np.sort(np.asarray(cx, dtype=np.int64))
+    lo, hi = int(cs[0]), int(cs[-1]) + 1
+    if hi - lo < 2 * world:
+        raise ValueError(f"bed is {hi - lo} cells wide: too narrow for {world} slabs")
+    cuts = []
+    prev = lo
+    for r in range(1, world):
+        c = int(cs[min(len(cs) - 1, (r * len(cs)) // world)])
+        c = max(c, prev + 2)
+        c = min(c, hi - 2 * (world - r))
+        cuts.append(c)
+        prev = c
+    return np.array(cuts, dtype=np.int64)
+
+
+def slab_bounds(cuts: np.ndarray, rank: int):
+    """(lo, hi, has_lo, has_hi) of rank's slab."""
+    world = len(cuts) + 1
+    has_lo = rank > 0
+    has_hi = rank < world - 1
+    lo = int(cuts[rank - 1]) if has_lo else 0
+    hi = int(cuts[rank]) if has_hi else 0
+    return lo, hi, has_lo, has_hi
+
+
+def owner_of(cx: np.ndarray, cuts: np.ndarray) -> np.ndarray:
+    """Rank owning each cell index."""
+    return np.searchsorted(cuts, cx, side="right")
+
+
+# ---------------------------------------------------------------------------
+class SlabTransport:
+    """Neighbour exchange of slab buffers with torch.distributed P2P ops.
+
+    backend "nccl": the buffers are device tensors and the operations are
+    ordered on the context stream (torch ExternalStream); "gloo": buffers are
+    staged through host memory.  world == 1 needs no process group."""
+
+    def __init__(self, rank: int, world: int, device: int, stream_ptr: int | None,
+                 backend: str | None = None):
+        self.rank, self.world, self.device = rank, world, device
+        self.lo = rank - 1 if rank > 0 else None
+        self.hi = rank + 1 if rank < world - 1 else None
+        import torch
+
+        self.torch = torch
+        self.dist = None
+        if world > 1:
+            import torch.distributed as td
+
+            if not td.is_initialized():
+                raise RuntimeError("SlabTransport: torch.distributed is not initialised")
+            self.dist = td
+            backend = backend or td.get_backend()
+        self.backend = backend or "gloo"
+        self.on_device = self.backend == "nccl"
+        self.dev = torch.device("cuda", device) if torch.cuda.is_available() else torch.device("cpu")
+        self.stream = (torch.cuda.ExternalStream(stream_ptr, device=self.dev)
+                       if (stream_ptr and torch.cuda.is_available()) else None)
+
+    def empty(self, n: int, width: int):
+        """A device buffer of n records (float32 x width)."""
+        return self.torch.empty((max(n, 1), width), dtype=self.torch.float32, device=self.dev)
+
+    def _ctx(self):
+        import contextlib
+
+        return self.torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
+
+    def _p2p(self, sends, recvs):
+        """sends/recvs: lists of (peer, tensor); all posted together."""
+        td = self.dist
+        ops = [td.P2POp(td.isend, t, p) for p, t in sends] + [td.P2POp(td.irecv, t, p) for p, t in recvs]
+        if not ops:
+            return
+        for r in td.batch_isend_irecv(ops):
+            r.wait()
+
+    def counts(self, c_lo: int, c_hi: int) -> tuple[int, int]:
+        """Send my counts to (lo, hi); return the counts they send me."""
+        if self.world == 1:
+            return 0, 0
+        torch = self.torch
+        dev = self.dev if self.on_device else torch.device("cpu")
+        out_lo = torch.tensor([c_lo], dtype=torch.int64, device=dev)
+        out_hi = torch.tensor([c_hi], dtype=torch.int64, device=dev)
+        in_lo = torch.zeros(1, dtype=torch.int64, device=dev)
+        in_hi = torch.zeros(1, dtype=torch.int64, device=dev)
+        sends, recvs = [], []
+        if self.lo is not None:
+            sends.append((self.lo, out_lo))
+            recvs.append((self.lo, in_lo))
+        if self.hi is not None:
+            sends.append((self.hi, out_hi))
+            recvs.append((self.hi, in_hi))
+        with self._ctx():
+            self._p2p(sends, recvs)
+        return int(in_lo.item()), int(in_hi.item())
+
+    def exchange(self, send_lo, n_lo: int, send_hi, n_hi: int, recv_lo, m_lo: int, recv_hi, m_hi: int):
+        """Send send_*[:n_*] to the neighbours and receive m_* records into recv_*."""
+        if self.world == 1:
+            return
+        torch = self.torch
+        with self._ctx():
+            sends, recvs, back = [], [], []
+            for peer, buf, n in ((self.lo, send_lo, n_lo), (self.hi, send_hi, n_hi)):
+                if peer is None or n == 0:
+                    continue
+                t = buf[:n]
+                sends.append((peer, t if self.on_device else t.cpu()))
+            for peer, buf, m in ((self.lo, recv_lo, m_lo), (self.hi, recv_hi, m_hi)):
+                if peer is None or m == 0:
+                    continue
+                if self.on_device:
+                    recvs.append((peer, buf[:m]))
+                else:
+                    h = torch.empty((m, buf.shape[1]), dtype=buf.dtype)
+                    recvs.append((peer, h))
+                    back.append((buf, h, m))
+            self._p2p(sends, recvs)
+            for buf, h, m in back:
+                buf[:m].copy_(h)
+
+    def allreduce(self, vals: np.ndarray, op: str) -> np.ndarray:
+        if self.world == 1:
+            return vals
+        torch = self.torch
+        dev = self.dev if self.on_device else torch.device("cpu")
+        t = torch.tensor(np.asarray(vals, dtype=np.float64), device=dev)
+        rop = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX,
+               "min": self.dist.ReduceOp.MIN}[op]
+        self.dist.all_reduce(t, op=rop)
+        return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+class SlabBed:
+    """Rank ``rank``'s slab of ``scene`` (every rank passes the same scene)."""
+
+    def __init__(self, scene, rank: int = 0, world: int = 1, device: int = 0,
+                 backend: str | None = None, cuts: np.ndarray | None = None,
+                 capacity: float = 1.6, max_contacts: int = 16, resort_every: int = 8):
+        from .engine import Engine
+
+        self.scene = scene
+        self.rank, self.world = rank, world
+        self.params = scene.params
+        r = float(self.params.radius)
+        x = np.asarray(scene.particles.positions, dtype=np.float64)
+        v = np.asarray(scene.particles.velocities, dtype=np.float64)
+        self.N = len(x)
+        self.n_h = int(scene.hashmap_size or default_table_size(self.N))  # GLOBAL table
+        cx = cell_x(x.astype(np.float32).astype(np.float64)[:, 0], r)
+        self.cuts = slab_cuts(cx, world) if cuts is None else np.asarray(cuts, dtype=np.int64)
+        lo, hi, has_lo, has_hi = slab_bounds(self.cuts, rank)
+        mine = np.nonzero(owner_of(cx, self.cuts) == rank)[0]
+        self.nb = len(scene.bodies)
+        self.cap = int(math.ceil(capacity * max(len(mine), 1) + 4096))
+        self.resort_every = resort_every
+        self.steps = 0
+        self.migrated = 0  # particles this rank sent to its neighbours
+        # context: capacity = owned + ghosts + immigrants
+        self.engine = Engine(device)
+        self.engine.max_contacts = max_contacts
+        self.engine._create(self.params, scene.boundary, self.cap, self.n_h, max(self.nb, 1))
+        self.ctx = self.engine.ctx
+        lib = N.lib()
+        N.check(self.ctx, lib.gg_slab_setup(self.ctx, lo, hi, int(has_lo), int(has_hi)), "slab setup")
+        gid = mine.astype(np.int32)
+        xs = np.ascontiguousarray(x[mine])
+        vs = np.ascontiguousarray(v[mine])
+        N.check(self.ctx, lib.gg_slab_load(self.ctx, N.ptr(xs), N.ptr(vs), N.ptr(gid), len(mine)),
+                "slab load")
+        self.tr = SlabTransport(rank, world, device, lib.gg_stream(self.ctx), backend)
+        self.buf_cap = max(4096, self.cap // 2)
+        self._alloc()
+
+    def _alloc(self):
+        e = self.tr.empty
+        c = self.buf_cap
+        self.s_lo, self.s_hi = e(c, REC_FLOATS), e(c, REC_FLOATS)
+        self.r_lo, self.r_hi = e(c, REC_FLOATS), e(c, REC_FLOATS)
+        self.h_slo, self.h_shi = e(c, HALO_FLOATS), e(c, HALO_FLOATS)
+        self.h_rlo, self.h_rhi = e(c, HALO_FLOATS), e(c, HALO_FLOATS)
+
+    @staticmethod
+    def _p(t) -> int:
+        return t.data_ptr()
+
+    def close(self):
+        self.engine.close()
+
+    @property
+    def n_owned(self) -> int:
+        return int(N.lib().gg_slab_owned(self.ctx))
+
+    # -- one step ------------------------------------------------------------
+    def _swap(self, pack, unpack, send, recv):
+        """pack -> exchange counts and records -> unpack; returns
+        ((sent lo, sent hi), (received lo, received hi))."""
+        cnt = np.zeros(2, dtype=np.int64)
+        N.check(self.ctx, pack(self.ctx, self._p(send[0]), self._p(send[1]), self.buf_cap, N.ptr(cnt)),
+                "slab pack")
+        m_lo, m_hi = self.tr.counts(int(cnt[0]), int(cnt[1]))
+        if max(m_lo, m_hi) > self.buf_cap:
+            raise RuntimeError("slab receive buffer too small")
+        self.tr.exchange(send[0], int(cnt[0]), send[1], int(cnt[1]), recv[0], m_lo, recv[1], m_hi)
+        N.check(self.ctx, unpack(self.ctx, self._p(recv[0]), m_lo, self._p(recv[1]), m_hi), "slab unpack")
+        return (int(cnt[0]), int(cnt[1])), (m_lo, m_hi)
+
+    def step(self) -> StepReport:
+        lib = N.lib()
+        sc = self.scene
+        # body poses at t + dt (stepper.py:65-67), identical on every rank
+        t = sc.t + sc.params.timestep
+        row = np.zeros(max(self.nb, 1), dtype=N.BODY_DTYPE)
+        for b, body in enumerate(sc.bodies):
+            body.update(t)
+            self.engine.body_row(body, float(sc.params.radius), row[b])
+        sc.t = t
+        # 1. migration, 2. (re-sort) + ghosts
+        sent, _ = self._swap(lib.gg_slab_migrate_pack, lib.gg_slab_migrate_unpack,
+                             (self.s_lo, self.s_hi), (self.r_lo, self.r_hi))
+        self.migrated += sent[0] + sent[1]
+        if self.steps % self.resort_every == 0:
+            N.check(self.ctx, lib.gg_slab_resort(self.ctx), "slab resort")
+        n_out, (g_lo, g_hi) = self._swap(lib.gg_slab_ghost_pack, lib.gg_slab_ghost_unpack,
+                                         (self.s_lo, self.s_hi), (self.r_lo, self.r_hi))
+        self.ghosts = (g_lo, g_hi)
+        # 3. step with per-sweep halo exchange of w
+        N.check(self.ctx, lib.gg_slab_detect(self.ctx, N.ptr(row), self.nb), "slab detect")
+        S = int(self.params.solver_iterations)
+        for s in range(S):
+            N.check(self.ctx, lib.gg_slab_sweep(self.ctx, s), "slab sweep")
+            if s < S - 1 and self.world > 1:
+                N.check(self.ctx, lib.gg_slab_halo_pack(self.ctx, s, self._p(self.h_slo),
+                                                        self._p(self.h_shi)), "halo pack")
+                self.tr.exchange(self.h_slo, n_out[0], self.h_shi, n_out[1], self.h_rlo, g_lo,
+                                 self.h_rhi, g_hi)
+                N.check(self.ctx, lib.gg_slab_halo_unpack(self.ctx, s, self._p(self.h_rlo),
+                                                          self._p(self.h_rhi)), "halo unpack")
+        rep = np.zeros(1, dtype=N.REPORT_DTYPE)
+        bm = np.zeros((max(self.nb, 1), 3))
+        st = lib.gg_slab_finish(self.ctx, N.ptr(rep), N.ptr(bm))
+        if st != N.GG_OK:
+            from .engine import raise_status
+
+            raise_status(st, N.last_error(self.ctx), self.steps)
+        self.steps += 1
+        return self._reduce(rep[0], bm[: self.nb])
+
+    def _reduce(self, r, bm) -> StepReport:
+        tr = self.tr
+        s = tr.allreduce(np.array([r["n_contacts"], r["n_candidates"], r["n_body_contacts"],
+                                   r["n_coincident"], r["n_degenerate"], r["kinetic_energy"]],
+                                  dtype=np.float64), "sum")
+        mx = tr.allreduce(np.array([r["max_penetration"], r["max_cone_violation"]]), "max")
+        mn = tr.allreduce(np.array([r["min_normal_impulse"]]), "min")
+        bms = tr.allreduce(np.asarray(bm, dtype=np.float64).reshape(-1), "sum").reshape(-1, 3)
+        n_pp, n_cand = int(s[0]), int(s[1])
+        m = float(mn[0])
+        return StepReport(n_contacts=n_pp, n_candidates=n_cand,
+                          candidate_hit_rate=n_pp / max(n_cand, 1),
+                          max_penetration=float(mx[0]), kinetic_energy=float(s[5]),
+                          n_body_contacts=int(s[2]), n_coincident_skipped=int(s[3]),
+                          n_degenerate_skipped=int(s[4]), max_cone_violation=float(mx[1]),
+                          min_normal_impulse=m if np.isfinite(m) else 0.0,
+                          body_momentum=bms, step_index=self.steps - 1)
+
+    def run(self, n_steps: int) -> list[StepReport]:
+        return [self.step() for _ in range(n_steps)]
+
+    # -- state -----------------------------------------------------------------
+    def owned_state(self):
+        """(x, v, gid) of this rank's particles (physical order)."""
+        lib = N.lib()
+        n = self.n_owned
+        x = np.zeros((max(n, 1), 3))
+        v = np.zeros((max(n, 1), 3))
+        gid = np.zeros(max(n, 1), dtype=np.int32)
+        got = ctypes.c_int64(0)
+        N.check(self.ctx, lib.gg_slab_get(self.ctx, N.ptr(x), N.ptr(v), N.ptr(gid), len(gid),
+                                          ctypes.byref(got)), "slab get")
+        n = got.value
+        return x[:n], v[:n], gid[:n]
+
+    def gather(self):
+        """Global (x, v) in particle-id order, assembled on every rank."""
+        x, v, gid = self.owned_state()
+        if self.world == 1:
+            X = np.zeros((self.N, 3))
+            V = np.zeros((self.N, 3))
+            X[gid], V[gid] = x, v
+            return X, V
+        import torch.distributed as td
+
+        parts = [None] * self.world
+        td.all_gather_object(parts, (x, v, gid))
+        X = np.zeros((self.N, 3))
+        V = np.zeros((self.N, 3))
+        for px, pv, pg in parts:
+            X[pg], V[pg] = px, pv
+        return X, V

@@ -37,6 +37,17 @@ __global__ void k_barriers(int iters) {
   }
 }
 
+// hardware cluster barrier: 16 CTAs of 1024 threads (or 8), iters barriers
+__global__ void k_cluster_barriers(int iters, int* out) {
+  int acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    acc += i;
+  }
+  if (acc == -1) *out = acc;
+}
+
 __global__ void k_chain(const int* __restrict__ next, int steps, int* out) {
   int p = threadIdx.x + blockIdx.x * blockDim.x;
   for (int i = 0; i < steps; ++i) p = next[p];
@@ -80,6 +91,34 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       printf("grid %d barrier variant %d: %.2f us per barrier (%s)\n", grid, var, ms * 1000 / iters,
              cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // 2b. cluster barriers
+  for (int cs : {8, 16}) {
+    for (int bs : {256, 1024}) {
+      cudaFuncSetAttribute(k_cluster_barriers, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(bs);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int* o = nullptr;
+      cudaMalloc(&o, 4);
+      cudaLaunchKernelEx(&cfg, k_cluster_barriers, 10, o);
+      cudaEventRecord(a, s);
+      cudaLaunchKernelEx(&cfg, k_cluster_barriers, iters, o);
+      cudaEventRecord(b, s);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+      printf("cluster %d x %d threads: %.3f us per cluster barrier (%s)\n", cs, bs, ms * 1000 / iters,
+             cudaGetErrorString(cudaGetLastError()));
+      cudaFree(o);
     }
   }
   // 3. dependent load chain: random permutation over 64 MB (L2-resident) and 1 GB
