@@ -233,7 +233,8 @@ int begin_batch(gg_ctx* ctx, cudaStream_t s) {
 }
 
 bool use_fused_step(const gg_ctx* ctx) {
-  if (ctx->solve_mode == 4 || ctx->solve_mode == 5 || ctx->solve_mode == 6) return true;
+  if (ctx->solve_mode == 4 || ctx->solve_mode == 5 || ctx->solve_mode == 6 || ctx->solve_mode == 7)
+    return true;
   if (ctx->solve_mode != 0) return false;
   return ctx->n <= static_cast<long long>(ctx->fused_grid) * kBlock;
 }
@@ -293,7 +294,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
     CK(cudaGetLastError());
     return GG_OK;
   }
-  return launch_coop(ctx, k_solve, ctx->solve_grid, D, s, ctx->solve_mode != 2);
+  return launch_coop(ctx, k_solve, ctx->solve_grid, D, s, ctx->solve_mode != 2);  // modes 1, 2
 }
 
 int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
@@ -317,6 +318,7 @@ Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
   D.resort = resort;
   D.key_morton = morton;
   D.fused_stop = 0;
+  D.sweep_barrier = (ctx->solve_mode == 7 || ctx->solve_mode == 0) ? 1 : 0;
   return D;
 }
 
@@ -683,7 +685,7 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
 int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
 
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode) {
-  if (!ctx || mode < 0 || mode > 6) return fail(ctx, GG_EINVAL, "solve mode must be 0..6");
+  if (!ctx || mode < 0 || mode > 7) return fail(ctx, GG_EINVAL, "solve mode must be 0..7");
   ctx->solve_mode = mode;
   ctx->graph_dirty = true;
   return GG_OK;

@@ -47,16 +47,16 @@ constexpr int kMaxFusedBlocks = 1024;  // neighbour-flag sweeps: block-set bitma
 struct Ctl {
   int cur;         // committed state buffer
   int ucur;        // committed uid buffer
-  int step;        // steps committed in this batch
+  // bar_count and err share one aligned 8-byte word: the grid barrier's
+  // final 64-bit acquire load returns the error flag with the arrival count
+  unsigned bar_count;  // grid barrier arrivals (monotonic within a launch, reset per launch)
   int err;         // first error code (0 = none)
+  int step;        // steps committed in this batch
   int err_step;    // batch-relative step of the error
   int cap_needed;  // largest per-owner contact count seen (capacity hint)
   int n_bad;       // non-finite particles recorded
-  int pad;
-  unsigned bar_count;  // grid barrier arrivals (monotonic within a launch, reset per launch)
   unsigned done_count; // last-block-done counter of the solve kernel
-  unsigned bar_gen;    // last completed barrier target (reset with bar_count)
-  unsigned pad2;
+  unsigned bar_gen;    // (unused; reset with bar_count)
   unsigned long long ccursor;  // contact records allocated this step (warp allocator)
   int bad_uid[kMaxBad];
 };
@@ -77,6 +77,7 @@ struct Dev {
   int n, K, nb, S, nblocks;
   int resort;     // this graph re-sorts the physical order first
   int fused_stop; // k_step_fused ends after the contacts (the cluster kernel solves)
+  int sweep_barrier;  // fused sweeps: 1 grid barrier per sweep, 0 neighbour-block flags
   int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
   // Independent environments (segments).  E == 1 is a single bed.  With
   // E > 1 env e owns particles [e*ne, (e+1)*ne) of the physical order and
@@ -269,28 +270,33 @@ __device__ __forceinline__ bool block_should_exit(const Ctl* ctl) {
 
 // Grid-wide barrier for the cooperative kernel (all blocks co-resident).
 // One release-add per block on a counter that only grows during a launch
-// (zeroed by a memset node before the launch); blocks wait with acquire loads
-// until it reaches the barrier's target (nblocks x barrier ordinal).
-__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned target) {
+// (zeroed before the launch); thread 0 polls the counter itself with acquire
+// loads until it reaches the barrier's target (nblocks x barrier ordinal).
+// The acquire load is LD.STRONG.GPU + CCTL.IVALL: it also invalidates this
+// SM's L1, so no block reads a line cached before other SMs rewrote it.
+// (Measured on B200, 148-296 blocks: 1.1 us per barrier; a separate
+// generation word 1.8 us, plus a __threadfence 2.0 us — tools/microbench_sync.cu.)
+// Returns ctl->err as seen after the barrier (every error is raised before
+// its block arrives, i.e. before a release the final acquire synchronises
+// with, and err is read by the same 64-bit load at the L2).
+__device__ __forceinline__ int grid_barrier(Ctl* ctl, unsigned target) {
+  __shared__ int s_err;
   __syncthreads();
   if (threadIdx.x == 0) {
-    // arrive on the counter; the last arriver publishes the barrier ordinal
-    // on a separate generation word, which is all the waiters poll (they
-    // never contend with the arrival atomics)
     unsigned v;
+    unsigned long long w;
     asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
-    if (v + 1 == target) {
-      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&ctl->bar_gen), "r"(target) : "memory");
-    } else {
-      do {
-        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&ctl->bar_gen) : "memory");
-      } while (static_cast<int>(v - target) < 0);
-    }
-    // gpu-scope fence: invalidates this SM's L1 (CCTL.IVALL) so no block
-    // reads a line cached before other SMs rewrote it in the previous phase
-    __threadfence();
+    v += 1;
+    // spin with relaxed (L1-bypassing) loads, then ONE acquire load: the
+    // L1 invalidation happens once, not on every poll (an invalidation per
+    // poll also evicts the lines the other block on this SM is working on)
+    while (static_cast<int>(v - target) < 0)
+      asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
+    asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(w) : "l"(&ctl->bar_count) : "memory");
+    s_err = static_cast<int>(w >> 32);
   }
   __syncthreads();
+  return s_err;
 }
 
 // the layout the step works on: re-sorted this step, or the committed one
@@ -1076,12 +1082,29 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
   const float4 wf = Win[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  for (int sl = 0; sl < ci.y; ++sl) {
-    const long long idx = static_cast<long long>(ci.x) + sl;
-    const float4 g = D.cgeo[idx];
-    const int j = D.coth[idx];
-    const float4 q = (j >= 0) ? Win[j] : D.cvb[idx];
-    contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
+  // contacts in batches of kSweepBatch: all record loads, then all partner
+  // gathers, then the impulses (in record order) — two dependent round trips
+  // per batch instead of two per contact
+  constexpr int kSweepBatch = 1;
+  for (int s0 = 0; s0 < ci.y; s0 += kSweepBatch) {
+    float4 g[kSweepBatch], q[kSweepBatch];
+    int j[kSweepBatch];
+#pragma unroll
+    for (int u = 0; u < kSweepBatch; ++u) {
+      if (s0 + u < ci.y) {
+        const long long idx = static_cast<long long>(ci.x) + s0 + u;
+        g[u] = D.cgeo[idx];
+        j[u] = D.coth[idx];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSweepBatch; ++u) {
+      if (s0 + u < ci.y)
+        q[u] = (j[u] >= 0) ? Win[j[u]] : D.cvb[static_cast<long long>(ci.x) + s0 + u];
+    }
+#pragma unroll
+    for (int u = 0; u < kSweepBatch; ++u)
+      if (s0 + u < ci.y) contact_impulse(D, wx, wy, wz, g[u], j[u], q[u], ax, ay, az, A);
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
                         static_cast<float>(wz + az), 0.f);
@@ -1383,11 +1406,9 @@ __device__ __forceinline__ void stamp(const Dev& D, int& idx) {
 __device__ __forceinline__ bool barrier_ok(const Dev& D, Ctl* ctl, unsigned& target, int* s_flag,
                                            int& ts) {
   target += gridDim.x;
-  grid_barrier(ctl, target);
-  if (threadIdx.x == 0) *s_flag = *((volatile int*)&ctl->err);
-  __syncthreads();
+  const int err = grid_barrier(ctl, target);
   stamp(D, ts);
-  return *s_flag == 0;
+  return err == 0;
 }
 
 __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
@@ -1486,15 +1507,17 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     __syncthreads();
     unsigned* flags = D.bflags;
     for (int s = 0; s < D.S; ++s) {
-      if (s > 0) {
+      if (s > 0 && D.sweep_barrier) {
+        ok = barrier_ok(D, ctl, target, &s_flag, ts) && ok;
+      } else if (s > 0) {
         for (int q = threadIdx.x; q < s_nnb; q += blockDim.x) {
           unsigned v;
           do {
-            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flags + s_nblist[q]) : "memory");
+            asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flags + s_nblist[q]) : "memory");
           } while (static_cast<int>(v - static_cast<unsigned>(s)) < 0);
+          asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flags + s_nblist[q]) : "memory");
         }
-        __syncthreads();
-        if (threadIdx.x == 0) __threadfence();  // invalidate stale L1 lines (CCTL.IVALL)
+        // (the acquire loads above invalidated this SM's L1: CCTL.IVALL)
         __syncthreads();
         if (threadIdx.x == 0) s_flag = *((volatile int*)&ctl->err);
         __syncthreads();
@@ -1502,9 +1525,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
         stamp(D, ts);
       }
       if (ok && t0 < D.n_own) RC.sweep(D, t0, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
-      __syncthreads();
-      if (threadIdx.x == 0)
-        asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(s + 1) : "memory");
+      if (!D.sweep_barrier) {
+        __syncthreads();
+        if (threadIdx.x == 0)
+          asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(s + 1) : "memory");
+      }
     }
   } else {
     for (int s = 0; s < D.S; ++s) {

@@ -22,6 +22,11 @@ __global__ void k_barriers(int iters) {
         v += 1;
         while ((int)(v - target) < 0)
           asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&g_count) : "memory");
+      } else if (kVariant == 3) {  // relaxed polls, one acquire
+        v += 1;
+        while ((int)(v - target) < 0)
+          asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&g_count) : "memory");
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&g_count) : "memory");
       } else {  // generation word
         if (v + 1 == target) {
           asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&g_gen), "r"(target) : "memory");
@@ -80,12 +85,13 @@ int main() {
   // 2. barriers
   const int iters = 1000;
   for (int grid : {148, 196, 296}) {
-    for (int var = 0; var < 3; ++var) {
+    for (int var = 0; var < 4; ++var) {
       k_reset<<<1, 1, 0, s>>>();
       cudaEventRecord(a, s);
       if (var == 0) k_barriers<0><<<grid, 256, 0, s>>>(iters);
       if (var == 1) k_barriers<1><<<grid, 256, 0, s>>>(iters);
       if (var == 2) k_barriers<2><<<grid, 256, 0, s>>>(iters);
+      if (var == 3) k_barriers<3><<<grid, 256, 0, s>>>(iters);
       cudaEventRecord(b, s);
       cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms, a, b);

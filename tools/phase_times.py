@@ -16,7 +16,7 @@ sc, desc = bench.make_scene(A)
 eng = engine_for(sc)
 eng.prepare(sc)
 lib = N.lib()
-lib.gg_set_solve_mode(eng.ctx, 4)
+lib.gg_set_solve_mode(eng.ctx, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 lib.gg_phase_timer(eng.ctx, 1, None, 0)
 nb = len(sc.bodies)
 for resort in (False, True):
