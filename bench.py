@@ -528,6 +528,29 @@ def run_envs(args, dist: Dist):
     env.close()
 
 
+def lattice_cpu_baseline(n_sample: int, budget_s: float, note: str) -> dict:
+    """Reference algorithm (oracle port) on a lattice bed of n_sample
+    particles with a floor, 1 host core, bounded by budget_s."""
+    import paper_2306_01369_b200 as gg
+    from oracle import granular_oracle as O
+
+    x = gg.lattice_bed(n_sample).astype(np.float32).astype(np.float64)
+    v = np.zeros_like(x)
+    params = gg.MaterialParams(timestep=5e-4)
+    floor = _BodyAt(gg.HalfSpace(), np.eye(4), np.zeros(3), np.zeros(3))
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        x, v, _, _, _ = O.step(x, v, params, [floor], O.table_size(n_sample))
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= 200:
+            break
+    return {"value": n_sample * steps / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{steps} oracle steps of lattice_bed({n_sample}) + floor from the lattice "
+                      f"start, {el:.1f}s, numpy single thread; {note}"}
+
+
 def run_slab(args, dist: Dist):
     import paper_2306_01369_b200 as gg
     from paper_2306_01369_b200 import _native as N
@@ -561,6 +584,7 @@ def run_slab(args, dist: Dist):
     torch.cuda.synchronize(dev)
     dist.barrier()
     clk = clocks.stop()
+    launches = int(lib.gg_kernel_launches(bed.ctx)) - l0
     t_ms = dist.max(float(e0.elapsed_time(e1)))
     value = n * K / (t_ms / 1000.0)
     c_pp = float(np.mean([r.n_contacts for r in reps])) / n
@@ -575,6 +599,30 @@ def run_slab(args, dist: Dist):
                 "step_bytes_per_particle": model["step_per_particle"],
                 "note": "whole-step byte model per GPU (SURVEY.md §8d); per-kernel fractions "
                         "are those of bed1m/envs (same kernels)"}
+    bed.close()
+    # e2e through the public API from host buffers: partition + upload
+    # (SlabBed), K steps, gather of the global state back to the host
+    dist.barrier()
+    t0 = time.perf_counter()
+    sc2 = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
+                   bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
+                   params=gg.MaterialParams(timestep=5e-4))
+    bed2 = SlabBed(sc2, rank=dist.rank, world=dist.world, device=dev,
+                   backend="nccl" if dist.world > 1 else None)
+    for _ in range(K):
+        bed2.step()
+    Xg, _ = bed2.gather()
+    _ = float(Xg[0, 0])
+    t_e2e = dist.max(time.perf_counter() - t0)
+    bed2.close()
+    e2e = {"value": n * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 48 * n / max(K, 1),
+           "d2h_bytes_per_step": 52 * n / max(K, 1), "wall_s": t_e2e,
+           "api": "SlabBed(scene) (partition + upload of the host state), K x SlabBed.step(), "
+                  "SlabBed.gather() (global state back on the host)"}
+    cb = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cb = lattice_cpu_baseline(100_000, args.cpu_seconds,
+                                  "the oracle is O(n): particle-steps/s carries over to 8M")
     if dist.rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
                 "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True,
@@ -585,14 +633,9 @@ def run_slab(args, dist: Dist):
                            "solver_iterations": 10, "parallelism": f"slabs x{dist.world}",
                            "n_h": bed.n_h, "c_pp": c_pp, "c_b": c_b, "max_owned": owned,
                            "l2": "state (>1 GB) exceeds L2"},
-                "roofline": roofline, "cpu_baseline": None,
-                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 240,
-                        "d2h_bytes_per_step": 72,
-                        "api": "SlabBed.step(): the public slab API (host orchestrated; the "
-                               "state stays resident)"},
-                "clocks": clk, "gpu_launches": int(lib.gg_kernel_launches(bed.ctx)) - l0}
+                "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "clocks": clk, "gpu_launches": launches}
         print(json.dumps(line), flush=True)
-    bed.close()
 
 
 def run_ours(args, dist: Dist):

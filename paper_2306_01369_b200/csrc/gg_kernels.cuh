@@ -578,11 +578,13 @@ __device__ __forceinline__ double pp_d2(double px, double py, double pz, float4 
 // psi = 2r - |d|, partner q (physical index).  Returns psi.
 __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double dx, double dy,
                                            double dz, double d2, int q) {
-  const double dist = __dsqrt_rn(d2);
+  // |d| and d / |d| from one reciprocal square root (1 ulp; both are stored
+  // as float32, and psi's absolute error stays ~1e-17 m)
+  const double inv = rsqrt(d2);
+  const double dist = d2 * inv;
   const double psi = __dsub_rn(D.two_r, dist);
-  D.cgeo[dst] = make_float4(static_cast<float>(__ddiv_rn(dx, dist)),
-                            static_cast<float>(__ddiv_rn(dy, dist)),
-                            static_cast<float>(__ddiv_rn(dz, dist)), static_cast<float>(psi));
+  D.cgeo[dst] = make_float4(static_cast<float>(dx * inv), static_cast<float>(dy * inv),
+                            static_cast<float>(dz * inv), static_cast<float>(psi));
   D.coth[dst] = q;
   return psi;
 }
@@ -1038,12 +1040,14 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   const double tn2 = btx * btx + bty * bty + btz * btz;
   const double lim = D.mu * b1;
   if (tn2 > lim * lim) {  // sliding: project onto the Coulomb cone
-    const double tn = sqrt(tn2);
-    const double sc = lim / fmax(tn, 1e-300);
+    // scale = lim / |bt| with one reciprocal square root (tn2 > lim^2 >= 0,
+    // so tn2 > 0); 1-ulp accurate, far inside the 1e-5 parity bar
+    const double inv = rsqrt(tn2);
+    const double sc = lim * inv;
     btx *= sc;
     bty *= sc;
     btz *= sc;
-    A.maxviol = nmax(A.maxviol, tn * sc - lim);
+    A.maxviol = nmax(A.maxviol, (tn2 * inv) * sc - lim);
   }
   const double ix = (e1x * b1 + btx) * eff;
   const double iy = (e1y * b1 + bty) * eff;

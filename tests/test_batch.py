@@ -283,3 +283,44 @@ def test_large_batch_sampled_envs_match_singles():
         assert np.array_equal(sc.particles.velocities, vb[e])
     assert env.batch.kernel_launches() > 0
     env.close()
+
+
+def _shard_worker(rank, world, port, out):
+    import os
+
+    import torch.distributed as td
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    mine = shard_envs(64, rank, world)
+    cfg = BulldozerEnvConfig(n_particles=300)
+    sums = [float(bulldozer_scene(int(e), cfg).particles.positions.sum()) for e in mine]
+    parts = [None] * world
+    td.all_gather_object(parts, (mine.tolist(), sums))
+    out[rank] = parts
+    td.destroy_process_group()
+
+
+def test_env_sharding_gloo_world2():
+    """The multi-GPU env path has no collective on the data path: every rank
+    builds exactly its shard (env e -> rank e mod N) and the union over ranks
+    is the whole batch, each env seeded as on one rank."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.spawn(_shard_worker, args=(2, port, out), nprocs=2, join=True)
+    parts = out[0]
+    ids = sorted(i for p in parts for i in p[0])
+    assert ids == list(range(64))
+    cfg = BulldozerEnvConfig(n_particles=300)
+    for p in parts:
+        for e, sm in zip(p[0], p[1]):
+            assert sm == float(bulldozer_scene(e, cfg).particles.positions.sum())
