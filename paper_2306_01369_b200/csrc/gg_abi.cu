@@ -1126,18 +1126,20 @@ int gg_tap_contacts(gg_ctx* ctx, int64_t cap_out, int64_t* count, int32_t* owner
   CK(cudaMemcpy(geo.data(), ctx->D.cgeo, sizeof(float4) * cap, cudaMemcpyDeviceToHost));
   long long m = 0;
   for (long long k = 0; k < n; ++k) {
-    for (int s = 0; s < ci[k].y; ++s, ++m) {
-      if (m >= cap_out) continue;
+    for (int s = 0; s < ci[k].y; ++s) {
       const size_t idx = static_cast<size_t>(ci[k].x) + s;
       const int j = oth[idx];
-      if (owner) owner[m] = uid[k];
-      if (other) other[m] = j >= 0 ? uid[j] : -(j + 1);
-      if (kind) kind[m] = j >= 0 ? 0 : 1;
-      if (psi) psi[m] = geo[idx].w;
+      if (j == kNullContact) continue;  // a prefilter pass that is no contact
+      if (m++ >= cap_out) continue;
+      const long long o = m - 1;
+      if (owner) owner[o] = uid[k];
+      if (other) other[o] = j >= 0 ? uid[j] : -(j + 1);
+      if (kind) kind[o] = j >= 0 ? 0 : 1;
+      if (psi) psi[o] = geo[idx].w;
       if (e1) {
-        e1[3 * m] = geo[idx].x;
-        e1[3 * m + 1] = geo[idx].y;
-        e1[3 * m + 2] = geo[idx].z;
+        e1[3 * o] = geo[idx].x;
+        e1[3 * o + 1] = geo[idx].y;
+        e1[3 * o + 2] = geo[idx].z;
       }
     }
   }

@@ -590,6 +590,7 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
 }
 
 constexpr int kPassCap = 16;  // prefilter passes queued per owner (more: exact inline path)
+constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass that is no contact)
 constexpr int kWarps = kBlock / 32;
 
 struct NarrowSmem {
@@ -598,32 +599,11 @@ struct NarrowSmem {
   uint32_t pass[kPassCap][kBlock]; // Xh index of every prefilter pass, per owner, in order
   float4 pos[kBlock];              // owner positions
   uint32_t off[kWarps][32];        // per-warp exclusive offsets of the owners' queue segments
-  uint32_t hit[kWarps][kPassCap];  // per-warp queue bits: exact contact
-  uint32_t coi[kWarps][kPassCap];  // per-warp queue bits: coincident
+  uint8_t qown[kWarps][32 * kPassCap];  // per-warp queue: owner lane of each entry
   unsigned long long wrec[kWarps]; // per-warp record totals -> bases (block allocation)
   double d[32];
   unsigned long long u[32];
 };
-
-// bits [s, s+len) of a bit array, len <= 32
-__device__ __forceinline__ uint32_t popc_range(const uint32_t* w, uint32_t s, uint32_t len) {
-  if (len == 0) return 0u;
-  const uint32_t e = s + len;
-  const uint32_t ws = s >> 5, we = (e - 1) >> 5;
-  const uint32_t lo = ~0u << (s & 31);
-  const uint32_t hi = (e & 31) ? ((1u << (e & 31)) - 1u) : ~0u;
-  if (ws == we) return __popc(w[ws] & lo & hi);
-  return __popc(w[ws] & lo) + __popc(w[we] & hi);
-}
-
-// the owner lane of queue entry idx: the largest o with off[o] <= idx
-__device__ __forceinline__ int queue_owner(const uint32_t* off, uint32_t idx) {
-  int o = 0;
-#pragma unroll
-  for (int step = 16; step > 0; step >>= 1)  // o + step <= 31 throughout
-    if (off[o + step] <= idx) o += step;
-  return o;
-}
 
 // Iterate over a thread's concatenated candidate list (its compacted
 // neighbour buckets) — the cursor of the flat candidate loop.
@@ -815,7 +795,11 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
     }
   }
   sm.pos[tid] = pf;
-  // ---- phase B: warp-cooperative exact test ---------------------------------
+  // ---- phase B: warp-cooperative exact test, one pass --------------------------
+  // Every queued candidate (a prefilter pass) gets a record slot: its owner's
+  // offset + its index in the owner's queue, so slots are known before the
+  // exact test runs.  The rare pass that is not a contact (coincident, or
+  // inside the prefilter's 1e-5 margin) leaves a null record the sweeps skip.
   const uint32_t np = npass < kPassCap ? npass : kPassCap;
   const bool ovf = npass > kPassCap;
   uint32_t incl = np;
@@ -827,39 +811,21 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
   const uint32_t excl = incl - np;
   const uint32_t Tw = __shfl_sync(0xffffffffu, incl, 31);
   sm.off[w][lane] = excl;
-  __syncwarp();
-  const uint32_t* offw = sm.off[w];
-  for (uint32_t r = 0; r * 32 < Tw; ++r) {
-    const uint32_t idx = r * 32 + lane;
-    bool hit = false, coi = false;
-    if (idx < Tw) {
-      const int o = queue_owner(offw, idx);
-      const float4 qf = Xh[sm.pass[idx - offw[o]][wb + o]];
-      const float4 of = sm.pos[wb + o];
-      double dx, dy, dz;
-      const double d2 = pp_d2(of.x, of.y, of.z, qf, dx, dy, dz);
-      coi = !(d2 >= D.coinc_d2);
-      hit = !coi && d2 < D.contact_d2;
-    }
-    const uint32_t bh = __ballot_sync(0xffffffffu, hit);
-    const uint32_t bc = __ballot_sync(0xffffffffu, coi);
-    if (lane == 0) {
-      sm.hit[w][r] = bh;
-      sm.coi[w][r] = bc;
-    }
-  }
-  __syncwarp();
-  int c_pp = static_cast<int>(popc_range(sm.hit[w], excl, np));
-  n_coinc = popc_range(sm.coi[w], excl, np);
+  for (uint32_t i = 0; i < np; ++i) sm.qown[w][excl + i] = static_cast<uint8_t>(lane);
+  int c_pp = 0;           // hits counted by this lane (queue entries it tested)
+  int c_own = np;         // record slots this owner needs for pp contacts
   double max_psi = 0.0;
   if (ovf) {  // more prefilter passes than the queue holds: exact inline count
-    scan_exact(D, sm, tid, k, pf, total, false, 0, c_pp, n_coinc, max_psi);
+    int c_ex = 0;
+    unsigned long long co_ex = 0;
+    scan_exact(D, sm, tid, k, pf, total, false, 0, c_ex, co_ex, max_psi);
+    c_own = c_ex;
   }
   // this env's bodies at this step: bodies[step][env][nb]
   const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
   const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, 0, n_deg, max_psi) : 0;
   // ---- allocation: one atomic per block ----------------------------------------
-  const int tot = c_pp + c_b;
+  const int tot = c_own + c_b;
   int wincl = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -888,33 +854,53 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
   const long long my_off = static_cast<long long>(wbase) + (wincl - tot);
   const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
   const bool fits = static_cast<long long>(wbase) + wtot <= D.cap_tot;
+  const uint32_t* offw = sm.off[w];
   if (fits) {
-    // pp records, cooperatively in queue order; each goes to its owner's
-    // offset + its rank among the owner's hits
+    // pp records, cooperatively in queue order
     const bool uni = (D.E == 1) || __all_sync(0xffffffffu, env == __shfl_sync(0xffffffffu, env, 0));
     for (uint32_t r = 0; r * 32 < Tw; ++r) {
       const uint32_t idx = r * 32 + lane;
-      const int o = idx < Tw ? queue_owner(offw, idx) : 0;
+      const int o = idx < Tw ? sm.qown[w][idx] : 0;
       const long long oo = __shfl_sync(0xffffffffu, my_off, o);
       const bool oovf = __shfl_sync(0xffffffffu, ovf, o);
-      if (idx < Tw && !oovf && ((sm.hit[w][r] >> lane) & 1u)) {
-        const uint32_t s = offw[o];
-        const float4 qf = Xh[sm.pass[idx - s][wb + o]];
-        const int q = __float_as_int(qf.w);
+      if (idx < Tw && !oovf) {
+        const uint32_t i = idx - offw[o];
+        const long long dst = oo + i;
+        const float4 qf = Xh[sm.pass[i][wb + o]];
         const float4 of = sm.pos[wb + o];
         double dx, dy, dz;
         const double d2 = pp_d2(of.x, of.y, of.z, qf, dx, dy, dz);
-        const double psi = pp_write(D, oo + popc_range(sm.hit[w], s, idx - s), dx, dy, dz, d2, q);
-        if (uni) {
-          max_psi = nmax(max_psi, psi);
-        } else if (psi > 0.0) {  // warp straddles two envs (rare): owner's env directly
-          atomicMax(&D.acc[env_of(D, base + wb + o)].max_psi_bits, dbits(psi));
+        const bool coi = !(d2 >= D.coinc_d2);
+        if (!coi && d2 < D.contact_d2) {
+          const double psi = pp_write(D, dst, dx, dy, dz, d2, __float_as_int(qf.w));
+          if (uni) {
+            max_psi = nmax(max_psi, psi);
+            ++c_pp;
+          } else {  // warp straddles two envs (rare): the owner's env directly
+            Acc* a = D.acc + env_of(D, base + wb + o);
+            if (psi > 0.0) atomicMax(&a->max_psi_bits, dbits(psi));
+            atomicAdd(&a->n_pp, 1ull);
+          }
+        } else {
+          D.coth[dst] = kNullContact;
+          if (coi) {
+            if (uni)
+              ++n_coinc;
+            else
+              atomicAdd(&D.acc[env_of(D, base + wb + o)].n_coinc, 1ull);
+          }
         }
       }
     }
     if (live) {
-      if (ovf) scan_exact(D, sm, tid, k, pf, total, true, my_off, c_pp, n_coinc, max_psi);
-      if (c_b > 0) body_contacts(D, bodies, pf, true, my_off + c_pp, n_deg, max_psi);
+      if (ovf) {
+        int c_ex = 0;
+        unsigned long long co_ex = 0;
+        scan_exact(D, sm, tid, k, pf, total, true, my_off, c_ex, co_ex, max_psi);
+        c_pp += c_ex;
+        n_coinc += co_ex;
+      }
+      if (c_b > 0) body_contacts(D, bodies, pf, true, my_off + c_own, n_deg, max_psi);
       D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
     }
   }
@@ -1086,29 +1072,13 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
   const float4 wf = Win[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  // contacts in batches of kSweepBatch: all record loads, then all partner
-  // gathers, then the impulses (in record order) — two dependent round trips
-  // per batch instead of two per contact
-  constexpr int kSweepBatch = 1;
-  for (int s0 = 0; s0 < ci.y; s0 += kSweepBatch) {
-    float4 g[kSweepBatch], q[kSweepBatch];
-    int j[kSweepBatch];
-#pragma unroll
-    for (int u = 0; u < kSweepBatch; ++u) {
-      if (s0 + u < ci.y) {
-        const long long idx = static_cast<long long>(ci.x) + s0 + u;
-        g[u] = D.cgeo[idx];
-        j[u] = D.coth[idx];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kSweepBatch; ++u) {
-      if (s0 + u < ci.y)
-        q[u] = (j[u] >= 0) ? Win[j[u]] : D.cvb[static_cast<long long>(ci.x) + s0 + u];
-    }
-#pragma unroll
-    for (int u = 0; u < kSweepBatch; ++u)
-      if (s0 + u < ci.y) contact_impulse(D, wx, wy, wz, g[u], j[u], q[u], ax, ay, az, A);
+  for (int sl = 0; sl < ci.y; ++sl) {
+    const long long idx = static_cast<long long>(ci.x) + sl;
+    const float4 g = D.cgeo[idx];
+    const int j = D.coth[idx];
+    if (j == kNullContact) continue;
+    const float4 q = (j >= 0) ? Win[j] : D.cvb[idx];
+    contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
                         static_cast<float>(wz + az), 0.f);
@@ -1150,15 +1120,16 @@ struct RegContacts {
     float4 q[kRegSlots];
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s)
-      if (s < c) q[s] = (j[s] >= 0) ? Win[j[s]] : qb[s];
+      if (s < c && j[s] != kNullContact) q[s] = (j[s] >= 0) ? Win[j[s]] : qb[s];
     double ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s)
-      if (s < c) contact_impulse(D, wx, wy, wz, g[s], j[s], q[s], ax, ay, az, A);
+      if (s < c && j[s] != kNullContact) contact_impulse(D, wx, wy, wz, g[s], j[s], q[s], ax, ay, az, A);
     for (int s = kRegSlots; s < c; ++s) {
       const long long idx = static_cast<long long>(off) + s;
       const float4 gg = D.cgeo[idx];
       const int jj = D.coth[idx];
+      if (jj == kNullContact) continue;
       const float4 qq = (jj >= 0) ? Win[jj] : D.cvb[idx];
       contact_impulse(D, wx, wy, wz, gg, jj, qq, ax, ay, az, A);
     }
@@ -1489,7 +1460,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     {
       for (int sl = 0; sl < RC.c; ++sl) {
         const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl];
-        if (j >= 0) {
+        if (j >= 0 && j != kNullContact) {
           const int b = j / blockDim.x;
           if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
         }
