@@ -103,6 +103,20 @@ typedef struct gg_report {
   double min_normal_impulse; /* +inf when no contact was live: host maps to 0.0 */
 } gg_report;
 
+/* A depth camera (render.py DepthCamera :19-32) with its world pose already
+ * resolved (attach_body applied by the caller).  Camera frame: +x right,
+ * +y down, +z forward. */
+typedef struct gg_camera {
+  int32_t kind;      /* 0 perspective, 1 orthographic                   */
+  int32_t width;
+  int32_t height;
+  int32_t reserved;
+  double pose[16];   /* world-from-camera, row-major 4x4                 */
+  double fov;        /* vertical field of view, radians (perspective)    */
+  double extent[2];  /* world width, height (orthographic)               */
+  double far;        /* depth of a pixel that hits nothing               */
+} gg_camera;
+
 typedef struct gg_ctx gg_ctx;
 
 /* Create a context for n particles and an n_h-bucket hash table.
@@ -248,6 +262,15 @@ void* gg_stream(gg_ctx* ctx);
  * this context (the bench's gpu_launches evidence). */
 const char* gg_build_info(void);
 int64_t gg_kernel_launches(const gg_ctx* ctx);
+
+/* Depth images of the current state (render_depth, render.py:119-135):
+ * particles as spheres of the context radius (ray_spheres_depth :61-82) and
+ * the bodies by sphere tracing their SDFs (sphere_trace_depth :85-116).
+ * cams: [n_envs][n_cams] if per_env else [n_cams] (camera c has the same size
+ * in every env); bodies: [n_envs][n_bodies] at their current poses.  out:
+ * float32, per env the n_cams images (height x width, row-major) back to back. */
+int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cams, int32_t per_env,
+                    const gg_body* bodies, int32_t n_bodies, float* out);
 
 /* ---- slab domain decomposition -----------------
  * One bed over several GPUs, one context per rank (single-bed context whose

@@ -44,12 +44,16 @@ from .stepper import (
 )
 from .beds import column_scene, hero_scene, lattice_bed, make_column_scene
 from .batch import SceneBatch, StaticBatch, TrackSteeringBatch, shard_envs
+from .render import DepthCamera, render_batch, render_depth
 from .envs import BatchedBulldozerEnv, BulldozerEnvConfig, GoalBox, bulldozer_reward, bulldozer_scene
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchedBulldozerEnv",
+    "DepthCamera",
+    "render_batch",
+    "render_depth",
     "BulldozerEnvConfig",
     "GoalBox",
     "SceneBatch",

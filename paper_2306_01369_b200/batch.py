@@ -58,6 +58,10 @@ class StaticBatch(BatchDriver):
         z = np.zeros((T, self.n_envs, 3))
         return np.broadcast_to(self.pose, (T, self.n_envs, 4, 4)), z, z
 
+    def current(self):
+        z = np.zeros((self.n_envs, 3))
+        return np.asarray(self.pose), z, z
+
 
 class TrackSteeringBatch(BatchDriver):
     """E tracked vehicles (TrackSteeringDriver + track_steering_advance,
@@ -105,6 +109,9 @@ class TrackSteeringBatch(BatchDriver):
         ref = np.stack([self.x, self.y, np.full(E, self.z)], axis=1)
         v = v_veh + np.cross(omega, pose[:, :3, 3] - ref)
         return pose, omega, v
+
+    def current(self):
+        return self.pose_now()
 
     def rollout(self, T, dt, ts):
         E = self.n_envs
@@ -301,6 +308,7 @@ class SceneBatch:
                         V[k, e] = body.v_origin
             self._fill(table[:, :, b], self._slots[b], P, W, V)
         self.t = ts[-1].copy()
+        self._last_table = table[-1].copy()
         return table
 
     @staticmethod
@@ -325,6 +333,28 @@ class SceneBatch:
         col["bounded"] = 1
         col["aabb_lo"] = world.min(axis=2)
         col["aabb_hi"] = world.max(axis=2)
+
+    def last_bodies(self) -> np.ndarray:
+        """(E, nb) gg_body rows at the current time (the last stepped poses,
+        or the drivers' current poses before the first step)."""
+        if getattr(self, "_last_table", None) is not None:
+            return self._last_table
+        nb = max(self.nb, 1)
+        row = np.zeros((1, self.E, nb), dtype=N.BODY_DTYPE)
+        for b in range(self.nb):
+            drv = self.body_drivers.get(b)
+            if drv is not None:
+                P, W, V = drv.current()
+            else:
+                P = np.empty((self.E, 4, 4))
+                W = np.empty((self.E, 3))
+                V = np.empty((self.E, 3))
+                for e, sc in enumerate(self.scenes):
+                    body = sc.bodies[b]
+                    body.update(float(self.t[e]))
+                    P[e], W[e], V[e] = body.pose, body.omega, body.v_origin
+            self._fill(row[:, :, b], self._slots[b], P[None], W[None], V[None])
+        return row[0]
 
     # -- stepping -------------------------------------------------------------
     def run_raw(self, T: int, mode=PipelineMode.TWO_LOOPS_SPLIT):

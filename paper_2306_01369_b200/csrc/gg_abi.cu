@@ -11,6 +11,7 @@
 
 #include "gg_kernels.cuh"
 #include "gg_slab.cuh"
+#include "gg_render.cuh"
 
 using namespace gg;
 
@@ -1558,3 +1559,56 @@ int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, in
 }
 
 }  // extern "C"
+
+extern "C" int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cams, int32_t per_env,
+                               const gg_body* bodies, int32_t n_bodies, float* out) {
+  if (!ctx || !cams || !out || n_cams < 1 || n_bodies < 0 || (n_bodies > 0 && !bodies))
+    return fail(ctx, GG_EINVAL, "bad render arguments");
+  const int E = ctx->E;
+  const int ncam_tot = per_env ? E * n_cams : n_cams;
+  std::vector<long long> off(n_cams + 1, 0);
+  int max_pix = 0;
+  for (int c = 0; c < n_cams; ++c) {
+    const gg_camera& C = cams[c];
+    if (C.width < 1 || C.height < 1 || !(C.far > 0) || (C.kind != 0 && C.kind != 1))
+      return fail(ctx, GG_EINVAL, "bad camera (size >= 1x1, far > 0, kind 0/1)");
+    off[c + 1] = off[c] + static_cast<long long>(C.width) * C.height;
+    max_pix = std::max(max_pix, C.width * C.height);
+  }
+  if (per_env)
+    for (int e = 1; e < E; ++e)
+      for (int c = 0; c < n_cams; ++c)
+        if (cams[e * n_cams + c].width != cams[c].width || cams[e * n_cams + c].height != cams[c].height)
+          return fail(ctx, GG_EINVAL, "camera sizes must agree across envs");
+  for (long long i = 0; i < static_cast<long long>(E) * n_bodies; ++i)
+    if (bodies[i].kind == GG_GEOM_GRID && (bodies[i].grid_id < 0 || bodies[i].grid_id >= (int)ctx->grids.size()))
+      return fail(ctx, GG_EINVAL, "unknown grid id");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const size_t cam_b = sizeof(gg_camera) * ncam_tot;
+  const size_t body_b = sizeof(gg_body) * static_cast<size_t>(E) * n_bodies;
+  const size_t off_b = sizeof(long long) * (n_cams + 1);
+  const size_t out_b = sizeof(float) * static_cast<size_t>(E) * off[n_cams];
+  char* buf = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), cam_b + body_b + off_b + out_b + 64, s));
+  gg_camera* dc = reinterpret_cast<gg_camera*>(buf);
+  gg_body* db = reinterpret_cast<gg_body*>(buf + cam_b);
+  long long* doff = reinterpret_cast<long long*>(buf + cam_b + body_b);
+  float* dout = reinterpret_cast<float*>(buf + cam_b + body_b + off_b);
+  cudaError_t e = cudaMemcpyAsync(dc, cams, cam_b, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && body_b) e = cudaMemcpyAsync(db, bodies, body_b, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(doff, off.data(), off_b, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    RenderArgs A{dc, n_cams, per_env ? 1 : 0, db, n_bodies, doff, dout};
+    dim3 grid((max_pix + kBlock - 1) / kBlock, n_cams, E);
+    refresh_dev(ctx);
+    k_render<<<grid, kBlock, 0, s>>>(ctx->D, A);
+    ctx->launches += 1;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, out_b, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gg_render_depth");
+  return GG_OK;
+}

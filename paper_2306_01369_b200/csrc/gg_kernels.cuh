@@ -1069,6 +1069,10 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
                                                SweepAcc& A) {
   sweep_acc_env(D, A, k);
   const int2 ci = D.cinfo[k];
+  // a particle without contacts keeps w = v and is nobody's partner
+  // (contacts are symmetric), so its w is never read: skip it entirely
+  // (integrate uses dv = 0 for it)
+  if (ci.y == 0) return;
   const float4 wf = Win[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
@@ -1117,6 +1121,7 @@ struct RegContacts {
 
   __device__ __forceinline__ void sweep(const Dev& D, int k, const float4* Win, float4* Wout,
                                         SweepAcc& A) {
+    if (c == 0) return;  // no contacts: w is never read (see sweep_particle)
     float4 q[kRegSlots];
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s)
@@ -1190,8 +1195,8 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
   for (int k = t0; k < D.n_own; k += G) {
     const float4 xo = L.x[k];
     const float4 vo = L.v[k];
-    const float4 wf = Wf[k];
     const bool has = D.cinfo[k].y > 0;
+    const float4 wf = has ? Wf[k] : vo;  // no contacts: no sweep wrote w
     const double dvx = has ? (double)wf.x - (double)vo.x : 0.0;
     const double dvy = has ? (double)wf.y - (double)vo.y : 0.0;
     const double dvz = has ? (double)wf.z - (double)vo.z : 0.0;
@@ -1455,31 +1460,33 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     RegContacts RC;
     RC.c = 0;
     if (ok && t0 < D.n_own) RC.load(D, t0, L.v[t0]);
-    for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
-    __syncthreads();
-    {
-      for (int sl = 0; sl < RC.c; ++sl) {
-        const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl];
-        if (j >= 0 && j != kNullContact) {
-          const int b = j / blockDim.x;
-          if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
+    if (!D.sweep_barrier) {  // neighbour-block list for the flag-synchronised sweeps
+      for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
+      __syncthreads();
+      {
+        for (int sl = 0; sl < RC.c; ++sl) {
+          const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl];
+          if (j >= 0 && j != kNullContact) {
+            const int b = j / blockDim.x;
+            if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
+          }
         }
       }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int m = 0;
-      for (int w = 0; w < (int)((gridDim.x + 31) / 32); ++w) {
-        unsigned bits = s_nbmask[w];
-        while (bits) {
-          const int bit = __ffs(bits) - 1;
-          bits &= bits - 1;
-          s_nblist[m++] = w * 32 + bit;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int m = 0;
+        for (int w = 0; w < (int)((gridDim.x + 31) / 32); ++w) {
+          unsigned bits = s_nbmask[w];
+          while (bits) {
+            const int bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            s_nblist[m++] = w * 32 + bit;
+          }
         }
+        s_nnb = m;
       }
-      s_nnb = m;
+      __syncthreads();
     }
-    __syncthreads();
     unsigned* flags = D.bflags;
     for (int s = 0; s < D.S; ++s) {
       if (s > 0 && D.sweep_barrier) {

@@ -9,8 +9,9 @@ all envs in one array, the tracked vehicles advanced with array math
 (``TrackSteeringBatch``), ``frame_skip`` physics substeps per control step as
 one device batch, and the reward (``bulldozer_reward``, envs.py:61-70)
 reduced per env on the device (``gg_env_box_stats``) so no particle state
-crosses PCIe.  Depth observations (render.py) are not produced: the
-observation is the vehicle pose (x, y, yaw), as in ``EnvObservation.pose``.
+crosses PCIe.  Observations are the reference's (``EnvObservation``,
+envs.py:73-78): the 36x36 ego and 72x36 sky depth images rendered on the
+device for every env in one launch (``render_batch``), and the vehicle pose.
 """
 
 from __future__ import annotations
@@ -22,6 +23,7 @@ import numpy as np
 
 from . import _native as N
 from .batch import SceneBatch, StaticBatch, TrackSteeringBatch
+from .render import DepthCamera, render_batch
 from .kinematics import TrackSteeringDriver, TrackSteeringState, make_pose
 from .scene import BoxRegion, MaterialParams, ParticleSet, RigidBody, Scene, seed_particles_grid
 from .sdf import Box, HalfSpace
@@ -80,6 +82,37 @@ class BulldozerEnvConfig:
     blade_half_extents: tuple = (0.05, 0.5, 0.25)
     blade_offset: float = 0.45
     jitter: float = 0.3
+    sky_extent: tuple = (8.0, 4.0)
+    sky_height: float = 6.0
+    far: float = 20.0
+
+
+@dataclass
+class BatchObservation:
+    """EnvObservation (envs.py:73-78) for E envs."""
+
+    ego: np.ndarray   # (E, 36, 36) float32 depth, meters
+    sky: np.ndarray   # (E, 36, 72) float32 depth, meters
+    pose: np.ndarray  # (E, 3) vehicle (x, y, yaw)
+
+
+def ego_camera(cfg: BulldozerEnvConfig) -> DepthCamera:
+    """The cockpit camera in the vehicle frame (envs.py:117-136)."""
+    tilt = make_pose(np.array([[0.0, 0.0, 1.0], [0.0, 1.0, 0.0], [-1.0, 0.0, 0.0]]).T,
+                     np.array([-0.2, 0.0, 0.8]))
+    pitch = 0.35
+    tilt[:3, :3] = tilt[:3, :3] @ np.array([[np.cos(pitch), 0.0, -np.sin(pitch)], [0.0, 1.0, 0.0],
+                                             [np.sin(pitch), 0.0, np.cos(pitch)]])
+    return DepthCamera(kind="perspective", pose=tilt, width=36, height=36, fov=np.pi / 2.5,
+                       far=cfg.far)
+
+
+def sky_camera(cfg: BulldozerEnvConfig) -> DepthCamera:
+    """The overhead orthographic camera (envs.py:137-148)."""
+    pose = make_pose(np.array([[1.0, 0.0, 0.0], [0.0, -1.0, 0.0], [0.0, 0.0, -1.0]]),
+                     np.array([0.0, 0.0, cfg.sky_height]))
+    return DepthCamera(kind="orthographic", pose=pose, width=72, height=36, extent=cfg.sky_extent,
+                       far=cfg.far)
 
 
 def blade_base_pose(cfg: BulldozerEnvConfig) -> np.ndarray:
@@ -107,15 +140,17 @@ def bulldozer_scene(seed: int, cfg: BulldozerEnvConfig | None = None) -> Scene:
 class BatchedBulldozerEnv:
     """E bulldozer envs in lock step on one device (BulldozerEnv, envs.py:102-230).
 
-    ``reset(seeds)`` -> poses (E, 3); ``step(actions (E, 2))`` ->
-    (poses (E,3), rewards (E,), dones (E,), info) with info holding the
+    ``reset(seeds)`` -> observation; ``step(actions (E, 2))`` ->
+    (observation, rewards (E,), dones (E,), info) with info holding the
     per-env StepReport arrays of the last substep and the particles inside
-    the goal box.  All envs share one episode clock, as a synchronous vector
-    env does."""
+    the goal box.  The observation is a ``BatchObservation`` (ego and sky
+    depth images + poses; render=False: the (E, 3) poses alone).  All envs
+    share one episode clock, as a synchronous vector env does."""
 
     action_shape = (2,)
 
-    def __init__(self, n_envs: int, config: BulldozerEnvConfig | None = None, device: int = 0):
+    def __init__(self, n_envs: int, config: BulldozerEnvConfig | None = None, device: int = 0,
+                 render: bool = True):
         if n_envs < 1:
             raise ValueError("n_envs must be >= 1")
         self.n_envs = n_envs
@@ -127,8 +162,11 @@ class BatchedBulldozerEnv:
         self.batch: SceneBatch | None = None
         self.driver: TrackSteeringBatch | None = None
         self._steps = 0
+        self.render = render
+        self.ego_camera = ego_camera(self.config)
+        self.sky_camera = sky_camera(self.config)
 
-    def reset(self, seeds=None) -> np.ndarray:
+    def reset(self, seeds=None):
         E = self.n_envs
         seeds = np.arange(E) if seeds is None else np.asarray(seeds, dtype=np.int64)
         if len(seeds) != E:
@@ -145,9 +183,19 @@ class BatchedBulldozerEnv:
         self._steps = 0
         return self._observe()
 
-    def _observe(self) -> np.ndarray:
+    def _observe(self):
+        """BatchObservation (render=True) or the (E, 3) poses alone."""
         d = self.driver
-        return np.stack([d.x, d.y, d.theta], axis=1)
+        pose = np.stack([d.x, d.y, d.theta], axis=1)
+        if not self.render:
+            return pose
+        # the camera rides the vehicle frame, not the blade offset (envs.py:182-186)
+        blade, _, _ = d.pose_now()
+        vehicle = blade.copy()
+        vehicle[:, :3, 3] -= np.einsum("eij,j->ei", blade[:, :3, :3], d.base_pose[:3, 3])
+        ego_poses = vehicle @ self.ego_camera.pose
+        ego, sky = render_batch(self.batch, [self.ego_camera, self.sky_camera], [ego_poses, None])
+        return BatchObservation(ego=ego, sky=sky, pose=pose)
 
     def goal_stats(self):
         """(rewards (E,), particles inside the goal box (E,)) on the device."""

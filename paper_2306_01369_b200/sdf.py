@@ -170,3 +170,41 @@ def penetration_depth(geom, body_pose: np.ndarray, world_points: np.ndarray, r: 
     if single:
         return float(psi[0]), nrm[0], bool(mask[0]), int(ndeg.value)
     return psi, nrm, mask, int(ndeg.value)
+
+
+# ---------------------------------------------------------------------------
+# GSDF grid cache (sdf.py:432-465 of the reference): "GSDF", u32 version 1,
+# u32 dims[3], f64 origin[3], f64 spacing[3], 32-byte mesh hash, then the
+# knot values as little-endian float32 in C order.
+# ---------------------------------------------------------------------------
+import struct as _struct
+
+GRID_MAGIC = b"GSDF"
+GRID_VERSION = 1
+
+
+def save_grid(path: str, grid: SdfGrid) -> None:
+    header = GRID_MAGIC + _struct.pack("<I3I3d3d", GRID_VERSION, *(int(d) for d in grid.dims),
+                                       *(float(o) for o in grid.origin),
+                                       *(float(s) for s in grid.spacing))
+    with open(path, "wb") as fh:
+        fh.write(header)
+        fh.write(bytes(grid.mesh_hash[:32]).ljust(32, b"\0"))
+        fh.write(np.ascontiguousarray(grid.values, dtype="<f4").tobytes())
+
+
+def load_grid(path: str) -> SdfGrid:
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[:4] != GRID_MAGIC:
+        raise ValueError(f"{path!r} is not an SDF grid cache file")
+    (version,) = _struct.unpack_from("<I", blob, 4)
+    if version != GRID_VERSION:
+        raise ValueError(f"unsupported grid cache version {version}")
+    fields = _struct.unpack_from("<3I3d3d", blob, 8)
+    dims, origin, spacing = fields[:3], fields[3:6], fields[6:9]
+    off = 8 + _struct.calcsize("<3I3d3d")
+    mesh_hash = blob[off:off + 32]
+    values = np.frombuffer(blob[off + 32:], dtype="<f4").astype(np.float64)
+    return SdfGrid(origin=np.array(origin), spacing=np.array(spacing), dims=np.array(dims),
+                   values=values.reshape(dims), mesh_hash=mesh_hash)

@@ -224,10 +224,12 @@ def test_batched_bulldozer_env_matches_reference():
 def test_batched_bulldozer_env_api():
     env = BatchedBulldozerEnv(8, BulldozerEnvConfig(n_particles=300))
     obs = env.reset()
-    assert obs.shape == (8, 3)
+    assert obs.pose.shape == (8, 3) and obs.ego.shape == (8, 36, 36) and obs.sky.shape == (8, 36, 72)
     obs, rew, done, info = env.step(np.tile([1.0, 0.0], (8, 1)))
-    assert obs.shape == (8, 3) and rew.shape == (8,) and done.shape == (8,)
-    assert np.all(obs[:, 0] > -2.0)  # vehicles drove forward
+    assert obs.pose.shape == (8, 3) and rew.shape == (8,) and done.shape == (8,)
+    assert np.all(obs.pose[:, 0] > -2.0)  # vehicles drove forward
+    assert np.all(obs.sky < env.config.far)  # the ground is under the whole sky view
+    assert np.all(obs.ego > 0)
     assert np.all(info["t"] == pytest.approx(10 * 2e-3))
     with pytest.raises(ValueError):
         env.step(np.zeros((8, 3)))

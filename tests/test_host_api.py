@@ -97,3 +97,23 @@ def test_step_report_fields_match_reference_names():
                      "max_penetration", "kinetic_energy", "n_body_contacts",
                      "n_coincident_skipped", "n_degenerate_skipped", "max_cone_violation",
                      "min_normal_impulse", "body_momentum", "step_index"}
+
+
+def test_gsdf_cache_matches_reference_format(tmp_path):
+    """GSDF v1 grid cache (sdf.py:432-465): a file written by the reference
+    loads, and saving it again reproduces the reference's bytes."""
+    from helpers import GOLDEN
+    from paper_2306_01369_b200.sdf import load_grid, save_grid
+
+    src = GOLDEN / "box.gsdf"
+    g = load_grid(str(src))
+    assert tuple(g.values.shape) == tuple(int(d) for d in g.dims)
+    out = tmp_path / "again.gsdf"
+    save_grid(str(out), g)
+    assert out.read_bytes() == src.read_bytes()
+    bad = tmp_path / "bad.gsdf"
+    bad.write_bytes(b"NOPE" + src.read_bytes()[4:])
+    import pytest
+
+    with pytest.raises(ValueError):
+        load_grid(str(bad))

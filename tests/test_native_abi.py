@@ -35,9 +35,10 @@ def test_struct_layouts_match_header(tmp_path):
     src = tmp_path / "sz.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "granusim_b200.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(gg_params),"
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(gg_params),"
         " sizeof(gg_body), sizeof(gg_report), offsetof(gg_params, z_max),"
-        " offsetof(gg_body, aabb_hi), offsetof(gg_report, min_normal_impulse));return 0;}\n"
+        " offsetof(gg_body, aabb_hi), offsetof(gg_report, min_normal_impulse),"
+        " sizeof(gg_camera), offsetof(gg_camera, far));return 0;}\n"
     )
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(HEADER.parent), str(src), "-o", str(exe)], check=True)
@@ -48,6 +49,10 @@ def test_struct_layouts_match_header(tmp_path):
     assert got[3] == N.GGParams.z_max.offset
     assert got[4] == N.BODY_DTYPE.fields["aabb_hi"][1]
     assert got[5] == N.REPORT_DTYPE.fields["min_normal_impulse"][1]
+    from paper_2306_01369_b200.render import CAMERA_DTYPE
+
+    assert got[6] == CAMERA_DTYPE.itemsize
+    assert got[7] == CAMERA_DTYPE.fields["far"][1]
 
 
 def test_library_is_sm100a_only():
