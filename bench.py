@@ -377,7 +377,7 @@ def envs_setup(args, dist: Dist, device: int):
 
     mine = shard_envs(args.envs, dist.rank, dist.world)
     cfg = BulldozerEnvConfig(n_particles=args.env_particles, radius=0.025)
-    env = BatchedBulldozerEnv(len(mine), cfg, device=device)
+    env = BatchedBulldozerEnv(len(mine), cfg, device=device, render=False)  # physics e2e
     env.reset(mine)  # seed = env id
     acts = np.stack([np.random.default_rng(int(e)).uniform(-1, 1, 2) for e in mine])
     acts[:, 0] = np.abs(acts[:, 0])  # drive forward into the bed

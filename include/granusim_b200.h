@@ -271,6 +271,11 @@ int64_t gg_kernel_launches(const gg_ctx* ctx);
  * float32, per env the n_cams images (height x width, row-major) back to back. */
 int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cams, int32_t per_env,
                     const gg_body* bodies, int32_t n_bodies, float* out);
+/* Renderer algorithm (process-wide): 0 every pixel tests every particle of
+ * its env through shared-memory tiles (the reference's algorithm; default),
+ * 1 splat each particle into the pixels its sphere can cover.  Both give
+ * bitwise identical images. */
+int gg_set_render_mode(int32_t mode);
 
 /* ---- slab domain decomposition -----------------
  * One bed over several GPUs, one context per rank (single-bed context whose

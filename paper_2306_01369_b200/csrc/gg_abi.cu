@@ -287,14 +287,23 @@ int launch_cluster_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
   return GG_OK;
 }
 
-int launch_solve(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
+int env_report_blocks(const gg_ctx* ctx) {
+  const long long work = std::max<long long>(ctx->E, static_cast<long long>(ctx->E) * ctx->D.nb * 3);
+  return static_cast<int>(std::min<long long>(4 * 148, (work + kBlock - 1) / kBlock));
+}
+
+int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
   if (!use_persistent_solve(ctx)) {
     // one thread per particle: S sweep launches + integrate/report
+    Dev D = D0;
+    D.env_kernel = ctx->E > 1 ? 1 : 0;
     for (int it = 0; it < D.S; ++it) k_sweep<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
     k_finish<<<ctx->nblocks, kBlock, 0, s>>>(D);
+    if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
     CK(cudaGetLastError());
     return GG_OK;
   }
+  const Dev& D = D0;
   return launch_coop(ctx, k_solve, ctx->solve_grid, D, s, ctx->solve_mode != 2);  // modes 1, 2
 }
 
@@ -320,6 +329,7 @@ Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
   D.key_morton = morton;
   D.fused_stop = 0;
   D.sweep_barrier = (ctx->solve_mode == 7 || ctx->solve_mode == 0) ? 1 : 0;
+  D.env_kernel = 0;
   return D;
 }
 
@@ -359,7 +369,8 @@ bool use_fused_step(const gg_ctx* ctx);
 int kernels_per_step(const gg_ctx* ctx, int resort) {
   if (use_fused_step(ctx)) return use_cluster_solve(ctx) ? 2 : 1;
   const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 1;
-  return 7 + solve + (resort ? 6 : 0);
+  const int env_reports = (ctx->E > 1 && !use_persistent_solve(ctx)) ? 1 : 0;
+  return 7 + solve + env_reports + (resort ? 6 : 0);
 }
 
 // Same schedule as enqueue_step, with an event after every kernel so each
@@ -437,7 +448,10 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
       k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
       mark(12);
     }
-    k_finish<<<nbn, kBlock, 0, s>>>(D);
+    Dev Df = D;
+    Df.env_kernel = ctx->E > 1 ? 1 : 0;
+    k_finish<<<nbn, kBlock, 0, s>>>(Df);
+    if (Df.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(Df);
     mark(13);
   }
   if (cudaGetLastError() != cudaSuccess) return -1;
@@ -601,6 +615,9 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
                                                      sizeof(NarrowSmem)));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     ctx->solve_grid = std::max(1, std::min(ctx->nblocks, per_sm * sms));
+    // n / kBlock blocks (packed) when they fit: measured faster than spreading
+    // the particles thinly over every co-resident block (hero50k 0.117 vs
+    // 0.130 ms/step); the kernel spreads particles evenly over its grid
     ctx->fused_grid = std::max(1, std::min(ctx->nblocks, per_sm_f * sms));
     // can one 16-CTA cluster of k_solve_cluster be resident?
     if (cudaFuncSetAttribute(k_solve_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
@@ -1560,6 +1577,18 @@ int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, in
 
 }  // extern "C"
 
+// 0 every pixel tests every particle of its env, tiled through shared memory
+// (default: measured 61 ms for 4096 envs x (36x36 + 72x36)); 1 splat every
+// particle into the pixels it can cover (100+ ms there: the 64-bit atomicMin
+// traffic on small images outweighs the saved tests).  Bitwise equal images.
+static int g_render_mode = 1;  // internal: 0 splat, 1 brute force
+
+extern "C" int gg_set_render_mode(int32_t mode) {
+  if (mode != 0 && mode != 1) return GG_EINVAL;
+  g_render_mode = mode ? 0 : 1;  // internal: 0 splat, 1 brute force
+  return GG_OK;
+}
+
 extern "C" int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cams, int32_t per_env,
                                const gg_body* bodies, int32_t n_bodies, float* out) {
   if (!ctx || !cams || !out || n_cams < 1 || n_bodies < 0 || (n_bodies > 0 && !bodies))
@@ -1578,8 +1607,11 @@ extern "C" int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cam
   if (per_env)
     for (int e = 1; e < E; ++e)
       for (int c = 0; c < n_cams; ++c)
-        if (cams[e * n_cams + c].width != cams[c].width || cams[e * n_cams + c].height != cams[c].height)
-          return fail(ctx, GG_EINVAL, "camera sizes must agree across envs");
+        if (cams[e * n_cams + c].width != cams[c].width || cams[e * n_cams + c].height != cams[c].height ||
+            cams[e * n_cams + c].kind != cams[c].kind || cams[e * n_cams + c].fov != cams[c].fov ||
+            cams[e * n_cams + c].extent[0] != cams[c].extent[0] ||
+            cams[e * n_cams + c].extent[1] != cams[c].extent[1])
+          return fail(ctx, GG_EINVAL, "camera c must have the same intrinsics in every env");
   for (long long i = 0; i < static_cast<long long>(E) * n_bodies; ++i)
     if (bodies[i].kind == GG_GEOM_GRID && (bodies[i].grid_id < 0 || bodies[i].grid_id >= (int)ctx->grids.size()))
       return fail(ctx, GG_EINVAL, "unknown grid id");
@@ -1589,8 +1621,10 @@ extern "C" int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cam
   const size_t body_b = sizeof(gg_body) * static_cast<size_t>(E) * n_bodies;
   const size_t off_b = sizeof(long long) * (n_cams + 1);
   const size_t out_b = sizeof(float) * static_cast<size_t>(E) * off[n_cams];
+  const size_t z_b = g_render_mode == 0 ? sizeof(unsigned long long) * static_cast<size_t>(E) * off[n_cams] : 0;
+  const size_t loc_b = sizeof(double) * 3 * static_cast<size_t>(off[n_cams]);
   char* buf = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), cam_b + body_b + off_b + out_b + 64, s));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&buf), cam_b + body_b + off_b + out_b + z_b + loc_b + 64, s));
   gg_camera* dc = reinterpret_cast<gg_camera*>(buf);
   gg_body* db = reinterpret_cast<gg_body*>(buf + cam_b);
   long long* doff = reinterpret_cast<long long*>(buf + cam_b + body_b);
@@ -1599,12 +1633,27 @@ extern "C" int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cam
   if (e == cudaSuccess && body_b) e = cudaMemcpyAsync(db, bodies, body_b, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(doff, off.data(), off_b, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) {
-    RenderArgs A{dc, n_cams, per_env ? 1 : 0, db, n_bodies, doff, dout};
+    // 8-byte aligned z-buffer and local-ray table after the float output
+    unsigned long long* zb = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(dout) + out_b + 7) & ~static_cast<uintptr_t>(7));
+    double* dloc = reinterpret_cast<double*>(reinterpret_cast<char*>(zb) + z_b);
+    RenderArgs A{dc, n_cams, per_env ? 1 : 0, db, n_bodies, doff, dout, dloc};
     dim3 grid((max_pix + kBlock - 1) / kBlock, n_cams, E);
     refresh_dev(ctx);
-    k_render<<<grid, kBlock, 0, s>>>(ctx->D, A);
-    ctx->launches += 1;
-    e = cudaGetLastError();
+    // camera-frame rays of camera index c (the intrinsics agree across envs)
+    k_render_local<<<dim3((max_pix + kBlock - 1) / kBlock, n_cams), kBlock, 0, s>>>(dc, n_cams, doff, dloc);
+    if (g_render_mode == 0) {
+      e = cudaMemsetAsync(zb, 0xff, z_b, s);
+      if (e == cudaSuccess) {
+        k_render_splat<<<dim3((ctx->ne + kBlock - 1) / kBlock, E), kBlock, 0, s>>>(ctx->D, A, zb);
+        k_render_bodies<<<grid, kBlock, 0, s>>>(ctx->D, A, zb);
+        ctx->launches += 2;
+      }
+    } else {
+      k_render<<<grid, kBlock, 0, s>>>(ctx->D, A);
+      ctx->launches += 1;
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, out_b, cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(buf, s);

@@ -78,6 +78,7 @@ struct Dev {
   int resort;     // this graph re-sorts the physical order first
   int fused_stop; // k_step_fused ends after the contacts (the cluster kernel solves)
   int sweep_barrier;  // fused sweeps: 1 grid barrier per sweep, 0 neighbour-block flags
+  int env_kernel;     // E > 1: per-env reports + body momentum written by k_env_reports
   int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
   // Independent environments (segments).  E == 1 is a single bed.  With
   // E > 1 env e owns particles [e*ne, (e+1)*ne) of the physical order and
@@ -713,7 +714,9 @@ __device__ __forceinline__ int body_contacts(const Dev& D, const gg_body* bodies
 //   the records are written in a second cooperative pass.  Records of one
 //   owner stay in candidate order, then bodies in index order, so results
 //   do not depend on where the allocator put them.
-__device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, NarrowSmem& sm) {
+// Particles base .. base + count - 1 (count <= blockDim.x) belong to this block.
+__device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, int count,
+                                            NarrowSmem& sm) {
   // plain (coherent) loads: in the fused kernel these buffers are written
   // earlier in the same launch, so the read-only (.nc) path is not allowed
   const float4* LX = layout(D, ctl).x;
@@ -721,7 +724,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, Na
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5, wb = w * 32;
   const int k = base + tid;
-  const bool live = k < D.n_own;
+  const bool live = tid < count && k < D.n_own;
   const int env = env_of(D, live ? k : D.n - 1);
   unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
   uint32_t total = 0, npass = 0;
@@ -940,14 +943,15 @@ struct SweepAcc {
   unsigned long long rb[kRegBodies][3];  // this thread's momentum of bodies 0..kRegBodies-1
 };
 
-// k0: the first particle this thread sweeps (its env seeds A.env)
+// k0: the first particle this thread sweeps (its env seeds A.env); kb: the
+// block's first particle (-1: blockIdx.x * blockDim.x)
 __device__ __forceinline__ void sweep_acc_init(const Dev& D, SweepAcc& A, unsigned long long* sbm,
-                                               int k0) {
+                                               int k0, int kb = -1) {
   A.maxviol = 0.0;
   A.minb1 = __longlong_as_double(0x7ff0000000000000ll);
   A.sbm = sbm;
   A.env = env_of(D, k0 < D.n ? k0 : D.n - 1);
-  const int kb = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x);
+  if (kb < 0) kb = static_cast<int>(blockIdx.x) * static_cast<int>(blockDim.x);
   A.gb_lo = env_of(D, kb < D.n ? kb : D.n - 1) * D.nb;
 #pragma unroll
   for (int b = 0; b < kRegBodies; ++b) A.rb[b][0] = A.rb[b][1] = A.rb[b][2] = 0ull;
@@ -1253,7 +1257,7 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
   if (threadIdx.x == 0) s_err = *((volatile int*)&ctl->err);
   __syncthreads();
   const long long nbm = static_cast<long long>(D.E) * D.nb * 3;
-  for (long long i = threadIdx.x; i < nbm; i += blockDim.x) {
+  for (long long i = threadIdx.x; !D.env_kernel && i < nbm; i += blockDim.x) {
     const long long f = static_cast<long long>(*((volatile unsigned long long*)&D.bm_fix[i]));
     if (!s_err) D.bm_out[static_cast<long long>(step) * nbm + i] = static_cast<double>(f) / kMomScale;
     D.bm_fix[i] = 0ull;
@@ -1262,7 +1266,7 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
   // barrier words and sweep flags can be reset here for the next launch
   for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
     if (D.bflags) D.bflags[b] = 0u;
-  if (D.E > 1 && !s_err) {
+  if (D.E > 1 && !s_err && !D.env_kernel) {
     for (int e = threadIdx.x; e < D.E; e += blockDim.x) {
       volatile unsigned long long* kf = D.ke_fix + e;
       write_report(D, D.reports[static_cast<long long>(step) * D.E + e], D.acc + e,
@@ -1284,6 +1288,29 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
     ctl->cur = cur ^ 1;
     if (D.resort) ctl->ucur ^= 1;
     ctl->step = step + 1;
+  }
+}
+
+// E > 1, large n: the per-env StepReports and body momenta of the step just
+// committed, written by the whole grid after k_finish (the last block of
+// k_finish alone would serialise 4096 envs x (report + 3 nb momenta)).
+__global__ void __launch_bounds__(kBlock) k_env_reports(Dev D) {
+  const Ctl* ctl = D.ctl;
+  if (*((volatile const int*)&ctl->err)) return;  // nothing committed (k_batch_begin resets)
+  const int step = ctl->step - 1;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long G = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long e = t; e < D.E; e += G) {
+    write_report(D, D.reports[static_cast<long long>(step) * D.E + e], D.acc + e,
+                 static_cast<double>(static_cast<long long>(D.ke_fix[e])) / kKeScale);
+    D.ke_fix[e] = 0ull;
+    acc_reset(D.acc + e);
+  }
+  const long long nbm = static_cast<long long>(D.E) * D.nb * 3;
+  for (long long i = t; i < nbm; i += G) {
+    D.bm_out[static_cast<long long>(step) * nbm + i] =
+        static_cast<double>(static_cast<long long>(D.bm_fix[i])) / kMomScale;
+    D.bm_fix[i] = 0ull;
   }
 }
 
@@ -1341,7 +1368,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
   NarrowSmem& sm = *reinterpret_cast<NarrowSmem*>(g_dsmem);
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  ph_contacts(D, ctl, blockIdx.x * blockDim.x, sm);
+  ph_contacts(D, ctl, blockIdx.x * blockDim.x, blockDim.x, sm);
 }
 
 __global__ void __launch_bounds__(kBlock, 4) k_sweep(Dev D, int s) {
@@ -1436,8 +1463,19 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   // narrowphase + bodies; the sweeps below use the same particle -> block
   // map, so a particle's records were written by its own block (visible
   // after the __syncthreads in sweep_acc_init)
+  // One particle per thread (G >= n): the particles are spread evenly over
+  // ALL co-resident blocks (P per block) rather than packed into the first
+  // n / blockDim blocks, so no SM carries two full blocks while others idle.
+  const bool one_per_thread = G >= D.n;
+  const int P = one_per_thread ? (D.n + gridDim.x - 1) / gridDim.x : blockDim.x;
+  const int kr = blockIdx.x * P + threadIdx.x;                // this thread's particle
+  const bool kr_live = one_per_thread && threadIdx.x < P && kr < D.n_own;
   if (ok) {
-    for (int base = blockIdx.x * blockDim.x; base < D.n; base += G) ph_contacts(D, ctl, base, sm);
+    if (one_per_thread)
+      ph_contacts(D, ctl, blockIdx.x * P, P, sm);
+    else
+      for (int base = blockIdx.x * blockDim.x; base < D.n; base += G)
+        ph_contacts(D, ctl, base, blockDim.x, sm);
   }
   stamp(D, ts);
   // split schedule: k_solve_cluster runs the sweeps and the commit (and
@@ -1446,8 +1484,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   const Layout L = layout(D, ctl);
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
-  sweep_acc_init(D, A, sbm, t0);
-  if (G >= D.n && gridDim.x <= kMaxFusedBlocks) {
+  sweep_acc_init(D, A, sbm, one_per_thread ? kr : t0, one_per_thread ? blockIdx.x * P : -1);
+  if (one_per_thread && gridDim.x <= kMaxFusedBlocks) {
     // One particle per thread: its contacts (first kRegSlots) and its own w
     // stay in registers for all sweeps.  Jacobi sweep s of a block only needs
     // sweep s-1 of the blocks that own its particles' contact partners, and
@@ -1459,7 +1497,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     __shared__ int s_nnb;
     RegContacts RC;
     RC.c = 0;
-    if (ok && t0 < D.n_own) RC.load(D, t0, L.v[t0]);
+    if (ok && kr_live) RC.load(D, kr, L.v[kr]);
     if (!D.sweep_barrier) {  // neighbour-block list for the flag-synchronised sweeps
       for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
       __syncthreads();
@@ -1467,7 +1505,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
         for (int sl = 0; sl < RC.c; ++sl) {
           const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl];
           if (j >= 0 && j != kNullContact) {
-            const int b = j / blockDim.x;
+            const int b = j / P;
             if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
           }
         }
@@ -1506,7 +1544,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
         ok = ok && s_flag == 0;
         stamp(D, ts);
       }
-      if (ok && t0 < D.n_own) RC.sweep(D, t0, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+      if (ok && kr_live) RC.sweep(D, kr, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
       if (!D.sweep_barrier) {
         __syncthreads();
         if (threadIdx.x == 0)
@@ -1525,7 +1563,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   }
   stamp(D, ts);
   sweep_acc_flush(D, A, sm.d);
-  integrate_and_finish(D, ctl, t0, G, sm.d, &s_last);
+  // integrate exactly the particles this thread swept: the last sweep's w of
+  // another block's particle is not ordered before this read (no barrier)
+  if (one_per_thread && gridDim.x <= kMaxFusedBlocks)
+    integrate_and_finish(D, ctl, kr_live ? kr : D.n_own, D.n_own + 1, sm.d, &s_last);
+  else
+    integrate_and_finish(D, ctl, t0, G, sm.d, &s_last);
   stamp(D, ts);
 }
 

@@ -104,3 +104,42 @@ def test_batch_render_equals_single_scene_render():
         assert np.array_equal(E_ego[k], render_depth(sc, ego[k]))
         assert np.array_equal(E_sky[k], render_depth(sc, sky))
     batch.close()
+
+
+@pytest.mark.gpu
+def test_splat_equals_brute_force():
+    """The splatting renderer (mode 1: each particle tests only the pixels its
+    sphere can cover) gives bitwise the image of the default (mode 0: every
+    pixel tests every particle, the reference's algorithm)."""
+    from paper_2306_01369_b200 import _native as N
+
+    g = golden()
+    try:
+        for k in range(int(g["n_env_cases"])):
+            sc = env_scene(g, k)
+            imgs = {}
+            for mode in (0, 1):
+                N.lib().gg_set_render_mode(mode)
+                imgs[mode] = (render_depth(sc, camera(g, f"c{k}_ego")),
+                              render_depth(sc, camera(g, f"c{k}_sky")))
+            assert np.array_equal(imgs[0][0], imgs[1][0])
+            assert np.array_equal(imgs[0][1], imgs[1][1])
+        # a dense random cloud seen from inside and around it
+        rng = np.random.default_rng(1)
+        x = rng.uniform(-1.0, 1.0, size=(3000, 3))
+        sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)), bodies=[],
+                      params=gg.MaterialParams(radius=0.03))
+        cams = [DepthCamera(kind="perspective", pose=gg.make_pose(gg.so3_exp(np.array([0.3, -0.2, 0.1])),
+                                                                 np.array([0.1, 0.0, -0.2])),
+                            width=64, height=48, fov=1.7, far=5.0),
+                DepthCamera(kind="orthographic", pose=gg.make_pose(np.eye(3), np.array([0.0, 0.0, -3.0])),
+                            width=50, height=40, extent=(2.5, 2.0), far=9.0)]
+        for cam in cams:
+            N.lib().gg_set_render_mode(0)
+            a = render_depth(sc, cam)
+            N.lib().gg_set_render_mode(1)
+            b = render_depth(sc, cam)
+            assert np.array_equal(a, b)
+            assert (a < cam.far).mean() > 0.3
+    finally:
+        N.lib().gg_set_render_mode(0)
