@@ -174,15 +174,17 @@ int alloc_slots(gg_ctx* ctx, int K) {
   D.cgeo = nullptr;
   D.coth = nullptr;
   D.cvb = nullptr;
-  // K records per particle on average: the warp allocator hands out
-  // [0, K * n) (per-owner counts are not limited by K)
-  const size_t slots = static_cast<size_t>(K) * static_cast<size_t>(std::max<long long>(ctx->n, 1));
+  // K records per particle on average: record 0 of particle k at index k,
+  // the block allocator hands out [n, K * n) (per-owner counts are not
+  // limited by K)
+  const size_t slots = static_cast<size_t>(std::max(K, 2)) * static_cast<size_t>(std::max<long long>(ctx->n, 1));
   CK(dalloc(ctx, &D.cgeo, slots));
   CK(dalloc(ctx, &D.coth, slots));
   CK(dalloc(ctx, &D.cvb, slots));
   ctx->K = K;
   D.K = K;
   D.cap_tot = static_cast<long long>(slots);
+  D.nrec0 = std::max<long long>(ctx->n, 1);
   ctx->graph_dirty = true;
   return GG_OK;
 }
@@ -1145,7 +1147,7 @@ int gg_tap_contacts(gg_ctx* ctx, int64_t cap_out, int64_t* count, int32_t* owner
   long long m = 0;
   for (long long k = 0; k < n; ++k) {
     for (int s = 0; s < ci[k].y; ++s) {
-      const size_t idx = static_cast<size_t>(ci[k].x) + s;
+      const size_t idx = s == 0 ? static_cast<size_t>(k) : static_cast<size_t>(ci[k].x) + s - 1;
       const int j = oth[idx];
       if (j == kNullContact) continue;  // a prefilter pass that is no contact
       if (m++ >= cap_out) continue;

@@ -118,8 +118,13 @@ struct Dev {
   float4* cgeo;     // contact records [cap_tot]: (e1.xyz, psi)
   int* coth;        // partner: physical index, or -(body + 1)
   float4* cvb;      // body surface velocity (body records)
-  int2* cinfo;      // per particle {first record, record count} (warp-contiguous CSR)
+  int2* cinfo;      // per particle {CSR offset of its record 1, record count}
   long long cap_tot;  // record capacity
+  // Record 0 of particle k lives at index k (the first nrec0 entries, one per
+  // particle slot, coalesced); records 1.. are warp-contiguous CSR entries
+  // allocated from nrec0 on.  A sweep can then fetch a particle's first
+  // contact together with its cinfo instead of after it.
+  long long nrec0;
   const gg_body* bodies;  // [batch][nb]
   const DevGrid* grids;
   const double* gvals;
@@ -352,7 +357,7 @@ __global__ void k_batch_begin(Dev D) {
     c->bar_count = 0;
     c->done_count = 0;
     c->bar_gen = 0;
-    c->ccursor = 0ull;
+    c->ccursor = static_cast<unsigned long long>(D.nrec0);
   }
   for (int e = t; e < D.E; e += G) {
     acc_reset(D.acc + e);
@@ -575,6 +580,11 @@ __device__ __forceinline__ double pp_d2(double px, double py, double pz, float4 
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
 }
 
+// index of record i of particle k whose CSR records start at off
+__device__ __forceinline__ long long ridx(const Dev& D, int k, long long off, int i) {
+  return i == 0 ? static_cast<long long>(k) : off + i - 1;
+}
+
 // One pp contact record (contact.py:264-272): e1 = d / |d| (j -> i),
 // psi = 2r - |d|, partner q (physical index).  Returns psi.
 __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double dx, double dy,
@@ -634,7 +644,7 @@ struct CandCursor {
 // kPassCap prefilter passes): counts (write == false) or writes records from
 // dst on (write == true), in candidate order — the same order the queue gives.
 __device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, int tid, int k,
-                                           float4 pf, uint32_t total, bool write, long long dst,
+                                           float4 pf, uint32_t total, bool write, long long off,
                                            int& c_pp, unsigned long long& n_coinc,
                                            double& max_psi) {
   const double px = pf.x, py = pf.y, pz = pf.z;
@@ -656,7 +666,7 @@ __device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, i
       continue;
     }
     if (d2 < D.contact_d2) {
-      if (write) max_psi = nmax(max_psi, pp_write(D, dst + c_pp, dx, dy, dz, d2, q));
+      if (write) max_psi = nmax(max_psi, pp_write(D, ridx(D, k, off, c_pp), dx, dy, dz, d2, q));
       ++c_pp;
     }
   }
@@ -666,8 +676,9 @@ __device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, i
 // prefilter (`_near_body`, contact.py:187-203), then the SDF penetration test
 // (sdf.py:472-512); bodies in index order after the particle's pp records,
 // like the reference's per-body concatenation.  write == false only counts.
+// Records of particle k at positions first, first + 1, ... (CSR base off).
 __device__ __forceinline__ int body_contacts(const Dev& D, const gg_body* bodies, float4 pf,
-                                             bool write, long long dst,
+                                             bool write, int k, long long off, int first,
                                              unsigned long long& n_deg, double& max_psi) {
   const double px = pf.x, py = pf.y, pz = pf.z;
   int c = 0;
@@ -684,7 +695,7 @@ __device__ __forceinline__ int body_contacts(const Dev& D, const gg_body* bodies
     int deg;
     if (penetrate(B, D.grids, D.gvals, px, py, pz, D.r, &psi, &nrm, &deg)) {
       if (write) {
-        const long long sl = dst + c;
+        const long long sl = ridx(D, k, off, first + c);
         const d3 vb = body_surface_velocity(B, px, py, pz, nrm, D.r, psi);
         D.cgeo[sl] = make_float4(static_cast<float>(nrm.x), static_cast<float>(nrm.y),
                                  static_cast<float>(nrm.z), static_cast<float>(psi));
@@ -826,10 +837,12 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   }
   // this env's bodies at this step: bodies[step][env][nb]
   const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
-  const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, 0, n_deg, max_psi) : 0;
+  const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, k, 0, 0, n_deg, max_psi) : 0;
   // ---- allocation: one atomic per block ----------------------------------------
+  // (record 0 of each owner is its own slot k; the rest come from the cursor)
   const int tot = c_own + c_b;
-  int wincl = tot;
+  const int talloc = tot > 0 ? tot - 1 : 0;
+  int wincl = talloc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, wincl, o);
@@ -854,7 +867,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   }
   __syncthreads();
   const unsigned long long wbase = sm.wrec[w];
-  const long long my_off = static_cast<long long>(wbase) + (wincl - tot);
+  const long long my_off = static_cast<long long>(wbase) + (wincl - talloc);
   const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
   const bool fits = static_cast<long long>(wbase) + wtot <= D.cap_tot;
   const uint32_t* offw = sm.off[w];
@@ -868,7 +881,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       const bool oovf = __shfl_sync(0xffffffffu, ovf, o);
       if (idx < Tw && !oovf) {
         const uint32_t i = idx - offw[o];
-        const long long dst = oo + i;
+        const long long dst = ridx(D, base + wb + o, oo, static_cast<int>(i));
         const float4 qf = Xh[sm.pass[i][wb + o]];
         const float4 of = sm.pos[wb + o];
         double dx, dy, dz;
@@ -903,7 +916,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         c_pp += c_ex;
         n_coinc += co_ex;
       }
-      if (c_b > 0) body_contacts(D, bodies, pf, true, my_off + c_own, n_deg, max_psi);
+      if (c_b > 0) body_contacts(D, bodies, pf, true, k, my_off, c_own, n_deg, max_psi);
       D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
     }
   }
@@ -1072,7 +1085,10 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
 __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* Win, float4* Wout,
                                                SweepAcc& A) {
   sweep_acc_env(D, A, k);
+  // record 0 (slot k) is fetched with cinfo: one dependent round trip fewer
   const int2 ci = D.cinfo[k];
+  const float4 g0 = D.cgeo[k];
+  const int j0 = D.coth[k];
   // a particle without contacts keeps w = v and is nobody's partner
   // (contacts are symmetric), so its w is never read: skip it entirely
   // (integrate uses dv = 0 for it)
@@ -1080,8 +1096,12 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
   const float4 wf = Win[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  for (int sl = 0; sl < ci.y; ++sl) {
-    const long long idx = static_cast<long long>(ci.x) + sl;
+  if (j0 != kNullContact) {
+    const float4 q0 = (j0 >= 0) ? Win[j0] : D.cvb[k];
+    contact_impulse(D, wx, wy, wz, g0, j0, q0, ax, ay, az, A);
+  }
+  for (int sl = 1; sl < ci.y; ++sl) {
+    const long long idx = static_cast<long long>(ci.x) + sl - 1;
     const float4 g = D.cgeo[idx];
     const int j = D.coth[idx];
     if (j == kNullContact) continue;
@@ -1113,9 +1133,10 @@ struct RegContacts {
     for (int s = 0; s < kRegSlots; ++s) {
       j[s] = 0;
       if (s < c) {
-        g[s] = D.cgeo[off + s];
-        j[s] = D.coth[off + s];
-        if (j[s] < 0) qb[s] = D.cvb[off + s];
+        const long long r = ridx(D, k, off, s);
+        g[s] = D.cgeo[r];
+        j[s] = D.coth[r];
+        if (j[s] < 0) qb[s] = D.cvb[r];
       }
     }
     wx = w0.x;
@@ -1135,7 +1156,7 @@ struct RegContacts {
     for (int s = 0; s < kRegSlots; ++s)
       if (s < c && j[s] != kNullContact) contact_impulse(D, wx, wy, wz, g[s], j[s], q[s], ax, ay, az, A);
     for (int s = kRegSlots; s < c; ++s) {
-      const long long idx = static_cast<long long>(off) + s;
+      const long long idx = static_cast<long long>(off) + s - 1;
       const float4 gg = D.cgeo[idx];
       const int jj = D.coth[idx];
       if (jj == kNullContact) continue;
@@ -1279,7 +1300,7 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
     ctl->done_count = 0;
     ctl->bar_count = 0;
     ctl->bar_gen = 0;
-    ctl->ccursor = 0ull;
+    ctl->ccursor = static_cast<unsigned long long>(D.nrec0);
     if (s_err) return;  // an error was raised this step: no commit
     if (D.E == 1) {
       write_report(D, D.reports[step], D.acc, ke_tot);
@@ -1463,19 +1484,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   // narrowphase + bodies; the sweeps below use the same particle -> block
   // map, so a particle's records were written by its own block (visible
   // after the __syncthreads in sweep_acc_init)
-  // One particle per thread (G >= n): the particles are spread evenly over
-  // ALL co-resident blocks (P per block) rather than packed into the first
-  // n / blockDim blocks, so no SM carries two full blocks while others idle.
+  // one particle per thread when G >= n: particle t0 (its contacts, sweeps
+  // and integration all on this thread)
   const bool one_per_thread = G >= D.n;
-  const int P = one_per_thread ? (D.n + gridDim.x - 1) / gridDim.x : blockDim.x;
-  const int kr = blockIdx.x * P + threadIdx.x;                // this thread's particle
-  const bool kr_live = one_per_thread && threadIdx.x < P && kr < D.n_own;
+  const int kr = t0;
+  const bool kr_live = one_per_thread && kr < D.n_own;
   if (ok) {
-    if (one_per_thread)
-      ph_contacts(D, ctl, blockIdx.x * P, P, sm);
-    else
-      for (int base = blockIdx.x * blockDim.x; base < D.n; base += G)
-        ph_contacts(D, ctl, base, blockDim.x, sm);
+    for (int base = blockIdx.x * blockDim.x; base < D.n; base += G)
+      ph_contacts(D, ctl, base, blockDim.x, sm);
   }
   stamp(D, ts);
   // split schedule: k_solve_cluster runs the sweeps and the commit (and
@@ -1484,7 +1500,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   const Layout L = layout(D, ctl);
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   SweepAcc A;
-  sweep_acc_init(D, A, sbm, one_per_thread ? kr : t0, one_per_thread ? blockIdx.x * P : -1);
+  sweep_acc_init(D, A, sbm, t0);
   if (one_per_thread && gridDim.x <= kMaxFusedBlocks) {
     // One particle per thread: its contacts (first kRegSlots) and its own w
     // stay in registers for all sweeps.  Jacobi sweep s of a block only needs
@@ -1503,9 +1519,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
       __syncthreads();
       {
         for (int sl = 0; sl < RC.c; ++sl) {
-          const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl];
+          const int j = sl < kRegSlots ? RC.j[sl] : D.coth[RC.off + sl - 1];
           if (j >= 0 && j != kNullContact) {
-            const int b = j / P;
+            const int b = j / blockDim.x;
             if (b != static_cast<int>(blockIdx.x)) atomicOr(&s_nbmask[b >> 5], 1u << (b & 31));
           }
         }
@@ -1563,12 +1579,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   }
   stamp(D, ts);
   sweep_acc_flush(D, A, sm.d);
-  // integrate exactly the particles this thread swept: the last sweep's w of
-  // another block's particle is not ordered before this read (no barrier)
-  if (one_per_thread && gridDim.x <= kMaxFusedBlocks)
-    integrate_and_finish(D, ctl, kr_live ? kr : D.n_own, D.n_own + 1, sm.d, &s_last);
-  else
-    integrate_and_finish(D, ctl, t0, G, sm.d, &s_last);
+  // integrate exactly the particles this thread swept (t0, t0 + G, ...): the
+  // last sweep's w of another block's particle is not ordered before the read
+  integrate_and_finish(D, ctl, t0, G, sm.d, &s_last);
   stamp(D, ts);
 }
 
