@@ -268,6 +268,9 @@ def merge_solve_kinds(lib, kind_ms, kind_n):
     if cnt.get("k_finish", 0) > 0:
         ms["k_solve"] = ms.get("k_solve", 0.0) + ms["k_sweep"] + ms["k_finish"]
         cnt["k_solve"] = cnt.get("k_solve", 0) + cnt["k_finish"]
+    if cnt.get("k_exact", 0) > 0:  # the large-n contact phase runs as k_cand + k_exact
+        ms["k_narrow"] = ms.get("k_narrow", 0.0) + ms["k_cand"] + ms["k_exact"]
+        cnt["k_narrow"] = cnt.get("k_narrow", 0) + cnt["k_exact"]
     out = [nm for nm in ms if nm != "(unused)"]
     return out, np.array([ms[nm] for nm in out]), np.array([cnt[nm] for nm in out])
 
@@ -276,7 +279,9 @@ def time_shares(names, kind_ms, kind_n) -> dict:
     """Share of the step per kernel kind (k_solve, when it is the sum of the
     per-sweep parts, is reported but not double counted)."""
     parts = "k_finish" in names and kind_n[names.index("k_finish")] > 0
-    total = sum(float(kind_ms[k]) for k, nm in enumerate(names) if not (parts and nm == "k_solve"))
+    nparts = "k_exact" in names and kind_n[names.index("k_exact")] > 0
+    total = sum(float(kind_ms[k]) for k, nm in enumerate(names)
+                if not ((parts and nm == "k_solve") or (nparts and nm == "k_narrow")))
     return {nm: float(kind_ms[k]) / max(total, 1e-9) for k, nm in enumerate(names) if kind_n[k] > 0}
 
 

@@ -565,7 +565,14 @@ __device__ __forceinline__ uint32_t nb_hash(const Dev& D, int o, long long c0, l
                                             long long c2, const uint32_t tx[3], const uint32_t ty[3],
                                             const uint32_t tz[3]) {
   const int ox = o / 9, oy = (o / 3) % 3, oz = o % 3;
-  if (D.H.pow2) return (tx[ox] ^ ty[oy] ^ tz[oz]) & D.H.mask;
+  // selects instead of array indexing: o is a runtime value in the
+  // de-duplication loop, and an indexed array would live in local memory
+  if (D.H.pow2) {
+    const uint32_t a = ox == 0 ? tx[0] : (ox == 1 ? tx[1] : tx[2]);
+    const uint32_t b = oy == 0 ? ty[0] : (oy == 1 ? ty[1] : ty[2]);
+    const uint32_t c = oz == 0 ? tz[0] : (oz == 1 ? tz[1] : tz[2]);
+    return (a ^ b ^ c) & D.H.mask;
+  }
   return hash_cell64(c0 + ox - 1, c1 + oy - 1, c2 + oz - 1, D.H.n_h);
 }
 
