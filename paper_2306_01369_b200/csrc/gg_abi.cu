@@ -181,6 +181,11 @@ int alloc_slots(gg_ctx* ctx, int K) {
   CK(dalloc(ctx, &D.cgeo, slots));
   CK(dalloc(ctx, &D.coth, slots));
   CK(dalloc(ctx, &D.cvb, slots));
+  // defined contents: the sweeps load a particle's slot-0 record together
+  // with its count, before knowing whether it has one
+  CK(cudaMemset(D.cgeo, 0, sizeof(float4) * slots));
+  CK(cudaMemset(D.coth, 0, sizeof(int) * slots));
+  CK(cudaMemset(D.cvb, 0, sizeof(float4) * slots));
   ctx->K = K;
   D.K = K;
   D.cap_tot = static_cast<long long>(slots);
@@ -226,7 +231,7 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
 // every entry point starts with zeroed bucket/tile counts (a failed step may
 // leave them dirty; within a batch each scatter re-zeroes them)
 int begin_batch(gg_ctx* ctx, cudaStream_t s) {
-  CK(cudaMemsetAsync(ctx->D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->n_h), s));
+  CK(cudaMemsetAsync(ctx->D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->D.nh_tot), s));  // every env's table
   CK(cudaMemsetAsync(ctx->D.tile, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->ntiles), s));
   CK(cudaMemsetAsync(ctx->D.bflags, 0, sizeof(unsigned) * std::max(ctx->fused_grid, 1), s));
   const long long work = std::max<long long>(ctx->E, static_cast<long long>(ctx->E) * std::max(ctx->max_bodies, 1) * 3);

@@ -277,3 +277,35 @@ def test_spatial_hash_kats():
             n_h = int(key.split("_")[1])
             cells = g["cells"] if key.startswith("h_") else g["big_cells"]
             assert np.array_equal(gg.spatial_hash(cells, n_h), g[key]), key
+
+
+@pytest.mark.parametrize("mode", [0, 3])
+def test_crowded_owners_overflow_path(mode):
+    """Clusters of 40 near-coincident particles: every owner has more float32
+    prefilter passes than the warp queue holds (16), so the owner's exact
+    inline path and the record-capacity growth run.  Contacts and the step
+    must still match the oracle (counters exact, state 1e-5)."""
+    from paper_2306_01369_b200 import _native as N
+    from paper_2306_01369_b200.engine import engine_for
+
+    rng = np.random.default_rng(5)
+    centres = rng.uniform(0.0, 2.0, size=(25, 3)) + np.array([0.0, 0.0, 0.2])
+    x = (np.repeat(centres, 40, axis=0) + rng.normal(scale=0.02, size=(1000, 3)))
+    x = x.astype(np.float32).astype(np.float64)
+    params = gg.MaterialParams(timestep=5e-4)
+    sc = gg.Scene(particles=gg.ParticleSet(x.copy(), np.zeros_like(x)),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")], params=params)
+    eng = engine_for(sc)
+    eng.max_contacts = 2  # force record-capacity growth as well
+    eng.prepare(sc)
+    N.lib().gg_set_solve_mode(eng.ctx, mode)
+    _, rep = gg.step(sc)
+    from helpers import BodyState
+
+    floor = [BodyState(gg.HalfSpace(), np.eye(4), np.zeros(3), np.zeros(3))]
+    x1, v1, orep, _, _ = O.step(x, np.zeros_like(x), params, floor, gg.default_table_size(1000))
+    assert rep.n_contacts == orep["n_contacts"] and rep.n_contacts > 1000 * 16
+    assert rep.n_candidates == orep["n_candidates"]
+    assert rep.n_coincident_skipped == orep["n_coincident_skipped"]
+    assert rel_err(sc.particles.positions, x1) <= TOL
+    assert rel_err(sc.particles.velocities, v1) <= TOL
