@@ -61,7 +61,9 @@ def parse():
     ap.add_argument("--envs", type=int, default=4096, help="envs workload: total envs")
     ap.add_argument("--env-particles", type=int, default=2000)
     ap.add_argument("--settle", type=int, default=3000)
-    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--flush-mb", type=int, default=-1,
+                    help="L2 flush before every timed step (MB); default: 512 for hero50k "
+                         "(its working set fits L2), 0 for the larger beds (inputs > L2)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=20)
@@ -523,8 +525,7 @@ def run_envs(args, dist: Dist):
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
             "data": "synthetic (seeded bulldozer beds, settled 100 substeps)",
             "config": {**desc, "parallelism": f"env shards x{dist.world}",
-                       "l2": f"flushed before every timed step ({args.flush_mb} MB write); "
-                             "state (~0.5 GB) exceeds L2 anyway",
+                       "l2": l2_note(args, batch.E * batch.n * 200 / 2**20),
                        "c_pp": c_pp, "c_b": c_b, "n_h_per_env": batch.n_h},
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(launches),
@@ -761,7 +762,7 @@ def run_ours(args, dist: Dist):
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
             "data": "synthetic (seeded bed, settled on GPU)",
             "config": {**desc, "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
-                       "l2": f"flushed before every timed step ({args.flush_mb} MB write)",
+                       "l2": l2_note(args, n * 200 / 2**20),
                        "c_pp": c_pp, "c_b": c_b, "n_h": eng.n_h,
                        "warm_ms_per_step": None if t_warm is None else t_warm / K},
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk,
@@ -770,8 +771,17 @@ def run_ours(args, dist: Dist):
         print(json.dumps(line), flush=True)
 
 
+def l2_note(args, working_set_mb: float) -> str:
+    if args.flush_mb > 0:
+        return f"flushed before every timed step ({args.flush_mb} MB write)"
+    return (f"not flushed: the step's working set (~{working_set_mb:.0f} MB) is larger than the "
+            f"126 MB L2")
+
+
 def main():
     args = parse()
+    if args.flush_mb < 0:
+        args.flush_mb = 512 if args.workload == "hero50k" else 0
     dist = Dist()
     try:
         if args.impl == "reference":
