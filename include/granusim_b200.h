@@ -310,6 +310,18 @@ int gg_slab_halo_pack(gg_ctx* ctx, int32_t sweep, void* out_lo, void* out_hi);
 int gg_slab_halo_unpack(gg_ctx* ctx, int32_t sweep, const void* in_lo, const void* in_hi);
 int gg_slab_finish(gg_ctx* ctx, gg_report* report, double* body_momentum);
 int64_t gg_slab_owned(const gg_ctx* ctx);
+/* Peer-memory halo (NVLink P2P): instead of halo_pack -> host exchange ->
+ * halo_unpack, every rank allocates a mailbox (gg_slab_mailbox: cap halo
+ * records per side, returns its 64-byte CUDA IPC handle), opens its
+ * neighbours' (gg_slab_connect, side 0 = lo, 1 = hi), and after sweep s calls
+ * gg_slab_halo_p2p(s, seq) with a sequence number that grows by one per sweep
+ * on every rank: it stores its boundary w straight into the neighbours'
+ * mailboxes, raises their flags (system-scope release) and waits on the
+ * device for its own (bounded: a dead neighbour fails the step with GG_ECUDA
+ * instead of hanging).  No host work between sweeps. */
+int gg_slab_mailbox(gg_ctx* ctx, int64_t cap, void* handle_out);
+int gg_slab_connect(gg_ctx* ctx, int32_t side, const void* handle);
+int gg_slab_halo_p2p(gg_ctx* ctx, int32_t sweep, uint64_t seq);
 int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, int64_t* n_own);
 
 #ifdef __cplusplus

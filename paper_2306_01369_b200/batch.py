@@ -124,6 +124,99 @@ class TrackSteeringBatch(BatchDriver):
         return P, W, V
 
 
+def so3_exp_batch(w: np.ndarray) -> np.ndarray:
+    """Rodrigues for (E, 3) rotation vectors (kinematics.py:39-47), first
+    order below 1e-12 rad like the reference."""
+    w = np.asarray(w, dtype=np.float64)
+    E = len(w)
+    angle = np.linalg.norm(w, axis=1)
+    small = angle < 1e-12
+    safe = np.where(small, 1.0, angle)
+    k = w / safe[:, None]
+    K = np.zeros((E, 3, 3))
+    K[:, 0, 1], K[:, 0, 2] = -k[:, 2], k[:, 1]
+    K[:, 1, 0], K[:, 1, 2] = k[:, 2], -k[:, 0]
+    K[:, 2, 0], K[:, 2, 1] = -k[:, 1], k[:, 0]
+    eye = np.broadcast_to(np.eye(3), (E, 3, 3))
+    R = eye + np.sin(angle)[:, None, None] * K + (1.0 - np.cos(angle))[:, None, None] * (K @ K)
+    if small.any():
+        S = np.zeros((E, 3, 3))
+        S[:, 0, 1], S[:, 0, 2] = -w[:, 2], w[:, 1]
+        S[:, 1, 0], S[:, 1, 2] = w[:, 2], -w[:, 0]
+        S[:, 2, 0], S[:, 2, 1] = -w[:, 1], w[:, 0]
+        R[small] = (eye + S)[small]
+    return R
+
+
+class ChainBatch(BatchDriver):
+    """E copies of a velocity-controlled kinematic chain (KinematicChain +
+    ChainLinkDriver, kinematics.py:256-322) with array joint state (E, J):
+    ``command(qd (E, J))``; every rollout step first advances the joints by dt
+    (ExcavationEnv's substep loop, envs.py:336-341), then evaluates the forward
+    kinematics of link ``link_index`` for all envs at once."""
+
+    def __init__(self, links, n_envs: int, link_index: int, base_pose: np.ndarray | None = None):
+        self.links = list(links)
+        self.n_envs = n_envs
+        self.link_index = link_index
+        J = len(self.links)
+        self.base_pose = np.eye(4) if base_pose is None else np.asarray(base_pose, dtype=np.float64)
+        self.q = np.zeros((n_envs, J))
+        self.qd = np.zeros((n_envs, J))
+        self.limits = np.array([l.velocity_limit for l in self.links])
+        self.cmd = np.zeros((n_envs, J))
+
+    def command(self, qd_cmd) -> None:
+        self.cmd = np.asarray(qd_cmd, dtype=np.float64).reshape(self.n_envs, len(self.links))
+
+    def advance(self, dt: float) -> None:
+        self.qd = np.clip(self.cmd, -self.limits, self.limits)
+        self.q = self.q + dt * self.qd
+
+    def fk(self):
+        """(poses (E, J, 4, 4), omega (E, J, 3), v_origin (E, J, 3)) like KinematicChain.fk."""
+        E, J = self.n_envs, len(self.links)
+        poses = np.empty((E, J, 4, 4))
+        sw = np.empty((E, J, 3))
+        sv = np.empty((E, J, 3))
+        for i, link in enumerate(self.links):
+            parent = np.broadcast_to(self.base_pose, (E, 4, 4)) if link.parent < 0 else poses[:, link.parent]
+            joint = parent @ link.origin
+            axis_w = joint[:, :3, :3] @ link.axis
+            local = np.zeros((E, 4, 4))
+            local[:, 3, 3] = 1.0
+            if link.joint_type == "revolute":
+                local[:, :3, :3] = so3_exp_batch(link.axis[None, :] * self.q[:, i:i + 1])
+                w_j = axis_w * self.qd[:, i:i + 1]
+                v_j = -np.cross(w_j, joint[:, :3, 3])
+            else:
+                local[:, :3, :3] = np.eye(3)
+                local[:, :3, 3] = link.axis[None, :] * self.q[:, i:i + 1]
+                w_j = np.zeros((E, 3))
+                v_j = axis_w * self.qd[:, i:i + 1]
+            poses[:, i] = joint @ local
+            if link.parent < 0:
+                sw[:, i], sv[:, i] = w_j, v_j
+            else:
+                sw[:, i], sv[:, i] = sw[:, link.parent] + w_j, sv[:, link.parent] + v_j
+        return poses, sw, sv + np.cross(sw, poses[:, :, :3, 3])
+
+    def current(self):
+        P, W, V = self.fk()
+        i = self.link_index
+        return P[:, i], W[:, i], V[:, i]
+
+    def rollout(self, T, dt, ts):
+        E = self.n_envs
+        P = np.empty((T, E, 4, 4))
+        W = np.empty((T, E, 3))
+        V = np.empty((T, E, 3))
+        for k in range(T):
+            self.advance(dt)
+            P[k], W[k], V[k] = self.current()
+        return P, W, V
+
+
 def shard_envs(n_envs: int, rank: int, world: int) -> np.ndarray:
     """Env ids owned by ``rank``: e with e mod world == rank (no communication)."""
     return np.arange(rank, n_envs, world)

@@ -82,6 +82,11 @@ struct gg_ctx {
   int* d_holes = nullptr;
   int* d_movers = nullptr;
   int* d_map[2] = {nullptr, nullptr};
+  // peer-memory halo (gg_slab_mailbox / gg_slab_connect / gg_slab_halo_p2p)
+  Mailbox* mbox = nullptr;
+  long long mbox_cap = 0;
+  Mailbox* peer[2] = {nullptr, nullptr};
+  bool peer_ipc[2] = {false, false};  // opened with cudaIpcOpenMemHandle
 };
 
 namespace {
@@ -677,6 +682,8 @@ int gg_destroy(gg_ctx* ctx) {
     for (int g = 0; g < 2; ++g)
       if (ctx->gexec[g]) cudaGraphExecDestroy(ctx->gexec[g]);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
+    for (int side = 0; side < 2; ++side)
+      if (ctx->peer_ipc[side] && ctx->peer[side]) cudaIpcCloseMemHandle(ctx->peer[side]);
     for (void* p : ctx->owned) cudaFree(p);
     ctx->owned.clear();
     if (ctx->h_bodies) cudaFreeHost(ctx->h_bodies);
@@ -1668,3 +1675,77 @@ extern "C" int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cam
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gg_render_depth");
   return GG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Peer-memory halo (gg_slab.cuh: Mailbox, k_halo_push, k_halo_pull)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int gg_slab_mailbox(gg_ctx* ctx, int64_t cap, void* handle_out) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (cap < 1 || !handle_out) return fail(ctx, GG_EINVAL, "mailbox needs cap >= 1 and a handle buffer");
+  DeviceGuard guard(ctx->device);
+  if (ctx->mbox && ctx->mbox_cap < cap) {
+    dfree(ctx, ctx->mbox);
+    ctx->mbox = nullptr;
+  }
+  const size_t bytes = sizeof(Mailbox) + sizeof(float4) * 4 * static_cast<size_t>(cap);
+  if (!ctx->mbox) {
+    // plain cudaMalloc (IPC-exportable), zeroed flags
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    ctx->owned.push_back(p);
+    ctx->mbox = static_cast<Mailbox*>(p);
+    ctx->mbox_cap = cap;
+    CK(cudaMemset(p, 0, bytes));
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->mbox));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return GG_OK;
+}
+
+int gg_slab_connect(gg_ctx* ctx, int32_t side, const void* handle) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (side != 0 && side != 1) return fail(ctx, GG_EINVAL, "side must be 0 (lo) or 1 (hi)");
+  DeviceGuard guard(ctx->device);
+  if (ctx->peer_ipc[side] && ctx->peer[side]) cudaIpcCloseMemHandle(ctx->peer[side]);
+  ctx->peer[side] = nullptr;
+  ctx->peer_ipc[side] = false;
+  if (!handle) return GG_OK;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ctx->peer[side] = static_cast<Mailbox*>(p);
+  ctx->peer_ipc[side] = true;
+  return GG_OK;
+}
+
+int gg_slab_halo_p2p(gg_ctx* ctx, int32_t sweep, uint64_t seq) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (!ctx->mbox) return fail(ctx, GG_EINVAL, "gg_slab_mailbox has not been called");
+  const long long cap = ctx->mbox_cap;
+  for (int side = 0; side < 2; ++side)
+    if (ctx->ghost_out[side] > cap || ctx->ghost_in[side] > cap)
+      return fail(ctx, GG_ECAPACITY, "slab mailbox too small for this step's halo");
+  if ((ctx->slab.has_lo && !ctx->peer[0]) || (ctx->slab.has_hi && !ctx->peer[1]))
+    return fail(ctx, GG_EINVAL, "slab neighbour mailbox not connected");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const Dev D = slab_dev(ctx);
+  k_halo_push<<<2, 1024, 0, s>>>(D, sweep, static_cast<unsigned long long>(seq), ctx->peer[0],
+                                 ctx->peer[1], cap, ctx->d_map[0], ctx->d_map[1],
+                                 static_cast<int>(ctx->ghost_out[0]), static_cast<int>(ctx->ghost_out[1]));
+  k_halo_pull<<<2, 1024, 0, s>>>(D, sweep, static_cast<unsigned long long>(seq), ctx->mbox, cap,
+                                 static_cast<int>(ctx->ghost_in[0]), static_cast<int>(ctx->ghost_in[1]),
+                                 20000000000ull /* 20 s */);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+}  // extern "C"

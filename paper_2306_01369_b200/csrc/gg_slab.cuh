@@ -175,3 +175,80 @@ __global__ void k_slab_load(Dev D, const double* __restrict__ x, const double* _
 }
 
 }  // namespace gg
+
+namespace gg {
+
+// ---------------------------------------------------------------------------
+// Peer-memory halo (NVLink P2P through CUDA IPC mappings).  Every rank owns a
+// mailbox that its neighbours write into directly; after every sweep a rank
+// pushes its boundary particles' w into the two neighbours' mailboxes and
+// raises a per-side sequence flag with a system-scope release, then pulls its
+// own mailbox once both flags reached this sweep's sequence number.  No host
+// work between sweeps.  Data is double-buffered by sweep parity: a sender can
+// only get one sweep ahead of its receiver (it waits for the receiver's own
+// push of that sweep before sweeping again).
+// ---------------------------------------------------------------------------
+struct Mailbox {
+  unsigned long long flag[2];  // [side]: last sequence number delivered from the lo / hi neighbour
+  unsigned long long pad[6];
+  // float4 data[2 parity][2 side][cap] follows
+};
+
+__device__ __forceinline__ float4* mailbox_data(Mailbox* m, long long cap, int parity, int side) {
+  return reinterpret_cast<float4*>(m + 1) + (static_cast<long long>(parity) * 2 + side) * cap;
+}
+
+// block 0 -> the lo neighbour (its side 1), block 1 -> the hi neighbour (its side 0)
+__global__ void k_halo_push(Dev D, int s, unsigned long long seq, Mailbox* peer_lo, Mailbox* peer_hi,
+                            long long cap, const int* __restrict__ map_lo, const int* __restrict__ map_hi,
+                            int n_lo, int n_hi) {
+  const int side = blockIdx.x;  // 0: push to lo, 1: push to hi
+  Mailbox* peer = side == 0 ? peer_lo : peer_hi;
+  const int m = side == 0 ? n_lo : n_hi;
+  if (peer == nullptr) return;  // block-uniform
+  const int* map = side == 0 ? map_lo : map_hi;
+  float4* dst = mailbox_data(peer, cap, s & 1, side == 0 ? 1 : 0);
+  const float4* W = D.W[s & 1];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) dst[i] = W[map[i]];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // cumulative: the block's peer stores before the flag
+    unsigned long long* f = &peer->flag[side == 0 ? 1 : 0];
+    asm volatile("st.release.sys.u64 [%0], %1;" ::"l"(f), "l"(seq) : "memory");
+  }
+}
+
+// block 0 <- the lo neighbour (my side 0), block 1 <- the hi neighbour (my side 1)
+__global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine, long long cap,
+                            int n_lo, int n_hi, unsigned long long timeout_ns) {
+  const int side = blockIdx.x;
+  const int m = side == 0 ? n_lo : n_hi;
+  if (m == 0) return;  // block-uniform: this side sends nothing this step
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int ok = 1;
+    for (;;) {
+      asm volatile("ld.relaxed.sys.u64 %0, [%1];" : "=l"(v) : "l"(&mine->flag[side]) : "memory");
+      if (v >= seq) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {  // a neighbour died: fail instead of hanging the GPU
+        ok = 0;
+        break;
+      }
+      __nanosleep(200);
+    }
+    asm volatile("ld.acquire.sys.u64 %0, [%1];" : "=l"(v) : "l"(&mine->flag[side]) : "memory");
+    s_ok = ok;
+    if (!ok) raise_err(D.ctl, GG_ECUDA);
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const float4* src = mailbox_data(mine, cap, s & 1, side);
+  const int at = D.n_own + (side == 0 ? 0 : n_lo);
+  float4* W = D.W[s & 1];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) W[at + i] = src[i];
+}
+
+}  // namespace gg

@@ -22,9 +22,16 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .batch import SceneBatch, StaticBatch, TrackSteeringBatch
+from .batch import ChainBatch, SceneBatch, StaticBatch, TrackSteeringBatch
 from .render import DepthCamera, render_batch
-from .kinematics import TrackSteeringDriver, TrackSteeringState, make_pose
+from .kinematics import (
+    ChainLink,
+    ChainLinkDriver,
+    KinematicChain,
+    TrackSteeringDriver,
+    TrackSteeringState,
+    make_pose,
+)
 from .scene import BoxRegion, MaterialParams, ParticleSet, RigidBody, Scene, seed_particles_grid
 from .sdf import Box, HalfSpace
 
@@ -226,6 +233,112 @@ class BatchedBulldozerEnv:
                 "kinetic_energy": last["kinetic_energy"].copy(),
                 "in_goal": ins, "t": self.batch.t.copy()}
         return self._observe(), rew, done, info
+
+    def close(self) -> None:
+        if self.batch is not None:
+            self.batch.close()
+            self.batch = None
+
+
+# ---------------------------------------------------------------------------
+# Excavation: the 7-joint arm with a Box scoop (envs.py:233-348)
+# ---------------------------------------------------------------------------
+def excavation_links() -> list:
+    """The ExcavationEnv chain (envs.py:250-266): 7 revolute joints, axes
+    up/side alternating then x, link heights 0.3 ... 0.1, velocity limit 1."""
+    up, side = np.array([0.0, 0.0, 1.0]), np.array([0.0, 1.0, 0.0])
+    axes = [up, side, up, side, up, side, np.array([1.0, 0.0, 0.0])]
+    heights = [0.3, 0.3, 0.25, 0.25, 0.2, 0.15, 0.1]
+    return [ChainLink(parent=k - 1, origin=make_pose(np.eye(3), np.array([0.0, 0.0, heights[k]])),
+                      joint_type="revolute", axis=axes[k], velocity_limit=1.0) for k in range(7)]
+
+
+def excavation_scene(seed: int, n_particles: int = 300, timestep: float = 2e-3) -> Scene:
+    """The scene of ``ExcavationEnv.reset(seed)`` (envs.py:268-292)."""
+    rng = np.random.default_rng(seed)
+    params = MaterialParams(radius=0.05, timestep=timestep)
+    particles = seed_particles_grid(BoxRegion(np.array([0.2, -0.6, 0.05]), np.array([1.4, 0.6, 0.35])),
+                                    params.radius, jitter=0.3, rng=rng)
+    if particles.count > n_particles:
+        particles = ParticleSet(particles.positions[:n_particles], particles.velocities[:n_particles])
+    chain = KinematicChain(excavation_links())
+    scoop = RigidBody(Box(np.array([0.15, 0.1, 0.04])), driver=ChainLinkDriver(chain, 6), name="scoop")
+    ground = RigidBody(HalfSpace(), name="ground")
+    return Scene(particles=particles, bodies=[ground, scoop], params=params, seed=seed)
+
+
+class BatchedExcavationEnv:
+    """E excavation envs in lock step (ExcavationEnv, envs.py:233-348): the
+    joints of all arms advance with array math (``ChainBatch``), the scoop
+    poses go to the device as one body table per substep batch, and the
+    observation (36x36 ego camera on the end effector, 72x36 sky) is rendered
+    on the device.  Task-less like the reference: reward 0."""
+
+    action_shape = (7,)
+
+    def __init__(self, n_envs: int, n_particles: int = 300, frame_skip: int = 10,
+                 time_budget: float = 20.0, timestep: float = 2e-3, device: int = 0,
+                 render: bool = True):
+        if n_envs < 1:
+            raise ValueError("n_envs must be >= 1")
+        self.n_envs, self.n_particles = n_envs, n_particles
+        self.frame_skip, self.timestep = frame_skip, timestep
+        self.episode_length = int(round(time_budget / (frame_skip * timestep)))
+        self.device, self.render = device, render
+        self.batch: SceneBatch | None = None
+        self.chain: ChainBatch | None = None
+        self._steps = 0
+        self.sky_camera = DepthCamera(
+            kind="orthographic",
+            pose=make_pose(np.array([[1.0, 0.0, 0.0], [0.0, -1.0, 0.0], [0.0, 0.0, -1.0]]),
+                           np.array([0.7, 0.0, 4.0])),
+            width=72, height=36, extent=(4.0, 2.0), far=10.0)
+        self.ego_local = make_pose(np.array([[0.0, 0.0, 1.0], [0.0, 1.0, 0.0], [-1.0, 0.0, 0.0]]).T,
+                                   np.array([0.0, 0.0, 0.2]))
+        self.ego_camera = DepthCamera(kind="perspective", width=36, height=36, far=10.0)
+
+    def reset(self, seeds=None):
+        E = self.n_envs
+        seeds = np.arange(E) if seeds is None else np.asarray(seeds, dtype=np.int64)
+        if len(seeds) != E:
+            raise ValueError(f"need {E} seeds, got {len(seeds)}")
+        scenes = [excavation_scene(int(s), self.n_particles, self.timestep) for s in seeds]
+        counts = {sc.particles.count for sc in scenes}
+        if len(counts) != 1:
+            raise ValueError(f"seeded beds differ in size {sorted(counts)}: lower n_particles")
+        self.chain = ChainBatch(excavation_links(), E, link_index=6)
+        if self.batch is not None:
+            self.batch.close()
+        self.batch = SceneBatch(scenes, body_drivers={0: StaticBatch(E), 1: self.chain},
+                                device=self.device)
+        self._steps = 0
+        return self._observe()
+
+    def _observe(self):
+        P, _, _ = self.chain.fk()
+        end = P[:, -1]
+        yaw = np.arctan2(end[:, 1, 0], end[:, 0, 0])
+        pose = np.stack([end[:, 0, 3], end[:, 1, 3], yaw], axis=1)
+        if not self.render:
+            return pose
+        ego, sky = render_batch(self.batch, [self.ego_camera, self.sky_camera],
+                                [end @ self.ego_local, None])
+        return BatchObservation(ego=ego, sky=sky, pose=pose)
+
+    def step(self, actions):
+        if self.batch is None:
+            raise RuntimeError("step called before reset")
+        a = np.asarray(actions, dtype=np.float64)
+        if a.shape != (self.n_envs, 7):
+            raise ValueError(f"actions shape must be ({self.n_envs}, 7), got {a.shape}")
+        if not np.all(np.isfinite(a)):
+            raise ValueError("action must be finite")
+        self.chain.command(np.clip(a, -1.0, 1.0) * self.chain.limits)
+        reps, _ = self.batch.run_raw(self.frame_skip)
+        self._steps += 1
+        done = np.full(self.n_envs, self._steps >= self.episode_length)
+        info = {"n_contacts": reps[-1]["n_contacts"].copy(), "t": self.batch.t.copy()}
+        return self._observe(), np.zeros(self.n_envs), done, info
 
     def close(self) -> None:
         if self.batch is not None:

@@ -192,7 +192,8 @@ class SlabBed:
 
     def __init__(self, scene, rank: int = 0, world: int = 1, device: int = 0,
                  backend: str | None = None, cuts: np.ndarray | None = None,
-                 capacity: float = 1.6, max_contacts: int = 16, resort_every: int = 8):
+                 capacity: float = 1.6, max_contacts: int = 16, resort_every: int = 8,
+                 halo: str = "host"):
         from .engine import Engine
 
         self.scene = scene
@@ -227,6 +228,31 @@ class SlabBed:
         self.tr = SlabTransport(rank, world, device, lib.gg_stream(self.ctx), backend)
         self.buf_cap = max(4096, self.cap // 2)
         self._alloc()
+        if halo not in ("host", "p2p"):
+            raise ValueError("halo must be 'host' or 'p2p'")
+        self.halo = halo if world > 1 else "host"
+        self.seq = 0
+        if self.halo == "p2p":
+            self._connect_mailboxes()
+
+    def _connect_mailboxes(self) -> None:
+        """Per-sweep halo through peer memory: export this rank's mailbox
+        (CUDA IPC), open the neighbours' (gg_slab_connect)."""
+        import torch.distributed as td
+
+        lib = N.lib()
+        # one mailbox size on every rank: a sender addresses the receiver's
+        # mailbox with its own copy of the capacity
+        cap = int(self.tr.allreduce(np.array([float(self.buf_cap)]), "max")[0])
+        h = np.zeros(64, dtype=np.uint8)
+        N.check(self.ctx, lib.gg_slab_mailbox(self.ctx, cap, N.ptr(h)), "mailbox")
+        handles = [None] * self.world
+        td.all_gather_object(handles, h.tobytes())
+        for side, peer in ((0, self.rank - 1), (1, self.rank + 1)):
+            if 0 <= peer < self.world:
+                hp = np.frombuffer(handles[peer], dtype=np.uint8).copy()
+                N.check(self.ctx, lib.gg_slab_connect(self.ctx, side, N.ptr(hp)), "connect")
+        td.barrier()
 
     def _alloc(self):
         e = self.tr.empty
@@ -285,7 +311,10 @@ class SlabBed:
         S = int(self.params.solver_iterations)
         for s in range(S):
             N.check(self.ctx, lib.gg_slab_sweep(self.ctx, s), "slab sweep")
-            if s < S - 1 and self.world > 1:
+            if s < S - 1 and self.halo == "p2p":
+                self.seq += 1
+                N.check(self.ctx, lib.gg_slab_halo_p2p(self.ctx, s, self.seq), "halo p2p")
+            elif s < S - 1 and self.world > 1:
                 N.check(self.ctx, lib.gg_slab_halo_pack(self.ctx, s, self._p(self.h_slo),
                                                         self._p(self.h_shi)), "halo pack")
                 self.tr.exchange(self.h_slo, n_out[0], self.h_shi, n_out[1], self.h_rlo, g_lo,

@@ -326,3 +326,63 @@ def test_env_sharding_gloo_world2():
     for p in parts:
         for e, sm in zip(p[0], p[1]):
             assert sm == float(bulldozer_scene(e, cfg).particles.positions.sum())
+
+
+# ---------------------------------------------------------------------------
+# Excavation env (the 7-joint arm + Box scoop, envs.py:233-348)
+# ---------------------------------------------------------------------------
+def golden_exc():
+    with np.load(GOLDEN / "excavation_env.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def test_excavation_scene_matches_reference_seeding():
+    from paper_2306_01369_b200.envs import excavation_scene
+
+    g = golden_exc()
+    for e, seed in enumerate(g["seeds"]):
+        sc = excavation_scene(int(seed))
+        assert np.array_equal(sc.particles.positions, g["x0"][e])
+        assert [type(b.geometry).__name__ for b in sc.bodies] == ["HalfSpace", "Box"]
+
+
+def test_chain_batch_matches_reference_chain():
+    from paper_2306_01369_b200.batch import ChainBatch
+    from paper_2306_01369_b200.envs import excavation_links
+
+    g = golden_exc()
+    E = len(g["seeds"])
+    chain = ChainBatch(excavation_links(), E, link_index=6)
+    chain.command(np.clip(g["actions"], -1, 1) * chain.limits)
+    P, W, V = chain.rollout(10, 2e-3, None)
+    np.testing.assert_allclose(np.transpose(P, (1, 0, 2, 3)), g["scoop_pose"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.transpose(W, (1, 0, 2)), g["scoop_omega"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.transpose(V, (1, 0, 2)), g["scoop_v"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(chain.q, g["q"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.gpu
+def test_batched_excavation_env_matches_reference():
+    from paper_2306_01369_b200.envs import BatchedExcavationEnv
+
+    g = golden_exc()
+    E = len(g["seeds"])
+    env = BatchedExcavationEnv(E)
+    env.reset(g["seeds"])
+    env.chain.command(np.clip(g["actions"], -1, 1) * env.chain.limits)
+    env.batch.run_raw(1)
+    xb, vb = env.batch.state()
+    for e in range(E):
+        assert rel_err(xb[e], g["x1"][e]) <= TOL and rel_err(vb[e], g["v1"][e]) <= TOL
+    env.batch.run_raw(9)
+    obs = env._observe()
+    xb, _ = env.batch.state()
+    for e in range(E):
+        assert rel_err(xb[e], g["xT"][e]) <= 1e-3
+        np.testing.assert_allclose(obs.pose[e], g["end_pose"][e], rtol=0, atol=1e-9)
+        for img, ref in ((obs.ego[e], g["ego"][e]), (obs.sky[e], g["sky"][e])):
+            bad = np.abs(img.astype(np.float64) - ref) > 2e-4
+            assert bad.mean() <= 0.01
+    obs, rew, done, info = env.step(np.zeros((E, 7)))
+    assert np.all(rew == 0) and obs.ego.shape == (E, 36, 36)
+    env.close()

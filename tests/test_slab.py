@@ -147,11 +147,11 @@ def _reference_run():
     return sc.particles.positions.copy(), sc.particles.velocities.copy(), reps
 
 
-def _slab_worker(rank, world, port, out):
+def _slab_worker(rank, world, port, out, halo="host"):
     from paper_2306_01369_b200.slab import SlabBed
 
     td = _init(rank, world, port) if world > 1 else None
-    bed = SlabBed(_bed(), rank=rank, world=world, device=0, backend="gloo", resort_every=5)
+    bed = SlabBed(_bed(), rank=rank, world=world, device=0, backend="gloo", resort_every=5, halo=halo)
     reps = bed.run(T_STEPS)
     X, V = bed.gather()
     if rank == 0:
@@ -165,8 +165,10 @@ def _slab_worker(rank, world, port, out):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_slab_step_bitwise_equals_one_gpu(world):
+@pytest.mark.parametrize("world,halo", [(1, "host"), (2, "host"), (3, "host"), (2, "p2p"), (3, "p2p")])
+def test_slab_step_bitwise_equals_one_gpu(world, halo):
+    """halo="p2p": the per-sweep halo goes through CUDA-IPC peer memory
+    (here several processes share one GPU; across GPUs it is NVLink)."""
     x1, v1, reps1 = _reference_run()
     if world == 1:
         out = {}
@@ -174,7 +176,7 @@ def test_slab_step_bitwise_equals_one_gpu(world):
     else:
         ctx = mp.get_context("spawn")
         out = ctx.Manager().dict()
-        mp.spawn(_slab_worker, args=(world, _port(), out), nprocs=world, join=True)
+        mp.spawn(_slab_worker, args=(world, _port(), out, halo), nprocs=world, join=True)
     assert np.array_equal(out["x"], x1)
     assert np.array_equal(out["v"], v1)
     for (n_pp, n_b, mp_, ke, mv), r in zip(out["reps"], reps1):

@@ -17,4 +17,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_n
 python tools/launches.py gpurun_out/prof/launches_*.csv > gpurun_out/prof/launches_summary.txt 2>&1
 python tools/ncu_summary.py gpurun_out/prof/full_*.ncu-rep > gpurun_out/prof/ncu_full_summary.txt 2>&1
 python tools/ncu_traffic.py gpurun_out/prof/ncu_summary.json hero50k=gpurun_out/prof/full_hero50k.ncu-rep bed1m=gpurun_out/prof/full_bed1m.ncu-rep envs=gpurun_out/prof/full_envs.ncu-rep > /dev/null 2>&1
+# source-level exports (per-line stalls / instructions) instead of the big .ncu-rep files
+ncu -i gpurun_out/prof/full_hero50k.ncu-rep --page source --csv --print-source cuda > gpurun_out/prof/src_hero50k_fused.csv 2>/dev/null
+ncu -i gpurun_out/prof/full_bed1m.ncu-rep --page source --csv --print-source cuda -k regex:k_narrow > gpurun_out/prof/src_bed1m_narrow.csv 2>/dev/null
+gzip -f gpurun_out/prof/src_*.csv
+rm -f gpurun_out/prof/*.ncu-rep
 ls -la gpurun_out/prof
