@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--solve-mode", type=int, default=0)
+    ap.add_argument("--pipeline", default="two-loops-split",
+                    choices=["two-loops-split", "two-loops-fused", "one-loop"],
+                    help="PipelineMode (loop structure; same results): the paper's Fig. 6 comparison")
     ap.add_argument("--resort-every", type=int, default=8)
     return ap.parse_args()
 
@@ -662,8 +665,9 @@ def run_ours(args, dist: Dist):
     K, W = args.steps, args.warmup
     table, _ = eng.body_tables(sc, W + K)
     # warm-up (untimed)
+    pmode = {"two-loops-split": 0, "two-loops-fused": 1, "one-loop": 2}[args.pipeline]
     if W:
-        reps, _, done, st, msg = eng.run_batch(table[:W], nb, 0)
+        reps, _, done, st, msg = eng.run_batch(table[:W], nb, pmode)
         if st:
             raise RuntimeError(msg)
     lib = N.lib()
@@ -693,7 +697,7 @@ def run_ours(args, dist: Dist):
     # warm (no flush) steady-state loop, for context
     table2, _ = eng.body_tables(sc, K)
     t_warm = None
-    reps, _, done, st2, _ = eng.run_batch(table2, nb, 0)
+    reps, _, done, st2, _ = eng.run_batch(table2, nb, pmode)
     if st2 == 0:
         t_warm = eng.last_batch_ms()
 
@@ -736,7 +740,7 @@ def run_ours(args, dist: Dist):
     lib.gg_host_register(N.ptr(pv), pv.nbytes)
     dist.barrier()
     t0 = time.perf_counter()
-    _, reports = gg.run(sc2, K)
+    _, reports = gg.run(sc2, K, mode=gg.PipelineMode(args.pipeline))
     xf = sc2.particles.positions  # device -> host
     _ = float(xf[0, 0]) + sum(r.kinetic_energy for r in reports)
     t_e2e = dist.max(time.perf_counter() - t0)
@@ -762,6 +766,7 @@ def run_ours(args, dist: Dist):
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
             "data": "synthetic (seeded bed, settled on GPU)",
             "config": {**desc, "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
+                       "pipeline": args.pipeline,
                        "l2": l2_note(args, n * 200 / 2**20),
                        "c_pp": c_pp, "c_b": c_b, "n_h": eng.n_h,
                        "warm_ms_per_step": None if t_warm is None else t_warm / K},

@@ -165,7 +165,11 @@ int gg_upload_grid(gg_ctx* ctx, const double* values, const int32_t dims[3],
                    const double origin[3], const double spacing[3], int32_t* grid_id);
 
 /* Enqueue n_steps timesteps (stepper.step, stepper.py:57-135) on the context
- * stream.  bodies = [n_steps][n_bodies] per-step body tables.  Asynchronous. */
+ * stream.  bodies = [n_steps][n_bodies] per-step body tables.  Asynchronous.
+ * mode = PipelineMode (stepper.py:74-98), the loop structure, same results:
+ * GG_MODE_TWO_LOOPS_SPLIT records only contacts; GG_MODE_TWO_LOOPS_FUSED
+ * keeps a (masked) record for every candidate and the sweeps run over all of
+ * them; GG_MODE_ONE_LOOP repeats the collision test inside every sweep. */
 int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
             int32_t mode);
 

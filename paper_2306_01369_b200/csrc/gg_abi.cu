@@ -65,6 +65,7 @@ struct gg_ctx {
   int solve_grid = 0;      // co-resident blocks of k_solve
   int resort_every = 8;    // physical re-sort period (steps)
   int solve_mode = 0;      // 0 auto, 1 coop solve, 2 plain persistent solve, 3 per-sweep, 4 fused step
+  int pipeline = 0;        // PipelineMode of the captured graphs (GG_MODE_*)
   int fused_grid = 0;      // co-resident blocks of k_step_fused
   bool cluster_ok = false; // a 16-CTA cluster of k_solve_cluster can be resident
   long long since_resort = 1 << 30;  // force a re-sort after upload
@@ -246,6 +247,7 @@ int begin_batch(gg_ctx* ctx, cudaStream_t s) {
 }
 
 bool use_fused_step(const gg_ctx* ctx) {
+  if (ctx->pipeline == GG_MODE_ONE_LOOP) return false;  // per-sweep k_sweep_oneloop launches
   if (ctx->solve_mode == 4 || ctx->solve_mode == 5 || ctx->solve_mode == 6 || ctx->solve_mode == 7)
     return true;
   if (ctx->solve_mode != 0) return false;
@@ -259,7 +261,7 @@ bool use_cluster_solve(const gg_ctx* ctx) {
 }
 
 bool use_persistent_solve(const gg_ctx* ctx) {
-  if (ctx->solve_mode == 3) return false;
+  if (ctx->solve_mode == 3 || ctx->pipeline == GG_MODE_ONE_LOOP) return false;
   if (ctx->solve_mode == 0) return false;  // auto: fused for small n, per-sweep otherwise
   return ctx->n <= static_cast<long long>(ctx->solve_grid) * kBlock;
 }
@@ -309,7 +311,12 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
     // one thread per particle: S sweep launches + integrate/report
     Dev D = D0;
     D.env_kernel = ctx->E > 1 ? 1 : 0;
-    for (int it = 0; it < D.S; ++it) k_sweep<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
+    for (int it = 0; it < D.S; ++it) {
+      if (D.pipeline == GG_MODE_ONE_LOOP)
+        k_sweep_oneloop<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
+      else
+        k_sweep<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
+    }
     k_finish<<<ctx->nblocks, kBlock, 0, s>>>(D);
     if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
     CK(cudaGetLastError());
@@ -342,6 +349,7 @@ Dev pass_dev(const gg_ctx* ctx, int resort, int morton) {
   D.fused_stop = 0;
   D.sweep_barrier = (ctx->solve_mode == 7 || ctx->solve_mode == 0) ? 1 : 0;
   D.env_kernel = 0;
+  D.pipeline = ctx->pipeline;
   return D;
 }
 
@@ -457,7 +465,10 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     mark(9);
   } else {
     for (int it = 0; it < D.S; ++it) {
-      k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
+      if (D.pipeline == GG_MODE_ONE_LOOP)
+        k_sweep_oneloop<<<nbn, kBlock, 0, s>>>(D, it);
+      else
+        k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
       mark(12);
     }
     Dev Df = D;
@@ -862,6 +873,10 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
   if (n_steps < 0) return fail(ctx, GG_EINVAL, "n_steps must be >= 0");
   if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
   if (mode < 0 || mode > 2) return fail(ctx, GG_EINVAL, "unknown pipeline mode");
+  if (mode != ctx->pipeline) {
+    ctx->pipeline = mode;
+    ctx->graph_dirty = true;
+  }
   for (long long i = 0; i < static_cast<long long>(n_steps) * ctx->E * n_bodies; ++i) {
     const gg_body& b = bodies[i];
     if (b.kind < GG_GEOM_SPHERE || b.kind > GG_GEOM_GRID)

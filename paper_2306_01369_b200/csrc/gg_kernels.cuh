@@ -79,6 +79,11 @@ struct Dev {
   int fused_stop; // k_step_fused ends after the contacts (the cluster kernel solves)
   int sweep_barrier;  // fused sweeps: 1 grid barrier per sweep, 0 neighbour-block flags
   int env_kernel;     // E > 1: per-env reports + body momentum written by k_env_reports
+  // PipelineMode (stepper.py:34-37, 74-98): 0 TWO_LOOPS_SPLIT (records for
+  // contacts only), 1 TWO_LOOPS_FUSED (a record for every candidate, masked:
+  // null if not colliding), 2 ONE_LOOP (no records used: every sweep repeats
+  // the collision test over the candidates).  Same results in all three.
+  int pipeline;
   int key_morton; // counting-sort key of the current pass (R: 1, H: 0)
   // Independent environments (segments).  E == 1 is a single bed.  With
   // E > 1 env e owns particles [e*ne, (e+1)*ne) of the physical order and
@@ -650,13 +655,16 @@ struct CandCursor {
 // Exact inline pass over ALL candidates of one owner (owners with more than
 // kPassCap prefilter passes): counts (write == false) or writes records from
 // dst on (write == true), in candidate order — the same order the queue gives.
+// c_slots: records (= contacts, or every candidate in TWO_LOOPS_FUSED);
+// c_pp: contacts.
 __device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, int tid, int k,
                                            float4 pf, uint32_t total, bool write, long long off,
-                                           int& c_pp, unsigned long long& n_coinc,
+                                           int& c_slots, int& c_pp, unsigned long long& n_coinc,
                                            double& max_psi) {
   const double px = pf.x, py = pf.y, pz = pf.z;
   CandCursor cur;
   cur.init(sm, tid);
+  c_slots = 0;
   c_pp = 0;
   n_coinc = 0;
   for (uint32_t i = 0; i < total; ++i) {
@@ -665,16 +673,19 @@ __device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, i
     const int q = __float_as_int(qf.w);
     if (q == k) continue;
     const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
-    if (!(fx * fx + fy * fy + fz * fz <= D.reject_d2f)) continue;
+    const bool all = D.pipeline == 1;  // TWO_LOOPS_FUSED: every candidate gets a record
+    if (!all && !(fx * fx + fy * fy + fz * fz <= D.reject_d2f)) continue;
     double dx, dy, dz;
     const double d2 = pp_d2(px, py, pz, qf, dx, dy, dz);
-    if (!(d2 >= D.coinc_d2)) {
-      ++n_coinc;
-      continue;
-    }
-    if (d2 < D.contact_d2) {
-      if (write) max_psi = nmax(max_psi, pp_write(D, ridx(D, k, off, c_pp), dx, dy, dz, d2, q));
+    const bool coi = !(d2 >= D.coinc_d2);
+    if (coi) ++n_coinc;
+    if (!coi && d2 < D.contact_d2) {
+      if (write) max_psi = nmax(max_psi, pp_write(D, ridx(D, k, off, c_slots), dx, dy, dz, d2, q));
+      ++c_slots;
       ++c_pp;
+    } else if (all) {
+      if (write) D.coth[ridx(D, k, off, c_slots)] = kNullContact;
+      ++c_slots;  // a masked candidate
     }
   }
 }
@@ -808,7 +819,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         // float32 pre-filter, conservative by a 1e-5 relative margin (the
         // float32 estimate is within ~4e-7 relative of the exact square)
         const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
-        if (fx * fx + fy * fy + fz * fz <= D.reject_d2f) {
+        if (fx * fx + fy * fy + fz * fz <= D.reject_d2f || D.pipeline == 1) {
           if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
           ++npass;
         }
@@ -837,10 +848,10 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   int c_own = np;         // record slots this owner needs for pp contacts
   double max_psi = 0.0;
   if (ovf) {  // more prefilter passes than the queue holds: exact inline count
-    int c_ex = 0;
+    int s_ex = 0, c_ex = 0;
     unsigned long long co_ex = 0;
-    scan_exact(D, sm, tid, k, pf, total, false, 0, c_ex, co_ex, max_psi);
-    c_own = c_ex;
+    scan_exact(D, sm, tid, k, pf, total, false, 0, s_ex, c_ex, co_ex, max_psi);
+    c_own = s_ex;
   }
   // this env's bodies at this step: bodies[step][env][nb]
   const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
@@ -917,9 +928,9 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     }
     if (live) {
       if (ovf) {
-        int c_ex = 0;
+        int s_ex = 0, c_ex = 0;
         unsigned long long co_ex = 0;
-        scan_exact(D, sm, tid, k, pf, total, true, my_off, c_ex, co_ex, max_psi);
+        scan_exact(D, sm, tid, k, pf, total, true, my_off, s_ex, c_ex, co_ex, max_psi);
         c_pp += c_ex;
         n_coinc += co_ex;
       }
@@ -1086,6 +1097,71 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
       atomicAdd(bm + 1, fy);
       atomicAdd(bm + 2, fz);
     }
+  }
+}
+
+// ONE_LOOP (stepper.py:86-98): the sweep repeats the collision test — the
+// 27 de-duplicated buckets, the candidates, the exact test, the body SDFs —
+// instead of reading contact records, and applies the impulses in the same
+// order with the same float32-stored geometry, so the result is bitwise that
+// of TWO_LOOPS_SPLIT.
+__device__ __forceinline__ void sweep_oneloop(const Dev& D, int k, const float4* Win, double wx,
+                                           double wy, double wz, double& ax, double& ay, double& az,
+                                           SweepAcc& A) {
+  const Layout L = layout(D, D.ctl);
+  const int env = env_of(D, k);
+  const uint32_t* start = D.start + static_cast<long long>(env) * D.H.n_h;
+  const float4 pf = L.x[k];
+  const double px = pf.x, py = pf.y, pz = pf.z;
+  const long long c0 = cell_coord(px, D.two_r);
+  const long long c1 = cell_coord(py, D.two_r);
+  const long long c2 = cell_coord(pz, D.two_r);
+  uint32_t tx[3], ty[3], tz[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    tx[d] = hash_term32(c0 + d - 1, kP0);
+    ty[d] = hash_term32(c1 + d - 1, kP1);
+    tz[d] = hash_term32(c2 + d - 1, kP2);
+  }
+  const bool dedup = !D.H.pow2 || may_alias(tx, ty, tz, D.H.mask);
+  for (int o = 0; o < 27; ++o) {
+    const uint32_t h = nb_hash(D, o, c0, c1, c2, tx, ty, tz);
+    bool keep = true;
+    if (dedup)
+      for (int q = 0; q < o; ++q) keep &= nb_hash(D, q, c0, c1, c2, tx, ty, tz) != h;
+    if (!keep) continue;
+    for (uint32_t m = start[h]; m < start[h + 1]; ++m) {
+      const float4 qf = D.Xh[m];
+      const int q = __float_as_int(qf.w);
+      if (q == k) continue;
+      const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
+      if (!(fx * fx + fy * fy + fz * fz <= D.reject_d2f)) continue;
+      double dx, dy, dz;
+      const double d2 = pp_d2(px, py, pz, qf, dx, dy, dz);
+      if (!(d2 >= D.coinc_d2) || !(d2 < D.contact_d2)) continue;
+      const double inv = rsqrt(d2);
+      const double psi = __dsub_rn(D.two_r, d2 * inv);
+      const float4 g = make_float4(static_cast<float>(dx * inv), static_cast<float>(dy * inv),
+                                   static_cast<float>(dz * inv), static_cast<float>(psi));
+      contact_impulse(D, wx, wy, wz, g, q, Win[q], ax, ay, az, A);
+    }
+  }
+  const gg_body* bodies = D.bodies + (static_cast<long long>(D.ctl->step) * D.E + env) * D.nb;
+  for (int b = 0; b < D.nb; ++b) {
+    const gg_body& B = bodies[b];
+    if (B.bounded && !(px >= B.aabb_lo[0] && px <= B.aabb_hi[0] && py >= B.aabb_lo[1] &&
+                       py <= B.aabb_hi[1] && pz >= B.aabb_lo[2] && pz <= B.aabb_hi[2]))
+      continue;
+    double psi;
+    d3 nrm;
+    int deg;
+    if (!penetrate(B, D.grids, D.gvals, px, py, pz, D.r, &psi, &nrm, &deg)) continue;
+    const d3 vb = body_surface_velocity(B, px, py, pz, nrm, D.r, psi);
+    const float4 g = make_float4(static_cast<float>(nrm.x), static_cast<float>(nrm.y),
+                                 static_cast<float>(nrm.z), static_cast<float>(psi));
+    const float4 qb = make_float4(static_cast<float>(vb.x), static_cast<float>(vb.y),
+                                  static_cast<float>(vb.z), 0.f);
+    contact_impulse(D, wx, wy, wz, g, -(b + 1), qb, ax, ay, az, A);
   }
 }
 
@@ -1409,6 +1485,32 @@ __global__ void __launch_bounds__(kBlock, 4) k_sweep(Dev D, int s) {
   SweepAcc A;
   sweep_acc_init(D, A, sbm, k);
   if (k < D.n_own) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+  sweep_acc_flush(D, A, smd);
+}
+
+// ONE_LOOP sweep (its own kernel: the inline collision test would cost the
+// record-reading sweep its registers)
+__global__ void __launch_bounds__(kBlock) k_sweep_oneloop(Dev D, int s) {
+  __shared__ unsigned long long sbm[kSmemBodies * 3];
+  __shared__ double smd[32];
+  const Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;
+  const Layout L = layout(D, ctl);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  SweepAcc A;
+  sweep_acc_init(D, A, sbm, k);
+  const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+  if (k < D.n_own) {
+    sweep_acc_env(D, A, k);
+    if (D.cinfo[k].y > 0) {  // same skip as sweep_particle
+      const float4 wf = Win[k];
+      double ax = 0.0, ay = 0.0, az = 0.0;
+      sweep_oneloop(D, k, Win, wf.x, wf.y, wf.z, ax, ay, az, A);
+      D.W[s & 1][k] = make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
+                                  static_cast<float>(static_cast<double>(wf.y) + ay),
+                                  static_cast<float>(static_cast<double>(wf.z) + az), 0.f);
+    }
+  }
   sweep_acc_flush(D, A, smd);
 }
 

@@ -128,17 +128,23 @@ def test_config1_free_running_bulk_statistics():
     assert max(abs(a[k] - b[k]) for k in common) <= 0.05 * height
 
 
-def test_modes_bitwise_identical():
-    g = load("lattice_500")
+@pytest.mark.parametrize("name", ["lattice_500", "lattice_5000", "primitives_3000", "grid_tool"])
+def test_modes_bitwise_identical(name):
+    """PipelineMode (stepper.py:74-98) changes the loop structure only:
+    TWO_LOOPS_FUSED keeps a masked record per candidate, ONE_LOOP repeats the
+    collision test in every sweep; states and counters equal TWO_LOOPS_SPLIT."""
+    g = load(name)
     out = {}
     for m in gg.PipelineMode:
         sc = scene_from(g)
-        for _ in range(5):
-            gg.step(sc, m)
-        out[m] = (sc.particles.positions.copy(), sc.particles.velocities.copy())
+        reps = [gg.step(sc, m)[1] for _ in range(5)]
+        out[m] = (sc.particles.positions.copy(), sc.particles.velocities.copy(),
+                  [(r.n_contacts, r.n_candidates, r.n_body_contacts, r.n_coincident_skipped,
+                    r.max_penetration) for r in reps])
     ref = out[gg.PipelineMode.TWO_LOOPS_SPLIT]
-    for m, (x, v) in out.items():
-        assert np.array_equal(x, ref[0]) and np.array_equal(v, ref[1])
+    for m, (x, v, rs) in out.items():
+        assert np.array_equal(x, ref[0]) and np.array_equal(v, ref[1]), m
+        assert rs == ref[2], m
 
 
 def test_determinism():
