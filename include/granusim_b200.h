@@ -281,6 +281,21 @@ int gg_render_depth(gg_ctx* ctx, const gg_camera* cams, int32_t n_cams, int32_t 
  * bitwise identical images. */
 int gg_set_render_mode(int32_t mode);
 
+/* ---- mesh SDF baking ---------------------------------
+ * Exact signed distance to a watertight triangle mesh, replacing
+ * MeshDistance.signed_distance (sdf.py:357-391) and the knot sampling of
+ * bake_mesh_sdf (sdf.py:393-419).  tri: [n_tri][30] float64 rows
+ * (a, b, c, unit face normal, pseudonormals of edges v0v1 / v1v2 / v2v0,
+ * pseudonormals of corners 0 / 1 / 2; paper_2306_01369_b200.meshes.
+ * triangle_table builds them).  points != NULL: out[i] = distance of
+ * points[i] (n_points x 3); points == NULL: the dims[0] x dims[1] x dims[2]
+ * knots origin + spacing * (i, j, k) in C order.  Host buffers in and out;
+ * runs on `device`, synchronous.  kernel_ms (may be NULL) receives the
+ * kernel's device time.  No context: errors via gg_last_error(NULL). */
+int gg_bake_mesh_sdf(int32_t device, const double* tri, int64_t n_tri, const double* points,
+                     int64_t n_points, const double origin[3], const double spacing[3],
+                     const int64_t dims[3], double* out, float* kernel_ms);
+
 /* ---- slab domain decomposition -----------------
  * One bed over several GPUs, one context per rank (single-bed context whose
  * n is the rank's particle CAPACITY: owned + ghosts).  The bed is cut along x

@@ -99,6 +99,7 @@ def _bind(lib: C.CDLL) -> None:
         "gg_env_box_stats": (C.c_int, [P, P, P, P, P]),
         "gg_render_depth": (C.c_int, [P, P, i32, i32, P, i32, P]),
         "gg_set_render_mode": (C.c_int, [i32]),
+        "gg_bake_mesh_sdf": (C.c_int, [i32, P, i64, P, i64, P, P, P, P, C.POINTER(C.c_float)]),
         "gg_slab_setup": (C.c_int, [P, i64, i64, i32, i32]),
         "gg_slab_load": (C.c_int, [P, P, P, P, i64]),
         "gg_slab_migrate_pack": (C.c_int, [P, P, P, i64, P]),

@@ -12,6 +12,7 @@
 #include "gg_kernels.cuh"
 #include "gg_slab.cuh"
 #include "gg_render.cuh"
+#include "gg_bake.cuh"
 
 using namespace gg;
 
@@ -545,7 +546,76 @@ const char* gg_build_info(void) { return kBuildInfo; }
 
 int64_t gg_kernel_launches(const gg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-const char* gg_last_error(const gg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+// context-free entry points (gg_bake_mesh_sdf) report here
+thread_local std::string g_free_err = "null context";
+
+const char* gg_last_error(const gg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_free_err.c_str(); }
+
+int gg_bake_mesh_sdf(int32_t device, const double* tri, int64_t n_tri, const double* points,
+                     int64_t n_points, const double origin[3], const double spacing[3],
+                     const int64_t dims[3], double* out, float* kernel_ms) {
+  auto ferr = [](int code, const std::string& m) {
+    g_free_err = m;
+    return code;
+  };
+  if (!tri || n_tri < 1 || !out) return ferr(GG_EINVAL, "bake: need at least one triangle and an output");
+  long long n = n_points;
+  if (!points) {
+    if (!origin || !spacing || !dims) return ferr(GG_EINVAL, "bake: grid mode needs origin, spacing, dims");
+    n = 1;
+    for (int a = 0; a < 3; ++a) {
+      if (dims[a] < 1) return ferr(GG_EINVAL, "bake: dims must be positive");
+      n *= dims[a];
+    }
+  }
+  if (n < 1) return ferr(GG_EINVAL, "bake: no points");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  double *d_tri = nullptr, *d_pts = nullptr, *d_out = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto step = [&](cudaError_t r) {
+    if (e == cudaSuccess) e = r;
+    return e == cudaSuccess;
+  };
+  const size_t tb = static_cast<size_t>(n_tri) * kTriDoubles * sizeof(double);
+  if (step(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) && step(cudaEventCreate(&e0)) &&
+      step(cudaEventCreate(&e1)) && step(cudaMalloc(&d_tri, tb)) &&
+      step(cudaMalloc(&d_out, static_cast<size_t>(n) * sizeof(double))) &&
+      (!points || step(cudaMalloc(&d_pts, static_cast<size_t>(n) * 3 * sizeof(double)))) &&
+      step(cudaMemcpyAsync(d_tri, tri, tb, cudaMemcpyHostToDevice, st)) &&
+      (!points || step(cudaMemcpyAsync(d_pts, points, static_cast<size_t>(n) * 3 * sizeof(double),
+                                       cudaMemcpyHostToDevice, st)))) {
+    BakeArgs A{};
+    A.tri = d_tri;
+    A.T = n_tri;
+    A.pts = d_pts;
+    for (int a = 0; a < 3; ++a) {
+      A.origin[a] = points ? 0.0 : origin[a];
+      A.spacing[a] = points ? 0.0 : spacing[a];
+      A.dims[a] = points ? 1 : dims[a];
+    }
+    A.n = n;
+    A.out = d_out;
+    const long long blocks = (n + 255) / 256;
+    step(cudaEventRecord(e0, st));
+    k_bake_sdf<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A);
+    step(cudaGetLastError());
+    step(cudaEventRecord(e1, st));
+    step(cudaMemcpyAsync(out, d_out, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (step(cudaStreamSynchronize(st)) && kernel_ms) step(cudaEventElapsedTime(kernel_ms, e0, e1));
+  }
+  cudaFree(d_tri);
+  cudaFree(d_pts);
+  cudaFree(d_out);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (prev >= 0) cudaSetDevice(prev);
+  if (e != cudaSuccess) return ferr(GG_ECUDA, std::string("bake: ") + cudaGetErrorString(e));
+  return GG_OK;
+}
 
 int gg_create(int device, const gg_params* params, int64_t n, int64_t n_h, int32_t max_bodies,
               int32_t max_contacts, gg_ctx** out) {

@@ -612,7 +612,13 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
   return psi;
 }
 
-constexpr int kPassCap = 16;  // prefilter passes queued per owner (more: exact inline path)
+#ifndef GG_PASSCAP
+#define GG_PASSCAP 16
+#endif
+#ifndef GG_NARROW_MINB
+#define GG_NARROW_MINB 2
+#endif
+constexpr int kPassCap = GG_PASSCAP;  // prefilter passes queued per owner (more: exact inline path)
 constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass that is no contact)
 constexpr int kWarps = kBlock / 32;
 
@@ -1018,31 +1024,80 @@ __device__ __forceinline__ void sweep_acc_env(const Dev& D, SweepAcc& A, int k) 
   A.env = e;
 }
 
-// per block: diagnostics (block max/min, one atomic each) + body momentum
-// (one atomic per non-zero component).  Called by every thread.
-__device__ __forceinline__ void sweep_acc_flush(const Dev& D, SweepAcc& A, double* smd) {
-  acc_ext<1>(D, A.env, A.maxviol, GG_ACC(max_viol_bits), smd);
-  acc_ext<2>(D, A.env, A.minb1, GG_ACC(min_b1_bits), smd);
-  // register momentum: warp sum, then one shared-memory add per warp
+// Max / min over a warp of non-negative doubles held as bit patterns (for
+// x >= +0.0 the IEEE order is the unsigned order of the bits): two 32-bit
+// REDUX reductions instead of five float64 shuffle + compare rounds.
+__device__ __forceinline__ unsigned long long warp_umax64(unsigned long long v) {
+  const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
+  const unsigned lo =
+      __reduce_max_sync(0xffffffffu, static_cast<unsigned>(v >> 32) == hi ? static_cast<unsigned>(v) : 0u);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long warp_umin64(unsigned long long v) {
+  const unsigned hi = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
+  const unsigned lo = __reduce_min_sync(
+      0xffffffffu, static_cast<unsigned>(v >> 32) == hi ? static_cast<unsigned>(v) : 0xffffffffu);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+
+// per block: diagnostics (max cone violation, min normal impulse: warp
+// reductions on the bit patterns, one atomic each per block) + body momentum
+// (warp sums only where a lane holds momentum, one atomic per non-zero
+// component).  One block barrier.  Called by every thread.
+// maxviol >= +0.0 and minb1 in [+0.0, +inf] by construction (contact_impulse
+// never stores a NaN: a NaN impulse makes w non-finite and the step raises).
+__device__ __forceinline__ void sweep_acc_flush(const Dev& D, SweepAcc& A, double* /*unused*/) {
+  __shared__ unsigned long long s_wred[2 * 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int e0 = A.env;
   const bool uni = D.E == 1 || warp_env_uniform(A.env, &e0);
   if (uni) {
+    const unsigned long long m1 = warp_umax64(dbits(A.maxviol));
+    const unsigned long long m2 = warp_umin64(dbits(A.minb1));
 #pragma unroll
     for (int b = 0; b < kRegBodies; ++b)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const unsigned long long t = warp_sum(A.rb[b][c]);
-        if ((threadIdx.x & 31) == 0 && t && b < D.nb) {
-          const int gb = e0 * D.nb + b;
-          const int sl = gb - A.gb_lo;
-          atomicAdd((sl >= 0 && sl < kSmemBodies) ? A.sbm + 3 * sl + c : D.bm_fix + 3 * gb + c, t);
+        if (__any_sync(0xffffffffu, A.rb[b][c] != 0ull)) {
+          const unsigned long long t = warp_sum(A.rb[b][c]);
+          if (lane == 0 && t && b < D.nb) {
+            const int gb = e0 * D.nb + b;
+            const int sl = gb - A.gb_lo;
+            atomicAdd((sl >= 0 && sl < kSmemBodies) ? A.sbm + 3 * sl + c : D.bm_fix + 3 * gb + c, t);
+          }
         }
         A.rb[b][c] = 0ull;
       }
+    if (lane == 0) {
+      if (D.E == 1) {
+        s_wred[2 * w] = m1;
+        s_wred[2 * w + 1] = m2;
+      } else {
+        Acc* a = D.acc + e0;
+        if (m1 != 0ull) atomicMax(&a->max_viol_bits, m1);
+        if (m2 < kInfBits) atomicMin(&a->min_b1_bits, m2);
+      }
+    }
   } else {
     sweep_acc_rb_global(D, A);
+    Acc* a = D.acc + A.env;
+    if (A.maxviol > 0.0) atomicMax(&a->max_viol_bits, dbits(A.maxviol));
+    if (A.minb1 < __longlong_as_double(kInfBits)) atomicMin(&a->min_b1_bits, dbits(A.minb1));
   }
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(kInfBits);
   __syncthreads();
+  if (D.E == 1 && threadIdx.x == 0) {
+    unsigned long long m1 = 0ull, m2 = kInfBits;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
+      m1 = s_wred[2 * q] > m1 ? s_wred[2 * q] : m1;
+      m2 = s_wred[2 * q + 1] < m2 ? s_wred[2 * q + 1] : m2;
+    }
+    if (m1 != 0ull) atomicMax(&D.acc->max_viol_bits, m1);
+    if (m2 < kInfBits) atomicMin(&D.acc->min_b1_bits, m2);
+  }
   for (int i = threadIdx.x; i < kSmemBodies * 3; i += blockDim.x)
     if (A.sbm[i]) atomicAdd(&D.bm_fix[A.gb_lo * 3 + i], A.sbm[i]);
 }
@@ -1056,7 +1111,9 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   const double uy = (wy - D.gamma * q.y) + D.gdt1;
   const double uz = (wz - D.gamma * q.z) + D.gdt2;
   const double un = ux * e1x + uy * e1y + uz * e1z;
-  const double b1 = nmax(D.bias_coef * (double)g.w - un, 0.0);
+  // np.maximum(x, 0): x if x > 0 or x is NaN, else +0.0 (one unordered compare)
+  const double bx = D.bias_coef * (double)g.w - un;
+  const double b1 = !(bx <= 0.0) ? bx : 0.0;
   double btx = un * e1x - ux, bty = un * e1y - uy, btz = un * e1z - uz;
   const double tn2 = btx * btx + bty * bty + btz * btz;
   const double lim = D.mu * b1;
@@ -1068,7 +1125,8 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
     btx *= sc;
     bty *= sc;
     btz *= sc;
-    A.maxviol = nmax(A.maxviol, (tn2 * inv) * sc - lim);
+    const double viol = (tn2 * inv) * sc - lim;
+    if (viol > A.maxviol) A.maxviol = viol;
   }
   const double ix = (e1x * b1 + btx) * eff;
   const double iy = (e1y * b1 + bty) * eff;
@@ -1076,7 +1134,7 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   ax += ix;
   ay += iy;
   az += iz;
-  A.minb1 = nmin(A.minb1, b1);
+  if (b1 < A.minb1) A.minb1 = b1;
   if (j < 0) {  // reaction momentum on the body (contact.py:489-495)
     const int b = -j - 1;
     const unsigned long long fx = to_fix(-D.mass * ix), fy = to_fix(-D.mass * iy),
@@ -1183,12 +1241,15 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
     const float4 q0 = (j0 >= 0) ? Win[j0] : D.cvb[k];
     contact_impulse(D, wx, wy, wz, g0, j0, q0, ax, ay, az, A);
   }
-  for (int sl = 1; sl < ci.y; ++sl) {
-    const long long idx = static_cast<long long>(ci.x) + sl - 1;
-    const float4 g = D.cgeo[idx];
-    const int j = D.coth[idx];
+  // records 1 .. c-1 at ci.x, ci.x + 1, ...
+  const float4* gp = D.cgeo + ci.x;
+  const int* jp = D.coth + ci.x;
+  const float4* vp = D.cvb + ci.x;
+  for (int sl = 0; sl < ci.y - 1; ++sl) {
+    const float4 g = gp[sl];
+    const int j = jp[sl];
     if (j == kNullContact) continue;
-    const float4 q = (j >= 0) ? Win[j] : D.cvb[idx];
+    const float4 q = (j >= 0) ? Win[j] : vp[sl];
     contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
@@ -1468,7 +1529,7 @@ __global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
 // NarrowSmem (> 48 KB) is dynamic shared memory: launch with sizeof(NarrowSmem)
 extern __shared__ __align__(16) unsigned char g_dsmem[];
 
-__global__ void __launch_bounds__(kBlock, 2) k_narrow(Dev D) {
+__global__ void __launch_bounds__(kBlock, GG_NARROW_MINB) k_narrow(Dev D) {
   NarrowSmem& sm = *reinterpret_cast<NarrowSmem*>(g_dsmem);
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;

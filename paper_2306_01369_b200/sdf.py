@@ -3,9 +3,10 @@
 The classes carry the parameters the device kernels evaluate (see
 csrc/gg_device.cuh) plus ``contact_bounds``, which the host needs for the
 `_near_body` AABB prefilter (contact.py:187-203).  ``penetration_depth``
-(sdf.py:472-512) runs on the GPU.  Mesh baking is offline preprocessing and
-out of scope for the hot path; an ``SdfGrid`` built anywhere (including the
-reference's ``bake_mesh_sdf``) is accepted.
+(sdf.py:472-512) runs on the GPU.  ``bake_mesh_sdf`` / ``MeshDistance``
+(sdf.py:248-419) sample a watertight mesh's exact signed distance on the
+device (``gg_bake_mesh_sdf``, csrc/gg_bake.cuh); an ``SdfGrid`` built anywhere
+(including the reference's own baker) is accepted.
 """
 
 from __future__ import annotations
@@ -208,3 +209,83 @@ def load_grid(path: str) -> SdfGrid:
     values = np.frombuffer(blob[off + 32:], dtype="<f4").astype(np.float64)
     return SdfGrid(origin=np.array(origin), spacing=np.array(spacing), dims=np.array(dims),
                    values=values.reshape(dims), mesh_hash=mesh_hash)
+
+
+# ---------------------------------------------------------------------------
+# Mesh signed distance and baking on the device (sdf.py:248-419)
+# ---------------------------------------------------------------------------
+class MeshDistance:
+    """Exact signed distance to a watertight triangle mesh (sdf.py:248-391):
+    nearest triangle by the region-based closest point, sign from the
+    angle-weighted pseudonormal of the nearest feature.  Evaluated by the
+    ``gg_bake_mesh_sdf`` kernel; the triangle table is built once."""
+
+    def __init__(self, vertices: np.ndarray, faces: np.ndarray, device: int | None = None):
+        from .meshes import check_watertight, triangle_table
+
+        self.vertices = np.asarray(vertices, dtype=np.float64)
+        self.faces = np.asarray(faces, dtype=np.int64)
+        check_watertight(self.vertices, self.faces)
+        self.table = triangle_table(self.vertices, self.faces)
+        self.device = _device_index(device)
+        self.last_kernel_ms = 0.0
+
+    def contact_bounds(self, r):
+        return self.vertices.min(axis=0) - r, self.vertices.max(axis=0) + r
+
+    def _run(self, points, origin=None, spacing=None, dims=None) -> np.ndarray:
+        ms = ctypes.c_float(0.0)
+        if points is not None:
+            pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+            out = np.empty(len(pts))
+            if len(pts) == 0:
+                return out
+            st = N.lib().gg_bake_mesh_sdf(self.device, N.ptr(self.table), len(self.table), N.ptr(pts),
+                                          len(pts), None, None, None, N.ptr(out), ctypes.byref(ms))
+        else:
+            o = np.ascontiguousarray(origin, dtype=np.float64)
+            s = np.ascontiguousarray(spacing, dtype=np.float64)
+            d = np.ascontiguousarray(dims, dtype=np.int64)
+            out = np.empty(int(np.prod(d)))
+            st = N.lib().gg_bake_mesh_sdf(self.device, N.ptr(self.table), len(self.table), None, 0,
+                                          N.ptr(o), N.ptr(s), N.ptr(d), N.ptr(out), ctypes.byref(ms))
+        N.check(None, st, "gg_bake_mesh_sdf")
+        self.last_kernel_ms = float(ms.value)
+        return out
+
+    def signed_distance(self, points: np.ndarray) -> np.ndarray:
+        p = np.asarray(points, dtype=np.float64)
+        out = self._run(p.reshape(-1, 3))
+        return out[0] if p.ndim == 1 else out
+
+
+def _device_index(device) -> int:
+    if device is not None:
+        return int(getattr(device, "index", device) or 0)
+    try:
+        import torch
+
+        return torch.cuda.current_device() if torch.cuda.is_available() else 0
+    except Exception:  # pragma: no cover - torch is plumbing only
+        return 0
+
+
+def bake_mesh_sdf(vertices: np.ndarray, faces: np.ndarray, spacing, margin: float | None = None,
+                  device: int | None = None) -> SdfGrid:
+    """Grid over the mesh box plus ``margin`` (default two spacings) on every
+    side, dims = max(ceil(extent / spacing) + 1, 2), knot values = exact signed
+    distance (sdf.py:393-419).  Raises MeshError for non-watertight meshes."""
+    from .meshes import mesh_content_hash
+
+    md = MeshDistance(vertices, faces, device)
+    spacing = np.broadcast_to(np.asarray(spacing, dtype=np.float64), 3).copy()
+    if margin is None:
+        margin = 2.0 * float(spacing.max())
+    lo = md.vertices.min(axis=0) - margin
+    hi = md.vertices.max(axis=0) + margin
+    dims = np.maximum(np.ceil((hi - lo) / spacing).astype(np.int64) + 1, 2)
+    values = md._run(None, lo, spacing, dims).reshape(tuple(dims))
+    grid = SdfGrid(origin=lo, spacing=spacing, dims=dims, values=values,
+                   mesh_hash=mesh_content_hash(md.vertices, md.faces))
+    grid.bake_kernel_ms = md.last_kernel_ms
+    return grid
