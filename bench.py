@@ -60,7 +60,11 @@ def parse():
     ap.add_argument("--slab-particles", type=int, default=8_000_000)
     ap.add_argument("--envs", type=int, default=4096, help="envs workload: total envs")
     ap.add_argument("--env-particles", type=int, default=2000)
-    ap.add_argument("--settle", type=int, default=3000)
+    ap.add_argument("--settle", type=int, default=3000, help="hero50k: settle steps when no state file")
+    ap.add_argument("--bed-state", default="",
+                    help="bed1m: settled-state cache (.npz): loaded if present, else written after settling")
+    ap.add_argument("--settle-bed", type=int, default=8000,
+                    help="bed1m: most settle steps (dt 1e-3) before KE/n < 2e-3 J")
     ap.add_argument("--flush-mb", type=int, default=-1,
                     help="L2 flush before every timed step (MB); default: 512 for hero50k "
                          "(its working set fits L2), 0 for the larger beds (inputs > L2)")
@@ -116,39 +120,46 @@ class Dist:
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
-def analytic_box_grid(half, spacing):
-    """SdfGrid of a box sampled from its exact SDF (stand-in for a baked mesh)."""
-    from paper_2306_01369_b200.sdf import SdfGrid
-
-    half = np.asarray(half, float)
-    lo = -half - 3 * spacing
-    dims = np.ceil((2 * half + 6 * spacing) / spacing).astype(int) + 1
-    ax = [lo[a] + spacing * np.arange(dims[a]) for a in range(3)]
-    P = np.stack(np.meshgrid(*ax, indexing="ij"), -1).reshape(-1, 3)
-    q = np.abs(P) - half
-    d = np.linalg.norm(np.maximum(q, 0), axis=1) + np.minimum(q.max(1), 0)
-    return SdfGrid(lo, np.full(3, spacing), dims, d.reshape(tuple(dims)))
-
-
-def hero_initial_state(args, with_gpu: bool):
-    """(x, v, t) of the settled 50k column."""
-    if SETTLED.exists():
-        z = np.load(SETTLED)
-        return z["x"].astype(np.float64), z["v"].astype(np.float64), float(z["t"])
-    if not with_gpu:
-        return None
+def bed1m_settled(args):
+    """SURVEY.md §8d config 4 initial state: lattice_bed(1e6) + floor, settled on
+    the GPU at dt = 1e-3 (checked every 250 steps, at most --settle-bed steps)
+    until KE / n < 2e-3 J, fp32-rounded.  SURVEY's 1e-3 J is below the PJA
+    solver's residual jitter on this pile (KE/n plateaus at ~1.1e-3 J after
+    2e4 steps, tools/settle_probe.py); 2e-3 J is the level of the reference's
+    own settled acceptance fixture (3.9 J over 2000 particles),
+    reached after ~7000 steps with c_pp ~1.45.  Deterministic
+    (bitwise-reproducible kernels), so every run starts from the same state."""
     import paper_2306_01369_b200 as gg
 
-    sc = gg.hero_scene(50_000)
-    gg.run(sc, args.settle)
+    if args.bed_state and os.path.exists(args.bed_state):
+        z = np.load(args.bed_state, allow_pickle=False)
+        return (z["x"].astype(np.float64), z["v"].astype(np.float64), float(z["t"]),
+                json.loads(str(z["settle"])))
+    x = gg.lattice_bed(1_000_000).astype(np.float32).astype(np.float64)
+    sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
+                  params=gg.MaterialParams(timestep=1e-3))
+    done, ke = 0, float("inf")
+    while done < args.settle_bed:
+        _, reps = gg.run(sc, 250)
+        done += 250
+        ke = reps[-1].kinetic_energy / sc.particles.count
+        if ke < 2e-3:
+            break
     x = sc.particles.positions.astype(np.float32).astype(np.float64)
     v = sc.particles.velocities.astype(np.float32).astype(np.float64)
-    return x, v, float(sc.t)
+    info = {"dt": 1e-3, "steps": done, "ke_per_particle_J": ke, "target_J": 2e-3}
+    if args.bed_state:
+        np.savez(args.bed_state, x=x.astype(np.float32), v=v.astype(np.float32), t=sc.t,
+                 settle=json.dumps(info))
+    return x, v, float(sc.t), info
 
 
 def make_scene(args, with_gpu=True):
     import paper_2306_01369_b200 as gg
     from paper_2306_01369_b200.beds import add_scoop
+    from paper_2306_01369_b200.meshes import make_box_mesh
+    from paper_2306_01369_b200.sdf import bake_mesh_sdf
 
     if args.workload == "hero50k":
         st = hero_initial_state(args, with_gpu)
@@ -164,19 +175,24 @@ def make_scene(args, with_gpu=True):
                 "n_particles": 50_000, "dt": 5e-4, "solver_iterations": 10,
                 "bodies": "floor + tube wall + Box(0.15,0.1,0.04) scoop on 7-joint chain @0.3 limits"}
     else:
-        x = gg.lattice_bed(1_000_000).astype(np.float32).astype(np.float64)
+        x, v, t, settle = bed1m_settled(args)
         params = gg.MaterialParams(timestep=5e-4)
-        grid = analytic_box_grid([0.6, 0.4, 0.2], 0.04)
-        top = float(x[:, 2].max())
+        verts, faces = make_box_mesh([0.15, 0.1, 0.04])
+        grid = bake_mesh_sdf(verts, faces, spacing=0.01)  # on the device (gg_bake_mesh_sdf)
+        top = float(np.quantile(x[:, 2], 0.999))
         cx, cy = float(np.median(x[:, 0])), float(np.median(x[:, 1]))
+        # the scoop box, spun about the vertical axis with its centre 2 cm under the surface
         tool = gg.RigidBody(grid, gg.SpinDriver(axis=[0, 0, 1], rate=1.0, center=[cx, cy, top],
-                                                base_pose=gg.make_pose(np.eye(3), [cx, cy, top - 0.1])),
+                                                base_pose=gg.make_pose(np.eye(3), [cx, cy, top - 0.02])),
                             name="tool")
-        sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
+        sc = gg.Scene(particles=gg.ParticleSet(x, v),
                       bodies=[gg.RigidBody(gg.HalfSpace(), name="floor"), tool], params=params)
-        desc = {"workload": "bed1m", "config": "BASELINE configs[3] scale: 1M lattice bed + grid SDF tool",
+        sc.t = t
+        desc = {"workload": "bed1m",
+                "config": "BASELINE configs[3]: lattice_bed(1e6) settled on the GPU + baked mesh tool",
                 "n_particles": 1_000_000, "dt": 5e-4, "solver_iterations": 10,
-                "bodies": "floor + spinning SdfGrid box tool"}
+                "bodies": "floor + make_box_mesh([0.15,0.1,0.04]) baked on the device at 1 cm, spinning 1 rad/s",
+                "settle": settle}
     return sc, desc
 
 
@@ -764,7 +780,7 @@ def run_ours(args, dist: Dist):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
             "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
-            "data": "synthetic (seeded bed, settled on GPU)",
+            "data": "synthetic (seeded lattice bed, settled on the GPU before the run)",
             "config": {**desc, "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
                        "pipeline": args.pipeline,
                        "l2": l2_note(args, n * 200 / 2**20),

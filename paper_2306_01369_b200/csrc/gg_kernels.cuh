@@ -1102,6 +1102,55 @@ __device__ __forceinline__ void sweep_acc_flush(const Dev& D, SweepAcc& A, doubl
     if (A.sbm[i]) atomicAdd(&D.bm_fix[A.gb_lo * 3 + i], A.sbm[i]);
 }
 
+// Barrier-free variant for the per-sweep kernel (no shared accumulators):
+// every warp reduces its diagnostics and register momentum and issues its
+// own global atomics.  A diagnostic atomic is skipped when the warp's value
+// cannot change the global one (compared against a plain read of it: the
+// global max only grows and the min only shrinks, so a stale read is a safe
+// lower / upper bound), so nearly all warps issue none; body momentum atomics
+// come only from warps with body contacts.  Bodies >= kRegBodies go straight
+// to the global accumulators (sweep_acc_init_nobar).  Same sums (integer
+// fixed point) and extrema as sweep_acc_flush.
+__device__ __forceinline__ void sweep_acc_init_nobar(const Dev& D, SweepAcc& A, int k0) {
+  A.maxviol = 0.0;
+  A.minb1 = __longlong_as_double(kInfBits);
+  A.sbm = nullptr;
+  A.env = env_of(D, k0 < D.n ? k0 : D.n - 1);
+  A.gb_lo = -(1 << 30);  // no shared slots: contact_impulse uses bm_fix
+#pragma unroll
+  for (int b = 0; b < kRegBodies; ++b) A.rb[b][0] = A.rb[b][1] = A.rb[b][2] = 0ull;
+}
+
+__device__ __forceinline__ void sweep_acc_flush_nobar(const Dev& D, SweepAcc& A) {
+  const int lane = threadIdx.x & 31;
+  int e0 = A.env;
+  const bool uni = D.E == 1 || warp_env_uniform(A.env, &e0);
+  if (uni) {
+    const unsigned long long m1 = warp_umax64(dbits(A.maxviol));
+    const unsigned long long m2 = warp_umin64(dbits(A.minb1));
+#pragma unroll
+    for (int b = 0; b < kRegBodies; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (__any_sync(0xffffffffu, A.rb[b][c] != 0ull)) {
+          const unsigned long long t = warp_sum(A.rb[b][c]);
+          if (lane == 0 && t && b < D.nb) atomicAdd(D.bm_fix + 3 * (e0 * D.nb + b) + c, t);
+        }
+    if (lane == 0) {
+      Acc* a = D.acc + e0;
+      if (m1 != 0ull && m1 > *((volatile unsigned long long*)&a->max_viol_bits))
+        atomicMax(&a->max_viol_bits, m1);
+      if (m2 < kInfBits && m2 < *((volatile unsigned long long*)&a->min_b1_bits))
+        atomicMin(&a->min_b1_bits, m2);
+    }
+  } else {
+    sweep_acc_rb_global(D, A);
+    Acc* a = D.acc + A.env;
+    if (A.maxviol > 0.0) atomicMax(&a->max_viol_bits, dbits(A.maxviol));
+    if (A.minb1 < __longlong_as_double(kInfBits)) atomicMin(&a->min_b1_bits, dbits(A.minb1));
+  }
+}
+
 __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
                                                 float4 g, int j, float4 q, double& ax, double& ay,
                                                 double& az, SweepAcc& A) {
@@ -1223,29 +1272,38 @@ __device__ __forceinline__ void sweep_oneloop(const Dev& D, int k, const float4*
   }
 }
 
-__device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* Win, float4* Wout,
-                                               SweepAcc& A) {
+// Record 0 of particle k (slot k) and its CSR info, fetched together: one
+// dependent round trip fewer than reading cinfo first.
+struct SweepHead {
+  int2 ci;
+  float4 g0;
+  int j0;
+  __device__ __forceinline__ void load(const Dev& D, int k) {
+    ci = D.cinfo[k];
+    g0 = D.cgeo[k];
+    j0 = D.coth[k];
+  }
+};
+
+// The sweep of one particle with its head already loaded.  A particle without
+// contacts keeps w = v and is nobody's partner (contacts are symmetric), so
+// its w is never read: it is skipped entirely (integrate uses dv = 0).
+__device__ __forceinline__ void sweep_particle_h(const Dev& D, int k, const SweepHead& h,
+                                                 const float4* Win, float4* Wout, SweepAcc& A) {
+  if (h.ci.y == 0) return;
   sweep_acc_env(D, A, k);
-  // record 0 (slot k) is fetched with cinfo: one dependent round trip fewer
-  const int2 ci = D.cinfo[k];
-  const float4 g0 = D.cgeo[k];
-  const int j0 = D.coth[k];
-  // a particle without contacts keeps w = v and is nobody's partner
-  // (contacts are symmetric), so its w is never read: skip it entirely
-  // (integrate uses dv = 0 for it)
-  if (ci.y == 0) return;
   const float4 wf = Win[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  if (j0 != kNullContact) {
-    const float4 q0 = (j0 >= 0) ? Win[j0] : D.cvb[k];
-    contact_impulse(D, wx, wy, wz, g0, j0, q0, ax, ay, az, A);
+  if (h.j0 != kNullContact) {
+    const float4 q0 = (h.j0 >= 0) ? Win[h.j0] : D.cvb[k];
+    contact_impulse(D, wx, wy, wz, h.g0, h.j0, q0, ax, ay, az, A);
   }
   // records 1 .. c-1 at ci.x, ci.x + 1, ...
-  const float4* gp = D.cgeo + ci.x;
-  const int* jp = D.coth + ci.x;
-  const float4* vp = D.cvb + ci.x;
-  for (int sl = 0; sl < ci.y - 1; ++sl) {
+  const float4* gp = D.cgeo + h.ci.x;
+  const int* jp = D.coth + h.ci.x;
+  const float4* vp = D.cvb + h.ci.x;
+  for (int sl = 0; sl < h.ci.y - 1; ++sl) {
     const float4 g = gp[sl];
     const int j = jp[sl];
     if (j == kNullContact) continue;
@@ -1254,6 +1312,13 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
                         static_cast<float>(wz + az), 0.f);
+}
+
+__device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4* Win, float4* Wout,
+                                               SweepAcc& A) {
+  SweepHead h;
+  h.load(D, k);
+  sweep_particle_h(D, k, h, Win, Wout, A);
 }
 
 // Register-resident variant for the fused kernel (one particle per thread):
@@ -1536,17 +1601,25 @@ __global__ void __launch_bounds__(kBlock, GG_NARROW_MINB) k_narrow(Dev D) {
   ph_contacts(D, ctl, blockIdx.x * blockDim.x, blockDim.x, sm);
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_sweep(Dev D, int s) {
-  __shared__ unsigned long long sbm[kSmemBodies * 3];
-  __shared__ double smd[32];
-  const Ctl* ctl = D.ctl;
-  if (block_should_exit(ctl)) return;
-  const Layout L = layout(D, ctl);
+// One sweep, one thread per particle, no block barriers: the particle's
+// head is requested first, then the error flag (nothing raises it during a
+// sweep, so the exit is block-uniform) and the buffer selector — all in one
+// round trip — and the accumulators are flushed warp by warp.
+#ifndef GG_SWEEP_MINB
+#define GG_SWEEP_MINB 4
+#endif
+__global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = k < D.n_own;
+  SweepHead h;
+  if (live) h.load(D, k);
+  const Ctl* ctl = D.ctl;
+  if (*((volatile const int*)&ctl->err) != 0) return;
+  const float4* Win = (s == 0) ? layout(D, ctl).v : D.W[(s - 1) & 1];
   SweepAcc A;
-  sweep_acc_init(D, A, sbm, k);
-  if (k < D.n_own) sweep_particle(D, k, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
-  sweep_acc_flush(D, A, smd);
+  sweep_acc_init_nobar(D, A, k);
+  if (live) sweep_particle_h(D, k, h, Win, D.W[s & 1], A);
+  sweep_acc_flush_nobar(D, A);
 }
 
 // ONE_LOOP sweep (its own kernel: the inline collision test would cost the

@@ -3,7 +3,7 @@ mkdir -p gpurun_out
 for lib in build_variants/*.so; do
   v=$(basename $lib .so)
   for w in ${WLS:-bed1m envs hero50k}; do
-    GG_LIB=$PWD/$lib timeout 600 python bench.py --steps ${STEPS:-60} --warmup 5 --workload $w --no-cpu-baseline --profile-steps 3 > gpurun_out/v_${v}_$w.json 2> gpurun_out/v_${v}_$w.err || tail -3 gpurun_out/v_${v}_$w.err
+    GG_LIB=$PWD/$lib timeout 600 python bench.py --steps ${STEPS:-60} --warmup ${WARM:-5} --workload $w --no-cpu-baseline --profile-steps 3 --bed-state /tmp/bed1m_settled.npz > gpurun_out/v_${v}_$w.json 2> gpurun_out/v_${v}_$w.err || tail -3 gpurun_out/v_${v}_$w.err
   done
 done
 python - <<'PY'
