@@ -120,6 +120,22 @@ class Dist:
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
+def hero_initial_state(args, with_gpu: bool):
+    """(x, v, t) of the settled 50k column."""
+    if SETTLED.exists():
+        z = np.load(SETTLED)
+        return z["x"].astype(np.float64), z["v"].astype(np.float64), float(z["t"])
+    if not with_gpu:
+        return None
+    import paper_2306_01369_b200 as gg
+
+    sc = gg.hero_scene(50_000)
+    gg.run(sc, args.settle)
+    x = sc.particles.positions.astype(np.float32).astype(np.float64)
+    v = sc.particles.velocities.astype(np.float32).astype(np.float64)
+    return x, v, float(sc.t)
+
+
 def bed1m_settled(args):
     """SURVEY.md §8d config 4 initial state: lattice_bed(1e6) + floor, settled on
     the GPU at dt = 1e-3 (checked every 250 steps, at most --settle-bed steps)
