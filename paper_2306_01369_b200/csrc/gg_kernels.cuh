@@ -615,6 +615,9 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
 #ifndef GG_PASSCAP
 #define GG_PASSCAP 16
 #endif
+#ifndef GG_KDEPTH
+#define GG_KDEPTH 6
+#endif
 #ifndef GG_NARROW_MINB
 #define GG_NARROW_MINB 2
 #endif
@@ -623,8 +626,8 @@ constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass th
 constexpr int kWarps = kBlock / 32;
 
 struct NarrowSmem {
-  uint32_t beg[27][kBlock];
-  uint16_t len[27][kBlock];        // bucket sizes are < 2^16
+  uint32_t beg[28][kBlock];        // compacted non-empty buckets + a sentinel
+  uint16_t len[28][kBlock];        // bucket sizes are < 2^16
   uint32_t pass[kPassCap][kBlock]; // Xh index of every prefilter pass, per owner, in order
   float4 pos[kBlock];              // owner positions
   uint32_t off[kWarps][32];        // per-warp exclusive offsets of the owners' queue segments
@@ -806,26 +809,31 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       }
     }
     n_cand = total - 1;  // minus the self pair (one per particle, broadphase.py:441-447)
+    // sentinel after the last bucket: the cursor may run up to kDepth - 1
+    // candidates past the end without a guard (valid indices, never tested)
+    sm.beg[nb][tid] = sm.beg[0][tid];
+    sm.len[nb][tid] = 0xffffu;
+    const bool all = D.pipeline == 1;
+    const float rej = D.reject_d2f;
     CandCursor cur;
     cur.init(sm, tid);
-    constexpr int kDepth = 4;  // candidates in flight per thread
+    constexpr int kDepth = GG_KDEPTH;  // candidates in flight per thread
     for (uint32_t i = 0; i < total; i += kDepth) {
       uint32_t mi[kDepth];
 #pragma unroll
-      for (int u = 0; u < kDepth; ++u) mi[u] = cur.next(sm, tid, i + u + 1 < total);
+      for (int u = 0; u < kDepth; ++u) mi[u] = cur.next(sm, tid, true);
       float4 qv[kDepth];
 #pragma unroll
-      for (int u = 0; u < kDepth; ++u)
-        if (i + u < total) qv[u] = Xh[mi[u]];
+      for (int u = 0; u < kDepth; ++u) qv[u] = Xh[mi[u]];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) {
-        if (i + u >= total) break;
         const float4 qf = qv[u];
-        if (__float_as_int(qf.w) == k) continue;
         // float32 pre-filter, conservative by a 1e-5 relative margin (the
         // float32 estimate is within ~4e-7 relative of the exact square)
         const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
-        if (fx * fx + fy * fy + fz * fz <= D.reject_d2f || D.pipeline == 1) {
+        const bool pass = i + u < total && __float_as_int(qf.w) != k &&
+                          (fx * fx + fy * fy + fz * fz <= rej || all);
+        if (pass) {
           if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
           ++npass;
         }
