@@ -184,7 +184,8 @@ int alloc_slots(gg_ctx* ctx, int K) {
   // K records per particle on average: record 0 of particle k at index k,
   // the block allocator hands out [n, K * n) (per-owner counts are not
   // limited by K)
-  const size_t slots = static_cast<size_t>(std::max(K, 2)) * static_cast<size_t>(std::max<long long>(ctx->n, 1));
+  const size_t slots = static_cast<size_t>(std::max(K, kFixedSlots + 1)) *
+                       static_cast<size_t>(std::max<long long>(ctx->n, 1));
   CK(dalloc(ctx, &D.cgeo, slots));
   CK(dalloc(ctx, &D.coth, slots));
   CK(dalloc(ctx, &D.cvb, slots));
@@ -196,7 +197,7 @@ int alloc_slots(gg_ctx* ctx, int K) {
   ctx->K = K;
   D.K = K;
   D.cap_tot = static_cast<long long>(slots);
-  D.nrec0 = std::max<long long>(ctx->n, 1);
+  D.nrec0 = static_cast<long long>(kFixedSlots) * std::max<long long>(ctx->n, 1);
   ctx->graph_dirty = true;
   return GG_OK;
 }
@@ -1244,7 +1245,8 @@ int gg_tap_contacts(gg_ctx* ctx, int64_t cap_out, int64_t* count, int32_t* owner
   long long m = 0;
   for (long long k = 0; k < n; ++k) {
     for (int s = 0; s < ci[k].y; ++s) {
-      const size_t idx = s == 0 ? static_cast<size_t>(k) : static_cast<size_t>(ci[k].x) + s - 1;
+      const size_t idx = s < kFixedSlots ? static_cast<size_t>(s) * n + k
+                                         : static_cast<size_t>(ci[k].x) + s - kFixedSlots;
       const int j = oth[idx];
       if (j == kNullContact) continue;  // a prefilter pass that is no contact
       if (m++ >= cap_out) continue;

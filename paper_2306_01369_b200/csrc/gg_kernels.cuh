@@ -73,6 +73,11 @@ __device__ __forceinline__ unsigned long long to_fix(double v) {
   return static_cast<unsigned long long>(__double2ll_rn(v * kMomScale));
 }
 
+#ifndef GG_FIXED_SLOTS
+#define GG_FIXED_SLOTS 1
+#endif
+constexpr int kFixedSlots = GG_FIXED_SLOTS;  // records per particle at fixed indices (1 or 2)
+
 struct Dev {
   int n, K, nb, S, nblocks;
   int resort;     // this graph re-sorts the physical order first
@@ -125,10 +130,10 @@ struct Dev {
   float4* cvb;      // body surface velocity (body records)
   int2* cinfo;      // per particle {CSR offset of its record 1, record count}
   long long cap_tot;  // record capacity
-  // Record 0 of particle k lives at index k (the first nrec0 entries, one per
-  // particle slot, coalesced); records 1.. are warp-contiguous CSR entries
-  // allocated from nrec0 on.  A sweep can then fetch a particle's first
-  // contact together with its cinfo instead of after it.
+  // Records 0 .. kFixedSlots-1 of particle k live at fixed indices i * n + k
+  // (slot-major columns, coalesced); records kFixedSlots.. are warp-contiguous
+  // CSR entries allocated from nrec0 = kFixedSlots * n on.  A sweep fetches a
+  // particle's first contacts together with its cinfo instead of after it.
   long long nrec0;
   const gg_body* bodies;  // [batch][nb]
   const DevGrid* grids;
@@ -594,7 +599,7 @@ __device__ __forceinline__ double pp_d2(double px, double py, double pz, float4 
 
 // index of record i of particle k whose CSR records start at off
 __device__ __forceinline__ long long ridx(const Dev& D, int k, long long off, int i) {
-  return i == 0 ? static_cast<long long>(k) : off + i - 1;
+  return i < kFixedSlots ? static_cast<long long>(i) * D.n + k : off + i - kFixedSlots;
 }
 
 // One pp contact record (contact.py:264-272): e1 = d / |d| (j -> i),
@@ -871,9 +876,10 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
   const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, k, 0, 0, n_deg, max_psi) : 0;
   // ---- allocation: one atomic per block ----------------------------------------
-  // (record 0 of each owner is its own slot k; the rest come from the cursor)
+  // (records 0 .. kFixedSlots-1 of each owner are its fixed slots; the rest
+  // come from the cursor)
   const int tot = c_own + c_b;
-  const int talloc = tot > 0 ? tot - 1 : 0;
+  const int talloc = tot > kFixedSlots ? tot - kFixedSlots : 0;
   int wincl = talloc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1280,16 +1286,20 @@ __device__ __forceinline__ void sweep_oneloop(const Dev& D, int k, const float4*
   }
 }
 
-// Record 0 of particle k (slot k) and its CSR info, fetched together: one
-// dependent round trip fewer than reading cinfo first.
+// The fixed records of particle k and its CSR info, fetched together: one
+// dependent round trip fewer than reading cinfo first (and, with two fixed
+// slots, a second one for particles with two contacts).
 struct SweepHead {
   int2 ci;
-  float4 g0;
-  int j0;
+  float4 g[kFixedSlots];
+  int j[kFixedSlots];
   __device__ __forceinline__ void load(const Dev& D, int k) {
     ci = D.cinfo[k];
-    g0 = D.cgeo[k];
-    j0 = D.coth[k];
+#pragma unroll
+    for (int i = 0; i < kFixedSlots; ++i) {
+      g[i] = D.cgeo[static_cast<long long>(i) * D.n + k];
+      j[i] = D.coth[static_cast<long long>(i) * D.n + k];
+    }
   }
 };
 
@@ -1303,20 +1313,25 @@ __device__ __forceinline__ void sweep_particle_h(const Dev& D, int k, const Swee
   const float4 wf = Win[k];
   const double wx = wf.x, wy = wf.y, wz = wf.z;
   double ax = 0.0, ay = 0.0, az = 0.0;
-  if (h.j0 != kNullContact) {
-    const float4 q0 = (h.j0 >= 0) ? Win[h.j0] : D.cvb[k];
-    contact_impulse(D, wx, wy, wz, h.g0, h.j0, q0, ax, ay, az, A);
-  }
-  // records 1 .. c-1 at ci.x, ci.x + 1, ...
+  float4 q[kFixedSlots];
+#pragma unroll
+  for (int i = 0; i < kFixedSlots; ++i)
+    if (i < h.ci.y && h.j[i] != kNullContact)
+      q[i] = (h.j[i] >= 0) ? Win[h.j[i]] : D.cvb[static_cast<long long>(i) * D.n + k];
+#pragma unroll
+  for (int i = 0; i < kFixedSlots; ++i)
+    if (i < h.ci.y && h.j[i] != kNullContact)
+      contact_impulse(D, wx, wy, wz, h.g[i], h.j[i], q[i], ax, ay, az, A);
+  // records kFixedSlots .. c-1 at ci.x, ci.x + 1, ...
   const float4* gp = D.cgeo + h.ci.x;
   const int* jp = D.coth + h.ci.x;
   const float4* vp = D.cvb + h.ci.x;
-  for (int sl = 0; sl < h.ci.y - 1; ++sl) {
+  for (int sl = 0; sl < h.ci.y - kFixedSlots; ++sl) {
     const float4 g = gp[sl];
     const int j = jp[sl];
     if (j == kNullContact) continue;
-    const float4 q = (j >= 0) ? Win[j] : vp[sl];
-    contact_impulse(D, wx, wy, wz, g, j, q, ax, ay, az, A);
+    const float4 qq = (j >= 0) ? Win[j] : vp[sl];
+    contact_impulse(D, wx, wy, wz, g, j, qq, ax, ay, az, A);
   }
   Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
                         static_cast<float>(wz + az), 0.f);
@@ -1373,7 +1388,7 @@ struct RegContacts {
     for (int s = 0; s < kRegSlots; ++s)
       if (s < c && j[s] != kNullContact) contact_impulse(D, wx, wy, wz, g[s], j[s], q[s], ax, ay, az, A);
     for (int s = kRegSlots; s < c; ++s) {
-      const long long idx = static_cast<long long>(off) + s - 1;
+      const long long idx = ridx(D, k, off, s);
       const float4 gg = D.cgeo[idx];
       const int jj = D.coth[idx];
       if (jj == kNullContact) continue;

@@ -1,0 +1,52 @@
+"""Write profiles/<round>/SUMMARY.md from the bench lines and launch lists in it.
+
+    python tools/summarize_profiles.py profiles/r1
+"""
+import json
+import sys
+from pathlib import Path
+
+d = Path(sys.argv[1])
+
+
+def line(name):
+    p = d / f"bench_{name}.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text().strip().splitlines()[-1])
+
+
+rows = []
+for w in ("hero50k", "bed1m", "envs", "slab"):
+    z = line(w)
+    if not z:
+        continue
+    r, c = z.get("roofline") or {}, z.get("config") or {}
+    cb = z.get("cpu_baseline") or {}
+    rows.append(f"| {w} | {z['value']:.3e} | {z['ms_per_step']:.4f} | {z['e2e']['value']:.3e} | "
+                f"{r.get('kernel')} | {r.get('frac', 0):.3f} | "
+                f"{'-' if r.get('step_frac') is None else format(r['step_frac'], '.3f')} | "
+                f"{cb.get('value', float('nan')):.3g} | {c.get('c_pp', 0):.2f} | {c.get('c_b', 0):.3f} | "
+                f"{c.get('l2', '-')} |")
+ref = line("reference")
+clk = (line("hero50k") or {}).get("clocks", {})
+out = [f"# Round 1 profiles (1x B200, sm_100a, SM clock {clk.get('sm_mhz')} MHz of "
+       f"{clk.get('sm_max_mhz')}, throttle reasons {clk.get('reasons')})", "",
+       "Bench lines: `bench_<workload>.json` (`python bench.py --workload <w>`; hero50k is the default "
+       "run: 2000 steps; bed1m: 500 steps after 50 warm-up steps from the GPU-settled bed).",
+       "Launch lists: `launches_<workload>.csv` (ncu `gpu__time_duration.sum --clock-control none`, "
+       "cold cache, serialised), summarised in `launches_summary.txt`.",
+       "Full-set ncu captures of the top kernels: `ncu_full_summary.txt` (per kernel: duration, DRAM "
+       "bytes, L1/L2 hit rates, occupancy, stall reasons); per-launch DRAM traffic in "
+       "`../ncu_summary.json` (read by bench.py as `roofline.traffic`); per-SASS-instruction "
+       "executions and stall samples in `sass_*.csv.gz` (attribute to source lines with "
+       "`tools/sass_lines.py`).",
+       "compute-sanitizer (memcheck, racecheck, synccheck, initcheck): `sanitizer/`.", "",
+       "| workload | particle-steps/s | ms/step | e2e particle-steps/s | top kernel | HBM frac (kernel) | "
+       "HBM frac (step model) | CPU oracle 1 core | c_pp | c_b | L2 |",
+       "|---|---|---|---|---|---|---|---|---|---|---|", *rows, ""]
+if ref:
+    out.append(f"Reference arm (`bench.py --impl reference`, oracle port, "
+               f"{ref['cpu_baseline']['cores']} core): {ref['value']:.3e} particle-steps/s on hero50k.")
+(d / "SUMMARY.md").write_text("\n".join(out) + "\n")
+print("\n".join(out))
