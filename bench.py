@@ -88,15 +88,21 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = None
         if self.world > 1:
             import torch
             import torch.distributed as td
 
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-            if backend == "nccl":
+            n_dev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+            # one GPU per rank (NCCL); with fewer GPUs than ranks (a plumbing
+            # check on a small box) ranks share GPUs round-robin over gloo
+            backend = "nccl" if n_dev >= self.world else "gloo"
+            if n_dev:
+                self.local = self.local % n_dev
                 torch.cuda.set_device(self.local)
             td.init_process_group(backend)
             self.pg = td
+            self.backend = backend
 
     def barrier(self):
         if self.pg:
@@ -107,7 +113,7 @@ class Dist:
             return x
         import torch
 
-        dev = f"cuda:{self.local}" if torch.cuda.is_available() else "cpu"
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
@@ -606,7 +612,7 @@ def run_slab(args, dist: Dist):
                   bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
                   params=gg.MaterialParams(timestep=5e-4))
     bed = SlabBed(sc, rank=dist.rank, world=dist.world, device=dev,
-                  backend="nccl" if dist.world > 1 else None)
+                  backend=dist.backend if dist.world > 1 else None)
     lib = N.lib()
     K, W = args.steps, args.warmup
     for _ in range(W):
@@ -649,7 +655,7 @@ def run_slab(args, dist: Dist):
                    bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
                    params=gg.MaterialParams(timestep=5e-4))
     bed2 = SlabBed(sc2, rank=dist.rank, world=dist.world, device=dev,
-                   backend="nccl" if dist.world > 1 else None)
+                   backend=dist.backend if dist.world > 1 else None)
     for _ in range(K):
         bed2.step()
     Xg, _ = bed2.gather()
