@@ -789,6 +789,22 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       tz[d] = hash_term32(c2 + d - 1, kP2);
     }
     const bool dedup = !D.H.pow2 || may_alias(tx, ty, tz, D.H.mask);
+    // bit o: neighbour o's bucket was already visited at an earlier offset
+    // (rare: only particles whose 27 cells can alias run this loop; a real
+    // branch, not predicated code every lane would issue)
+    uint32_t dupmask = 0u;
+    if (dedup) {
+      uint32_t hh[27];
+#pragma unroll
+      for (int o = 0; o < 27; ++o) hh[o] = nb_hash(D, o, c0, c1, c2, tx, ty, tz);
+#pragma unroll
+      for (int o = 1; o < 27; ++o) {
+        bool dup = false;
+#pragma unroll
+        for (int q = 0; q < o; ++q) dup |= hh[q] == hh[o];
+        dupmask |= dup ? (1u << o) : 0u;
+      }
+    }
     int nb = 0;
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
@@ -801,10 +817,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       }
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
-        bool keep = eb[j] > sb[j];
-        if (keep && dedup) {
-          for (int q = 0; q < g * 9 + j; ++q) keep &= nb_hash(D, q, c0, c1, c2, tx, ty, tz) != hb[j];
-        }
+        const bool keep = eb[j] > sb[j] && !((dupmask >> (g * 9 + j)) & 1u);
         if (keep) {
           sm.beg[nb][tid] = sb[j];
           sm.len[nb][tid] = static_cast<uint16_t>(eb[j] - sb[j]);
