@@ -164,6 +164,24 @@ __device__ __forceinline__ T warp_sum(T v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   return v;
 }
+// Max / min over a warp of non-negative doubles held as bit patterns (for
+// x >= +0.0 the IEEE order is the unsigned order of the bits): two 32-bit
+// REDUX reductions instead of five float64 shuffle + compare rounds.
+__device__ __forceinline__ unsigned long long warp_umax64(unsigned long long v) {
+  const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
+  const unsigned lo =
+      __reduce_max_sync(0xffffffffu, static_cast<unsigned>(v >> 32) == hi ? static_cast<unsigned>(v) : 0u);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long warp_umin64(unsigned long long v) {
+  const unsigned hi = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
+  const unsigned lo = __reduce_min_sync(
+      0xffffffffu, static_cast<unsigned>(v >> 32) == hi ? static_cast<unsigned>(v) : 0xffffffffu);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = nmax(v, __shfl_down_sync(0xffffffffu, v, o));
@@ -743,6 +761,64 @@ __device__ __forceinline__ int body_contacts(const Dev& D, const gg_body* bodies
   return c;
 }
 
+// The contact phase's six per-step counters in one pass: warp sums (and the
+// max of max_psi on its bit pattern, which orders like the value for x >= +0),
+// one block barrier, then six threads each reduce one counter over the warps
+// and issue its atomic.  E > 1: env-uniform warps issue their own atomics,
+// warps straddling two envs per lane.  Called by every thread of the block.
+__device__ __forceinline__ void acc_contacts(const Dev& D, int env, unsigned long long n_pp,
+                                             unsigned long long n_cand, unsigned long long n_coinc,
+                                             unsigned long long n_body, unsigned long long n_deg,
+                                             double max_psi) {
+  __shared__ unsigned long long s_acc[kWarps][6];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned long long mp = dbits(max_psi > 0.0 ? max_psi : 0.0);
+  // counter f's byte offset in Acc (selects, not an indexed array: f can be
+  // a runtime value and an array would live in local memory)
+  auto offs = [](int f) -> size_t {
+    return f == 0 ? GG_ACC(n_pp)
+                  : f == 1 ? GG_ACC(n_cand)
+                           : f == 2 ? GG_ACC(n_coinc)
+                                    : f == 3 ? GG_ACC(n_body) : f == 4 ? GG_ACC(n_deg) : GG_ACC(max_psi_bits);
+  };
+  int e0 = 0;
+  const bool uni = D.E == 1 || warp_env_uniform(env, &e0);
+  if (uni) {
+    const unsigned long long v[6] = {warp_sum(n_pp), warp_sum(n_cand), warp_sum(n_coinc),
+                                     warp_sum(n_body), warp_sum(n_deg), warp_umax64(mp)};
+    if (D.E == 1) {
+      if (lane == 0)
+#pragma unroll
+        for (int f = 0; f < 6; ++f) s_acc[w][f] = v[f];
+    } else if (lane == 0) {
+#pragma unroll
+      for (int f = 0; f < 5; ++f)
+        if (v[f]) atomicAdd(acc_field(D, e0, offs(f)), v[f]);
+      if (v[5]) atomicMax(acc_field(D, e0, offs(5)), v[5]);
+    }
+  } else {
+    const unsigned long long v[6] = {n_pp, n_cand, n_coinc, n_body, n_deg, mp};
+#pragma unroll
+    for (int f = 0; f < 5; ++f)
+      if (v[f]) atomicAdd(acc_field(D, env, offs(f)), v[f]);
+    if (mp) atomicMax(acc_field(D, env, offs(5)), mp);
+  }
+  if (D.E != 1) return;
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int f = threadIdx.x;
+    unsigned long long t = 0;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q)
+      t = f < 5 ? t + s_acc[q][f] : (s_acc[q][f] > t ? s_acc[q][f] : t);
+    if (t) {
+      if (f < 5)
+        atomicAdd(acc_field(D, 0, offs(f)), t);
+      else
+        atomicMax(acc_field(D, 0, offs(f)), t);
+    }
+  }
+}
+
 // K5+K6: all contacts of particles base .. base+blockDim (contact.py:244-300).
 //
 // Phase A (per thread): the 27 neighbour-bucket bounds (three batches of 9
@@ -971,12 +1047,8 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
     }
   }
-  acc_add(D, env, static_cast<unsigned long long>(c_pp), GG_ACC(n_pp), sm.u);
-  acc_add(D, env, n_cand, GG_ACC(n_cand), sm.u);
-  acc_add(D, env, n_coinc, GG_ACC(n_coinc), sm.u);
-  acc_add(D, env, static_cast<unsigned long long>(c_b), GG_ACC(n_body), sm.u);
-  acc_add(D, env, n_deg, GG_ACC(n_deg), sm.u);
-  acc_ext<1>(D, env, max_psi, GG_ACC(max_psi_bits), sm.d);
+  acc_contacts(D, env, static_cast<unsigned long long>(c_pp), n_cand, n_coinc,
+               static_cast<unsigned long long>(c_b), n_deg, max_psi);
 }
 
 // ---------------------------------------------------------------------------
@@ -1051,23 +1123,6 @@ __device__ __forceinline__ void sweep_acc_env(const Dev& D, SweepAcc& A, int k) 
   A.env = e;
 }
 
-// Max / min over a warp of non-negative doubles held as bit patterns (for
-// x >= +0.0 the IEEE order is the unsigned order of the bits): two 32-bit
-// REDUX reductions instead of five float64 shuffle + compare rounds.
-__device__ __forceinline__ unsigned long long warp_umax64(unsigned long long v) {
-  const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
-  const unsigned lo =
-      __reduce_max_sync(0xffffffffu, static_cast<unsigned>(v >> 32) == hi ? static_cast<unsigned>(v) : 0u);
-  return (static_cast<unsigned long long>(hi) << 32) | lo;
-}
-__device__ __forceinline__ unsigned long long warp_umin64(unsigned long long v) {
-  const unsigned hi = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
-  const unsigned lo = __reduce_min_sync(
-      0xffffffffu, static_cast<unsigned>(v >> 32) == hi ? static_cast<unsigned>(v) : 0xffffffffu);
-  return (static_cast<unsigned long long>(hi) << 32) | lo;
-}
-
-constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 
 // per block: diagnostics (max cone violation, min normal impulse: warp
 // reductions on the bit patterns, one atomic each per block) + body momentum
