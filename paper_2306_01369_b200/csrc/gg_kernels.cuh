@@ -313,6 +313,9 @@ __device__ __forceinline__ bool block_should_exit(const Ctl* ctl) {
 // Returns ctl->err as seen after the barrier (every error is raised before
 // its block arrives, i.e. before a release the final acquire synchronises
 // with, and err is read by the same 64-bit load at the L2).
+#ifndef GG_BAR_SLEEP
+#define GG_BAR_SLEEP 0
+#endif
 __device__ __forceinline__ int grid_barrier(Ctl* ctl, unsigned target) {
   __shared__ int s_err;
   __syncthreads();
@@ -324,8 +327,12 @@ __device__ __forceinline__ int grid_barrier(Ctl* ctl, unsigned target) {
     // spin with relaxed (L1-bypassing) loads, then ONE acquire load: the
     // L1 invalidation happens once, not on every poll (an invalidation per
     // poll also evicts the lines the other block on this SM is working on)
-    while (static_cast<int>(v - target) < 0)
+    while (static_cast<int>(v - target) < 0) {
+#if GG_BAR_SLEEP
+      __nanosleep(GG_BAR_SLEEP);
+#endif
       asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&ctl->bar_count) : "memory");
+    }
     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(w) : "l"(&ctl->bar_count) : "memory");
     s_err = static_cast<int>(w >> 32);
   }
@@ -1426,11 +1433,24 @@ struct RegContacts {
 
   int off;
   __device__ __forceinline__ void load(const Dev& D, int k, float4 w0) {
+    // the fixed records are requested together with the count (their
+    // indices do not depend on it), the CSR ones after it
+#pragma unroll
+    for (int s = 0; s < kFixedSlots; ++s) {
+      const long long r = static_cast<long long>(s) * D.n + k;
+      g[s] = D.cgeo[r];
+      j[s] = D.coth[r];
+    }
     const int2 ci = D.cinfo[k];
     c = ci.y;
     off = ci.x;
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s) {
+      if (s < kFixedSlots) {
+        if (s >= c) j[s] = 0;
+        else if (j[s] < 0) qb[s] = D.cvb[static_cast<long long>(s) * D.n + k];
+        continue;
+      }
       j[s] = 0;
       if (s < c) {
         const long long r = ridx(D, k, off, s);
