@@ -30,4 +30,4 @@ for resort in (False, True):
     lib.gg_phase_timer(eng.ctx, 1, N.ptr(st), 64)
     k = int(np.nonzero(st)[0].max()) + 1
     d = np.diff(st[:k].astype(np.int64)) / 1000.0
-    print(f"resort={resort} total {(st[k-1]-st[0])/1000:.1f} us; phases (us):", np.round(d, 2).tolist())
+    print(f"resort={resort} total {(int(st[k-1]) - int(st[0])) / 1000:.1f} us; phases (us):", np.round(d, 2).tolist())
