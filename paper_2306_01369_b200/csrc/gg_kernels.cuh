@@ -1423,12 +1423,20 @@ __device__ __forceinline__ void sweep_particle(const Dev& D, int k, const float4
 // the first kRegSlots contacts and the particle's own w are loaded once and
 // kept across all sweeps; each sweep issues its neighbour gathers together.
 // Arithmetic and accumulation order are exactly those of sweep_particle.
-constexpr int kRegSlots = 4;
+#ifndef GG_REG_SLOTS
+#define GG_REG_SLOTS 6
+#endif
+constexpr int kRegSlots = GG_REG_SLOTS;
+#ifndef GG_REG_QB
+#define GG_REG_QB 0
+#endif
 struct RegContacts {
   int c;
   float4 g[kRegSlots];
   int j[kRegSlots];
-  float4 qb[kRegSlots];
+#if GG_REG_QB
+  float4 qb[kRegSlots];  // body records' surface velocity (else re-read from cvb per sweep)
+#endif
   float wx, wy, wz;
 
   int off;
@@ -1448,7 +1456,9 @@ struct RegContacts {
     for (int s = 0; s < kRegSlots; ++s) {
       if (s < kFixedSlots) {
         if (s >= c) j[s] = 0;
+#if GG_REG_QB
         else if (j[s] < 0) qb[s] = D.cvb[static_cast<long long>(s) * D.n + k];
+#endif
         continue;
       }
       j[s] = 0;
@@ -1456,7 +1466,9 @@ struct RegContacts {
         const long long r = ridx(D, k, off, s);
         g[s] = D.cgeo[r];
         j[s] = D.coth[r];
+#if GG_REG_QB
         if (j[s] < 0) qb[s] = D.cvb[r];
+#endif
       }
     }
     wx = w0.x;
@@ -1470,7 +1482,12 @@ struct RegContacts {
     float4 q[kRegSlots];
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s)
-      if (s < c && j[s] != kNullContact) q[s] = (j[s] >= 0) ? Win[j[s]] : qb[s];
+      if (s < c && j[s] != kNullContact)
+#if GG_REG_QB
+        q[s] = (j[s] >= 0) ? Win[j[s]] : qb[s];
+#else
+        q[s] = (j[s] >= 0) ? Win[j[s]] : D.cvb[ridx(D, k, off, s)];
+#endif
     double ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
     for (int s = 0; s < kRegSlots; ++s)
