@@ -44,3 +44,17 @@ sc = bed(500)
 img = render_depth(sc, DepthCamera(kind="perspective", pose=gg.make_pose(np.eye(3), [0.5, 0.5, -2.0]),
                                    width=16, height=12))
 print("render ok", float(img.min()))
+for pipe in (gg.PipelineMode.TWO_LOOPS_FUSED, gg.PipelineMode.ONE_LOOP):
+    sc = bed(2000)
+    gg.run(sc, 2, mode=pipe)
+    print("pipeline", pipe.value, "ok")
+big = bed(40000)  # > fused grid? exercises k_narrow / k_sweep / k_finish when not fused
+eng = engine_for(big)
+eng.prepare(big)
+N.lib().gg_set_solve_mode(eng.ctx, 3)
+gg.run(big, 2)
+print("per-sweep kernels ok")
+from paper_2306_01369_b200.meshes import make_gear_mesh
+from paper_2306_01369_b200.sdf import bake_mesh_sdf
+g = bake_mesh_sdf(*make_gear_mesh(n_teeth=5, root_radius=0.05, tip_radius=0.08, thickness=0.03, n_layers=2), 0.01)
+print("bake ok", g.values.shape)
