@@ -732,7 +732,11 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
     }
     cudaGetLastError();  // a refused query only disables the cluster path
   }
-  CK(dalloc(ctx, &D.Xh, n));
+  // kXhPad entries past the end: the candidate loop's sentinel bucket may read
+  // up to GG_KDEPTH - 1 entries beyond a bucket that ends at the last entry
+  // (values never tested); zeroed so every read is of initialised memory
+  CK(dalloc(ctx, &D.Xh, n + kXhPad));
+  CK(cudaMemset(D.Xh, 0, sizeof(float4) * (n + kXhPad)));
   CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks,
                                                           kClusterCTAs}))));

@@ -645,6 +645,7 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
 #ifndef GG_PASSCAP
 #define GG_PASSCAP 16
 #endif
+constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidate copy
 #ifndef GG_KDEPTH
 #define GG_KDEPTH 6
 #endif
@@ -911,7 +912,8 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     }
     n_cand = total - 1;  // minus the self pair (one per particle, broadphase.py:441-447)
     // sentinel after the last bucket: the cursor may run up to kDepth - 1
-    // candidates past the end without a guard (valid indices, never tested)
+    // candidates past the end without a guard (indices < n + kXhPad: Xh is
+    // padded; never tested)
     sm.beg[nb][tid] = sm.beg[0][tid];
     sm.len[nb][tid] = 0xffffu;
     const bool all = D.pipeline == 1;
@@ -919,6 +921,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     CandCursor cur;
     cur.init(sm, tid);
     constexpr int kDepth = GG_KDEPTH;  // candidates in flight per thread
+    static_assert(kDepth <= kXhPad, "the sentinel bucket reads up to kDepth - 1 entries past n");
     for (uint32_t i = 0; i < total; i += kDepth) {
       uint32_t mi[kDepth];
 #pragma unroll
