@@ -420,12 +420,17 @@ class SceneBatch:
         if slot.corners is None:
             col["bounded"] = 0
             return
-        # corners @ R^T + t (the _near_body AABB, contact.py:196-201); the box
-        # is conservative by r, so rounding of its faces cannot decide a contact
-        world = np.einsum("eci,teji->tecj", slot.corners, R, optimize=True) + tr[:, :, None, :]
+        # the world AABB of the body-local contact box (the _near_body box,
+        # contact.py:196-201), in closed form: centre R c + t, half extents
+        # |R| h (the corners' min / max up to rounding).  The box is
+        # conservative by r, so rounding of its faces cannot decide a contact.
+        lo, hi = slot.corners.min(axis=1), slot.corners.max(axis=1)  # (E, 3)
+        c, h = 0.5 * (lo + hi), 0.5 * (hi - lo)
+        wc = np.einsum("teij,ej->tei", R, c) + tr
+        ext = np.einsum("teij,ej->tei", np.abs(R), h)
         col["bounded"] = 1
-        col["aabb_lo"] = world.min(axis=2)
-        col["aabb_hi"] = world.max(axis=2)
+        col["aabb_lo"] = wc - ext
+        col["aabb_hi"] = wc + ext
 
     def last_bodies(self) -> np.ndarray:
         """(E, nb) gg_body rows at the current time (the last stepped poses,
