@@ -386,3 +386,29 @@ def test_batched_excavation_env_matches_reference():
     obs, rew, done, info = env.step(np.zeros((E, 7)))
     assert np.all(rew == 0) and obs.ego.shape == (E, 36, 36)
     env.close()
+
+
+def test_closed_form_body_aabb_matches_corners():
+    """SceneBatch._fill's world AABB (centre R c + t, half extents |R| h) is the
+    min / max of the 8 transformed contact-box corners up to rounding (CPU)."""
+    from paper_2306_01369_b200 import _native as N
+    from paper_2306_01369_b200.batch import SceneBatch, _BodySlot, so3_exp_batch
+
+    T, E = 3, 50
+    rng = np.random.default_rng(3)
+    lo = rng.uniform(-1, 0, (E, 3))
+    hi = lo + rng.uniform(0.1, 1, (E, 3))
+    corners = np.stack([[np.where([i & 4, i & 2, i & 1], hi[e], lo[e]) for i in range(8)]
+                        for e in range(E)])
+    slot = _BodySlot(kind=np.ones(E, np.int32), shape=np.zeros((E, 4)), grid_id=np.zeros(E, np.int32),
+                     corners=corners)
+    P = np.zeros((T, E, 4, 4))
+    P[..., :3, :3] = so3_exp_batch(rng.normal(size=(T * E, 3))).reshape(T, E, 3, 3)
+    P[..., :3, 3] = rng.normal(size=(T, E, 3))
+    P[..., 3, 3] = 1.0
+    col = np.zeros((T, E), dtype=N.BODY_DTYPE)
+    SceneBatch._fill(col, slot, P, np.zeros((T, E, 3)), np.zeros((T, E, 3)))
+    world = np.einsum("eci,teji->tecj", corners, P[..., :3, :3]) + P[..., None, :3, 3]
+    assert np.abs(col["aabb_lo"] - world.min(axis=2)).max() <= 1e-14
+    assert np.abs(col["aabb_hi"] - world.max(axis=2)).max() <= 1e-14
+    assert (col["bounded"] == 1).all()
