@@ -297,6 +297,44 @@ def test_empty_scene_report():
     assert sc.t == pytest.approx(sc.params.timestep)
 
 
+@pytest.mark.parametrize("case", ["one_on_floor", "touching_pair", "pair_in_box_corner", "far_apart"])
+def test_tiny_scenes_vs_oracle(case):
+    """Smallest inputs (1-3 particles, n_h = 2 .. 8): the kernels' edge paths
+    (single-block grids, tables smaller than a warp, owners with one contact)
+    against the oracle over 20 steps, bit-exact counters every step."""
+    r = 0.05
+    if case == "one_on_floor":
+        x = np.array([[0.0, 0.0, 0.049]])
+        bodies = [gg.RigidBody(gg.HalfSpace(), name="floor")]
+    elif case == "touching_pair":
+        x = np.array([[0.0, 0.0, 0.3], [0.0, 0.0, 0.399]])
+        bodies = []
+    elif case == "pair_in_box_corner":
+        x = np.array([[0.02, 0.02, 0.049], [0.02, 0.119, 0.049], [0.118, 0.02, 0.049]])
+        bodies = [gg.RigidBody(gg.HalfSpace(), name="floor"),
+                  gg.RigidBody(gg.Box([0.1, 0.1, 0.1]),
+                               gg.StaticDriver(gg.make_pose(np.eye(3), [-0.1, -0.1, 0.1])), name="wall")]
+    else:
+        x = np.array([[0.0, 0.0, 0.5], [100.0, -50.0, 0.5]])
+        bodies = [gg.RigidBody(gg.HalfSpace(), name="floor")]
+    x = x.astype(np.float32).astype(np.float64)
+    params = gg.MaterialParams(radius=r, timestep=5e-4)
+    sc = gg.Scene(particles=gg.ParticleSet(x.copy(), np.zeros_like(x)), bodies=bodies, params=params)
+    n_h = gg.default_table_size(len(x))
+    xo, vo = x.copy(), np.zeros_like(x)
+    for k in range(20):
+        _, rep = gg.step(sc)
+        xo, vo, orep, _, _ = O.step(xo, vo, params, sc.bodies, n_h)
+        assert rep.n_contacts == orep["n_contacts"], k
+        assert rep.n_body_contacts == orep["n_body_contacts"], k
+        assert rep.n_candidates == orep["n_candidates"], k
+        assert rel_err(sc.particles.positions, xo) <= TOL, k
+        assert rel_err(sc.particles.velocities, vo) <= TOL, k
+        # the oracle continues from the device state (teacher forcing, as in the parity protocol)
+        xo = sc.particles.positions.astype(np.float32).astype(np.float64)
+        vo = sc.particles.velocities.astype(np.float32).astype(np.float64)
+
+
 def test_penetration_depth_kats():
     # tests/test_sdf.py:204-231 hand values
     psi, n, hit, deg = gg.penetration_depth(gg.Sphere(1.0), gg.identity_pose(),
