@@ -802,7 +802,9 @@ def run_ours(args, dist: Dist):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
             "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
-            "data": "synthetic (seeded lattice bed, settled on the GPU before the run)",
+            "data": ("synthetic (50k column bed settled on the GPU, bench_data/hero50k_settled.npz)"
+                     if args.workload == "hero50k" else
+                     "synthetic (lattice_bed(1e6) settled on the GPU before the run)"),
             "config": {**desc, "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
                        "pipeline": args.pipeline,
                        "l2": l2_note(args, n * 200 / 2**20),
