@@ -131,6 +131,7 @@ void dfree(gg_ctx* ctx, void* p) {
 }
 
 int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock); }
+int narrow_blocks(long long n) { return static_cast<int>((n + kNarrowBlock - 1) / kNarrowBlock); }
 
 int validate_params(gg_ctx* ctx, const gg_params* p) {
   if (!p) return fail(ctx, GG_EINVAL, "params is NULL");
@@ -380,7 +381,7 @@ int enqueue_step(gg_ctx* ctx, int resort) {
   const Dev D = pass_dev(ctx, resort, 0);
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
-  k_narrow<<<ctx->nblocks, kBlock, sizeof(NarrowSmem), s>>>(D);
+  k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
   CK(cudaGetLastError());
   return launch_solve(ctx, D, s);
 }
@@ -460,7 +461,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     }
   }
   const Dev D = pass_dev(ctx, resort, 0);
-  k_narrow<<<nbn, kBlock, sizeof(NarrowSmem), s>>>(D);
+  k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
   mark(8);
   if (use_persistent_solve(ctx)) {
     if (launch_solve(ctx, D, s) != GG_OK) return -1;
@@ -692,7 +693,7 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   CK(dalloc(ctx, &D.cinfo, n));
   CK(cudaMemset(D.cinfo, 0, sizeof(int2) * n));
   CK(cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(sizeof(NarrowSmem))));
+                          static_cast<int>(sizeof(NarrowSmemN))));
   CK(cudaFuncSetAttribute(k_step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(sizeof(NarrowSmem))));
   CK(dalloc(ctx, &D.acc, E));
@@ -1014,7 +1015,7 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
   if (st != GG_OK) return st;
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
-  k_narrow<<<ctx->nblocks, kBlock, sizeof(NarrowSmem), s>>>(D);
+  k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
   ctx->launches += 9;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
@@ -1580,7 +1581,7 @@ int gg_slab_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies) {
     st = enqueue_sort_pass(ctx, D, s);
     ctx->nblocks = nb_save;
     if (st != GG_OK) return st;
-    k_narrow<<<blocks_for(ctx->n_cur), kBlock, sizeof(NarrowSmem), s>>>(D);
+    k_narrow<<<narrow_blocks(ctx->n_cur), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
   }
   ctx->launches += 9;
   ctx->last_batch = 1;

@@ -656,29 +656,39 @@ constexpr int kPassCap = GG_PASSCAP;  // prefilter passes queued per owner (more
 constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass that is no contact)
 constexpr int kWarps = kBlock / 32;
 
-struct NarrowSmem {
-  uint32_t beg[28][kBlock];        // compacted non-empty buckets + a sentinel
-  uint16_t len[28][kBlock];        // bucket sizes are < 2^16
-  uint32_t pass[kPassCap][kBlock]; // Xh index of every prefilter pass, per owner, in order
-  float4 pos[kBlock];              // owner positions
-  uint32_t off[kWarps][32];        // per-warp exclusive offsets of the owners' queue segments
-  uint8_t qown[kWarps][32 * kPassCap];  // per-warp queue: owner lane of each entry
-  unsigned long long wrec[kWarps]; // per-warp record totals -> bases (block allocation)
+template <int B>
+struct NarrowSmemT {
+  static constexpr int kW = B / 32;
+  uint32_t beg[28][B];        // compacted non-empty buckets + a sentinel
+  uint16_t len[28][B];        // bucket sizes are < 2^16
+  uint32_t pass[kPassCap][B]; // Xh index of every prefilter pass, per owner, in order
+  float4 pos[B];              // owner positions
+  uint32_t off[kW][32];       // per-warp exclusive offsets of the owners' queue segments
+  uint8_t qown[kW][32 * kPassCap];  // per-warp queue: owner lane of each entry
+  unsigned long long wrec[kW];      // per-warp record totals -> bases (block allocation)
   double d[32];
   unsigned long long u[32];
 };
+using NarrowSmem = NarrowSmemT<kBlock>;
+#ifndef GG_NARROW_BLOCK
+#define GG_NARROW_BLOCK 256
+#endif
+constexpr int kNarrowBlock = GG_NARROW_BLOCK;  // k_narrow block size (large-n contact kernel)
+using NarrowSmemN = NarrowSmemT<kNarrowBlock>;
 
 // Iterate over a thread's concatenated candidate list (its compacted
 // neighbour buckets) — the cursor of the flat candidate loop.
 struct CandCursor {
   int b;
   uint32_t m, left;
-  __device__ __forceinline__ void init(const NarrowSmem& sm, int tid) {
+  template <class SM>
+  __device__ __forceinline__ void init(const SM& sm, int tid) {
     b = 0;
     m = sm.beg[0][tid];
     left = sm.len[0][tid];
   }
-  __device__ __forceinline__ uint32_t next(const NarrowSmem& sm, int tid, bool more) {
+  template <class SM>
+  __device__ __forceinline__ uint32_t next(const SM& sm, int tid, bool more) {
     const uint32_t cur = m;
     if (more) {
       ++m;
@@ -697,7 +707,8 @@ struct CandCursor {
 // dst on (write == true), in candidate order — the same order the queue gives.
 // c_slots: records (= contacts, or every candidate in TWO_LOOPS_FUSED);
 // c_pp: contacts.
-__device__ __forceinline__ void scan_exact(const Dev& D, const NarrowSmem& sm, int tid, int k,
+template <class SM>
+__device__ __forceinline__ void scan_exact(const Dev& D, const SM& sm, int tid, int k,
                                            float4 pf, uint32_t total, bool write, long long off,
                                            int& c_slots, int& c_pp, unsigned long long& n_coinc,
                                            double& max_psi) {
@@ -842,8 +853,10 @@ __device__ __forceinline__ void acc_contacts(const Dev& D, int env, unsigned lon
 //   owner stay in candidate order, then bodies in index order, so results
 //   do not depend on where the allocator put them.
 // Particles base .. base + count - 1 (count <= blockDim.x) belong to this block.
+template <class SM>
 __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, int count,
-                                            NarrowSmem& sm) {
+                                            SM& sm) {
+  constexpr int kWarps = SM::kW;
   // plain (coherent) loads: in the fused kernel these buffers are written
   // earlier in the same launch, so the read-only (.nc) path is not allowed
   const float4* LX = layout(D, ctl).x;
@@ -1725,8 +1738,8 @@ __global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
 // NarrowSmem (> 48 KB) is dynamic shared memory: launch with sizeof(NarrowSmem)
 extern __shared__ __align__(16) unsigned char g_dsmem[];
 
-__global__ void __launch_bounds__(kBlock, GG_NARROW_MINB) k_narrow(Dev D) {
-  NarrowSmem& sm = *reinterpret_cast<NarrowSmem*>(g_dsmem);
+__global__ void __launch_bounds__(kNarrowBlock, GG_NARROW_MINB) k_narrow(Dev D) {
+  NarrowSmemN& sm = *reinterpret_cast<NarrowSmemN*>(g_dsmem);
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
   ph_contacts(D, ctl, blockIdx.x * blockDim.x, blockDim.x, sm);
