@@ -48,5 +48,48 @@ out = [f"# Round 1 profiles (1x B200, sm_100a, SM clock {clk.get('sm_mhz')} MHz 
 if ref:
     out.append(f"Reference arm (`bench.py --impl reference`, oracle port, "
                f"{ref['cpu_baseline']['cores']} core): {ref['value']:.3e} particle-steps/s on hero50k.")
+# where the time goes: kernel shares of each workload's step (bench roofline pass)
+out += ["", "## Kernel time shares (device, per step)", ""]
+for w in ("hero50k", "bed1m", "envs"):
+    z = line(w)
+    if not z:
+        continue
+    sh = (z.get("roofline") or {}).get("kernel_time_share", {})
+    parts = ", ".join(f"{k} {v:.1%}" for k, v in sorted(sh.items(), key=lambda kv: -kv[1])
+                      if v >= 0.01 and k != "k_solve")
+    out.append(f"* {w}: {parts}")
+# ncu full-set digest: one line per captured kernel (first capture of each name)
+ncu = d / "ncu_full_summary.txt"
+if ncu.exists():
+    import re
+    out += ["", "## ncu full-set digest (cold cache, one launch each)", "",
+            "| capture | kernel | us | DRAM MB (r+w) | warps active | L1 hit | L2 hit | top stall (cycles per issue) |",
+            "|---|---|---|---|---|---|---|---|"]
+    cap, cur, seen = None, None, set()
+    rows = {}
+    for ln in ncu.read_text().splitlines():
+        if ln.endswith(".ncu-rep"):
+            cap = Path(ln.strip()).stem
+            continue
+        m = re.match(r"\s+--- (\S+)\(", ln)
+        if m:
+            cur = (cap, m.group(1))
+            if cur not in rows:
+                rows[cur] = {}
+            continue
+        m = re.match(r"\s+(\S+)\s+([0-9.]+)\s*(\S*)", ln)
+        if m and cur and m.group(1) not in rows[cur]:
+            scale = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6, "byte": 1e-6, "Kbyte": 1e-3,
+                     "Mbyte": 1.0, "Gbyte": 1e3}.get(m.group(3), 1.0)
+            rows[cur][m.group(1)] = float(m.group(2)) * scale
+    for (c, k), r in rows.items():
+        stalls = {n.split("stalled_")[1].split("_per_issue")[0]: v for n, v in r.items() if "stalled_" in n
+                  and "selected" not in n}
+        top = max(stalls.items(), key=lambda kv: kv[1]) if stalls else ("-", 0)
+        out.append(f"| {c} | {k} | {r.get('gpu__time_duration.sum', 0):.1f} | "
+                   f"{r.get('dram__bytes_read.sum', 0) + r.get('dram__bytes_write.sum', 0):.1f} | "
+                   f"{r.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.0f}% | "
+                   f"{r.get('l1tex__t_sector_hit_rate.pct', 0):.0f}% | {r.get('lts__t_sector_hit_rate.pct', 0):.0f}% | "
+                   f"{top[0]} {top[1]:.1f} |")
 (d / "SUMMARY.md").write_text("\n".join(out) + "\n")
 print("\n".join(out))
