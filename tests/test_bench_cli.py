@@ -10,6 +10,7 @@ import sys
 from pathlib import Path
 
 import numpy as np
+import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
@@ -43,3 +44,29 @@ def test_reference_arm_line():
     assert line["impl"] == "reference" and line["unit"] == "particle-steps/s"
     assert line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "port"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [
+    ["--workload", "hero50k", "--steps", "3", "--warmup", "3", "--cpu-seconds", "0.5", "--profile-steps", "1"],
+    ["--workload", "bed1m", "--steps", "3", "--warmup", "3", "--settle-bed", "250", "--no-cpu-baseline",
+     "--profile-steps", "1"],
+    ["--workload", "envs", "--envs", "16", "--steps", "20", "--warmup", "3", "--no-cpu-baseline",
+     "--profile-steps", "1"],
+    ["--workload", "slab", "--slab-particles", "100000", "--steps", "3", "--warmup", "3",
+     "--no-cpu-baseline"],
+], ids=["hero50k", "bed1m", "envs", "slab"])
+def test_bench_line_contract(args):
+    """Every workload prints ONE JSON line with the contract's keys (GPU)."""
+    out = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks",
+                "gpu_launches"):
+        assert key in d, key
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
+    assert d["roofline"]["peak"] > 0 and 0 < d["roofline"]["frac"] < 1
