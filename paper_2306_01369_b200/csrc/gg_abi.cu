@@ -131,6 +131,11 @@ void dfree(gg_ctx* ctx, void* p) {
 }
 
 int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock); }
+#ifndef GG_SWEEP_BLOCK
+#define GG_SWEEP_BLOCK 64
+#endif
+constexpr int kSweepBlock = GG_SWEEP_BLOCK;  // k_sweep block size (<= kBlock)
+int sweep_grid(long long n) { return static_cast<int>((n + kSweepBlock - 1) / kSweepBlock); }
 int narrow_blocks(long long n) { return static_cast<int>((n + kNarrowBlock - 1) / kNarrowBlock); }
 
 int validate_params(gg_ctx* ctx, const gg_params* p) {
@@ -318,7 +323,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
       if (D.pipeline == GG_MODE_ONE_LOOP)
         k_sweep_oneloop<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
       else
-        k_sweep<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
+        k_sweep<<<sweep_grid(ctx->n), kSweepBlock, 0, s>>>(D, it);
     }
     k_finish<<<ctx->nblocks, kBlock, 0, s>>>(D);
     if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
@@ -471,7 +476,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
       if (D.pipeline == GG_MODE_ONE_LOOP)
         k_sweep_oneloop<<<nbn, kBlock, 0, s>>>(D, it);
       else
-        k_sweep<<<nbn, kBlock, 0, s>>>(D, it);
+        k_sweep<<<sweep_grid(ctx->n), kSweepBlock, 0, s>>>(D, it);
       mark(12);
     }
     Dev Df = D;
@@ -1596,7 +1601,7 @@ int gg_slab_sweep(gg_ctx* ctx, int32_t sweep) {
   if (sweep < 0 || sweep >= ctx->D.S) return fail(ctx, GG_EINVAL, "sweep index out of range");
   DeviceGuard guard(ctx->device);
   if (ctx->n_own > 0)
-    k_sweep<<<blocks_for(ctx->n_own), kBlock, 0, ctx->stream>>>(slab_dev(ctx), sweep);
+    k_sweep<<<sweep_grid(ctx->n_own), kSweepBlock, 0, ctx->stream>>>(slab_dev(ctx), sweep);
   ctx->launches += 1;
   CK(cudaGetLastError());
   return GG_OK;
