@@ -136,6 +136,11 @@ int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock)
 #endif
 constexpr int kSweepBlock = GG_SWEEP_BLOCK;  // k_sweep block size (<= kBlock)
 int sweep_grid(long long n) { return static_cast<int>((n + kSweepBlock - 1) / kSweepBlock); }
+#ifndef GG_FINISH_BLOCK
+#define GG_FINISH_BLOCK 256
+#endif
+constexpr int kFinishBlock = GG_FINISH_BLOCK;  // k_finish block size (<= kBlock)
+int finish_grid(long long n) { return static_cast<int>((n + kFinishBlock - 1) / kFinishBlock); }
 int narrow_blocks(long long n) { return static_cast<int>((n + kNarrowBlock - 1) / kNarrowBlock); }
 
 int validate_params(gg_ctx* ctx, const gg_params* p) {
@@ -325,7 +330,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
       else
         k_sweep<<<sweep_grid(ctx->n), kSweepBlock, 0, s>>>(D, it);
     }
-    k_finish<<<ctx->nblocks, kBlock, 0, s>>>(D);
+    k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
     if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
     CK(cudaGetLastError());
     return GG_OK;
@@ -481,7 +486,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     }
     Dev Df = D;
     Df.env_kernel = ctx->E > 1 ? 1 : 0;
-    k_finish<<<nbn, kBlock, 0, s>>>(Df);
+    k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(Df);
     if (Df.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(Df);
     mark(13);
   }
@@ -745,7 +750,7 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   CK(cudaMemset(D.Xh, 0, sizeof(float4) * (n + kXhPad)));
   CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks,
-                                                          kClusterCTAs}))));
+                                                          finish_grid(n), kClusterCTAs}))));
   CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3 * E));
   CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3 * E));
   CK(dalloc(ctx, &D.ctl, 1));
@@ -1651,7 +1656,7 @@ int gg_slab_finish(gg_ctx* ctx, gg_report* report, double* body_momentum) {
   if (st != GG_OK) return st;
   DeviceGuard guard(ctx->device);
   cudaStream_t s = ctx->stream;
-  k_finish<<<blocks_for(std::max<long long>(ctx->n_own, 1)), kBlock, 0, s>>>(slab_dev(ctx));
+  k_finish<<<finish_grid(std::max<long long>(ctx->n_own, 1)), kFinishBlock, 0, s>>>(slab_dev(ctx));
   ctx->launches += 1;
   CK(cudaGetLastError());
   int32_t nd = 0, es = -1;
