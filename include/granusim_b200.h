@@ -210,12 +210,82 @@ const char* gg_profile_kind_name(int32_t k);
  * order: np.argsort(hashes, kind="stable") (broadphase.py:160), user ids.   */
 int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order);
 
-/* Contacts detected by the last step (narrowphase_contacts, contact.py:244-300)
- * as user-id directed pairs.  kind 0 = particle (other = particle id),
- * kind 1 = body (other = body index).  e1/psi in float64 (computed in fp64,
- * stored fp32 on device).  *count = total; arrays must hold cap entries. */
+/* Contacts detected by the last step or gg_detect (narrowphase_contacts,
+ * contact.py:244-300) as user-id directed pairs, in the reference's
+ * ContactSet order: particle contacts by owner, an owner's in candidate order
+ * (neighbour buckets by ascending hash, a bucket's particles in stable order,
+ * broadphase.py:149-182), then body contacts body by body, each body's by
+ * owner.  kind 0 = particle (other = particle id), kind 1 = body (other = body
+ * index).  e1/psi/vj in float64 (computed in fp64, stored fp32 on device);
+ * vj = body surface velocity at the contact point (contact.py:279,286), zero
+ * for particle contacts.  Any output may be NULL.  *count = total; at most
+ * cap rows are written. */
 int gg_tap_contacts(gg_ctx* ctx, int64_t cap, int64_t* count, int32_t* owner,
-                    int32_t* other, int32_t* kind, double* psi, double* e1);
+                    int32_t* other, int32_t* kind, double* psi, double* e1, double* vj);
+
+/* position_cells (broadphase.py:33-41) of n float64 positions (n,3):
+ * round_half_away(x / 2r) per coordinate -> cells (n,3) int64.
+ * GG_EPOSITIONS if a coordinate is not finite (broadphase.py:104-107). */
+int gg_position_cells(gg_ctx* ctx, const double* x, int64_t n, double radius, int64_t* cells);
+
+/* candidate_pairs (broadphase.py:185-196) of the context's current state:
+ * every directed candidate (i, j != i), i ascending, i's candidates in the
+ * order _candidate_csr enumerates them (broadphase.py:149-182).  *count =
+ * total; ci/cj are written only if both are non-NULL and cap >= total
+ * (call once with NULL to size).  Single-scene contexts only. */
+int gg_tap_candidates(gg_ctx* ctx, int64_t cap, int64_t* count, int64_t* ci, int64_t* cj);
+
+/* narrowphase_candidates (contact.py:206-223, _assemble_candidates :303-369)
+ * on explicit candidate pairs of n float64 positions x (n,3):
+ *   pp_e1 (m,3), pp_psi (m), pp_colliding (m): e1 = d/|d|, psi = 2r - |d|
+ *     for colliding pairs (|d| < 2r, not coincident), zeros otherwise;
+ *     *n_coincident = pairs with |d|^2 < COINCIDENT_EPS^2;
+ *   per body b and particle i (arrays [n_bodies][n], normals/vj [..][3]):
+ *     b_near (_near_body's AABB test, contact.py:187-203), and for near
+ *     particles b_hit / b_psi / b_normal (penetration_depth, sdf.py:472-512)
+ *     and b_vj = velocity_at(contact point) (contact.py:327-333);
+ *     *n_degenerate over near particles.
+ * Grid bodies refer to grids uploaded to ctx (gg_upload_grid). */
+int gg_narrow_pairs(gg_ctx* ctx, const double* x, int64_t n, const int64_t* ci, const int64_t* cj,
+                    int64_t m, double radius, const gg_body* bodies, int32_t n_bodies,
+                    double* pp_e1, double* pp_psi, uint8_t* pp_colliding, int64_t* n_coincident,
+                    uint8_t* b_near, uint8_t* b_hit, double* b_psi, double* b_normal, double* b_vj,
+                    int64_t* n_degenerate);
+
+/* A contact list in the reference's array layout: ContactSet, or
+ * CandidateContacts when colliding != NULL (contact.py:103-184). */
+typedef struct gg_contact_list {
+  int64_t m;
+  const int64_t* owner;
+  const int64_t* kind;     /* 0 particle, 1 body */
+  const int64_t* other;    /* particle index or body index */
+  const double* e1;        /* (m,3) unit normal, j -> i */
+  const double* psi;       /* (m) */
+  const double* vj;        /* (m,3) body surface velocity (particle rows ignored) */
+  const uint8_t* colliding;/* CandidateContacts.colliding, or NULL */
+} gg_contact_list;
+
+/* solve_contacts_pja (contact.py:393-518) on a caller-supplied contact list
+ * and n float64 velocities v (n,3): sweeps first_sweep .. first_sweep +
+ * n_sweeps - 1 of params->solver_iterations (a caller that refreshes the
+ * candidates between sweeps, contact.py:455-461, calls it once per sweep).
+ * In/out: dv (n,3) (zeros before sweep 0), body_momentum (n_bodies,3)
+ * (accumulated), diag[2] = {max cone violation, min normal impulse}
+ * (start {0, +inf}).  *n_live = live contacts.  After the last sweep a
+ * non-finite dv returns GG_ENONFINITE with the reference's SolverError
+ * text.  The frame (e2, e3) is built as contact_frames does (contact.py:47-56);
+ * dot products, cross products and the per-owner accumulation follow numpy's
+ * operation order; body momentum is summed in 2^-36 fixed point. */
+int gg_solve_contacts(gg_ctx* ctx, const gg_contact_list* contacts, int64_t n, const double* v,
+                      const gg_params* params, int32_t n_bodies, int32_t first_sweep,
+                      int32_t n_sweeps, double* dv, double* body_momentum, double* diag,
+                      int64_t* n_live);
+
+/* project_friction_cone (contact.py:59-81) in place on k contact-frame
+ * impulses b (k,3); psi has k entries, or one if psi_scalar.  GG_EINVAL
+ * ("require mu >= 0 and dt > 0") like the reference's ValueError. */
+int gg_project_cone(gg_ctx* ctx, double* b, int64_t k, const double* psi, int32_t psi_scalar,
+                    double mu, double alpha, double dt);
 
 /* Standalone SDF query (penetration_depth, sdf.py:472-512) for n world points
  * against one posed body; out psi[n], normal[n*3], hit[n] (0/1), n_degenerate. */

@@ -6,8 +6,28 @@ The physics runs in hand-written sm_100a kernels behind the C-ABI in
 no CPU fallback; importing works without a GPU, stepping does not.
 """
 
-from .broadphase import SpatialHashmap, build_hashmap, default_table_size, spatial_hash
-from .contact import ContactSet, detect_contacts, narrowphase_contacts
+from .broadphase import (
+    SpatialHashmap,
+    build_hashmap,
+    candidate_pairs,
+    default_table_size,
+    position_cells,
+    query_candidates,
+    spatial_hash,
+)
+from .contact import (
+    CandidateContacts,
+    Contact,
+    ContactSet,
+    ImpulseBuffer,
+    contact_frames,
+    detect_contacts,
+    make_contact_frame,
+    narrowphase_candidates,
+    narrowphase_contacts,
+    project_friction_cone,
+    solve_contacts_pja,
+)
 from .errors import SceneError, SolverError, ValidationError
 from .kinematics import (
     ChainLink,
@@ -50,6 +70,17 @@ from .envs import BatchedBulldozerEnv, BulldozerEnvConfig, GoalBox, bulldozer_re
 __version__ = "0.1.0"
 
 __all__ = [
+    "CandidateContacts",
+    "Contact",
+    "ImpulseBuffer",
+    "candidate_pairs",
+    "contact_frames",
+    "make_contact_frame",
+    "narrowphase_candidates",
+    "position_cells",
+    "project_friction_cone",
+    "query_candidates",
+    "solve_contacts_pja",
     "BatchedBulldozerEnv",
     "DepthCamera",
     "render_batch",

@@ -51,6 +51,21 @@ class GGParams(C.Structure):
     ]
 
 
+class GGContactList(C.Structure):
+    """gg_contact_list: a ContactSet / CandidateContacts in array form."""
+
+    _fields_ = [
+        ("m", C.c_int64),
+        ("owner", C.c_void_p),
+        ("kind", C.c_void_p),
+        ("other", C.c_void_p),
+        ("e1", C.c_void_p),
+        ("psi", C.c_void_p),
+        ("vj", C.c_void_p),
+        ("colliding", C.c_void_p),
+    ]
+
+
 # gg_body as a numpy structured dtype so per-step body tables for a whole
 # batch are filled with array ops and handed over as one pointer.
 BODY_DTYPE = np.dtype(
@@ -133,7 +148,14 @@ def _bind(lib: C.CDLL) -> None:
         "gg_sync": (C.c_int, [P, P, P, i32, C.POINTER(i32), C.POINTER(i32)]),
         "gg_last_batch_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
         "gg_tap_hash": (C.c_int, [P, P, P, P]),
-        "gg_tap_contacts": (C.c_int, [P, i64, C.POINTER(i64), P, P, P, P, P]),
+        "gg_tap_contacts": (C.c_int, [P, i64, C.POINTER(i64), P, P, P, P, P, P]),
+        "gg_position_cells": (C.c_int, [P, P, i64, dbl, P]),
+        "gg_tap_candidates": (C.c_int, [P, i64, C.POINTER(i64), P, P]),
+        "gg_narrow_pairs": (C.c_int, [P, P, i64, P, P, i64, dbl, P, i32, P, P, P, C.POINTER(i64),
+                                      P, P, P, P, P, C.POINTER(i64)]),
+        "gg_solve_contacts": (C.c_int, [P, C.POINTER(GGContactList), i64, P, C.POINTER(GGParams),
+                                        i32, i32, i32, P, P, P, C.POINTER(i64)]),
+        "gg_project_cone": (C.c_int, [P, P, i64, P, i32, dbl, dbl, dbl]),
         "gg_penetration": (C.c_int, [P, P, P, i64, dbl, P, P, P, C.POINTER(i64)]),
         "gg_spatial_hash": (C.c_int, [P, P, i64, i64, P]),
         "gg_set_max_contacts": (C.c_int, [P, i32]),

@@ -18,7 +18,8 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libgranusim_b200.so"
 SOURCES = [CSRC / "gg_abi.cu"]
-DEPS = [CSRC / "gg_kernels.cuh", CSRC / "gg_device.cuh", CSRC / "gg_slab.cuh", CSRC / "gg_render.cuh", ROOT / "include" / "granusim_b200.h"]
+# every header the library includes (globbed: a new .cuh cannot be missed)
+DEPS = sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "granusim_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

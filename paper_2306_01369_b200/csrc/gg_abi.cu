@@ -13,6 +13,7 @@
 #include "gg_slab.cuh"
 #include "gg_render.cuh"
 #include "gg_bake.cuh"
+#include "gg_l1.cuh"
 
 using namespace gg;
 
@@ -702,6 +703,8 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   CK(dalloc(ctx, &D.V0, n));
   CK(dalloc(ctx, &D.cinfo, n));
   CK(cudaMemset(D.cinfo, 0, sizeof(int2) * n));
+  CK(dalloc(ctx, &D.bad, n));
+  CK(cudaMemset(D.bad, 0, sizeof(int) * n));
   CK(cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(sizeof(NarrowSmemN))));
   CK(cudaFuncSetAttribute(k_step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1164,6 +1167,12 @@ int gg_last_batch_ms(gg_ctx* ctx, float* ms) {
   return GG_OK;
 }
 
+}  // extern "C"
+namespace {
+std::string nonfinite_message(gg_ctx* ctx, int err_step, std::vector<int> bad);
+}
+extern "C" {
+
 int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
             int32_t* n_done, int32_t* err_step) {
   if (!ctx) return GG_EINVAL;
@@ -1187,17 +1196,17 @@ int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
     case GG_EPOSITIONS:
       return fail(ctx, GG_EPOSITIONS, "positions must be finite");
     case GG_ENONFINITE: {
-      std::vector<int> bad(c.bad_uid, c.bad_uid + std::min(c.n_bad, kMaxBad));
-      std::sort(bad.begin(), bad.end());
-      std::string s = "non-finite velocity correction for particles [";
-      for (size_t i = 0; i < bad.size() && i < 5; ++i) {
-        if (i) s += ", ";
-        s += std::to_string(bad[i]);
-      }
-      s += "] (";
-      s += std::to_string(c.n_bad);
-      s += " particles)";
-      return fail(ctx, GG_ENONFINITE, s);
+      // every particle whose correction is non-finite (D.bad: uid + 1 per
+      // physical index, written only on failure), then cleared
+      std::vector<int> flags(ctx->n);
+      CK(cudaMemcpy(flags.data(), ctx->D.bad, sizeof(int) * ctx->n, cudaMemcpyDeviceToHost));
+      CK(cudaMemset(ctx->D.bad, 0, sizeof(int) * ctx->n));
+      std::vector<int> bad;
+      for (int f : flags)
+        if (f) bad.push_back(f - 1);
+      if (bad.empty()) bad.assign(c.bad_uid, c.bad_uid + std::min(c.n_bad, kMaxBad));
+      const int es = c.err_step;
+      return fail(ctx, GG_ENONFINITE, nonfinite_message(ctx, es, bad));
     }
     case GG_ECAPACITY:
       std::snprintf(buf, sizeof(buf),
@@ -1241,43 +1250,474 @@ int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order) {
   return GG_OK;
 }
 
-int gg_tap_contacts(gg_ctx* ctx, int64_t cap_out, int64_t* count, int32_t* owner, int32_t* other,
-                    int32_t* kind, double* psi, double* e1) {
-  if (!ctx || !count) return GG_EINVAL;
+}  // extern "C"
+
+namespace {
+
+// One detected contact as the reference's ContactSet row (contact.py:244-300).
+struct TapRec {
+  int owner, other, kind;
+  long long key;  // pp: partner's position in bucket order; body: 0
+  float4 geo, vb;
+};
+
+// Contacts recorded by the last detection (step or gg_detect), in the
+// reference's ContactSet order: particle contacts by owner, within an owner
+// in candidate order — buckets by ascending hash, a bucket's particles in
+// stable order, i.e. ascending position in the bucket-ordered array Xh
+// (broadphase.py:149-182) — then body contacts body by body, each body's by
+// owner (contact.py:274-298).
+int collect_contacts(gg_ctx* ctx, std::vector<TapRec>& out) {
   DeviceGuard guard(ctx->device);
   CK(cudaStreamSynchronize(ctx->stream));
   const long long n = ctx->n;
   const long long cap = ctx->D.cap_tot;
   std::vector<int2> ci(n);
   std::vector<int> uid(n), oth(cap);
-  std::vector<float4> geo(cap);
+  std::vector<float4> geo(cap), vb(cap), xh(n);
   int ucur = 0;
   CK(cudaMemcpy(&ucur, &ctx->D.ctl->ucur, sizeof(int), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(ci.data(), ctx->D.cinfo, sizeof(int2) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(uid.data(), ctx->D.UID[ucur], sizeof(int) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(oth.data(), ctx->D.coth, sizeof(int) * cap, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(geo.data(), ctx->D.cgeo, sizeof(float4) * cap, cudaMemcpyDeviceToHost));
-  long long m = 0;
+  CK(cudaMemcpy(vb.data(), ctx->D.cvb, sizeof(float4) * cap, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(xh.data(), ctx->D.Xh, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+  std::vector<long long> pos(n, 0);  // physical index -> position in bucket order
+  for (long long m = 0; m < n; ++m) {
+    int q;
+    std::memcpy(&q, &xh[m].w, sizeof(int));
+    if (q >= 0 && q < n) pos[q] = m;
+  }
+  out.clear();
   for (long long k = 0; k < n; ++k) {
     for (int s = 0; s < ci[k].y; ++s) {
       const size_t idx = s < kFixedSlots ? static_cast<size_t>(s) * n + k
                                          : static_cast<size_t>(ci[k].x) + s - kFixedSlots;
       const int j = oth[idx];
       if (j == kNullContact) continue;  // a prefilter pass that is no contact
-      if (m++ >= cap_out) continue;
-      const long long o = m - 1;
-      if (owner) owner[o] = uid[k];
-      if (other) other[o] = j >= 0 ? uid[j] : -(j + 1);
-      if (kind) kind[o] = j >= 0 ? 0 : 1;
-      if (psi) psi[o] = geo[idx].w;
-      if (e1) {
-        e1[3 * o] = geo[idx].x;
-        e1[3 * o + 1] = geo[idx].y;
-        e1[3 * o + 2] = geo[idx].z;
-      }
+      TapRec r;
+      r.owner = uid[k];
+      r.kind = j >= 0 ? 0 : 1;
+      r.other = j >= 0 ? uid[j] : -(j + 1);
+      r.key = j >= 0 ? pos[j] : 0;
+      r.geo = geo[idx];
+      r.vb = j >= 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : vb[idx];
+      out.push_back(r);
+    }
+  }
+  std::sort(out.begin(), out.end(), [](const TapRec& a, const TapRec& b) {
+    if (a.kind != b.kind) return a.kind < b.kind;
+    if (a.kind == 0) return a.owner != b.owner ? a.owner < b.owner : a.key < b.key;
+    return a.other != b.other ? a.other < b.other : a.owner < b.owner;
+  });
+  return GG_OK;
+}
+
+// The reference's SolverError text (contact.py:503-509): the first five
+// particles whose correction is non-finite and the first five indices of
+// their contacts in ContactSet order.  The contacts are those of the failing
+// step's input state (the state is not committed on failure), detected again
+// with that step's body rows.
+std::string nonfinite_message(gg_ctx* ctx, int err_step, std::vector<int> bad) {
+  std::sort(bad.begin(), bad.end());
+  bad.erase(std::unique(bad.begin(), bad.end()), bad.end());
+  std::string s = "non-finite velocity correction for particles [";
+  for (size_t i = 0; i < bad.size() && i < 5; ++i) {
+    if (i) s += ", ";
+    s += std::to_string(bad[i]);
+  }
+  s += "] (contacts [";
+  std::vector<TapRec> recs;
+  bool ok = ctx->E == 1 && err_step >= 0;
+  if (ok) {
+    refresh_dev(ctx);
+    Dev D = pass_dev(ctx, 0, 0);
+    D.bodies = ctx->d_bodies + static_cast<long long>(err_step) * ctx->E * D.nb;
+    cudaStream_t st = ctx->stream;
+    ok = begin_batch(ctx, st) == GG_OK && enqueue_sort_pass(ctx, D, st) == GG_OK;
+    if (ok) {
+      k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), st>>>(D);
+      ctx->launches += 9;
+      ok = cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess &&
+           collect_contacts(ctx, recs) == GG_OK;
+    }
+  }
+  int shown = 0;
+  for (size_t c = 0; ok && c < recs.size() && shown < 5; ++c)
+    if (std::binary_search(bad.begin(), bad.end(), recs[c].owner)) {
+      if (shown++) s += ", ";
+      s += std::to_string(c);
+    }
+  s += "])";
+  return s;
+}
+
+// RAII device scratch for the context-level entry points below
+struct DevScratch {
+  std::vector<void*> ptrs;
+  template <typename T>
+  cudaError_t get(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) {
+      ptrs.push_back(q);
+      *p = static_cast<T*>(q);
+    }
+    return e;
+  }
+  ~DevScratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int gg_tap_contacts(gg_ctx* ctx, int64_t cap_out, int64_t* count, int32_t* owner, int32_t* other,
+                    int32_t* kind, double* psi, double* e1, double* vj) {
+  if (!ctx || !count) return GG_EINVAL;
+  std::vector<TapRec> recs;
+  int st = collect_contacts(ctx, recs);
+  if (st != GG_OK) return st;
+  const long long m = static_cast<long long>(recs.size());
+  for (long long o = 0; o < m && o < cap_out; ++o) {
+    const TapRec& r = recs[o];
+    if (owner) owner[o] = r.owner;
+    if (other) other[o] = r.other;
+    if (kind) kind[o] = r.kind;
+    if (psi) psi[o] = r.geo.w;
+    if (e1) {
+      e1[3 * o] = r.geo.x;
+      e1[3 * o + 1] = r.geo.y;
+      e1[3 * o + 2] = r.geo.z;
+    }
+    if (vj) {
+      vj[3 * o] = r.vb.x;
+      vj[3 * o + 1] = r.vb.y;
+      vj[3 * o + 2] = r.vb.z;
     }
   }
   *count = m;
+  return GG_OK;
+}
+
+int gg_position_cells(gg_ctx* ctx, const double* x, int64_t n, double radius, int64_t* cells) {
+  if (!ctx) return GG_EINVAL;
+  if (n < 0 || (n > 0 && (!x || !cells))) return fail(ctx, GG_EINVAL, "position_cells: bad arguments");
+  if (n == 0) return GG_OK;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamSynchronize(s));
+  DevScratch tmp;
+  double* d_x = nullptr;
+  long long* d_c = nullptr;
+  int* d_bad = nullptr;
+  CK(tmp.get(&d_x, 3 * n));
+  CK(tmp.get(&d_c, 3 * n));
+  CK(tmp.get(&d_bad, 1));
+  CK(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+  CK(cudaMemcpyAsync(d_x, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  k_cells_f64<<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(d_x, n, 2.0 * radius,
+                                                                                 d_c, d_bad);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(cells, d_c, sizeof(long long) * 3 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) return fail(ctx, GG_EPOSITIONS, "positions must be finite");
+  return GG_OK;
+}
+
+int gg_tap_candidates(gg_ctx* ctx, int64_t cap_out, int64_t* count, int64_t* ci, int64_t* cj) {
+  if (!ctx || !count) return GG_EINVAL;
+  if (ctx->E != 1) return fail(ctx, GG_EINVAL, "gg_tap_candidates: single-scene contexts only");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const long long n = ctx->n;
+  refresh_dev(ctx);
+  const Dev D = pass_dev(ctx, 0, 0);
+  cudaStream_t s = ctx->stream;
+  int st = begin_batch(ctx, s);
+  if (st != GG_OK) return st;
+  st = enqueue_sort_pass(ctx, D, s);
+  if (st != GG_OK) return st;
+  DevScratch tmp;
+  long long *d_cnt = nullptr, *d_off = nullptr;
+  CK(tmp.get(&d_cnt, n));
+  CK(tmp.get(&d_off, n));
+  k_cand_count<<<ctx->nblocks, kBlock, 0, s>>>(D, d_cnt);
+  ctx->launches += 8;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpy(ctx->h_ctl, D.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  if (ctx->h_ctl->err == GG_EPOSITIONS) return fail(ctx, GG_EPOSITIONS, "positions must be finite");
+  std::vector<long long> cnt(n), off(n);
+  CK(cudaMemcpy(cnt.data(), d_cnt, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  long long total = 0;
+  for (long long i = 0; i < n; ++i) {
+    off[i] = total;
+    total += cnt[i];
+  }
+  *count = total;
+  if (!ci || !cj || cap_out < total || total == 0) return GG_OK;
+  long long *d_ci = nullptr, *d_cj = nullptr;
+  CK(tmp.get(&d_ci, total));
+  CK(tmp.get(&d_cj, total));
+  CK(cudaMemcpyAsync(d_off, off.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, s));
+  k_cand_fill<<<ctx->nblocks, kBlock, 0, s>>>(D, d_off, d_ci, d_cj);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ci, d_ci, sizeof(long long) * total, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(cj, d_cj, sizeof(long long) * total, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return GG_OK;
+}
+
+int gg_narrow_pairs(gg_ctx* ctx, const double* x, int64_t n, const int64_t* ci, const int64_t* cj,
+                    int64_t m, double radius, const gg_body* bodies, int32_t n_bodies,
+                    double* pp_e1, double* pp_psi, uint8_t* pp_colliding, int64_t* n_coincident,
+                    uint8_t* b_near, uint8_t* b_hit, double* b_psi, double* b_normal, double* b_vj,
+                    int64_t* n_degenerate) {
+  if (!ctx) return GG_EINVAL;
+  if (n < 0 || m < 0 || (n > 0 && !x) || (m > 0 && (!ci || !cj || !pp_e1 || !pp_psi || !pp_colliding)))
+    return fail(ctx, GG_EINVAL, "narrowphase_candidates: bad arguments");
+  if (n_bodies < 0 || (n_bodies > 0 && (!bodies || !b_near || !b_hit || !b_psi || !b_normal || !b_vj)))
+    return fail(ctx, GG_EINVAL, "narrowphase_candidates: bad body arguments");
+  if (!(radius > 0.0)) return fail(ctx, GG_EINVAL, "particle radius must be positive");
+  for (long long t = 0; t < m; ++t)
+    if (ci[t] < 0 || ci[t] >= n || cj[t] < 0 || cj[t] >= n)
+      return fail(ctx, GG_EINVAL, "candidate index out of range");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamSynchronize(s));
+  DevScratch tmp;
+  double *d_x = nullptr, *d_e1 = nullptr, *d_psi = nullptr, *d_bpsi = nullptr, *d_bn = nullptr,
+         *d_bvj = nullptr;
+  long long *d_ci = nullptr, *d_cj = nullptr;
+  unsigned char *d_col = nullptr, *d_near = nullptr, *d_hit = nullptr;
+  unsigned long long* d_cnt = nullptr;
+  gg_body* d_bodies = nullptr;
+  CK(tmp.get(&d_x, 3 * n));
+  CK(tmp.get(&d_cnt, 2));
+  CK(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned long long), s));
+  if (n > 0) CK(cudaMemcpyAsync(d_x, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  if (m > 0) {
+    CK(tmp.get(&d_ci, m));
+    CK(tmp.get(&d_cj, m));
+    CK(tmp.get(&d_e1, 3 * m));
+    CK(tmp.get(&d_psi, m));
+    CK(tmp.get(&d_col, m));
+    CK(cudaMemcpyAsync(d_ci, ci, sizeof(long long) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_cj, cj, sizeof(long long) * m, cudaMemcpyHostToDevice, s));
+    const double two_r = 2.0 * radius;
+    k_pairs_pp<<<static_cast<unsigned>((m + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+        d_x, d_ci, d_cj, m, two_r, two_r * two_r, 1e-12 * 1e-12, d_e1, d_psi, d_col, d_cnt);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(pp_e1, d_e1, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(pp_psi, d_psi, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(pp_colliding, d_col, m, cudaMemcpyDeviceToHost, s));
+  }
+  if (n_bodies > 0 && n > 0) {
+    refresh_dev(ctx);
+    const long long nb = n_bodies;
+    CK(tmp.get(&d_bodies, nb));
+    CK(tmp.get(&d_near, nb * n));
+    CK(tmp.get(&d_hit, nb * n));
+    CK(tmp.get(&d_bpsi, nb * n));
+    CK(tmp.get(&d_bn, 3 * nb * n));
+    CK(tmp.get(&d_bvj, 3 * nb * n));
+    CK(cudaMemcpyAsync(d_bodies, bodies, sizeof(gg_body) * nb, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(d_hit, 0, nb * n, s));
+    CK(cudaMemsetAsync(d_bpsi, 0, sizeof(double) * nb * n, s));
+    CK(cudaMemsetAsync(d_bn, 0, sizeof(double) * 3 * nb * n, s));
+    CK(cudaMemsetAsync(d_bvj, 0, sizeof(double) * 3 * nb * n, s));
+    k_pairs_body<<<dim3(static_cast<unsigned>((n + kBlock - 1) / kBlock), static_cast<unsigned>(nb)),
+                   kBlock, 0, s>>>(d_bodies, ctx->d_grids, ctx->d_gvals, d_x, n, radius, d_near,
+                                   d_hit, d_bpsi, d_bn, d_bvj, d_cnt + 1);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(b_near, d_near, nb * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_hit, d_hit, nb * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_psi, d_bpsi, sizeof(double) * nb * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_normal, d_bn, sizeof(double) * 3 * nb * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b_vj, d_bvj, sizeof(double) * 3 * nb * n, cudaMemcpyDeviceToHost, s));
+  }
+  unsigned long long cnt[2] = {0, 0};
+  CK(cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (n_coincident) *n_coincident = static_cast<int64_t>(cnt[0]);
+  if (n_degenerate) *n_degenerate = static_cast<int64_t>(cnt[1]);
+  return GG_OK;
+}
+
+int gg_solve_contacts(gg_ctx* ctx, const gg_contact_list* c, int64_t n, const double* v,
+                      const gg_params* p, int32_t n_bodies, int32_t first_sweep, int32_t n_sweeps,
+                      double* dv, double* body_momentum, double* diag, int64_t* n_live) {
+  if (!ctx) return GG_EINVAL;
+  if (!c || !p || n < 0 || c->m < 0 || (n > 0 && (!v || !dv)) || n_bodies < 0 || first_sweep < 0 ||
+      n_sweeps < 0 || (n_bodies > 0 && !body_momentum) || !diag)
+    return fail(ctx, GG_EINVAL, "solve_contacts_pja: bad arguments");
+  const long long m = c->m;
+  if (m > 0 && (!c->owner || !c->kind || !c->other || !c->e1 || !c->psi || !c->vj))
+    return fail(ctx, GG_EINVAL, "solve_contacts_pja: contact arrays missing");
+  if (n >= (1ll << 31) || m >= (1ll << 31))
+    return fail(ctx, GG_EINVAL, "solve_contacts_pja: at most 2^31 - 1 particles and contacts");
+  // CSR of the contacts by owner, contact order kept (a stable counting sort)
+  std::vector<int> rowptr(n + 1, 0), cidx(m);
+  long long live = 0;
+  for (long long k = 0; k < m; ++k) {
+    const long long o = c->owner[k];
+    if (o < 0 || o >= n) return fail(ctx, GG_EINVAL, "contact owner out of range");
+    if (c->kind[k] == 0 && (c->other[k] < 0 || c->other[k] >= n))
+      return fail(ctx, GG_EINVAL, "contact partner out of range");
+    rowptr[o + 1] += 1;
+    live += (!c->colliding || c->colliding[k]) ? 1 : 0;
+  }
+  if (n_live) *n_live = live;
+  for (long long i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
+  {
+    std::vector<int> fillp(rowptr.begin(), rowptr.end() - 1);
+    for (long long k = 0; k < m; ++k) cidx[fillp[c->owner[k]]++] = static_cast<int>(k);
+  }
+  if (n == 0 || m == 0 || n_sweeps == 0) return GG_OK;  // dv stays as given (zeros)
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamSynchronize(s));
+  DevScratch tmp;
+  int *d_row = nullptr, *d_cidx = nullptr;
+  long long *d_kind = nullptr, *d_other = nullptr;
+  unsigned char* d_mask = nullptr;
+  double *d_e1 = nullptr, *d_e2 = nullptr, *d_e3 = nullptr, *d_psi = nullptr, *d_vj = nullptr,
+         *d_v = nullptr, *d_dv[2] = {nullptr, nullptr};
+  unsigned long long *d_bm = nullptr, *d_diag = nullptr;
+  CK(tmp.get(&d_row, n + 1));
+  CK(tmp.get(&d_cidx, m));
+  CK(tmp.get(&d_kind, m));
+  CK(tmp.get(&d_other, m));
+  CK(tmp.get(&d_e1, 3 * m));
+  CK(tmp.get(&d_e2, 3 * m));
+  CK(tmp.get(&d_e3, 3 * m));
+  CK(tmp.get(&d_psi, m));
+  CK(tmp.get(&d_vj, 3 * m));
+  CK(tmp.get(&d_v, 3 * n));
+  CK(tmp.get(&d_dv[0], 3 * n));
+  CK(tmp.get(&d_dv[1], 3 * n));
+  CK(tmp.get(&d_bm, 3 * std::max(n_bodies, 1)));
+  CK(tmp.get(&d_diag, 2));
+  if (c->colliding) {
+    CK(tmp.get(&d_mask, m));
+    CK(cudaMemcpyAsync(d_mask, c->colliding, m, cudaMemcpyHostToDevice, s));
+  }
+  // vj0: body surface velocity, or velocities[other] for particle contacts
+  // (contact.py:440-443) — gathered on the host while the copies run
+  std::vector<double> vj0(c->vj, c->vj + 3 * m);
+  for (long long k = 0; k < m; ++k)
+    if (c->kind[k] == 0)
+      for (int a = 0; a < 3; ++a) vj0[3 * k + a] = v[3 * c->other[k] + a];
+  CK(cudaMemcpyAsync(d_row, rowptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_cidx, cidx.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_kind, c->kind, sizeof(long long) * m, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_other, c->other, sizeof(long long) * m, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_e1, c->e1, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_psi, c->psi, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_vj, vj0.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_v, v, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_dv[0], dv, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(d_bm, 0, sizeof(unsigned long long) * 3 * std::max(n_bodies, 1), s));
+  unsigned long long dg[2];
+  std::memcpy(&dg[0], &diag[0], sizeof(double));
+  std::memcpy(&dg[1], &diag[1], sizeof(double));
+  if (!(diag[0] > 0.0)) dg[0] = 0ull;
+  if (!(diag[1] >= 0.0)) dg[1] = 0x7ff0000000000000ull;
+  CK(cudaMemcpyAsync(d_diag, dg, sizeof(dg), cudaMemcpyHostToDevice, s));
+  const unsigned mb = static_cast<unsigned>((m + kBlock - 1) / kBlock);
+  k_l1_frames<<<mb, kBlock, 0, s>>>(m, d_e1, d_mask, d_e2, d_e3);
+  L1Solve L{};
+  L.n = static_cast<int>(n);
+  L.m = m;
+  L.rowptr = d_row;
+  L.cidx = d_cidx;
+  L.kind = d_kind;
+  L.other = d_other;
+  L.mask = d_mask;
+  L.e1 = d_e1;
+  L.e2 = d_e2;
+  L.e3 = d_e3;
+  L.psi = d_psi;
+  L.vj0 = d_vj;
+  L.v = d_v;
+  L.gamma = p->gamma;
+  L.mu = p->friction;
+  L.alpha = p->baumgarte_alpha;
+  L.dt = p->timestep;
+  L.mass = p->particle_mass;
+  L.gdt0 = p->gdt[0];
+  L.gdt1 = p->gdt[1];
+  L.gdt2 = p->gdt[2];
+  L.nb = n_bodies;
+  L.bm_fix = d_bm;
+  L.diag = d_diag;
+  const unsigned nbk = static_cast<unsigned>((n + kBlock - 1) / kBlock);
+  for (int it = 0; it < n_sweeps; ++it)
+    k_l1_sweep<<<nbk, kBlock, 0, s>>>(L, d_dv[it & 1], d_dv[(it + 1) & 1]);
+  ctx->launches += 1 + n_sweeps;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(dv, d_dv[n_sweeps & 1], sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> bm(3 * std::max(n_bodies, 1));
+  CK(cudaMemcpyAsync(bm.data(), d_bm, sizeof(unsigned long long) * bm.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(dg, d_diag, sizeof(dg), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < 3 * n_bodies; ++i)
+    body_momentum[i] += static_cast<double>(static_cast<long long>(bm[i])) / kMomScale;
+  std::memcpy(&diag[0], &dg[0], sizeof(double));
+  std::memcpy(&diag[1], &dg[1], sizeof(double));
+  // SolverError after the last sweep (contact.py:503-509)
+  if (first_sweep + n_sweeps >= p->solver_iterations) {
+    std::vector<int> bad;
+    for (long long i = 0; i < n; ++i)
+      if (!std::isfinite(dv[3 * i]) || !std::isfinite(dv[3 * i + 1]) || !std::isfinite(dv[3 * i + 2]))
+        bad.push_back(static_cast<int>(i));
+    if (!bad.empty()) {
+      std::string msg = "non-finite velocity correction for particles [";
+      for (size_t i = 0; i < bad.size() && i < 5; ++i) msg += (i ? ", " : "") + std::to_string(bad[i]);
+      msg += "] (contacts [";
+      int shown = 0;
+      for (long long k = 0; k < m && shown < 5; ++k)
+        if (std::binary_search(bad.begin(), bad.end(), static_cast<int>(c->owner[k])))
+          msg += (shown++ ? ", " : "") + std::to_string(k);
+      msg += "])";
+      return fail(ctx, GG_ENONFINITE, msg);
+    }
+  }
+  return GG_OK;
+}
+
+int gg_project_cone(gg_ctx* ctx, double* b, int64_t k, const double* psi, int32_t psi_scalar,
+                    double mu, double alpha, double dt) {
+  if (!ctx) return GG_EINVAL;
+  if (mu < 0 || !(dt > 0)) return fail(ctx, GG_EINVAL, "require mu >= 0 and dt > 0");
+  if (k < 0 || (k > 0 && (!b || !psi))) return fail(ctx, GG_EINVAL, "project_friction_cone: bad arguments");
+  if (k == 0) return GG_OK;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamSynchronize(s));
+  DevScratch tmp;
+  double *d_b = nullptr, *d_psi = nullptr;
+  const long long np_ = psi_scalar ? 1 : k;
+  CK(tmp.get(&d_b, 3 * k));
+  CK(tmp.get(&d_psi, np_));
+  CK(cudaMemcpyAsync(d_b, b, sizeof(double) * 3 * k, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_psi, psi, sizeof(double) * np_, cudaMemcpyHostToDevice, s));
+  k_cone<<<static_cast<unsigned>((k + kBlock - 1) / kBlock), kBlock, 0, s>>>(d_b, d_psi, k, psi_scalar,
+                                                                             mu, alpha, dt);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(b, d_b, sizeof(double) * 3 * k, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return GG_OK;
 }
 
@@ -1844,6 +2284,7 @@ int gg_slab_halo_p2p(gg_ctx* ctx, int32_t sweep, uint64_t seq) {
                                  static_cast<int>(ctx->ghost_out[0]), static_cast<int>(ctx->ghost_out[1]));
   k_halo_pull<<<2, 1024, 0, s>>>(D, sweep, static_cast<unsigned long long>(seq), ctx->mbox, cap,
                                  static_cast<int>(ctx->ghost_in[0]), static_cast<int>(ctx->ghost_in[1]),
+                                 ctx->slab.has_lo ? 1 : 0, ctx->slab.has_hi ? 1 : 0,
                                  20000000000ull /* 20 s */);
   ctx->launches += 2;
   CK(cudaGetLastError());

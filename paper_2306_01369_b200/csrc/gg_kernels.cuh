@@ -129,6 +129,7 @@ struct Dev {
   int* coth;        // partner: physical index, or -(body + 1)
   float4* cvb;      // body surface velocity (body records)
   int2* cinfo;      // per particle {CSR offset of its record 1, record count}
+  int* bad;         // [n] uid + 1 of a particle whose correction was non-finite (0: fine)
   long long cap_tot;  // record capacity
   // Records 0 .. kFixedSlots-1 of particle k live at fixed indices i * n + k
   // (slot-major columns, coalesced); records kFixedSlots.. are warp-contiguous
@@ -660,7 +661,7 @@ template <int B>
 struct NarrowSmemT {
   static constexpr int kW = B / 32;
   uint32_t beg[28][B];        // compacted non-empty buckets + a sentinel
-  uint16_t len[28][B];        // bucket sizes are < 2^16
+  uint32_t len[28][B];        // bucket sizes (any n: a bucket may hold every particle)
   uint32_t pass[kPassCap][B]; // Xh index of every prefilter pass, per owner, in order
   float4 pos[B];              // owner positions
   uint32_t off[kW][32];       // per-warp exclusive offsets of the owners' queue segments
@@ -917,7 +918,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         const bool keep = eb[j] > sb[j] && !((dupmask >> (g * 9 + j)) & 1u);
         if (keep) {
           sm.beg[nb][tid] = sb[j];
-          sm.len[nb][tid] = static_cast<uint16_t>(eb[j] - sb[j]);
+          sm.len[nb][tid] = eb[j] - sb[j];
           total += eb[j] - sb[j];
           ++nb;
         }
@@ -928,7 +929,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     // candidates past the end without a guard (indices < n + kXhPad: Xh is
     // padded; never tested)
     sm.beg[nb][tid] = sm.beg[0][tid];
-    sm.len[nb][tid] = 0xffffu;
+    sm.len[nb][tid] = 0xffffffffu;
     const bool all = D.pipeline == 1;
     const float rej = D.reject_d2f;
     CandCursor cur;
@@ -1581,6 +1582,7 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
     if (!isfinite(dvx) || !isfinite(dvy) || !isfinite(dvz)) {
       const int slot = atomicAdd(&ctl->n_bad, 1);
       if (slot < kMaxBad) ctl->bad_uid[slot] = L.uid[k];
+      if (D.bad) D.bad[k] = L.uid[k] + 1;
       raise_err(ctl, GG_ENONFINITE);
     }
     // v += dt*g + dv ; x += dt*v

@@ -218,12 +218,18 @@ __global__ void k_halo_push(Dev D, int s, unsigned long long seq, Mailbox* peer_
   }
 }
 
-// block 0 <- the lo neighbour (my side 0), block 1 <- the hi neighbour (my side 1)
+// block 0 <- the lo neighbour (my side 0), block 1 <- the hi neighbour (my side 1).
+// The flag of an existing neighbour is awaited even when it sends no ghosts
+// this step: the neighbour raises it after every sweep regardless, and the
+// wait is what keeps it from running more than one sweep ahead of us (and
+// overwriting the parity buffer we have not pulled yet) when halos are
+// asymmetric.
 __global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine, long long cap,
-                            int n_lo, int n_hi, unsigned long long timeout_ns) {
+                            int n_lo, int n_hi, int has_lo, int has_hi,
+                            unsigned long long timeout_ns) {
   const int side = blockIdx.x;
   const int m = side == 0 ? n_lo : n_hi;
-  if (m == 0) return;  // block-uniform: this side sends nothing this step
+  if (!(side == 0 ? has_lo : has_hi)) return;  // block-uniform: no neighbour on this side
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     unsigned long long t0, t, v;
@@ -244,7 +250,7 @@ __global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine,
     if (!ok) raise_err(D.ctl, GG_ECUDA);
   }
   __syncthreads();
-  if (!s_ok) return;
+  if (!s_ok || m == 0) return;
   const float4* src = mailbox_data(mine, cap, s & 1, side);
   const int at = D.n_own + (side == 0 ? 0 : n_lo);
   float4* W = D.W[s & 1];

@@ -114,6 +114,28 @@ class ParticleSet:
         if not np.all(np.isfinite(self._v)):
             raise ValidationError("velocities must be finite")
 
+    # copies and pickles carry the CURRENT state: download first, and the copy
+    # owns only host arrays (its next step uploads them to its own context)
+    def __deepcopy__(self, memo):
+        self._refresh()
+        new = ParticleSet.__new__(ParticleSet)
+        memo[id(self)] = new
+        new._x = self._x.copy()
+        new._v = self._v.copy()
+        new._engine = None
+        new._host_dirty = True
+        return new
+
+    def __getstate__(self):
+        self._refresh()
+        return {"_x": self._x.copy(), "_v": self._v.copy()}
+
+    def __setstate__(self, state):
+        self._x = state["_x"]
+        self._v = state["_v"]
+        self._engine = None
+        self._host_dirty = True
+
     @staticmethod
     def empty() -> "ParticleSet":
         return ParticleSet(np.zeros((0, 3)), np.zeros((0, 3)))

@@ -11,9 +11,14 @@ step a rank
      only), exchanging the ghosts' predicted velocity after every Jacobi sweep,
   4. reduces the StepReport over ranks.
 Ghosts carry their global id, which the device uses as the stable-sort tie
-key, so every owned particle sees the same candidates in the same order as
-on one GPU: states are bitwise identical to the one-GPU run
-(tests/test_slab.py).  The library only packs and unpacks device buffers
+key, so every owned particle sees the same contacts in the same order as on
+one GPU: states and every StepReport field except ``n_candidates`` are
+bitwise identical to the one-GPU run (tests/test_slab.py).
+``n_candidates`` (and so ``candidate_hit_rate``) is NOT the one-GPU value
+when the hash aliases: a rank hashes only its owned and ghost particles, so
+far-away particles of other slabs that share a bucket with a neighbour cell
+are missing from its candidate counts.  Aliases are never contacts (a
+contact is within 2r, i.e. within +-1 cell), so nothing else changes.  The library only packs and unpacks device buffers
 (gg_slab_* in include/granusim_b200.h); this module moves them with
 torch.distributed point-to-point operations — NCCL on device buffers over
 NVLink in production, or gloo staged through host memory (tests, and several

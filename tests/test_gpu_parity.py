@@ -255,8 +255,27 @@ def test_error_labels_step_index():
     sc = gg.Scene(particles=gg.ParticleSet(np.array([[0, 0, 0], [0.07, 0, 0]], float),
                                            np.zeros((2, 3))), bodies=[], params=gg.MaterialParams())
     sc.particles.velocities[0, 0] = np.inf
-    with pytest.raises(gg.SolverError, match="step 7"):
+    # the reference's exact text (stepper.py:99-100 + contact.py:503-509,
+    # generated by running the reference on this scene)
+    with pytest.raises(gg.SolverError, match=r"^step 7: non-finite velocity correction for particles "
+                                             r"\[0, 1\] \(contacts \[0, 1\]\)$"):
         gg.step(sc, step_index=7)
+
+
+def test_solver_error_lists_contacts_in_reference_order():
+    """Bad particles 0..2 own pp contacts 0..3; the floor contacts follow
+    (indices 4..7): the message names the first five of them, as the
+    reference does ("step 3: ... particles [0, 1, 2] (contacts [0, 1, 2, 3, 4])")."""
+    pos = np.array([[0, 0, 0.04], [0.09, 0, 0.04], [0.18, 0, 0.04], [1.0, 0, 0.04]], float)
+    sc = gg.Scene(particles=gg.ParticleSet(pos, np.zeros((4, 3))),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="f")], params=gg.MaterialParams())
+    sc.particles.velocities[1, 2] = np.nan
+    with pytest.raises(gg.SolverError, match=r"^step 3: non-finite velocity correction for particles "
+                                             r"\[0, 1, 2\] \(contacts \[0, 1, 2, 3, 4\]\)$"):
+        gg.step(sc, step_index=3)
+    # the failing step is not committed: the state is the step's input
+    assert np.isnan(sc.particles.velocities[1, 2])
+    assert np.array_equal(sc.particles.positions, pos)
 
 
 def test_nonfinite_positions_raise_value_error():
@@ -386,3 +405,39 @@ def test_crowded_owners_overflow_path(mode):
     assert rep.n_coincident_skipped == orep["n_coincident_skipped"]
     assert rel_err(sc.particles.positions, x1) <= TOL
     assert rel_err(sc.particles.velocities, v1) <= TOL
+
+
+def test_deepcopy_and_pickle_after_run_carry_current_state():
+    """A copy made after device steps holds the state of the last step (the
+    reference's cli.clone_scene deep-copies scenes), and stepping the copy
+    continues from there exactly like the original."""
+    import copy
+    import pickle
+
+    pos = gg.lattice_bed(3000).astype(np.float32).astype(np.float64)
+    sc = gg.Scene(particles=gg.ParticleSet(pos, np.zeros_like(pos)),
+                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")], params=gg.MaterialParams())
+    gg.run(sc, 5)
+    clone = copy.deepcopy(sc)
+    pick = pickle.loads(pickle.dumps(sc.particles))
+    assert np.array_equal(clone.particles.positions, sc.particles.positions)
+    assert np.array_equal(pick.velocities, sc.particles.velocities)
+    assert not np.array_equal(clone.particles.positions, pos)
+    gg.run(sc, 3)
+    gg.run(clone, 3)
+    assert np.array_equal(clone.particles.positions, sc.particles.positions)
+    assert np.array_equal(clone.particles.velocities, sc.particles.velocities)
+
+
+def test_huge_bucket_tiny_table():
+    """A bucket with more than 2^16 particles (n_h = 1: every cell aliases to
+    bucket 0) gives the contacts of the default table and n(n-1) candidates
+    (bucket lengths were stored in 16 bits)."""
+    n = 66000
+    pos = gg.lattice_bed(n).astype(np.float32).astype(np.float64)
+    r = 0.05
+    cs1, rep1 = device_detect(pos, r, 1)
+    cs2, rep2 = device_detect(pos, r, gg.default_table_size(n))
+    assert int(rep1["n_candidates"]) == n * (n - 1)
+    assert np.array_equal(cs1.directed(), cs2.directed())
+    assert int(rep1["n_contacts"]) == int(rep2["n_contacts"]) > 0

@@ -141,23 +141,47 @@ def _bed(n=12000, seed=3):
 T_STEPS = 16
 
 
-def _reference_run():
-    sc = _bed()
+GAP_CUT = 4  # the explicit slab cut of the gap bed (cell index along x)
+
+
+def _gap_bed():
+    """A bed whose cell column GAP_CUT - 1 (rank 0's boundary cell) is empty
+    while column GAP_CUT (rank 1's) is full: rank 0 sends no ghosts to rank 1,
+    rank 1 sends ghosts to rank 0 — the asymmetric halo of a sparse bed."""
+    x = gg.lattice_bed(12000, seed=5).astype(np.float32).astype(np.float64)
+    x[:, 0] -= x[:, 0].min() - 0.01
+    cx = cell_x(x[:, 0], 0.05)
+    keep = cx != GAP_CUT - 1
+    x = x[keep]
+    rng = np.random.default_rng(5)
+    v = rng.normal(scale=0.2, size=x.shape).astype(np.float32).astype(np.float64)
+    params = gg.MaterialParams(timestep=5e-4)
+    return gg.Scene(particles=gg.ParticleSet(x, v), bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
+                    params=params)
+
+
+def _reference_run(make=None):
+    sc = (make or _bed)()
     reps = [gg.step(sc)[1] for _ in range(T_STEPS)]
     return sc.particles.positions.copy(), sc.particles.velocities.copy(), reps
 
 
-def _slab_worker(rank, world, port, out, halo="host"):
+def _slab_worker(rank, world, port, out, halo="host", gap=False):
     from paper_2306_01369_b200.slab import SlabBed
 
     td = _init(rank, world, port) if world > 1 else None
-    bed = SlabBed(_bed(), rank=rank, world=world, device=0, backend="gloo", resort_every=5, halo=halo)
+    scene = _gap_bed() if gap else _bed()
+    cuts = np.array([GAP_CUT]) if gap else None
+    bed = SlabBed(scene, rank=rank, world=world, device=0, backend="gloo", resort_every=5, halo=halo,
+                  cuts=cuts)
     reps = bed.run(T_STEPS)
     X, V = bed.gather()
+    out[f"ghosts{rank}"] = bed.ghosts
     if rank == 0:
         out["x"], out["v"] = X, V
         out["reps"] = [(r.n_contacts, r.n_body_contacts, r.max_penetration, r.kinetic_energy,
-                        r.max_cone_violation) for r in reps]
+                        r.max_cone_violation, r.n_coincident_skipped, r.n_degenerate_skipped,
+                        r.min_normal_impulse) for r in reps]
     out[f"moved{rank}"] = bed.migrated
     bed.close()
     if td:
@@ -179,9 +203,32 @@ def test_slab_step_bitwise_equals_one_gpu(world, halo):
         mp.spawn(_slab_worker, args=(world, _port(), out, halo), nprocs=world, join=True)
     assert np.array_equal(out["x"], x1)
     assert np.array_equal(out["v"], v1)
-    for (n_pp, n_b, mp_, ke, mv), r in zip(out["reps"], reps1):
-        assert n_pp == r.n_contacts and n_b == r.n_body_contacts
-        assert mp_ == r.max_penetration and mv == r.max_cone_violation
-        assert ke == pytest.approx(r.kinetic_energy, rel=1e-9)
+    _check_reports(out["reps"], reps1)
     if world > 1:
         assert sum(out[f"moved{r}"] for r in range(world)) > 0, "no particle migrated"
+
+
+def _check_reports(slab_reps, reps1):
+    # every counter but n_candidates is the one-GPU value (candidates differ
+    # under hash aliasing: a rank does not hash the other slabs' particles)
+    for (n_pp, n_b, mp_, ke, mv, nco, ndg, mnb), r in zip(slab_reps, reps1):
+        assert n_pp == r.n_contacts and n_b == r.n_body_contacts
+        assert nco == r.n_coincident_skipped and ndg == r.n_degenerate_skipped
+        assert mp_ == r.max_penetration and mv == r.max_cone_violation
+        assert mnb == r.min_normal_impulse
+        assert ke == pytest.approx(r.kinetic_energy, rel=1e-9)
+
+
+@pytest.mark.gpu
+def test_slab_p2p_asymmetric_halo():
+    """Peer-memory halo when one side of a cut sends no ghosts:
+    the receiver still waits on the neighbour's per-sweep flag, so neither
+    rank runs a sweep ahead of the other's parity buffer."""
+    x1, v1, reps1 = _reference_run(_gap_bed)
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.spawn(_slab_worker, args=(2, _port(), out, "p2p", True), nprocs=2, join=True)
+    assert out["ghosts0"][1] > 0 and out["ghosts1"][0] == 0, (out["ghosts0"], out["ghosts1"])
+    assert np.array_equal(out["x"], x1)
+    assert np.array_equal(out["v"], v1)
+    _check_reports(out["reps"], reps1)
