@@ -145,6 +145,66 @@ class JointTrajectoryDriver(MotionDriver):
         return w[0], v[0]
 
 
+@dataclass
+class DigDriver(MotionDriver):
+    """One digging pass of a bucket (analytic pose and twist, so a batch of
+    steps is evaluated with array operations).  Until ``t0`` the bucket
+    waits at ``start``; over ``duration`` seconds it travels ``length``
+    metres along the horizontal unit vector ``direction`` while dipping to
+    ``depth`` below its start height on a half sine and pitching from
+    ``pitch0`` to ``pitch1`` (radians, about the horizontal axis
+    ``z x direction``); afterwards it rises at ``lift_speed`` m/s.  The body
+    frame origin follows the path; twist = (pitch rate x axis, path velocity)."""
+
+    start: np.ndarray
+    direction: np.ndarray
+    length: float
+    depth: float
+    duration: float
+    pitch0: float = 0.0
+    pitch1: float = 0.0
+    t0: float = 0.0
+    lift_speed: float = 0.0
+
+    def __post_init__(self):
+        self.start = np.asarray(self.start, dtype=np.float64)
+        d = np.asarray(self.direction, dtype=np.float64)
+        d = d - np.array([0.0, 0.0, d[2]])
+        self.direction = d / np.linalg.norm(d)
+        ax = np.cross([0.0, 0.0, 1.0], self.direction)
+        self.axis = ax / np.linalg.norm(ax)
+
+    def pose_batch(self, ts):
+        ts = np.atleast_1d(np.asarray(ts, dtype=np.float64))
+        T = len(ts)
+        u = (ts - self.t0) / self.duration
+        s = np.clip(u, 0.0, 1.0)
+        inside = (u > 0.0) & (u < 1.0)
+        after = np.maximum(ts - self.t0 - self.duration, 0.0)
+        ez = np.array([0.0, 0.0, 1.0])
+        pos = (self.start[None, :] + self.direction[None, :] * (self.length * s)[:, None]
+               - ez[None, :] * (self.depth * np.sin(np.pi * s))[:, None]
+               + ez[None, :] * (self.lift_speed * after)[:, None])
+        pitch = self.pitch0 + (self.pitch1 - self.pitch0) * s
+        P = np.zeros((T, 4, 4))
+        P[:, :3, :3] = _rot_batch(self.axis, pitch)
+        P[:, :3, 3] = pos
+        P[:, 3, 3] = 1.0
+        rate = np.where(inside, 1.0 / self.duration, 0.0)
+        v = (self.direction[None, :] * (self.length * rate)[:, None]
+             - ez[None, :] * (self.depth * np.pi * np.cos(np.pi * s) * rate)[:, None]
+             + ez[None, :] * np.where(u >= 1.0, self.lift_speed, 0.0)[:, None])
+        w = self.axis[None, :] * ((self.pitch1 - self.pitch0) * rate)[:, None]
+        return P, w, v
+
+    def pose_at(self, t):
+        return self.pose_batch([t])[0][0]
+
+    def twist_at(self, t):
+        _, w, v = self.pose_batch([t])
+        return w[0], v[0]
+
+
 def excavation_chain(base_translation=(0.0, 0.0, 0.0)) -> KinematicChain:
     """ExcavationEnv._build_chain (envs.py:250-266), base moved by a translation."""
     up, side = np.array([0.0, 0.0, 1.0]), np.array([0.0, 1.0, 0.0])

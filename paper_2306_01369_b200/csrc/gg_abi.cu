@@ -69,6 +69,8 @@ struct gg_ctx {
   int solve_mode = 0;      // 0 auto, 1 coop solve, 2 plain persistent solve, 3 per-sweep, 4 fused step
   int pipeline = 0;        // PipelineMode of the captured graphs (GG_MODE_*)
   int fused_grid = 0;      // co-resident blocks of k_step_fused
+  int staged_grid = 0;     // co-resident blocks of k_solve_staged (one per SM)
+  size_t staged_smem = 0;  // its dynamic shared memory per block
   bool cluster_ok = false; // a 16-CTA cluster of k_solve_cluster can be resident
   long long since_resort = 1 << 30;  // force a re-sort after upload
 
@@ -274,9 +276,18 @@ bool use_cluster_solve(const gg_ctx* ctx) {
   return ctx->solve_mode == 6;
 }
 
+// k_solve_staged: the auto choice whenever the step is not fused; usable
+// while a block's per-particle count bytes fit its shared memory
+bool use_staged_solve(const gg_ctx* ctx) {
+  if (ctx->pipeline == GG_MODE_ONE_LOOP || ctx->staged_grid < 1 || ctx->D.stage_cap < 0) return false;
+  if (ctx->solve_mode == 8) return true;
+  return ctx->solve_mode == 0;
+}
+
 bool use_persistent_solve(const gg_ctx* ctx) {
   if (ctx->solve_mode == 3 || ctx->pipeline == GG_MODE_ONE_LOOP) return false;
-  if (ctx->solve_mode == 0) return false;  // auto: fused for small n, per-sweep otherwise
+  if (use_staged_solve(ctx)) return true;
+  if (ctx->solve_mode == 0) return false;
   return ctx->n <= static_cast<long long>(ctx->solve_grid) * kBlock;
 }
 
@@ -337,6 +348,20 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
     return GG_OK;
   }
   const Dev& D = D0;
+  if (use_staged_solve(ctx)) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctx->staged_grid);
+    cfg.blockDim = dim3(kStageBlock);
+    cfg.dynamicSmemBytes = ctx->staged_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_solve_staged, D));
+    return GG_OK;
+  }
   return launch_coop(ctx, k_solve, ctx->solve_grid, D, s, ctx->solve_mode != 2);  // modes 1, 2
 }
 
@@ -399,6 +424,8 @@ int enqueue_step(gg_ctx* ctx, int resort) {
 
 bool use_persistent_solve(const gg_ctx* ctx);
 bool use_fused_step(const gg_ctx* ctx);
+
+bool use_staged_solve(const gg_ctx* ctx);
 
 int kernels_per_step(const gg_ctx* ctx, int resort) {
   if (use_fused_step(ctx)) return use_cluster_solve(ctx) ? 2 : 1;
@@ -727,6 +754,33 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
     // the particles thinly over every co-resident block (hero50k 0.117 vs
     // 0.130 ms/step); the kernel spreads particles evenly over its grid
     ctx->fused_grid = std::max(1, std::min(ctx->nblocks, per_sm_f * sms));
+    // k_solve_staged: one block of kStageBlock threads per SM with (nearly)
+    // all of the SM's shared memory for the staged contact records
+    {
+      int optin = 0;
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+      cudaFuncAttributes fa{};
+      CK(cudaFuncGetAttributes(&fa, k_solve_staged));
+      const long long dyn = static_cast<long long>(optin) - static_cast<long long>(fa.sharedSizeBytes) - 1024;
+      int per_sm_s = 0;
+      if (dyn > 0 &&
+          cudaFuncSetAttribute(k_solve_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(dyn)) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_solve_staged, kStageBlock,
+                                                        static_cast<size_t>(dyn)) == cudaSuccess &&
+          per_sm_s > 0) {
+        ctx->staged_grid = per_sm_s * sms;
+        ctx->staged_smem = static_cast<size_t>(dyn);
+        const long long pb = (n + ctx->staged_grid - 1) / ctx->staged_grid;
+        const long long cbytes = (pb + 15) & ~15ll;
+        D.stage_pb = static_cast<int>(pb);
+        D.stage_cap = cbytes < dyn ? static_cast<int>((dyn - cbytes) / (sizeof(float4) + sizeof(int))) : -1;
+      } else {
+        ctx->staged_grid = 0;
+        D.stage_cap = -1;
+      }
+      cudaGetLastError();
+    }
     // can one 16-CTA cluster of k_solve_cluster be resident?
     if (cudaFuncSetAttribute(k_solve_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
         cudaSuccess) {
@@ -753,7 +807,8 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   CK(cudaMemset(D.Xh, 0, sizeof(float4) * (n + kXhPad)));
   CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks,
-                                                          finish_grid(n), kClusterCTAs}))));
+                                                          finish_grid(n), kClusterCTAs,
+                                                          ctx->staged_grid}))));
   CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3 * E));
   CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3 * E));
   CK(dalloc(ctx, &D.ctl, 1));
@@ -817,7 +872,7 @@ int gg_set_max_contacts(gg_ctx* ctx, int32_t K) {
 int gg_max_contacts(const gg_ctx* ctx) { return ctx ? ctx->K : 0; }
 
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode) {
-  if (!ctx || mode < 0 || mode > 7) return fail(ctx, GG_EINVAL, "solve mode must be 0..7");
+  if (!ctx || mode < 0 || mode > 8) return fail(ctx, GG_EINVAL, "solve mode must be 0..8");
   ctx->solve_mode = mode;
   ctx->graph_dirty = true;
   return GG_OK;

@@ -136,6 +136,9 @@ struct Dev {
   // CSR entries allocated from nrec0 = kFixedSlots * n on.  A sweep fetches a
   // particle's first contacts together with its cinfo instead of after it.
   long long nrec0;
+  // k_solve_staged: particles per block and contact records staged in each
+  // block's shared memory (the rest are read from global memory)
+  int stage_pb, stage_cap;
   const gg_body* bodies;  // [batch][nb]
   const DevGrid* grids;
   const double* gvals;
@@ -1562,16 +1565,19 @@ __device__ __forceinline__ void write_report(const Dev& D, gg_report& R, const A
 // finish reduces the per-block partials in fixed order into the StepReport(s)
 // — one per env — and commits the new state.  Called by every thread of
 // every block.
-__device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int t0, int G,
-                                                     double* smd, int* s_last) {
+// This thread integrates particles kb, kb + step, ... < ke (its particles
+// of the last sweep: another thread's w is not ordered before this read).
+__device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ctl, int kb, int kend,
+                                                           int kstep, double* smd, int* s_last) {
   const int cur = ctl->cur;
   const int step = ctl->step;
   const Layout L = layout(D, ctl);
   const float4* Wf = D.W[(D.S - 1) & 1];
   double ke = 0.0;
   unsigned long long kef = 0;  // E > 1: this thread's fixed-point sum for env kenv
-  int kenv = env_of(D, t0 < D.n ? t0 : D.n - 1);
-  for (int k = t0; k < D.n_own; k += G) {
+  int kenv = env_of(D, kb < D.n ? kb : D.n - 1);
+  const int klim = kend < D.n_own ? kend : D.n_own;
+  for (int k = kb; k < klim; k += kstep) {
     const float4 xo = L.x[k];
     const float4 vo = L.v[k];
     const bool has = D.cinfo[k].y > 0;
@@ -1665,6 +1671,11 @@ __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int
     if (D.resort) ctl->ucur ^= 1;
     ctl->step = step + 1;
   }
+}
+
+__device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int t0, int G,
+                                                     double* smd, int* s_last) {
+  integrate_and_finish_range(D, ctl, t0, D.n_own, G, smd, s_last);
 }
 
 // E > 1, large n: the per-env StepReports and body momenta of the step just
@@ -1994,6 +2005,139 @@ __global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
   }
   sweep_acc_flush(D, A, smd);
   integrate_and_finish(D, ctl, t0, G, smd, &s_last);
+}
+
+// ---------------------------------------------------------------------------
+// Large-n solve (mode 8, the auto choice when the step is not fused): the S
+// sweeps, the integration and the report in ONE cooperative persistent
+// launch (grid = co-resident blocks of kStageBlock threads, one per SM).
+// Block b owns particles [b P, (b + 1) P) and thread t a contiguous run of
+// them; before sweep 0 the block copies its contact records (e1, psi,
+// partner) into shared memory, in its particles' order, so every sweep reads
+// them from there: a sweep gathers only w (own + partners, L2-resident) and
+// writes w — 32 + 16 c_pp bytes per particle instead of 48 + 20 c_pp + 32 c_b
+// from global memory, and ONE dependent global round trip per particle
+// instead of two per record.  Records beyond the block's shared-memory
+// capacity, and body surface velocities, are read from global memory.
+// Impulses are accumulated in record order with the arithmetic of
+// sweep_particle_h, so the result is bitwise that of the other schedules.
+// ---------------------------------------------------------------------------
+#ifndef GG_STAGE_BATCH
+#define GG_STAGE_BATCH 2
+#endif
+constexpr int kStageBlock = 1024;
+constexpr int kStageSat = 255;  // per-particle count saturates: read cinfo from global
+constexpr int kStageBatch = GG_STAGE_BATCH;  // partner gathers in flight per particle
+
+__device__ __forceinline__ int stage_counts_bytes(int pb) { return (pb + 15) & ~15; }
+
+__global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
+  __shared__ double smd[32];
+  __shared__ uint32_t smu[32];
+  __shared__ int s_last;
+  __shared__ unsigned long long sbm[kSmemBodies * 3];
+  Ctl* ctl = D.ctl;
+  if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
+  const int P = D.stage_pb;
+  const int CAP = D.stage_cap;
+  uint8_t* scnt = g_dsmem;
+  float4* sg = reinterpret_cast<float4*>(g_dsmem + stage_counts_bytes(P));
+  int* sj = reinterpret_cast<int*>(sg + CAP);
+  const Layout L = layout(D, ctl);
+  const int kb = static_cast<int>(blockIdx.x) * P;                       // block's first particle
+  const int ke = min(kb + P, D.n_own);                                    // block's end
+  const int q = (P + kStageBlock - 1) / kStageBlock;                      // particles per thread
+  const int k0 = min(kb + static_cast<int>(threadIdx.x) * q, ke);         // thread's run
+  const int k1 = min(k0 + q, ke);
+  // ---- stage: counts, block scan, records ----------------------------------
+  uint32_t mine = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int c = D.cinfo[k].y;
+    scnt[k - kb] = static_cast<uint8_t>(c < kStageSat ? c : kStageSat);
+    mine += static_cast<uint32_t>(c);
+  }
+  uint32_t total;
+  const uint32_t off = block_excl_scan_u32(mine, smu, &total);
+  {
+    uint32_t r = off;
+    for (int k = k0; k < k1 && r < static_cast<uint32_t>(CAP); ++k) {
+      const int2 ci = D.cinfo[k];
+      for (int i = 0; i < ci.y && r < static_cast<uint32_t>(CAP); ++i, ++r) {
+        const long long idx = ridx(D, k, ci.x, i);
+        sg[r] = D.cgeo[idx];
+        sj[r] = D.coth[idx];
+      }
+    }
+  }
+  SweepAcc A;
+  sweep_acc_init(D, A, sbm, k0, kb);  // (its __syncthreads publishes the staged records)
+  // ---- sweeps ---------------------------------------------------------------
+  for (int s = 0; s < D.S; ++s) {
+    if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
+    const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
+    float4* Wout = D.W[s & 1];
+    uint32_t r = off;
+    for (int k = k0; k < k1; ++k) {
+      int c = scnt[k - kb];
+      int2 ci = make_int2(0, 0);
+      bool have_ci = false;
+      if (c == kStageSat) {
+        ci = D.cinfo[k];
+        c = ci.y;
+        have_ci = true;
+      }
+      if (c == 0) continue;  // no contacts: w never read (see sweep_particle)
+      sweep_acc_env(D, A, k);
+      const float4 wf = Win[k];
+      const double wx = wf.x, wy = wf.y, wz = wf.z;
+      double ax = 0.0, ay = 0.0, az = 0.0;
+      for (int i0 = 0; i0 < c; i0 += kStageBatch) {
+        float4 g[kStageBatch], qv[kStageBatch];
+        int j[kStageBatch];
+#pragma unroll
+        for (int u = 0; u < kStageBatch; ++u) {
+          const int i = i0 + u;
+          j[u] = kNullContact;
+          if (i < c) {
+            const uint32_t rr = r + static_cast<uint32_t>(i);
+            if (rr < static_cast<uint32_t>(CAP)) {
+              g[u] = sg[rr];
+              j[u] = sj[rr];
+            } else {
+              if (!have_ci) {
+                ci = D.cinfo[k];
+                have_ci = true;
+              }
+              const long long idx = ridx(D, k, ci.x, i);
+              g[u] = D.cgeo[idx];
+              j[u] = D.coth[idx];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kStageBatch; ++u) {
+          if (j[u] == kNullContact) continue;
+          if (j[u] >= 0) {
+            qv[u] = Win[j[u]];
+          } else {
+            if (!have_ci) {
+              ci = D.cinfo[k];
+              have_ci = true;
+            }
+            qv[u] = D.cvb[ridx(D, k, ci.x, i0 + u)];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kStageBatch; ++u)
+          if (j[u] != kNullContact) contact_impulse(D, wx, wy, wz, g[u], j[u], qv[u], ax, ay, az, A);
+      }
+      Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
+                            static_cast<float>(wz + az), 0.f);
+      r += static_cast<uint32_t>(c);
+    }
+  }
+  sweep_acc_flush(D, A, smd);
+  integrate_and_finish_range(D, ctl, k0, k1, 1, smd, &s_last);
 }
 
 // ---------------------------------------------------------------------------

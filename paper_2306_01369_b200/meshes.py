@@ -69,6 +69,36 @@ def make_box_mesh(half_extents) -> tuple[np.ndarray, np.ndarray]:
     return v, ensure_outward(v, f)
 
 
+def make_bucket_mesh(half_extents, wall: float) -> tuple[np.ndarray, np.ndarray]:
+    """An excavator bucket: the box of ``half_extents`` with a box-shaped
+    cavity open at the top (walls and floor ``wall`` thick), as ONE closed
+    genus-0 mesh (16 vertices, 28 triangles) so the baked SDF's sign is
+    well defined everywhere (sdf.py:357-391).  Vertices: outer bottom 0-3,
+    outer top 4-7, cavity top 8-11, cavity bottom 12-15, each ring
+    counter-clockwise seen from +z."""
+    hx, hy, hz = (float(a) for a in half_extents)
+    w = float(wall)
+    if not (0.0 < w < min(hx, hy, hz)):
+        raise MeshError("bucket wall must be thinner than every half extent")
+    ix, iy = hx - w, hy - w
+    ring = np.array([[-1.0, -1.0], [1.0, -1.0], [1.0, 1.0], [-1.0, 1.0]])
+    v = np.concatenate([
+        np.column_stack([ring * [hx, hy], np.full(4, -hz)]),
+        np.column_stack([ring * [hx, hy], np.full(4, hz)]),
+        np.column_stack([ring * [ix, iy], np.full(4, hz)]),
+        np.column_stack([ring * [ix, iy], np.full(4, -hz + w)]),
+    ])
+    f = [(0, 2, 1), (0, 3, 2), (12, 13, 14), (12, 14, 15)]  # outer bottom (-z), cavity floor (+z)
+    for k in range(4):
+        n = (k + 1) % 4
+        f += [(k, n, 4 + n), (k, 4 + n, 4 + k)]                  # outer side
+        f += [(4 + k, 4 + n, 8 + n), (4 + k, 8 + n, 8 + k)]      # rim (+z)
+        f += [(12 + k, 8 + n, 12 + n), (12 + k, 8 + k, 8 + n)]  # cavity wall (faces the cavity)
+    f = np.array(f, dtype=np.int64)
+    check_watertight(v, f)
+    return v, ensure_outward(v, f)
+
+
 def make_icosphere(subdivisions: int = 2, radius: float = 1.0) -> tuple[np.ndarray, np.ndarray]:
     """Icosahedron refined ``subdivisions`` times, midpoints pushed to the sphere (meshes.py:51-93)."""
     g = (1.0 + np.sqrt(5.0)) / 2.0

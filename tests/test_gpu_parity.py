@@ -212,14 +212,15 @@ def test_physical_order_does_not_change_results():
 @pytest.mark.parametrize("name", ["grid_tool", "primitives_3000", "lattice_5000", "cyl_slope_cyclic"])
 def test_launch_modes_bitwise_identical(name):
     """Fused single-kernel step, per-phase kernels with a cooperative solve,
-    and one launch per sweep must give identical states (race detector for
-    the grid barriers: run the fused mode twice)."""
+    one launch per sweep, and the persistent solve with shared-memory staged
+    records (mode 8) must give identical states (race detector for the grid
+    barriers: run the persistent modes twice)."""
     from paper_2306_01369_b200 import _native as N
     from paper_2306_01369_b200.engine import engine_for
 
     g = load(name)
     out = {}
-    for mode in (4, 4, 1, 3):
+    for mode in (4, 4, 1, 3, 8, 8):
         sc = scene_from(g)
         eng = engine_for(sc)
         eng.max_contacts = 64
@@ -231,7 +232,7 @@ def test_launch_modes_bitwise_identical(name):
         if mode in out:
             assert np.array_equal(xv[0], out[mode][0]) and np.array_equal(xv[1], out[mode][1])
         out[mode] = xv
-    for m in (1, 3):
+    for m in (1, 3, 8):
         assert np.array_equal(out[m][0], out[4][0]) and np.array_equal(out[m][1], out[4][1]), m
 
 
