@@ -771,10 +771,11 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
           per_sm_s > 0) {
         ctx->staged_grid = per_sm_s * sms;
         ctx->staged_smem = static_cast<size_t>(dyn);
-        const long long pb = (n + ctx->staged_grid - 1) / ctx->staged_grid;
-        const long long cbytes = (pb + 15) & ~15ll;
+        // particles per block: a multiple of 32 (whole chunks per block)
+        const long long pb = ((n + ctx->staged_grid - 1) / ctx->staged_grid + 31) / 32 * 32;
+        const long long head = stage_head_bytes(pb);
         D.stage_pb = static_cast<int>(pb);
-        D.stage_cap = cbytes < dyn ? static_cast<int>((dyn - cbytes) / (sizeof(float4) + sizeof(int))) : -1;
+        D.stage_cap = head < dyn ? static_cast<int>((dyn - head) / kStageRecBytes) : -1;
       } else {
         ctx->staged_grid = 0;
         D.stage_cap = -1;

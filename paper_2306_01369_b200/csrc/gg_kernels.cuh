@@ -2011,25 +2011,38 @@ __global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
 // Large-n solve (mode 8, the auto choice when the step is not fused): the S
 // sweeps, the integration and the report in ONE cooperative persistent
 // launch (grid = co-resident blocks of kStageBlock threads, one per SM).
-// Block b owns particles [b P, (b + 1) P) and thread t a contiguous run of
-// them; before sweep 0 the block copies its contact records (e1, psi,
-// partner) into shared memory, in its particles' order, so every sweep reads
-// them from there: a sweep gathers only w (own + partners, L2-resident) and
-// writes w — 32 + 16 c_pp bytes per particle instead of 48 + 20 c_pp + 32 c_b
-// from global memory, and ONE dependent global round trip per particle
-// instead of two per record.  Records beyond the block's shared-memory
-// capacity, and body surface velocities, are read from global memory.
-// Impulses are accumulated in record order with the arithmetic of
-// sweep_particle_h, so the result is bitwise that of the other schedules.
+//
+// Block b owns particles [b P, (b + 1) P), cut into chunks of 32 consecutive
+// particles; warp w takes chunks w, w + 32, ...  Before sweep 0 the block
+// copies its contact records (e1, psi, partner) and each record's owner lane
+// into shared memory, in particle order, so every sweep reads them from
+// there and gathers only w (own + partners, L2-resident) from global memory.
+//
+// A sweep is RECORD-parallel: the chunk's records are laid end to end and
+// each lane evaluates one record's impulse (owner w by shuffle from the owner
+// lane, partner w gathered); then each owner lane adds its records' impulses
+// in record order, fetched by shuffle, and writes its w.  The per-particle
+// loop of k_sweep runs as long as the busiest particle of the warp (SIMD
+// efficiency ~13 of 32 lanes, ncu); here every lane evaluates a record.
+// The impulse arithmetic and the per-owner accumulation order are those of
+// sweep_particle_h (the owner adds its impulses to 0.0 in record order), so
+// the result is bitwise that of the other schedules.  Records beyond the
+// block's shared-memory capacity, and body surface velocities, are read
+// from global memory.
 // ---------------------------------------------------------------------------
-#ifndef GG_STAGE_BATCH
-#define GG_STAGE_BATCH 2
-#endif
 constexpr int kStageBlock = 1024;
-constexpr int kStageSat = 255;  // per-particle count saturates: read cinfo from global
-constexpr int kStageBatch = GG_STAGE_BATCH;  // partner gathers in flight per particle
+constexpr int kStageWarps = kStageBlock / 32;
+constexpr int kStageSat = 255;  // a count this large is re-read from cinfo
 
-__device__ __forceinline__ int stage_counts_bytes(int pb) { return (pb + 15) & ~15; }
+// shared-memory layout of k_solve_staged (dynamic): counts[P] (u8), chunk
+// record bases[ceil(P/32)] (u32), then per record float4 (e1, psi) and int
+// partner
+__device__ __host__ __forceinline__ long long stage_head_bytes(long long pb) {
+  const long long cnt = (pb + 15) & ~15ll;
+  const long long base = (((pb + 31) / 32) * 4 + 15) & ~15ll;
+  return cnt + base;
+}
+constexpr int kStageRecBytes = 16 + 4;
 
 __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   __shared__ double smd[32];
@@ -2039,105 +2052,159 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
   const int P = D.stage_pb;
-  const int CAP = D.stage_cap;
+  const uint32_t CAP = static_cast<uint32_t>(D.stage_cap);
+  const int nchunk = (P + 31) / 32;
   uint8_t* scnt = g_dsmem;
-  float4* sg = reinterpret_cast<float4*>(g_dsmem + stage_counts_bytes(P));
+  uint32_t* sbase = reinterpret_cast<uint32_t*>(g_dsmem + ((P + 15) & ~15));
+  float4* sg = reinterpret_cast<float4*>(g_dsmem + stage_head_bytes(P));
   int* sj = reinterpret_cast<int*>(sg + CAP);
   const Layout L = layout(D, ctl);
-  const int kb = static_cast<int>(blockIdx.x) * P;                       // block's first particle
-  const int ke = min(kb + P, D.n_own);                                    // block's end
-  const int q = (P + kStageBlock - 1) / kStageBlock;                      // particles per thread
-  const int k0 = min(kb + static_cast<int>(threadIdx.x) * q, ke);         // thread's run
-  const int k1 = min(k0 + q, ke);
-  // ---- stage: counts, block scan, records ----------------------------------
-  uint32_t mine = 0;
-  for (int k = k0; k < k1; ++k) {
-    const int c = D.cinfo[k].y;
-    scnt[k - kb] = static_cast<uint8_t>(c < kStageSat ? c : kStageSat);
-    mine += static_cast<uint32_t>(c);
-  }
-  uint32_t total;
-  const uint32_t off = block_excl_scan_u32(mine, smu, &total);
-  {
-    uint32_t r = off;
-    for (int k = k0; k < k1 && r < static_cast<uint32_t>(CAP); ++k) {
-      const int2 ci = D.cinfo[k];
-      for (int i = 0; i < ci.y && r < static_cast<uint32_t>(CAP); ++i, ++r) {
-        const long long idx = ridx(D, k, ci.x, i);
-        sg[r] = D.cgeo[idx];
-        sj[r] = D.coth[idx];
-      }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kb = static_cast<int>(blockIdx.x) * P;  // block's first particle
+  const int ke = min(kb + P, D.n_own);              // block's end
+  // ---- stage: counts, chunk bases, records (block scans in particle order) --
+  uint32_t run = 0;  // records of the earlier rounds
+  for (int m = 0; m * kStageBlock < P; ++m) {
+    const int k = kb + m * kStageBlock + static_cast<int>(threadIdx.x);
+    int2 ci = make_int2(0, 0);
+    if (k < ke) {
+      ci = D.cinfo[k];
+      scnt[k - kb] = static_cast<uint8_t>(ci.y < kStageSat ? ci.y : kStageSat);
     }
+    uint32_t total;
+    const uint32_t ex = block_excl_scan_u32(static_cast<uint32_t>(ci.y), smu, &total) + run;
+    const int chunk = m * kStageWarps + warp;
+    if (lane == 0 && chunk < nchunk) sbase[chunk] = ex;
+    for (int i = 0; i < ci.y && ex + i < CAP; ++i) {
+      const long long idx = ridx(D, k, ci.x, i);
+      sg[ex + i] = D.cgeo[idx];
+      sj[ex + i] = D.coth[idx];
+    }
+    run += total;
   }
   SweepAcc A;
-  sweep_acc_init(D, A, sbm, k0, kb);  // (its __syncthreads publishes the staged records)
+  sweep_acc_init(D, A, sbm, kb + static_cast<int>(threadIdx.x), kb);  // (__syncthreads: staging visible)
   // ---- sweeps ---------------------------------------------------------------
   for (int s = 0; s < D.S; ++s) {
     if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
     const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
     float4* Wout = D.W[s & 1];
-    uint32_t r = off;
-    for (int k = k0; k < k1; ++k) {
-      int c = scnt[k - kb];
-      int2 ci = make_int2(0, 0);
-      bool have_ci = false;
-      if (c == kStageSat) {
-        ci = D.cinfo[k];
-        c = ci.y;
-        have_ci = true;
-      }
-      if (c == 0) continue;  // no contacts: w never read (see sweep_particle)
-      sweep_acc_env(D, A, k);
-      const float4 wf = Win[k];
-      const double wx = wf.x, wy = wf.y, wz = wf.z;
-      double ax = 0.0, ay = 0.0, az = 0.0;
-      for (int i0 = 0; i0 < c; i0 += kStageBatch) {
-        float4 g[kStageBatch], qv[kStageBatch];
-        int j[kStageBatch];
+    for (int ch = warp; ch < nchunk; ch += kStageWarps) {
+      const int k = kb + ch * 32 + lane;
+      const bool live = k < ke;
+      int c = live ? scnt[k - kb] : 0;
+      const bool sat = __any_sync(0xffffffffu, c == kStageSat);
+      int incl = c;
+      const uint32_t base = sbase[ch];
+      int T;
+      bool glob;
+      int cix = 0;
+      {
+        int x = c;
 #pragma unroll
-        for (int u = 0; u < kStageBatch; ++u) {
-          const int i = i0 + u;
-          j[u] = kNullContact;
-          if (i < c) {
-            const uint32_t rr = r + static_cast<uint32_t>(i);
-            if (rr < static_cast<uint32_t>(CAP)) {
-              g[u] = sg[rr];
-              j[u] = sj[rr];
-            } else {
-              if (!have_ci) {
-                ci = D.cinfo[k];
-                have_ci = true;
-              }
-              const long long idx = ridx(D, k, ci.x, i);
-              g[u] = D.cgeo[idx];
-              j[u] = D.coth[idx];
-            }
-          }
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
         }
+        T = __shfl_sync(0xffffffffu, x, 31);
+        // staged records cover [base, base + T) unless a count saturated or
+        // the chunk runs past the capacity: then records come from global
+        glob = sat || base + static_cast<uint32_t>(T) > CAP;
+        if (glob && live) {
+          const int2 ci = D.cinfo[k];
+          c = ci.y;
+          cix = ci.x;
+          x = c;
 #pragma unroll
-        for (int u = 0; u < kStageBatch; ++u) {
-          if (j[u] == kNullContact) continue;
-          if (j[u] >= 0) {
-            qv[u] = Win[j[u]];
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          T = __shfl_sync(0xffffffffu, x, 31);
+        } else if (glob) {
+          c = 0;
+          x = 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          T = __shfl_sync(0xffffffffu, x, 31);
+        }
+        incl = x;
+      }
+      if (T == 0) continue;
+      const int excl = incl - c;
+      const float4 wf = (live && c > 0) ? Win[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      double ax = 0.0, ay = 0.0, az = 0.0;  // this lane's particle: its impulses in record order
+      for (int rb = 0; rb < T; rb += 32) {
+        const int ri = rb + lane;  // this lane's record (chunk-relative)
+        // owner lane: the number of lanes whose records end at or before ri
+        int o = 0;
+#pragma unroll
+        for (int b = 16; b >= 1; b >>= 1) {
+          const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
+          if (v <= ri) o += b;
+        }
+        o = min(o, 31);
+        const float wox = __shfl_sync(0xffffffffu, wf.x, o);
+        const float woy = __shfl_sync(0xffffffffu, wf.y, o);
+        const float woz = __shfl_sync(0xffffffffu, wf.z, o);
+        const int oex = __shfl_sync(0xffffffffu, excl, o);
+        const int ocx = __shfl_sync(0xffffffffu, cix, o);
+        double ix = 0.0, iy = 0.0, iz = 0.0;
+        if (ri < T) {
+          const int ko = kb + ch * 32 + o;
+          const int il = ri - oex;  // record index within the owner
+          float4 g;
+          int j;
+          long long gidx = -1;
+          if (!glob) {
+            g = sg[base + ri];
+            j = sj[base + ri];
           } else {
-            if (!have_ci) {
-              ci = D.cinfo[k];
-              have_ci = true;
+            gidx = ridx(D, ko, ocx, il);
+            g = D.cgeo[gidx];
+            j = D.coth[gidx];
+          }
+          if (j != kNullContact) {
+            float4 q;
+            if (j >= 0) {
+              q = Win[j];
+            } else {
+              if (gidx < 0) gidx = ridx(D, ko, D.cinfo[ko].x, il);
+              q = D.cvb[gidx];
             }
-            qv[u] = D.cvb[ridx(D, k, ci.x, i0 + u)];
+            sweep_acc_env(D, A, ko);
+            contact_impulse(D, wox, woy, woz, g, j, q, ix, iy, iz, A);
           }
         }
-#pragma unroll
-        for (int u = 0; u < kStageBatch; ++u)
-          if (j[u] != kNullContact) contact_impulse(D, wx, wy, wz, g[u], j[u], qv[u], ax, ay, az, A);
+        // each owner adds its records of this batch in record order
+        const int lo = max(excl - rb, 0), hi = min(incl - rb, 32);
+        const int nmine = hi > lo ? hi - lo : 0;
+        const int nmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nmine)));
+        for (int u = 0; u < nmax; ++u) {
+          const int src = min(lo + u, 31);
+          const double tx = __shfl_sync(0xffffffffu, ix, src);
+          const double ty = __shfl_sync(0xffffffffu, iy, src);
+          const double tz = __shfl_sync(0xffffffffu, iz, src);
+          if (u < nmine) {
+            ax += tx;
+            ay += ty;
+            az += tz;
+          }
+        }
       }
-      Wout[k] = make_float4(static_cast<float>(wx + ax), static_cast<float>(wy + ay),
-                            static_cast<float>(wz + az), 0.f);
-      r += static_cast<uint32_t>(c);
+      if (live && c > 0)
+        Wout[k] = make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
+                              static_cast<float>(static_cast<double>(wf.y) + ay),
+                              static_cast<float>(static_cast<double>(wf.z) + az), 0.f);
     }
   }
   sweep_acc_flush(D, A, smd);
-  integrate_and_finish_range(D, ctl, k0, k1, 1, smd, &s_last);
+  // integrate exactly the particles this lane owned in its warp's chunks
+  // (k = kb + 32 warp + lane + 1024 m): their last-sweep w was written here
+  integrate_and_finish_range(D, ctl, kb + warp * 32 + lane, ke, kStageBlock, smd, &s_last);
 }
 
 // ---------------------------------------------------------------------------
