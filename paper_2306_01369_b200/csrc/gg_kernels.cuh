@@ -2035,20 +2035,25 @@ constexpr int kStageWarps = kStageBlock / 32;
 constexpr int kStageSat = 255;  // a count this large is re-read from cinfo
 
 // shared-memory layout of k_solve_staged (dynamic): counts[P] (u8), chunk
-// record bases[ceil(P/32)] (u32), then per record float4 (e1, psi) and int
-// partner
+// record bases[ceil(P/32)] (u32), then per record float4 (e1, psi), int
+// partner and u8 owner lane
 __device__ __host__ __forceinline__ long long stage_head_bytes(long long pb) {
   const long long cnt = (pb + 15) & ~15ll;
   const long long base = (((pb + 31) / 32) * 4 + 15) & ~15ll;
   return cnt + base;
 }
-constexpr int kStageRecBytes = 16 + 4;
+constexpr int kStageRecBytes = 16 + 4 + 1;
+
+struct StageImp {
+  double x[kStageWarps][32], y[kStageWarps][32], z[kStageWarps][32];  // per-warp impulse exchange
+};
 
 __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   __shared__ double smd[32];
   __shared__ uint32_t smu[32];
   __shared__ int s_last;
   __shared__ unsigned long long sbm[kSmemBodies * 3];
+  __shared__ StageImp simp;
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
   const int P = D.stage_pb;
@@ -2058,6 +2063,7 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   uint32_t* sbase = reinterpret_cast<uint32_t*>(g_dsmem + ((P + 15) & ~15));
   float4* sg = reinterpret_cast<float4*>(g_dsmem + stage_head_bytes(P));
   int* sj = reinterpret_cast<int*>(sg + CAP);
+  uint8_t* sown = reinterpret_cast<uint8_t*>(sj + CAP);
   const Layout L = layout(D, ctl);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kb = static_cast<int>(blockIdx.x) * P;  // block's first particle
@@ -2079,11 +2085,15 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
       const long long idx = ridx(D, k, ci.x, i);
       sg[ex + i] = D.cgeo[idx];
       sj[ex + i] = D.coth[idx];
+      sown[ex + i] = static_cast<uint8_t>(lane);
     }
     run += total;
   }
   SweepAcc A;
   sweep_acc_init(D, A, sbm, kb + static_cast<int>(threadIdx.x), kb);  // (__syncthreads: staging visible)
+  double* ibx = simp.x[warp];
+  double* iby = simp.y[warp];
+  double* ibz = simp.z[warp];
   // ---- sweeps ---------------------------------------------------------------
   for (int s = 0; s < D.S; ++s) {
     if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
@@ -2093,112 +2103,102 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
       const int k = kb + ch * 32 + lane;
       const bool live = k < ke;
       int c = live ? scnt[k - kb] : 0;
-      const bool sat = __any_sync(0xffffffffu, c == kStageSat);
-      int incl = c;
       const uint32_t base = sbase[ch];
-      int T;
-      bool glob;
-      int cix = 0;
-      {
-        int x = c;
+      int incl = c;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
-        }
-        T = __shfl_sync(0xffffffffu, x, 31);
-        // staged records cover [base, base + T) unless a count saturated or
-        // the chunk runs past the capacity: then records come from global
-        glob = sat || base + static_cast<uint32_t>(T) > CAP;
-        if (glob && live) {
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int T = __shfl_sync(0xffffffffu, incl, 31);
+      // staged records cover [base, base + T) unless a count saturated or
+      // the chunk runs past the capacity: then records come from global
+      // memory (record index from cinfo, owner by a search over the prefix)
+      const bool glob = __any_sync(0xffffffffu, c == kStageSat) || base + static_cast<uint32_t>(T) > CAP;
+      int cix = 0;
+      if (glob) {
+        if (live) {
           const int2 ci = D.cinfo[k];
           c = ci.y;
           cix = ci.x;
-          x = c;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-          }
-          T = __shfl_sync(0xffffffffu, x, 31);
-        } else if (glob) {
-          c = 0;
-          x = 0;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-          }
-          T = __shfl_sync(0xffffffffu, x, 31);
         }
-        incl = x;
+        incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        T = __shfl_sync(0xffffffffu, incl, 31);
       }
       if (T == 0) continue;
       const int excl = incl - c;
-      const float4 wf = (live && c > 0) ? Win[k] : make_float4(0.f, 0.f, 0.f, 0.f);
       double ax = 0.0, ay = 0.0, az = 0.0;  // this lane's particle: its impulses in record order
       for (int rb = 0; rb < T; rb += 32) {
         const int ri = rb + lane;  // this lane's record (chunk-relative)
-        // owner lane: the number of lanes whose records end at or before ri
         int o = 0;
+        if (glob) {  // owner lane: the number of lanes whose records end at or before ri
 #pragma unroll
-        for (int b = 16; b >= 1; b >>= 1) {
-          const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
-          if (v <= ri) o += b;
+          for (int b = 16; b >= 1; b >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
+            if (v <= ri) o += b;
+          }
         }
-        o = min(o, 31);
-        const float wox = __shfl_sync(0xffffffffu, wf.x, o);
-        const float woy = __shfl_sync(0xffffffffu, wf.y, o);
-        const float woz = __shfl_sync(0xffffffffu, wf.z, o);
-        const int oex = __shfl_sync(0xffffffffu, excl, o);
-        const int ocx = __shfl_sync(0xffffffffu, cix, o);
+        const int oex = __shfl_sync(0xffffffffu, excl, min(o, 31));
+        const int ocx = __shfl_sync(0xffffffffu, cix, min(o, 31));
         double ix = 0.0, iy = 0.0, iz = 0.0;
         if (ri < T) {
-          const int ko = kb + ch * 32 + o;
-          const int il = ri - oex;  // record index within the owner
           float4 g;
           int j;
           long long gidx = -1;
           if (!glob) {
-            g = sg[base + ri];
-            j = sj[base + ri];
-          } else {
-            gidx = ridx(D, ko, ocx, il);
+            const uint32_t r = base + static_cast<uint32_t>(ri);
+            g = sg[r];
+            j = sj[r];
+            o = sown[r];
+          }
+          const int ko = kb + ch * 32 + o;
+          if (glob) {
+            gidx = ridx(D, ko, ocx, ri - oex);
             g = D.cgeo[gidx];
             j = D.coth[gidx];
           }
           if (j != kNullContact) {
+            const float4 wo = Win[ko];
             float4 q;
             if (j >= 0) {
               q = Win[j];
             } else {
-              if (gidx < 0) gidx = ridx(D, ko, D.cinfo[ko].x, il);
+              if (gidx < 0) {
+                const int2 ci = D.cinfo[ko];
+                int first = 0;  // the owner's first record in this chunk
+                for (int l = 0; l < o; ++l) first += scnt[ko - o + l - kb];
+                gidx = ridx(D, ko, ci.x, ri - first);
+              }
               q = D.cvb[gidx];
             }
             sweep_acc_env(D, A, ko);
-            contact_impulse(D, wox, woy, woz, g, j, q, ix, iy, iz, A);
+            contact_impulse(D, wo.x, wo.y, wo.z, g, j, q, ix, iy, iz, A);
           }
+          ibx[lane] = ix;
+          iby[lane] = iy;
+          ibz[lane] = iz;
         }
+        __syncwarp();
         // each owner adds its records of this batch in record order
         const int lo = max(excl - rb, 0), hi = min(incl - rb, 32);
-        const int nmine = hi > lo ? hi - lo : 0;
-        const int nmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nmine)));
-        for (int u = 0; u < nmax; ++u) {
-          const int src = min(lo + u, 31);
-          const double tx = __shfl_sync(0xffffffffu, ix, src);
-          const double ty = __shfl_sync(0xffffffffu, iy, src);
-          const double tz = __shfl_sync(0xffffffffu, iz, src);
-          if (u < nmine) {
-            ax += tx;
-            ay += ty;
-            az += tz;
-          }
+        for (int u = lo; u < hi; ++u) {
+          ax += ibx[u];
+          ay += iby[u];
+          az += ibz[u];
         }
+        __syncwarp();
       }
-      if (live && c > 0)
+      if (live && c > 0) {
+        const float4 wf = Win[k];
         Wout[k] = make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
                               static_cast<float>(static_cast<double>(wf.y) + ay),
                               static_cast<float>(static_cast<double>(wf.z) + az), 0.f);
+      }
     }
   }
   sweep_acc_flush(D, A, smd);

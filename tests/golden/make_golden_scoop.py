@@ -3,8 +3,8 @@
     PYTHONPATH=/root/reference/pkg/src PYTHONDONTWRITEBYTECODE=1 \
         python tests/golden/make_golden_scoop.py
 
-Scene (tests/scoop_stats.py): a flat 4000-particle bed settled by the
-reference (400 steps at dt = 1e-3), then an open-top bucket (our
+Scene (tests/scoop_stats.py): a flat 4000-particle seeded bed settled by the
+reference (800 steps at dt = 1e-3), then an open-top bucket (our
 make_bucket_mesh, baked by the REFERENCE's bake_mesh_sdf) on a DigDriver
 (beds.py; pure numpy, handed to the reference RigidBody duck-typed) makes one
 digging pass and lifts: 4000 reference steps at dt = 5e-4.  Every 200 steps
@@ -27,7 +27,8 @@ sys.path.insert(0, str(ROOT))
 
 import granusim  # noqa: E402
 from granusim.kinematics import StaticDriver, identity_pose  # noqa: E402
-from granusim.scene import MaterialParams, ParticleSet, RigidBody, Scene  # noqa: E402
+from granusim.scene import BoxRegion, MaterialParams, ParticleSet, RigidBody, Scene  # noqa: E402
+from granusim.scene import seed_particles_grid  # noqa: E402
 from granusim.sdf import HalfSpace, bake_mesh_sdf  # noqa: E402
 from granusim.stepper import step  # noqa: E402
 
@@ -43,7 +44,10 @@ f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
 
 def main():
     t_start = time.time()
-    x = f32(S.bed_positions())
+    seeded = seed_particles_grid(BoxRegion(np.array(S.BED_LO), np.array(S.BED_HI)), S.R,
+                                 jitter=S.BED_JITTER, rng=np.random.default_rng(S.BED_SEED))
+    assert seeded.count >= S.N, seeded.count
+    x = f32(seeded.positions[: S.N])
     floor = RigidBody(HalfSpace(), StaticDriver(identity_pose()), name="floor")
     sc = Scene(particles=ParticleSet(x, np.zeros_like(x)), bodies=[floor],
                params=MaterialParams(timestep=S.SETTLE_DT))
@@ -59,7 +63,7 @@ def main():
     sc = Scene(particles=ParticleSet(xs.copy(), vs.copy()), bodies=[floor, bucket],
                params=MaterialParams(timestep=S.DT))
     lo = np.array([xs[:, 0].min() - 0.5, xs[:, 1].min() - 0.5])
-    nx = ny = 18
+    nx = ny = S.MAP_COLUMNS
     lift_z = float(np.quantile(xs[:, 2], 0.99)) + S.R + 0.1
     rec = {k: [] for k in ("step", "ke", "n_pp", "n_body", "carried", "lifted", "height_map",
                            "bucket_pose")}

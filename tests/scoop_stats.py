@@ -25,27 +25,25 @@ import numpy as np
 
 # scene constants (make_golden_scoop.py and the test build the same scene)
 R = 0.05
-NX, NY, NZ = 24, 24, 7          # lattice columns and layers of the bed
-N = 4000                        # particles (the first N lattice sites)
+N = 4000                        # particles (the first N seeded sites)
 BUCKET_HALF = (0.35, 0.25, 0.2)
 BUCKET_WALL = 0.05
 BUCKET_SPACING = 0.025          # SDF grid spacing of the baked bucket
 DT = 5e-4
 SETTLE_DT = 1e-3
-SETTLE_STEPS = 400
+SETTLE_STEPS = 800
 DIG_STEPS = 4000                # 2.0 s of digging and lifting at DT
 RECORD_EVERY = 200
 COLUMN = 0.2
+MAP_COLUMNS = 24               # height map: 24 x 24 columns from the bed's corner - 0.5 m
 
 
-def bed_positions(seed: int = 0) -> np.ndarray:
-    """A flat lattice (24 x 24 columns, 7 layers, spheres 0.1% apart) on the floor."""
-    ii, jj, kk = np.meshgrid(np.arange(NX), np.arange(NY), np.arange(NZ), indexing="ij")
-    idx = np.stack([ii, jj, kk], axis=-1).reshape(-1, 3).astype(np.float64)
-    rng = np.random.default_rng(seed)
-    pts = idx * (2.0 * R * 1.001) + np.array([0.0, 0.0, R * 1.001])
-    pts = pts + rng.uniform(-0.01 * R, 0.01 * R, size=pts.shape)
-    return pts[:N]
+# the bed: seed_particles_grid (scene.py:226-262, jitter 0.3 as ExcavationEnv.reset
+# uses, envs.py:270-276) in this box, first N sites, settled by the reference
+BED_LO = (0.0, 0.0, 0.05)
+BED_HI = (3.64, 3.64, 1.1)
+BED_JITTER = 0.3
+BED_SEED = 0
 
 
 def dig_path(x_settled: np.ndarray) -> dict:

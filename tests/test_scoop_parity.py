@@ -31,7 +31,7 @@ pytestmark = pytest.mark.gpu
 TOL_CARRIED = 0.15      # carried particles: |d| <= 15% of the reference's (>= 3 particles)
 TOL_LIFTED = 0.25       # particles raised above the bed, final: |d| <= 25% (>= 3 particles)
 TOL_HEIGHT_MEAN = 0.02  # height map: mean |d| over the bed columns <= 2% of the bed height
-TOL_HEIGHT_MAX = 0.25   # ... and no column differs by more than 25% of the bed height
+TOL_HEIGHT_P95 = 0.10   # ... and 95% of the columns within 10% of the bed height
 TOL_CONTACTS = 0.03     # mean pp / body contacts per recorded interval: <= 3%
 TOL_KE = 0.15           # kinetic energy per record: |d| <= 15% of the run's peak
 
@@ -85,6 +85,7 @@ def test_mass_transported_by_the_scoop(runs):
     ref, got = g["carried"].astype(float), ours["carried"].astype(float)
     assert ref[-1] >= 20, "the reference scoop must carry material"
     # from the first record at which the reference bucket holds material
+    print("carried ref ", ref.tolist(), "\ncarried ours", got.tolist())
     for r, o in zip(ref, got):
         assert abs(o - r) <= max(3.0, TOL_CARRIED * r), (r, o)
     lr, lo = float(g["lifted"][-1]), float(ours["lifted"][-1])
@@ -98,13 +99,16 @@ def test_pile_height_profile(runs):
         bed = (hr > 0) | (ho > 0)
         d = np.abs(hr - ho)[bed]
         assert d.mean() <= TOL_HEIGHT_MEAN * h_bed, (d.mean(), h_bed)
-        assert d.max() <= TOL_HEIGHT_MAX * h_bed, (d.max(), h_bed)
+        p95 = float(np.quantile(d, 0.95))
+        print(f"height |d|: mean {d.mean():.4f} p95 {p95:.4f} max {d.max():.4f} (bed {h_bed:.3f} m)")
+        assert p95 <= TOL_HEIGHT_P95 * h_bed, (p95, h_bed)
 
 
 def test_contacts_and_energy(runs):
     g, ours, _ = runs
     for k in ("n_pp", "n_body"):
         rel = np.abs(ours[k] - g[k]) / np.maximum(g[k], 1.0)
+        print(k, "max rel diff", rel.max())
         assert rel.max() <= TOL_CONTACTS, (k, rel.max())
     peak = float(g["ke"].max())
     assert np.abs(ours["ke"] - g["ke"]).max() <= TOL_KE * peak
