@@ -771,11 +771,13 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
           per_sm_s > 0) {
         ctx->staged_grid = per_sm_s * sms;
         ctx->staged_smem = static_cast<size_t>(dyn);
-        // particles per block: a multiple of 32 (whole chunks per block)
-        const long long pb = ((n + ctx->staged_grid - 1) / ctx->staged_grid + 31) / 32 * 32;
-        const long long head = stage_head_bytes(pb);
+        // average particles per block; blocks size their ranges by work at run time
+        const long long pb = (n + ctx->staged_grid - 1) / ctx->staged_grid;
         D.stage_pb = static_cast<int>(pb);
-        D.stage_cap = head < dyn ? static_cast<int>((dyn - head) / kStageRecBytes) : -1;
+        D.stage_smem = dyn;
+        // shared-memory staging pays while a block's counts and most of its
+        // records fit: beyond ~16k particles per block the per-sweep kernels win
+        D.stage_cap = (pb <= 16384 && ctx->staged_grid <= kStageMaxGrid) ? 1 : -1;
       } else {
         ctx->staged_grid = 0;
         D.stage_cap = -1;
@@ -811,6 +813,7 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
                                                           finish_grid(n), kClusterCTAs,
                                                           ctx->staged_grid}))));
   CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3 * E));
+  CK(dalloc(ctx, &D.stage_seg, static_cast<size_t>(std::max(ctx->staged_grid, 1))));
   CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3 * E));
   CK(dalloc(ctx, &D.ctl, 1));
   CK(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));

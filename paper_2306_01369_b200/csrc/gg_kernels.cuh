@@ -139,6 +139,8 @@ struct Dev {
   // k_solve_staged: particles per block and contact records staged in each
   // block's shared memory (the rest are read from global memory)
   int stage_pb, stage_cap;
+  long long stage_smem;             // dynamic shared memory of a k_solve_staged block
+  unsigned long long* stage_seg;    // [grid] work of the fixed segments (k_solve_staged plan)
   const gg_body* bodies;  // [batch][nb]
   const DevGrid* grids;
   const double* gvals;
@@ -1260,20 +1262,26 @@ __device__ __forceinline__ void sweep_acc_flush_nobar(const Dev& D, SweepAcc& A)
   }
 }
 
+// The impulse of one contact record on its owner (contact.py:463-488), in
+// float64 with explicit fused multiply-adds (the library is built with
+// --fmad=false so that contact DECISIONS follow numpy's operation order;
+// the solver's arithmetic only has to meet the 1e-5 parity bar, and every
+// schedule evaluates this same function, so they stay bitwise identical).
 __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
                                                 float4 g, int j, float4 q, double& ax, double& ay,
                                                 double& az, SweepAcc& A) {
   const double eff = (j >= 0) ? 0.5 : 1.0;  // both partners mobile (contact.py:457-460)
   const double e1x = g.x, e1y = g.y, e1z = g.z;
-  const double ux = (wx - D.gamma * q.x) + D.gdt0;
-  const double uy = (wy - D.gamma * q.y) + D.gdt1;
-  const double uz = (wz - D.gamma * q.z) + D.gdt2;
-  const double un = ux * e1x + uy * e1y + uz * e1z;
+  const double ng = -D.gamma;
+  const double ux = fma(ng, static_cast<double>(q.x), wx) + D.gdt0;
+  const double uy = fma(ng, static_cast<double>(q.y), wy) + D.gdt1;
+  const double uz = fma(ng, static_cast<double>(q.z), wz) + D.gdt2;
+  const double un = fma(uz, e1z, fma(uy, e1y, ux * e1x));
   // np.maximum(x, 0): x if x > 0 or x is NaN, else +0.0 (one unordered compare)
-  const double bx = D.bias_coef * (double)g.w - un;
+  const double bx = fma(D.bias_coef, static_cast<double>(g.w), -un);
   const double b1 = !(bx <= 0.0) ? bx : 0.0;
-  double btx = un * e1x - ux, bty = un * e1y - uy, btz = un * e1z - uz;
-  const double tn2 = btx * btx + bty * bty + btz * btz;
+  double btx = fma(un, e1x, -ux), bty = fma(un, e1y, -uy), btz = fma(un, e1z, -uz);
+  const double tn2 = fma(btz, btz, fma(bty, bty, btx * btx));
   const double lim = D.mu * b1;
   if (tn2 > lim * lim) {  // sliding: project onto the Coulomb cone
     // scale = lim / |bt| with one reciprocal square root (tn2 > lim^2 >= 0,
@@ -1283,12 +1291,12 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
     btx *= sc;
     bty *= sc;
     btz *= sc;
-    const double viol = (tn2 * inv) * sc - lim;
+    const double viol = fma(tn2 * inv, sc, -lim);
     if (viol > A.maxviol) A.maxviol = viol;
   }
-  const double ix = (e1x * b1 + btx) * eff;
-  const double iy = (e1y * b1 + bty) * eff;
-  const double iz = (e1z * b1 + btz) * eff;
+  const double ix = fma(e1x, b1, btx) * eff;
+  const double iy = fma(e1y, b1, bty) * eff;
+  const double iz = fma(e1z, b1, btz) * eff;
   ax += ix;
   ay += iy;
   az += iz;
@@ -2033,6 +2041,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_solve(Dev D) {
 constexpr int kStageBlock = 1024;
 constexpr int kStageWarps = kStageBlock / 32;
 constexpr int kStageSat = 255;  // a count this large is re-read from cinfo
+constexpr int kStageMaxGrid = 511;  // blocks of k_solve_staged (one per SM)
 
 // shared-memory layout of k_solve_staged (dynamic): counts[P] (u8), chunk
 // record bases[ceil(P/32)] (u32), then per record float4 (e1, psi), int
@@ -2048,29 +2057,93 @@ struct StageImp {
   double x[kStageWarps][32], y[kStageWarps][32], z[kStageWarps][32];  // per-warp impulse exchange
 };
 
+// First particle k of [lo, hi) whose exclusive work prefix E(k) reaches t,
+// where E(lo) = e0 and a particle weighs its record count + 1 (block-wide;
+// hi if none).  E is non-decreasing, so the first round with a hit decides.
+__device__ __forceinline__ int stage_locate(const Dev& D, int lo, int hi, unsigned long long e0,
+                                            unsigned long long t, uint32_t* smu, int* s_hit) {
+  if (threadIdx.x == 0) *s_hit = hi;
+  __syncthreads();
+  unsigned long long run = e0;
+  for (int base = lo; base < hi; base += kStageBlock) {
+    const int k = base + static_cast<int>(threadIdx.x);
+    const uint32_t w = k < hi ? static_cast<uint32_t>(D.cinfo[k].y) + 1u : 0u;
+    uint32_t total;
+    const uint32_t ex = block_excl_scan_u32(w, smu, &total);
+    if (k < hi && run + ex >= t) atomicMin(s_hit, k);
+    __syncthreads();
+    if (*s_hit < hi) break;  // block-uniform
+    run += total;
+  }
+  const int r = *s_hit;
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   __shared__ double smd[32];
   __shared__ uint32_t smu[32];
-  __shared__ int s_last;
+  __shared__ int s_last, s_hit, s_next;
+  __shared__ unsigned long long s_pre[kStageMaxGrid + 1];
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   __shared__ StageImp simp;
   Ctl* ctl = D.ctl;
+  int ts = 0;
+  stamp(D, ts);
   if (block_should_exit(ctl)) return;  // uniform: err cannot change before the last barrier
-  const int P = D.stage_pb;
-  const uint32_t CAP = static_cast<uint32_t>(D.stage_cap);
+  const int G = static_cast<int>(gridDim.x);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // ---- plan: contiguous particle ranges of equal work ------------------------
+  // (records + particles; the grid barrier of every sweep waits for the
+  // busiest block).  Work of fixed segments, then each block locates its
+  // bounds inside the segments that contain them.
+  const int S0 = (D.n_own + G - 1) / G;
+  {
+    const int lo = min(static_cast<int>(blockIdx.x) * S0, D.n_own), hi = min(lo + S0, D.n_own);
+    unsigned long long w = 0;
+    for (int k = lo + static_cast<int>(threadIdx.x); k < hi; k += kStageBlock)
+      w += static_cast<unsigned long long>(D.cinfo[k].y) + 1ull;
+    w = block_sum_u64(w, reinterpret_cast<unsigned long long*>(smd));
+    if (threadIdx.x == 0) D.stage_seg[blockIdx.x] = w;
+  }
+  grid_barrier(ctl, static_cast<unsigned>(G));
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (int b = 0; b < G; ++b) {
+      s_pre[b] = acc;
+      acc += *((volatile unsigned long long*)&D.stage_seg[b]);
+    }
+    s_pre[G] = acc;
+  }
+  __syncthreads();
+  const unsigned long long Wtot = s_pre[G];
+  auto bound = [&](int b) -> int {
+    if (b <= 0) return 0;
+    if (b >= G) return D.n_own;
+    const unsigned long long t = (Wtot * static_cast<unsigned long long>(b)) / static_cast<unsigned long long>(G);
+    int j = 0;  // the segment holding t: the last with prefix <= t
+    while (j + 1 < G && s_pre[j + 1] <= t) ++j;
+    const int lo = min(j * S0, D.n_own), hi = min(lo + S0, D.n_own);
+    return stage_locate(D, lo, hi, s_pre[j], t, smu, &s_hit);
+  };
+  const int kb = bound(static_cast<int>(blockIdx.x));
+  const int ke = bound(static_cast<int>(blockIdx.x) + 1);
+  const int P = ke - kb;
+  // shared-memory layout for this block's P particles
+  const long long head = stage_head_bytes(P);
+  const long long capl = (static_cast<long long>(D.stage_smem) - head) / kStageRecBytes;
+  const uint32_t CAP = capl > 0 ? static_cast<uint32_t>(capl) : 0u;
   const int nchunk = (P + 31) / 32;
   uint8_t* scnt = g_dsmem;
   uint32_t* sbase = reinterpret_cast<uint32_t*>(g_dsmem + ((P + 15) & ~15));
-  float4* sg = reinterpret_cast<float4*>(g_dsmem + stage_head_bytes(P));
+  float4* sg = reinterpret_cast<float4*>(g_dsmem + head);
   int* sj = reinterpret_cast<int*>(sg + CAP);
   uint8_t* sown = reinterpret_cast<uint8_t*>(sj + CAP);
+  const bool counts_fit = head <= static_cast<long long>(D.stage_smem);
   const Layout L = layout(D, ctl);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int kb = static_cast<int>(blockIdx.x) * P;  // block's first particle
-  const int ke = min(kb + P, D.n_own);              // block's end
   // ---- stage: counts, chunk bases, records (block scans in particle order) --
   uint32_t run = 0;  // records of the earlier rounds
-  for (int m = 0; m * kStageBlock < P; ++m) {
+  for (int m = 0; counts_fit && m * kStageBlock < P; ++m) {
     const int k = kb + m * kStageBlock + static_cast<int>(threadIdx.x);
     int2 ci = make_int2(0, 0);
     if (k < ke) {
@@ -2094,16 +2167,28 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   double* ibx = simp.x[warp];
   double* iby = simp.y[warp];
   double* ibz = simp.z[warp];
+  stamp(D, ts);
   // ---- sweeps ---------------------------------------------------------------
   for (int s = 0; s < D.S; ++s) {
-    if (s > 0) grid_barrier(ctl, gridDim.x * static_cast<unsigned>(s));
+    if (threadIdx.x == 0) s_next = 0;
+    if (s > 0) {
+      grid_barrier(ctl, static_cast<unsigned>(G) * static_cast<unsigned>(s + 1));
+      stamp(D, ts);
+    } else {
+      __syncthreads();
+    }
     const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
     float4* Wout = D.W[s & 1];
-    for (int ch = warp; ch < nchunk; ch += kStageWarps) {
+    for (;;) {
+      // chunks are claimed dynamically: warps of one block finish together
+      int ch = 0;
+      if (lane == 0) ch = atomicAdd(&s_next, 1);
+      ch = __shfl_sync(0xffffffffu, ch, 0);
+      if (ch >= nchunk) break;
       const int k = kb + ch * 32 + lane;
       const bool live = k < ke;
-      int c = live ? scnt[k - kb] : 0;
-      const uint32_t base = sbase[ch];
+      int c = (live && counts_fit) ? scnt[k - kb] : 0;
+      const uint32_t base = counts_fit ? sbase[ch] : 0u;
       int incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -2114,9 +2199,11 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
       // staged records cover [base, base + T) unless a count saturated or
       // the chunk runs past the capacity: then records come from global
       // memory (record index from cinfo, owner by a search over the prefix)
-      const bool glob = __any_sync(0xffffffffu, c == kStageSat) || base + static_cast<uint32_t>(T) > CAP;
+      const bool glob = !counts_fit || __any_sync(0xffffffffu, c == kStageSat) ||
+                        base + static_cast<uint32_t>(T) > CAP;
       int cix = 0;
       if (glob) {
+        c = 0;
         if (live) {
           const int2 ci = D.cinfo[k];
           c = ci.y;
@@ -2132,6 +2219,7 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
       }
       if (T == 0) continue;
       const int excl = incl - c;
+      const float4 wf = (live && c > 0) ? Win[k] : make_float4(0.f, 0.f, 0.f, 0.f);
       double ax = 0.0, ay = 0.0, az = 0.0;  // this lane's particle: its impulses in record order
       for (int rb = 0; rb < T; rb += 32) {
         const int ri = rb + lane;  // this lane's record (chunk-relative)
@@ -2145,8 +2233,8 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
         }
         const int oex = __shfl_sync(0xffffffffu, excl, min(o, 31));
         const int ocx = __shfl_sync(0xffffffffu, cix, min(o, 31));
-        double ix = 0.0, iy = 0.0, iz = 0.0;
         if (ri < T) {
+          double ix = 0.0, iy = 0.0, iz = 0.0;
           float4 g;
           int j;
           long long gidx = -1;
@@ -2169,10 +2257,9 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
               q = Win[j];
             } else {
               if (gidx < 0) {
-                const int2 ci = D.cinfo[ko];
                 int first = 0;  // the owner's first record in this chunk
                 for (int l = 0; l < o; ++l) first += scnt[ko - o + l - kb];
-                gidx = ridx(D, ko, ci.x, ri - first);
+                gidx = ridx(D, ko, D.cinfo[ko].x, ri - first);
               }
               q = D.cvb[gidx];
             }
@@ -2193,18 +2280,17 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
         }
         __syncwarp();
       }
-      if (live && c > 0) {
-        const float4 wf = Win[k];
+      if (live && c > 0)
         Wout[k] = make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
                               static_cast<float>(static_cast<double>(wf.y) + ay),
                               static_cast<float>(static_cast<double>(wf.z) + az), 0.f);
-      }
     }
   }
-  sweep_acc_flush(D, A, smd);
-  // integrate exactly the particles this lane owned in its warp's chunks
-  // (k = kb + 32 warp + lane + 1024 m): their last-sweep w was written here
-  integrate_and_finish_range(D, ctl, kb + warp * 32 + lane, ke, kStageBlock, smd, &s_last);
+  stamp(D, ts);
+  sweep_acc_flush(D, A, smd);  // (its __syncthreads orders the block's last-sweep writes)
+  // the block's particles (its warps wrote their last-sweep w)
+  integrate_and_finish_range(D, ctl, kb + static_cast<int>(threadIdx.x), ke, kStageBlock, smd, &s_last);
+  stamp(D, ts);
 }
 
 // ---------------------------------------------------------------------------

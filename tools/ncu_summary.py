@@ -28,6 +28,10 @@ WANT = [
     "smsp__average_warps_issue_stalled_tex_throttle_per_issue_active.ratio",
     "smsp__inst_executed_pipe_fp64.sum", "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
     "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__cycles_active.avg", "sm__cycles_active.max", "sm__cycles_active.min",
+    "smsp__inst_executed_pipe_fp64.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "l1tex__t_sector_hit_rate.pct", "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum",
+    "lts__t_sectors_srcunit_tex_op_read.sum",
 ]
 
 for rep in sys.argv[1:]:
