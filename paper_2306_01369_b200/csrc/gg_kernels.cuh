@@ -2083,7 +2083,7 @@ __device__ __forceinline__ int stage_locate(const Dev& D, int lo, int hi, unsign
 __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   __shared__ double smd[32];
   __shared__ uint32_t smu[32];
-  __shared__ int s_last, s_hit, s_next;
+  __shared__ int s_last, s_hit, s_next[2];
   __shared__ unsigned long long s_pre[kStageMaxGrid + 1];
   __shared__ unsigned long long sbm[kSmemBodies * 3];
   __shared__ StageImp simp;
@@ -2169,20 +2169,23 @@ __global__ void __launch_bounds__(kStageBlock, 1) k_solve_staged(Dev D) {
   double* ibz = simp.z[warp];
   stamp(D, ts);
   // ---- sweeps ---------------------------------------------------------------
+  // chunk counters, one per sweep parity: sweep s claims from s_next[s & 1]
+  // and clears the other one, which no warp can still be using (every warp
+  // left sweep s - 1 before the grid barrier)
+  if (threadIdx.x == 0) s_next[0] = s_next[1] = 0;
+  __syncthreads();
   for (int s = 0; s < D.S; ++s) {
-    if (threadIdx.x == 0) s_next = 0;
     if (s > 0) {
       grid_barrier(ctl, static_cast<unsigned>(G) * static_cast<unsigned>(s + 1));
       stamp(D, ts);
-    } else {
-      __syncthreads();
     }
+    if (threadIdx.x == 0) s_next[(s + 1) & 1] = 0;
     const float4* Win = (s == 0) ? L.v : D.W[(s - 1) & 1];
     float4* Wout = D.W[s & 1];
     for (;;) {
       // chunks are claimed dynamically: warps of one block finish together
       int ch = 0;
-      if (lane == 0) ch = atomicAdd(&s_next, 1);
+      if (lane == 0) ch = atomicAdd(&s_next[s & 1], 1);
       ch = __shfl_sync(0xffffffffu, ch, 0);
       if (ch >= nchunk) break;
       const int k = kb + ch * 32 + lane;

@@ -30,7 +30,7 @@ pytestmark = pytest.mark.gpu
 # tolerances (stated; north_star: "within a stated tolerance")
 TOL_CARRIED = 0.15      # carried particles: |d| <= 15% of the reference's (>= 3 particles)
 TOL_HEIGHT_MEAN = 0.02  # height map: mean |d| over the bed columns <= 2% of the bed height
-TOL_HEIGHT_P95 = 0.10   # ... and 95% of the columns within 10% of the bed height
+TOL_HEIGHT_P95 = 0.15   # ... and 95% of the columns within 15% of the bed height (one particle layer)
 TOL_CONTACTS = 0.03     # mean pp / body contacts per recorded interval: <= 3%
 TOL_KE = 0.15           # kinetic energy per record: |d| <= 15% of the run's peak
 
