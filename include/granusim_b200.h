@@ -310,7 +310,7 @@ int gg_required_contacts(gg_ctx* ctx);
  * it (contact enumeration order is the bucket order); only locality does. */
 int gg_set_resort_every(gg_ctx* ctx, int32_t steps);
 
-/* Launch strategy: 0 auto (small n: mode 7; large n: mode 8), 1 per-phase kernels + cooperative persistent
+/* Launch strategy: 0 auto (small n: mode 7; large n: mode 3), 1 per-phase kernels + cooperative persistent
  * solve, 2 same without the cooperative attribute, 3 per-phase kernels and
  * one launch per sweep, 4 the whole step as ONE persistent cooperative
  * kernel (grid barriers between phases), 5 mode 4 without the cooperative
@@ -319,7 +319,7 @@ int gg_set_resort_every(gg_ctx* ctx, int32_t steps);
  * 7 mode 4 with a grid barrier per sweep instead of neighbour-block flags,
  * 8 per-phase kernels for sort and contacts, then the S sweeps, the
  * integration and the report in ONE persistent kernel whose blocks keep
- * their particles' contact records in shared memory (auto for large n).
+ * their particles' contact records in shared memory (record-parallel sweeps).
  * Results are identical in every mode. */
 int gg_set_solve_mode(gg_ctx* ctx, int32_t mode);
 
