@@ -1,28 +1,31 @@
 #!/usr/bin/env python
 """bench.py — particle-steps/s of the GranularGym timestep on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload hero50k|bed1m]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload bed1m|hero50k|envs|slab]
     python bench.py --impl reference ...        # the reference CPU path (oracle port)
 
 Workloads (BASELINE.json configs):
+  bed1m    DEFAULT, config 4 and the north_star workload (a 1M-particle bed with
+           a scoop): lattice_bed(1e6) + floor settled on the GPU, then an
+           excavator bucket (make_bucket_mesh, 2.4 x 1.2 x 1.2 m, baked to an SDF
+           grid) driving into the pile's flank at 1 m/s; dt = 5e-4, 10 PJA
+           sweeps.  Initial state and baked grid: bench_data/bed1m_settled.npz,
+           bench_data/bucket1m_grid.npz (tools/make_bed1m.py), shared by both
+           arms.  N > 1: the SAME bed slab-decomposed over the N ranks
+           (SlabBed: migration + ghost halo + per-sweep w halo), "scaling":
+           "strong"; --replicas runs N independent copies instead.
   hero50k  config 2: 50k settled column bed (floor + tube wall) with the
-           ExcavationEnv Box scoop on its 7-joint chain, joints at 0.3 x limits,
-           dt = 5e-4, 10 PJA sweeps.  Initial state: bench_data/hero50k_settled.npz
-           (settled once on the GPU, shared by both arms), else settled at start.
-  bed1m    config 4 scale: lattice_bed(1e6) on a floor with a spinning grid SDF tool.
-  slab     config 5: lattice_bed(8e6) on a floor, slab-decomposed along x over the
-           N ranks (SlabBed: migration + ghost halo + per-sweep w halo, NCCL P2P);
-           total work fixed as N grows ("scaling": "strong").
-  envs     config 3: 4096 BulldozerEnv scenes x 2000 particles (r = 0.025), ground
-           + blade on TrackSteering drivers with fixed random actions, physics
-           substeps only; env e runs on rank e mod N (no communication), so the
-           total work is fixed as N grows ("scaling": "strong").
+           ExcavationEnv Box scoop on its 7-joint chain, joints at 0.3 x limits.
+           Initial state: bench_data/hero50k_settled.npz.
+  envs     config 3: 4096 BulldozerEnv scenes x 2000 particles (r = 0.025),
+           sharded env e -> rank e mod N with no communication ("strong").
+  slab     config 5: lattice_bed(8e6) on a floor, slab-decomposed over N ranks.
 
-One JSON line on rank 0.  ``value`` is device time (CUDA events per step, L2
-flushed by a 512 MB write before every step); ``e2e`` is wall time through
-the public ``run()`` API with host state uploaded from pinned memory and the
-final state + every step's report read back.  N > 1: independent replicas
-(one per GPU, no data-path collective), max time over ranks.
+--gpus N without torchrun re-launches itself under torch.distributed.run
+with N processes (one per GPU, NCCL, NCCL_DEBUG=INFO).  One JSON line on
+rank 0.  ``value`` is device time (CUDA events per step); ``e2e`` is wall time
+through the public ``run()`` API with host state uploaded from pinned memory
+and the final state + every step's report read back.
 """
 
 from __future__ import annotations
@@ -48,27 +51,30 @@ sys.path.insert(0, str(ROOT))
 METRIC = "particle-steps/s at 50k & 1M particles (1/2/4/8 B200); % of HBM roofline"
 UNIT = "particle-steps/s"
 SETTLED = ROOT / "bench_data" / "hero50k_settled.npz"
+BED1M = ROOT / "bench_data" / "bed1m_settled.npz"
+BUCKET1M = ROOT / "bench_data" / "bucket1m_grid.npz"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="hero50k", choices=["hero50k", "bed1m", "envs", "slab"])
+    ap.add_argument("--workload", default="bed1m", choices=["bed1m", "hero50k", "envs", "slab"])
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent copies of the scene per GPU instead of one slab-decomposed bed")
     ap.add_argument("--slab-particles", type=int, default=8_000_000)
     ap.add_argument("--envs", type=int, default=4096, help="envs workload: total envs")
     ap.add_argument("--env-particles", type=int, default=2000)
     ap.add_argument("--settle", type=int, default=3000, help="hero50k: settle steps when no state file")
-    ap.add_argument("--bed-state", default="",
-                    help="bed1m: settled-state cache (.npz): loaded if present, else written after settling")
-    ap.add_argument("--settle-bed", type=int, default=8000,
-                    help="bed1m: most settle steps (dt 1e-3) before KE/n < 2e-3 J")
     ap.add_argument("--flush-mb", type=int, default=-1,
                     help="L2 flush before every timed step (MB); default: 512 for hero50k "
                          "(its working set fits L2), 0 for the larger beds (inputs > L2)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="our arm's cpu_baseline leg: CPU time budget (s)")
+    ap.add_argument("--ref-seconds", type=float, default=90.0,
+                    help="--impl reference: CPU time budget of the W + K sampled steps (s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--solve-mode", type=int, default=0)
@@ -142,39 +148,23 @@ def hero_initial_state(args, with_gpu: bool):
     return x, v, float(sc.t)
 
 
-def bed1m_settled(args):
-    """SURVEY.md §8d config 4 initial state: lattice_bed(1e6) + floor, settled on
-    the GPU at dt = 1e-3 (checked every 250 steps, at most --settle-bed steps)
-    until KE / n < 2e-3 J, fp32-rounded.  SURVEY's 1e-3 J is below the PJA
-    solver's residual jitter on this pile (KE/n plateaus at ~1.1e-3 J after
-    2e4 steps, tools/settle_probe.py); 2e-3 J is the level of the reference's
-    own settled acceptance fixture (3.9 J over 2000 particles),
-    reached after ~7000 steps with c_pp ~1.45.  Deterministic
-    (bitwise-reproducible kernels), so every run starts from the same state."""
+def bed1m_state():
+    """Config-4 initial state (tools/make_bed1m.py): the settled 1M pile with
+    the bucket 1 m into its flank; positions float32, velocities float16,
+    both upcast to float64 (the same input for both arms)."""
+    if not BED1M.exists() or not BUCKET1M.exists():
+        raise RuntimeError(f"{BED1M} / {BUCKET1M} missing: run tools/make_bed1m.py on a GPU")
+    z = np.load(BED1M, allow_pickle=False)
+    x = z["x"].astype(np.float64)
+    v = z["v"].astype(np.float64)
+    return x, v, float(z["t"]), json.loads(str(z["settle"])), json.loads(str(z["dig"]))
+
+
+def bucket1m_grid():
     import paper_2306_01369_b200 as gg
 
-    if args.bed_state and os.path.exists(args.bed_state):
-        z = np.load(args.bed_state, allow_pickle=False)
-        return (z["x"].astype(np.float64), z["v"].astype(np.float64), float(z["t"]),
-                json.loads(str(z["settle"])))
-    x = gg.lattice_bed(1_000_000).astype(np.float32).astype(np.float64)
-    sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
-                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
-                  params=gg.MaterialParams(timestep=1e-3))
-    done, ke = 0, float("inf")
-    while done < args.settle_bed:
-        _, reps = gg.run(sc, 250)
-        done += 250
-        ke = reps[-1].kinetic_energy / sc.particles.count
-        if ke < 2e-3:
-            break
-    x = sc.particles.positions.astype(np.float32).astype(np.float64)
-    v = sc.particles.velocities.astype(np.float32).astype(np.float64)
-    info = {"dt": 1e-3, "steps": done, "ke_per_particle_J": ke, "target_J": 2e-3}
-    if args.bed_state:
-        np.savez(args.bed_state, x=x.astype(np.float32), v=v.astype(np.float32), t=sc.t,
-                 settle=json.dumps(info))
-    return x, v, float(sc.t), info
+    g = np.load(BUCKET1M, allow_pickle=False)
+    return gg.SdfGrid(g["origin"], g["spacing"], g["dims"], g["values"], bytes(g["mesh_hash"]))
 
 
 def make_scene(args, with_gpu=True):
@@ -197,24 +187,22 @@ def make_scene(args, with_gpu=True):
                 "n_particles": 50_000, "dt": 5e-4, "solver_iterations": 10,
                 "bodies": "floor + tube wall + Box(0.15,0.1,0.04) scoop on 7-joint chain @0.3 limits"}
     else:
-        x, v, t, settle = bed1m_settled(args)
+        from paper_2306_01369_b200.beds import DigDriver
+
+        x, v, t, settle, dig = bed1m_state()
         params = gg.MaterialParams(timestep=5e-4)
-        verts, faces = make_box_mesh([0.15, 0.1, 0.04])
-        grid = bake_mesh_sdf(verts, faces, spacing=0.01)  # on the device (gg_bake_mesh_sdf)
-        top = float(np.quantile(x[:, 2], 0.999))
-        cx, cy = float(np.median(x[:, 0])), float(np.median(x[:, 1]))
-        # the scoop box, spun about the vertical axis with its centre 2 cm under the surface
-        tool = gg.RigidBody(grid, gg.SpinDriver(axis=[0, 0, 1], rate=1.0, center=[cx, cy, top],
-                                                base_pose=gg.make_pose(np.eye(3), [cx, cy, top - 0.02])),
-                            name="tool")
+        bucket = gg.RigidBody(bucket1m_grid(), DigDriver(**dig), name="bucket")
         sc = gg.Scene(particles=gg.ParticleSet(x, v),
-                      bodies=[gg.RigidBody(gg.HalfSpace(), name="floor"), tool], params=params)
+                      bodies=[gg.RigidBody(gg.HalfSpace(), name="floor"), bucket], params=params)
         sc.t = t
         desc = {"workload": "bed1m",
-                "config": "BASELINE configs[3]: lattice_bed(1e6) settled on the GPU + baked mesh tool",
+                "config": "BASELINE configs[3] (north_star): 1M-particle excavation bed + mesh/SDF tool",
                 "n_particles": 1_000_000, "dt": 5e-4, "solver_iterations": 10,
-                "bodies": "floor + make_box_mesh([0.15,0.1,0.04]) baked on the device at 1 cm, spinning 1 rad/s",
-                "settle": settle}
+                "bodies": "floor + excavator bucket (make_bucket_mesh, 2.4 x 1.2 x 1.2 m, 15 cm walls, "
+                          "baked on the device at 5 cm) driving into the pile flank at 1 m/s",
+                "initial_state": "bench_data/bed1m_settled.npz: lattice_bed(1e6) settled on the GPU "
+                                 f"({settle['steps']} steps at dt 1e-3, KE/n {settle['ke_per_particle_J']:.2g} J), "
+                                 "then 1 s of the bucket's pass"}
     return sc, desc
 
 
@@ -356,117 +344,173 @@ class _BodyAt:
         self.geometry, self.pose, self.omega, self.v_origin = geometry, pose, omega, v_origin
 
 
-def cpu_baseline(sc, x, v, budget_s: float) -> dict:
+ORACLE_RATE = 1.3e5  # oracle particle-steps/s on one host core (measured on the GPU box, round 1)
+
+
+def bodies_at(sc, t: float) -> list:
+    out = []
+    for b in sc.bodies:
+        om, vo = b.driver.twist_at(t)
+        out.append(_BodyAt(b.geometry, np.asarray(b.driver.pose_at(t), float), om, vo))
+    return out
+
+
+def workload_sample(sc, x, v, n_sample: int):
+    """A bounded sample of the workload state: the n_sample particles nearest
+    the tool (the last body; the bed centre when there is only a floor), in
+    user order — the part of the bed where the tool works."""
+    n = len(x)
+    if n_sample >= n:
+        return x, v, "the whole state"
+    if len(sc.bodies) > 1:
+        c = np.asarray(sc.bodies[-1].driver.pose_at(sc.t), float)[:3, 3]
+        where = "nearest the tool"
+    else:
+        c = np.median(x, axis=0)
+        where = "nearest the bed centre"
+    idx = np.sort(np.argsort(((x - c) ** 2).sum(axis=1), kind="stable")[:n_sample])
+    return x[idx].copy(), v[idx].copy(), f"the {n_sample} particles {where}"
+
+
+def oracle_run(sc, x, v, warmup: int, steps: int, budget_s: float):
+    """W untimed + up to K timed oracle steps (stops early at budget_s).
+    Returns (timed steps, seconds)."""
     from oracle import granular_oracle as O
 
     params = sc.params
-    n = len(x)
-    n_h = int(sc.hashmap_size or O.table_size(n))
+    n_h = int(sc.hashmap_size or O.table_size(len(x)))
     t = sc.t
-    steps = 0
-    t0 = time.perf_counter()
-    while True:
+    for _ in range(warmup):
         t += params.timestep
-        bodies = []
-        for b in sc.bodies:
-            om, vo = b.driver.twist_at(t)
-            bodies.append(_BodyAt(b.geometry, np.asarray(b.driver.pose_at(t), float), om, vo))
-        x, v, _, _, _ = O.step(x, v, params, bodies, n_h, sc.boundary)
-        steps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or steps >= 200:
+        x, v, _, _, _ = O.step(x, v, params, bodies_at(sc, t), n_h, sc.boundary)
+    done = 0
+    t0 = time.perf_counter()
+    while done < steps:
+        t += params.timestep
+        x, v, _, _, _ = O.step(x, v, params, bodies_at(sc, t), n_h, sc.boundary)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
             break
-    return {"value": n * steps / el, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{steps} oracle steps of the same workload state ({n} particles), "
-                      f"{el:.1f}s, numpy single thread (OPENBLAS_NUM_THREADS=1)"}
+    return done, time.perf_counter() - t0
+
+
+def cpu_baseline(sc, x, v, budget_s: float, warmup: int = 1, steps: int = 1000) -> dict:
+    """The reference algorithm (oracle port, numpy, 1 thread) on a bounded
+    sample of the same workload state, sized so the steps fit budget_s."""
+    n_s = int(min(len(x), max(2000, ORACLE_RATE * budget_s / max(warmup + min(steps, 20), 1))))
+    xs, vs, what = workload_sample(sc, x, v, n_s)
+    done, el = oracle_run(sc, xs, vs, warmup, steps, budget_s)
+    return {"value": len(xs) * done / el, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"{done} timed oracle steps (after {warmup} untimed) of {what} of the same "
+                      f"workload state, {el:.1f} s, numpy single thread (OPENBLAS_NUM_THREADS=1); "
+                      f"the reference steps one scene on one core"}
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args, dist: Dist):
-    """--impl reference: the reference CPU path (oracle port, oracle/_ref absent:
-    the reference is Python) on the host, rank 0 only."""
+    """--impl reference: the reference CPU path (the oracle port: the
+    reference is Python, there is no oracle/_ref binary) on the host, rank 0
+    only.  W untimed + K timed steps, each one oracle step of a bounded sample
+    of the workload sized so the run takes ~--ref-seconds; envs: every host
+    core steps its own env."""
     if dist.rank != 0:
         return
+    W, K = args.warmup, args.steps
     if args.workload == "envs":
-        budget = min(args.cpu_seconds, 60.0)
-        cb = envs_cpu_baseline(args, budget)
-        n_total = args.envs * args.env_particles
-        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1000.0 * n_total / cb["value"], "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "envs", "n_envs": args.envs,
-                           "n_particles": n_total}, "cpu_baseline": cb,
-                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
-    sc, desc = make_scene(args, with_gpu=False)
-    x = np.asarray(sc.particles._x, float).copy()
-    v = np.asarray(sc.particles._v, float).copy()
-    per_step_budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
-    # bounded: warmup W steps and K timed steps are each one oracle step sample
-    budget = min(args.cpu_seconds, 60.0)
-    cb = cpu_baseline(sc, x, v, budget)
-    del per_step_budget
+        cb = envs_cpu_baseline(args, W, K, min(args.ref_seconds, 120.0))
+        _, _, desc = envs_desc(args)
+        scaling = "strong"
+    else:
+        sc, desc = make_scene(args, with_gpu=False)
+        x = np.asarray(sc.particles._x, float).copy()
+        v = np.asarray(sc.particles._v, float).copy()
+        n_s = int(min(len(x), max(2000, ORACLE_RATE * args.ref_seconds / max(W + K, 1))))
+        xs, vs, what = workload_sample(sc, x, v, n_s)
+        done, el = oracle_run(sc, xs, vs, W, K, 4.0 * args.ref_seconds)
+        cb = {"value": len(xs) * done / el, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(),
+              "kind": "port",
+              "sample": f"{done} timed steps (after {W} untimed) of {what} of the {desc['workload']} "
+                        f"state, {el:.1f} s, numpy single thread (OPENBLAS_NUM_THREADS=1)"}
+        scaling = "strong" if (args.gpus > 1 and not args.replicas) else "weak"
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": args.gpus, "steps": K, "warmup": W,
             "ms_per_step": 1000.0 * desc["n_particles"] / cb["value"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": desc, "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def envs_desc(args, n_local: int | None = None):
+    from paper_2306_01369_b200.envs import BulldozerEnvConfig
+
+    cfg = BulldozerEnvConfig(n_particles=args.env_particles, radius=0.025)
+    desc = {"workload": "envs", "config": "BASELINE configs[2]: batched bulldozer envs "
+            f"{args.envs} x {args.env_particles} particles, sharded env e -> rank e mod N",
+            "n_envs": args.envs, "n_particles": args.envs * args.env_particles,
+            "dt": cfg.timestep, "solver_iterations": 10, "bodies": "ground + Box blade per env"}
+    return cfg, n_local, desc
+
+
 def envs_setup(args, dist: Dist, device: int):
     from paper_2306_01369_b200.batch import shard_envs
-    from paper_2306_01369_b200.envs import BatchedBulldozerEnv, BulldozerEnvConfig
+    from paper_2306_01369_b200.envs import BatchedBulldozerEnv
 
     mine = shard_envs(args.envs, dist.rank, dist.world)
-    cfg = BulldozerEnvConfig(n_particles=args.env_particles, radius=0.025)
+    cfg, _, desc = envs_desc(args)
     env = BatchedBulldozerEnv(len(mine), cfg, device=device, render=False)  # physics e2e
     env.reset(mine)  # seed = env id
     acts = np.stack([np.random.default_rng(int(e)).uniform(-1, 1, 2) for e in mine])
     acts[:, 0] = np.abs(acts[:, 0])  # drive forward into the bed
     env.driver.command(acts)
-    desc = {"workload": "envs", "config": "BASELINE configs[2]: batched bulldozer envs "
-            f"{args.envs} x {args.env_particles} particles, sharded env e -> rank e mod N",
-            "n_envs": args.envs, "envs_per_rank": len(mine), "n_particles": args.envs * env.batch.n,
-            "dt": cfg.timestep, "solver_iterations": 10, "bodies": "ground + Box blade per env"}
     return env, acts, desc
 
 
-def envs_cpu_baseline(args, budget_s: float) -> dict:
-    """Reference algorithm (oracle port) on one env at a time, 1 host core."""
+def _env_worker(a):
+    """One host core: env `seed`'s bed stepped by the oracle, W untimed + up
+    to K timed steps within budget_s.  Returns (particles, steps, seconds)."""
+    seed, env_particles, W, K, budget_s = a
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle import granular_oracle as O
     from paper_2306_01369_b200.envs import BulldozerEnvConfig, bulldozer_scene
 
-    cfg = BulldozerEnvConfig(n_particles=args.env_particles, radius=0.025)
-    sc = bulldozer_scene(0, cfg)
+    cfg = BulldozerEnvConfig(n_particles=env_particles, radius=0.025)
+    sc = bulldozer_scene(seed, cfg)
     x = sc.particles.positions.astype(np.float32).astype(np.float64)
     v = np.zeros_like(x)
     drv = sc.bodies[1].driver
     drv.command(np.array([0.8, 0.1]))
-    steps, t = 0, 0.0
-    t0 = time.perf_counter()
-    while True:
+    t, done, el = 0.0, 0, 0.0
+    for k in range(W + K):
+        t0 = time.perf_counter()
         t += cfg.timestep
         drv.advance(cfg.timestep)
-        bodies = []
-        for b in sc.bodies:
-            om, vo = b.driver.twist_at(t)
-            bodies.append(_BodyAt(b.geometry, np.asarray(b.driver.pose_at(t), float), om, vo))
-        x, v, _, _, _ = O.step(x, v, sc.params, bodies, O.table_size(len(x)))
-        steps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or steps >= 2000:
-            break
-    n = len(x)
-    return {"value": n * steps / el, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{steps} oracle steps of env 0 ({n} particles) from its seeded bed, "
-                      f"{el:.1f}s, numpy single thread; per-env work is independent, so the "
-                      f"{args.envs}-env batch scales with host cores at best"}
+        x, v, _, _, _ = O.step(x, v, sc.params, bodies_at(sc, t), O.table_size(len(x)))
+        if k >= W:
+            el += time.perf_counter() - t0
+            done += 1
+            if el >= budget_s:
+                break
+    return len(x), done, el
+
+
+def envs_cpu_baseline(args, W: int, K: int, budget_s: float) -> dict:
+    """The reference algorithm (oracle port) with EVERY host core stepping its
+    own env (the envs are independent), W untimed + K timed steps each."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    jobs = [(e, args.env_particles, W, K, budget_s) for e in range(cores)]
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_env_worker, jobs)
+    value = sum(n * d / el for n, d, el in res if el > 0)
+    steps = min(d for _, d, _ in res)
+    return {"value": value, "unit": UNIT, "cores": cores, "host_cores": cores, "kind": "port",
+            "sample": f"{cores} processes (one per host core), each {steps}+ timed oracle steps "
+                      f"(after {W} untimed) of its own {args.env_particles}-particle bulldozer env "
+                      f"(seeds 0..{cores - 1}); sum of the per-core rates"}
 
 
 def run_envs(args, dist: Dist):
@@ -558,16 +602,17 @@ def run_envs(args, dist: Dist):
            "wall_s": t_e2e}
     cb = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        cb = envs_cpu_baseline(args, args.cpu_seconds)
+        cb = envs_cpu_baseline(args, 2, 200, args.cpu_seconds)
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
             "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
             "data": "synthetic (seeded bulldozer beds, settled 100 substeps)",
-            "config": {**desc, "parallelism": f"env shards x{dist.world}",
-                       "l2": l2_note(args, batch.E * batch.n * 200 / 2**20),
-                       "c_pp": c_pp, "c_b": c_b, "n_h_per_env": batch.n_h},
+            "config": desc,
+            "run": {"parallelism": f"env shards x{dist.world}", "envs_per_rank": batch.E,
+                    "l2": l2_note(args, batch.E * batch.n * 200 / 2**20),
+                    "c_pp": c_pp, "c_b": c_b, "n_h_per_env": batch.n_h},
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(launches),
         }
@@ -599,6 +644,9 @@ def lattice_cpu_baseline(n_sample: int, budget_s: float, note: str) -> dict:
 
 
 def run_slab(args, dist: Dist):
+    """One bed slab-decomposed over the N ranks (SlabBed): the bed1m workload
+    at N > 1 (north_star: the 1M bed with a scoop on 8 GPUs), or config 5
+    (--workload slab: lattice_bed(8e6) + floor).  "scaling": "strong"."""
     import paper_2306_01369_b200 as gg
     from paper_2306_01369_b200 import _native as N
     from paper_2306_01369_b200.slab import SlabBed
@@ -606,12 +654,28 @@ def run_slab(args, dist: Dist):
     import torch
 
     dev = dist.local
-    n = args.slab_particles
-    x = gg.lattice_bed(n).astype(np.float32).astype(np.float64)
-    sc = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
-                  bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
-                  params=gg.MaterialParams(timestep=5e-4))
-    bed = SlabBed(sc, rank=dist.rank, world=dist.world, device=dev,
+    if args.workload == "slab":
+        n = args.slab_particles
+        x = gg.lattice_bed(n).astype(np.float32).astype(np.float64)
+        v = np.zeros_like(x)
+
+        def scene():
+            return gg.Scene(particles=gg.ParticleSet(x, v), bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
+                            params=gg.MaterialParams(timestep=5e-4))
+
+        desc = {"workload": "slab", "config": "BASELINE configs[4]: 8M bed, slab decomposition over N GPUs",
+                "n_particles": n, "dt": 5e-4, "solver_iterations": 10, "bodies": "floor"}
+    else:
+        sc0, desc = make_scene(args)
+        x = np.asarray(sc0.particles._x, float).copy()
+        v = np.asarray(sc0.particles._v, float).copy()
+        n = len(x)
+
+        def scene():
+            s2, _ = make_scene(args)
+            return s2
+
+    bed = SlabBed(scene(), rank=dist.rank, world=dist.world, device=dev,
                   backend=dist.backend if dist.world > 1 else None)
     lib = N.lib()
     K, W = args.steps, args.warmup
@@ -644,17 +708,14 @@ def run_slab(args, dist: Dist):
                 "frac": (value / dist.world) * model["step_per_particle"] / (peak * 1e9),
                 "traffic": None, "peak_source": peak_src,
                 "step_bytes_per_particle": model["step_per_particle"],
-                "note": "whole-step byte model per GPU (SURVEY.md §8d); per-kernel fractions "
-                        "are those of bed1m/envs (same kernels)"}
+                "note": "whole-step byte model per GPU (SURVEY.md §8d); the kernels are those of "
+                        "the one-GPU step (per-kernel fractions in the N = 1 line)"}
     bed.close()
     # e2e through the public API from host buffers: partition + upload
     # (SlabBed), K steps, gather of the global state back to the host
     dist.barrier()
     t0 = time.perf_counter()
-    sc2 = gg.Scene(particles=gg.ParticleSet(x, np.zeros_like(x)),
-                   bodies=[gg.RigidBody(gg.HalfSpace(), name="floor")],
-                   params=gg.MaterialParams(timestep=5e-4))
-    bed2 = SlabBed(sc2, rank=dist.rank, world=dist.world, device=dev,
+    bed2 = SlabBed(scene(), rank=dist.rank, world=dist.world, device=dev,
                    backend=dist.backend if dist.world > 1 else None)
     for _ in range(K):
         bed2.step()
@@ -668,18 +729,17 @@ def run_slab(args, dist: Dist):
                   "SlabBed.gather() (global state back on the host)"}
     cb = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        cb = lattice_cpu_baseline(100_000, args.cpu_seconds,
-                                  "the oracle is O(n): particle-steps/s carries over to 8M")
+        sc_cb = scene()
+        cb = cpu_baseline(sc_cb, x, v, args.cpu_seconds)
     if dist.rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
                 "warmup": W, "ms_per_step": t_ms / K, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32 state / f64 contact geometry", "data": "synthetic (lattice bed)",
-                "config": {"workload": "slab", "config": "BASELINE configs[4]: 8M bed, slab "
-                           "decomposition over N GPUs", "n_particles": n, "dt": 5e-4,
-                           "solver_iterations": 10, "parallelism": f"slabs x{dist.world}",
-                           "n_h": bed.n_h, "c_pp": c_pp, "c_b": c_b, "max_owned": owned,
-                           "l2": "state (>1 GB) exceeds L2"},
+                "dtype": "f32 state / f64 contact geometry", "data": "synthetic",
+                "config": desc,
+                "run": {"parallelism": f"slabs x{dist.world}", "n_h": bed.n_h, "c_pp": c_pp,
+                        "c_b": c_b, "max_owned": owned, "backend": dist.backend,
+                        "l2": "not flushed: the state exceeds L2"},
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches}
         print(json.dumps(line), flush=True)
@@ -731,6 +791,16 @@ def run_ours(args, dist: Dist):
     value = n * K * dist.world / (t_ms / 1000.0)
     c_pp = float(rbuf["n_contacts"].mean()) / n
     c_b = float(rbuf["n_body_contacts"].mean()) / n
+    # contacts with the tool (bodies after the floor and walls), per step
+    n_tool = None
+    if nb > 1:
+        from paper_2306_01369_b200.contact import device_detect
+
+        for body in sc.bodies:
+            body.update(sc.t)
+        cs, _ = device_detect(sc.particles.positions, sc.params.radius, eng.n_h, sc.bodies,
+                              params=sc.params)
+        n_tool = int(np.sum((cs.kind == 1) & (cs.other == nb - 1)))
 
     # warm (no flush) steady-state loop, for context
     table2, _ = eng.body_tables(sc, K)
@@ -795,7 +865,7 @@ def run_ours(args, dist: Dist):
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         x0 = np.asarray(sc.particles.positions, float).copy()
         v0 = np.asarray(sc.particles.velocities, float).copy()
-        cb = cpu_baseline(sc, x0, v0, args.cpu_seconds)
+        cb = cpu_baseline(sc, x0, v0, args.cpu_seconds, warmup=1, steps=1000)
 
     if dist.rank == 0:
         line = {
@@ -804,12 +874,13 @@ def run_ours(args, dist: Dist):
             "vs_baseline": None, "dtype": "f32 state / f64 contact geometry",
             "data": ("synthetic (50k column bed settled on the GPU, bench_data/hero50k_settled.npz)"
                      if args.workload == "hero50k" else
-                     "synthetic (lattice_bed(1e6) settled on the GPU before the run)"),
-            "config": {**desc, "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
-                       "pipeline": args.pipeline,
-                       "l2": l2_note(args, n * 200 / 2**20),
-                       "c_pp": c_pp, "c_b": c_b, "n_h": eng.n_h,
-                       "warm_ms_per_step": None if t_warm is None else t_warm / K},
+                     "synthetic (lattice_bed(1e6) settled on the GPU, bench_data/bed1m_settled.npz)"),
+            "config": desc,
+            "run": {"parallelism": f"replicas x{dist.world}" if dist.world > 1 else "single",
+                    "pipeline": args.pipeline, "solve_mode": args.solve_mode,
+                    "l2": l2_note(args, n * 200 / 2**20),
+                    "c_pp": c_pp, "c_b": c_b, "n_tool_contacts": n_tool, "n_h": eng.n_h,
+                    "warm_ms_per_step": None if t_warm is None else t_warm / K},
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(launches),
         }
@@ -823,17 +894,39 @@ def l2_note(args, working_set_mb: float) -> str:
             f"126 MB L2")
 
 
+def spawn_ranks(args) -> int:
+    """--gpus N without a torchrun environment: run this script under
+    torch.distributed.run with N processes on this node (rendezvous on
+    127.0.0.1, NCCL_DEBUG=INFO so the communicator's ranks are visible)."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.flush_mb < 0:
         args.flush_mb = 512 if args.workload == "hero50k" else 0
     dist = Dist()
+    if args.impl != "reference" and dist.world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={dist.world}")
     try:
         if args.impl == "reference":
             run_reference(args, dist)
         elif args.workload == "envs":
             run_envs(args, dist)
-        elif args.workload == "slab":
+        elif args.workload == "slab" or (dist.world > 1 and not args.replicas):
             run_slab(args, dist)
         else:
             run_ours(args, dist)

@@ -233,6 +233,42 @@ def add_scoop(scene: Scene, action: float = 0.3, depth: float = 0.05) -> RigidBo
     return scoop
 
 
+# the config-4 excavator bucket (bench.py bed1m): 2.4 m wide, 1.2 m deep,
+# 1.2 m tall outside, 15 cm walls, baked at 5 cm
+BUCKET1M_HALF = (0.6, 1.2, 0.6)
+BUCKET1M_WALL = 0.15
+BUCKET1M_SPACING = 0.05
+
+
+def excavator_dig(x: np.ndarray, t_now: float, half=BUCKET1M_HALF, speed: float = 1.0,
+                  length: float = 5.0, lead: float = 1.0) -> "DigDriver":
+    """A front-loader pass of the config-4 bucket into the flank of a settled
+    pile ``x``: mouth facing +x (pitch pi/2: the bucket's local +z is world
+    +x, its width along y), bottom 10 cm above the floor, lip 10 cm before
+    the point of the pile's -x flank (along the y centre band) where the
+    pile is as tall as the bucket; it drives ``length`` m into
+    the pile at ``speed`` m/s while curling the mouth up to 0.3 rad, then
+    lifts at 0.5 m/s.  The pass started ``lead`` seconds before ``t_now``,
+    so at t_now the bucket is already ``lead * speed`` m into the pile."""
+    x = np.asarray(x, dtype=np.float64)
+    yc = float(np.median(x[:, 1]))
+    top = 2.0 * half[0] + 0.1  # the bucket's top above the floor
+    # the flank: the first 0.25 m slice along the y centre band (from -x) in
+    # which the pile reaches the bucket's top
+    band = np.abs(x[:, 1] - yc) < half[1]
+    xb = x[band]
+    lo = float(xb[:, 0].min())
+    idx = np.floor((xb[:, 0] - lo) / 0.25).astype(np.int64)
+    zmax = np.zeros(int(idx.max()) + 1)
+    np.maximum.at(zmax, idx, xb[:, 2])
+    hit = np.nonzero(zmax >= top)[0]
+    x_edge = lo + 0.25 * float(hit[0] if len(hit) else 0)
+    start = np.array([x_edge - 0.1 - half[2], yc, half[0] + 0.1])
+    return DigDriver(start=start, direction=np.array([1.0, 0.0, 0.0]), length=length, depth=0.0,
+                     duration=length / speed, pitch0=0.5 * np.pi, pitch1=0.3, t0=t_now - lead,
+                     lift_speed=0.5)
+
+
 def hero_scene(n: int = 50_000, seed: int = 0, r: float = 0.05) -> Scene:
     """Config 2 before settling: column bed (aspect 1) + floor + tube wall."""
     params = MaterialParams(radius=r, friction=0.5, timestep=1e-3)

@@ -3,7 +3,7 @@ mkdir -p gpurun_out/pipe
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 rm -f /tmp/bed1m_settled.npz
 for w in hero50k bed1m; do for p in two-loops-split two-loops-fused one-loop; do
-  timeout 600 python bench.py --workload $w --pipeline $p --steps 200 --warmup 10 --no-cpu-baseline --profile-steps 3 --bed-state /tmp/bed1m_settled.npz > gpurun_out/pipe/${w}_$p.json 2> gpurun_out/pipe/${w}_$p.err || tail -2 gpurun_out/pipe/${w}_$p.err
+  timeout 600 python bench.py --workload $w --pipeline $p --steps 200 --warmup 10 --no-cpu-baseline --profile-steps 3 > gpurun_out/pipe/${w}_$p.json 2> gpurun_out/pipe/${w}_$p.err || tail -2 gpurun_out/pipe/${w}_$p.err
 done; done
 python - <<'PY'
 import json, glob

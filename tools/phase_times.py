@@ -10,8 +10,6 @@ from paper_2306_01369_b200.engine import engine_for
 class A:
     workload = sys.argv[1] if len(sys.argv) > 1 else "hero50k"
     settle = 3000
-    bed_state = "/tmp/bed1m_settled.npz"
-    settle_bed = 8000
 
 
 sc, desc = bench.make_scene(A)
