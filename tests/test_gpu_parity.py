@@ -70,11 +70,18 @@ def test_single_step_matches_reference(name):
     assert rep.n_degenerate_skipped == int(g["rep_n_degenerate"])
     assert rep.max_penetration == pytest.approx(float(g["rep_max_penetration"]), rel=1e-6)
     assert rep.kinetic_energy == pytest.approx(float(g["rep_kinetic_energy"]), rel=1e-4, abs=1e-9)
-    assert rep.max_cone_violation <= 1e-9
-    assert rep.min_normal_impulse >= 0.0
+    # solver diagnostics vs the reference's own values: the cone is satisfied
+    # to rounding in both; the smallest normal impulse agrees like the
+    # velocities (contact normals are stored float32: 6e-8 relative)
+    assert rep.max_cone_violation <= 1e-9 and float(g["rep_max_cone_violation"]) <= 1e-9
+    mn_ref = float(g["rep_min_normal_impulse"])
+    assert rep.min_normal_impulse == pytest.approx(mn_ref, rel=TOL, abs=1e-9)
+    # body momentum: per-contact impulses in float64 from float32 records,
+    # summed in 2^-36 fixed point (order independent); measured <= 3e-7
+    # relative on these cases
     bm_ref = np.asarray(g["rep_body_momentum"])
-    scale = max(1.0, np.abs(bm_ref).max(initial=0))
-    assert np.abs(rep.body_momentum - bm_ref).max(initial=0) / scale <= 1e-3
+    scale = max(1e-6, np.abs(bm_ref).max(initial=0))
+    assert np.abs(rep.body_momentum - bm_ref).max(initial=0) / scale <= 1e-5
 
 
 @pytest.mark.parametrize("n", [20_000, 50_000])
@@ -125,6 +132,50 @@ def test_full_size_bed1m_step_vs_oracle():
     back = pp[srt[pos_rev]]
     assert np.array_equal(cs.e1[back], -cs.e1[pp])
     assert np.array_equal(cs.psi[back], cs.psi[pp])
+
+
+def _bench_scene(workload):
+    import bench
+
+    class A:
+        pass
+
+    A.workload = workload
+    A.settle = 0
+    sc, _ = bench.make_scene(A, with_gpu=False)
+    return sc
+
+
+@pytest.mark.parametrize("workload", ["hero50k", "bed1m"])
+def test_teacher_forced_step_on_bench_state(workload):
+    """The exact states the bench times (the settled hero column with the
+    chain-driven scoop and the tube wall; the settled 1M pile with the baked
+    excavator bucket in its flank): one device step against one oracle step
+    from the same float32-representable state.  Directed contacts bit-exact,
+    counters exact, x / v within 1e-5."""
+    import copy
+
+    sc = _bench_scene(workload)
+    x0 = np.asarray(sc.particles._x, float).copy()
+    v0 = np.asarray(sc.particles._v, float).copy()
+    t1 = sc.t + sc.params.timestep
+    n_h = int(sc.hashmap_size or gg.default_table_size(len(x0)))
+    ref_bodies = copy.deepcopy(sc.bodies)
+    for b in ref_bodies:
+        b.update(t1)
+    _, rep = gg.step(sc)
+    x1, v1, orep, c, _ = O.step(x0, v0, sc.params, ref_bodies, n_h, sc.boundary)
+    cs, drep = device_detect(x0, sc.params.radius, n_h, ref_bodies, params=sc.params)
+    got = directed_rows(cs.owner, cs.kind, cs.other)
+    want = directed_rows(c.owner, c.kind, c.other)
+    assert got.shape == want.shape and np.array_equal(got, want)
+    assert rep.n_contacts == orep["n_contacts"] and rep.n_candidates == orep["n_candidates"]
+    assert rep.n_body_contacts == orep["n_body_contacts"] > 0
+    assert rep.n_coincident_skipped == orep["n_coincident_skipped"]
+    assert rep.n_degenerate_skipped == orep["n_degenerate_skipped"]
+    assert int(np.sum(cs.kind == 1) - np.sum((cs.kind == 1) & (cs.other == 0))) > 0  # the tool works
+    assert rel_err(sc.particles.positions, x1) <= TOL
+    assert rel_err(sc.particles.velocities, v1) <= TOL
 
 
 def test_config1_free_running_bulk_statistics():
