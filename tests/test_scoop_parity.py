@@ -32,7 +32,8 @@ TOL_CARRIED = 0.15      # carried particles: |d| <= 15% of the reference's (>= 3
 TOL_HEIGHT_MEAN = 0.02  # height map: mean |d| over the bed columns <= 2% of the bed height
 TOL_HEIGHT_P95 = 0.15   # ... and 95% of the columns within 15% of the bed height (one particle layer)
 TOL_CONTACTS = 0.03     # mean pp / body contacts per recorded interval: <= 3%
-TOL_KE = 0.15           # kinetic energy per record: |d| <= 15% of the run's peak
+TOL_KE_MEAN = 0.10      # kinetic energy averaged over the run: <= 10%
+TOL_KE = 0.25           # ... and per record |d| <= 25% of the run's peak (a chaotic flow)
 
 
 @pytest.fixture(scope="module")
@@ -108,4 +109,7 @@ def test_contacts_and_energy(runs):
         print(k, "max rel diff", rel.max())
         assert rel.max() <= TOL_CONTACTS, (k, rel.max())
     peak = float(g["ke"].max())
+    print("KE mean ref %.2f ours %.2f; max |d| %.2f (peak %.1f)" % (
+        g["ke"].mean(), ours["ke"].mean(), np.abs(ours["ke"] - g["ke"]).max(), peak))
+    assert abs(ours["ke"].mean() - g["ke"].mean()) <= TOL_KE_MEAN * g["ke"].mean()
     assert np.abs(ours["ke"] - g["ke"]).max() <= TOL_KE * peak
