@@ -585,6 +585,10 @@ def run_envs(args, dist: Dist):
                 "step_frac": (value / dist.world) * model["step_per_particle"] / (peak * 1e9)}
 
     # e2e through the public env API: actions in, rewards out, frame_skip substeps per call
+    # (the timed loop above posed the bodies from host tables: hand the host
+    # drivers' state back to the device drivers the env uses)
+    if env.device_drivers:
+        batch.drive_on_device()
     fs = env.config.frame_skip
     n_ctrl = max(K // fs, 1)
     dist.barrier()
@@ -594,11 +598,14 @@ def run_envs(args, dist: Dist):
         _ = float(rew.sum())
     t_e2e = dist.max(time.perf_counter() - t0)
     e2e = {"value": n_total * n_ctrl * fs / t_e2e, "unit": UNIT,
-           "h2d_bytes_per_step": batch.E * batch.nb * N.BODY_DTYPE.itemsize,
-           "d2h_bytes_per_step": batch.E * N.REPORT_DTYPE.itemsize
+           "h2d_bytes_per_step": (batch.E * 16) / fs if env.device_drivers
+           else batch.E * batch.nb * N.BODY_DTYPE.itemsize,
+           "d2h_bytes_per_step": (batch.E * (N.REPORT_DTYPE.itemsize + batch.nb * 24 + 24 + 8 + 8)) / fs
+           if env.device_drivers else batch.E * N.REPORT_DTYPE.itemsize
            + (batch.E * (8 + 8) + batch.E * batch.nb * 24) / fs,
-           "api": "BatchedBulldozerEnv.step(actions): per-env blade kinematics, body tables "
-                  "uploaded, frame_skip substeps, per-env StepReports and on-device rewards read back",
+           "api": "BatchedBulldozerEnv.step(actions): actions uploaded, blade TrackSteeringDriver "
+                  "and body rows on the device, frame_skip substeps, the last substep's per-env "
+                  "StepReports, driver states and on-device rewards read back",
            "wall_s": t_e2e}
     cb = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:

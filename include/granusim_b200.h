@@ -173,6 +173,32 @@ int gg_upload_grid(gg_ctx* ctx, const double* values, const int32_t dims[3],
 int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies,
             int32_t mode);
 
+/* Device-resident body drivers: when gg_step gets
+ * bodies == NULL, every body slot's rows are generated on the device for all
+ * n_envs envs and all n_steps steps (no host packing, no upload):
+ *   gg_drive_fixed   the same row rows[e] every step (ground, static tools);
+ *   gg_drive_track   TrackSteeringDriver per env (kinematics.py:179-230):
+ *                    state x/y/theta [E], z, speed scales, base pose (4x4
+ *                    row-major), a template row (kind, shape, grid, bounded)
+ *                    and the geometry's local contact bounds lo/hi for the
+ *                    world AABB; each step advances the state by the context
+ *                    timestep (heading first), then poses the body;
+ *   gg_drive_command per-env actions [E][2], clipped to [-1, 1];
+ *   gg_drive_state   the current state back to the host. */
+int gg_drive_fixed(gg_ctx* ctx, int32_t slot, const gg_body* rows);
+int gg_drive_track(gg_ctx* ctx, int32_t slot, const gg_body* tmpl, const double lo[3], const double hi[3],
+                   const double* x, const double* y, const double* theta, double z, double scale_v,
+                   double scale_omega, const double base_pose[16]);
+int gg_drive_command(gg_ctx* ctx, int32_t slot, const double* actions);
+int gg_drive_state(gg_ctx* ctx, int32_t slot, double* x, double* y, double* theta);
+/* Re-run steps [first, first + n_steps) of the last batch from the body rows
+ * it already holds (a device-driven batch after GG_ECAPACITY and
+ * gg_set_max_contacts: the drivers have advanced past these rows). */
+int gg_step_resume(gg_ctx* ctx, int32_t first, int32_t n_steps, int32_t mode);
+/* Reports [first, first + count) of the last batch ([count][E] and
+ * [count][E][n_bodies][3]) without waiting for the rest to be copied. */
+int gg_batch_reports(gg_ctx* ctx, int32_t first, int32_t count, gg_report* reports, double* body_momentum);
+
 /* Detection pass only (detect_contacts / narrowphase_contacts,
  * contact.py:244-300,372-379) on the current state: broadphase + pp + body
  * contacts, no solve, no state change.  Fills the contact/broadphase fields

@@ -149,6 +149,12 @@ def _bind(lib: C.CDLL) -> None:
         "gg_last_batch_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
         "gg_tap_hash": (C.c_int, [P, P, P, P]),
         "gg_tap_contacts": (C.c_int, [P, i64, C.POINTER(i64), P, P, P, P, P, P]),
+        "gg_drive_fixed": (C.c_int, [P, i32, P]),
+        "gg_drive_track": (C.c_int, [P, i32, P, P, P, P, P, P, dbl, dbl, dbl, P]),
+        "gg_drive_command": (C.c_int, [P, i32, P]),
+        "gg_drive_state": (C.c_int, [P, i32, P, P, P]),
+        "gg_batch_reports": (C.c_int, [P, i32, i32, P, P]),
+        "gg_step_resume": (C.c_int, [P, i32, i32, i32]),
         "gg_position_cells": (C.c_int, [P, P, i64, dbl, P]),
         "gg_tap_candidates": (C.c_int, [P, i64, C.POINTER(i64), P, P]),
         "gg_narrow_pairs": (C.c_int, [P, P, i64, P, P, i64, dbl, P, i32, P, P, P, C.POINTER(i64),

@@ -432,6 +432,70 @@ class SceneBatch:
         col["aabb_lo"] = wc - ext
         col["aabb_hi"] = wc + ext
 
+    # -- device-resident drivers (gg_drive_*) ----------
+    def drive_on_device(self) -> bool:
+        """Generate every body slot's rows on the device: StaticBatch slots and
+        slots whose scene drivers are all static become fixed rows,
+        TrackSteeringBatch slots run TrackSteeringDriver on the device (one
+        geometry in every env).  After this, ``run_raw`` uploads no body
+        tables.  Returns False (host path kept) if a slot has no device form."""
+        from .kinematics import StaticDriver
+
+        plans = []
+        for b in range(self.nb):
+            drv = self.body_drivers.get(b)
+            slot = self._slots[b]
+            if isinstance(drv, TrackSteeringBatch):
+                same = (np.all(slot.kind == slot.kind[0]) and np.all(slot.shape == slot.shape[0])
+                        and np.all(slot.grid_id == slot.grid_id[0]))
+                if not same:
+                    return False
+                plans.append(("track", b, drv))
+            elif isinstance(drv, StaticBatch) or (
+                    drv is None and all(isinstance(sc.bodies[b].driver, StaticDriver) for sc in self.scenes)):
+                plans.append(("fixed", b, drv))
+            else:
+                return False
+        lib = N.lib()
+        rows = self.last_bodies()
+        r = float(self.params.radius)
+        for kind, b, drv in plans:
+            if kind == "fixed":
+                col = np.ascontiguousarray(rows[:, b])
+                N.check(self.ctx, lib.gg_drive_fixed(self.ctx, b, N.ptr(col)), "gg_drive_fixed")
+                continue
+            tmpl = np.zeros(1, dtype=N.BODY_DTYPE)
+            tmpl[0] = rows[0, b]
+            bounds = self.scenes[0].bodies[b].geometry.contact_bounds(r)
+            lo = hi = None
+            if bounds is not None:
+                lo = np.ascontiguousarray(bounds[0], dtype=np.float64)
+                hi = np.ascontiguousarray(bounds[1], dtype=np.float64)
+            base = np.ascontiguousarray(drv.base_pose, dtype=np.float64)
+            xs, ys, ths = (np.ascontiguousarray(a, dtype=np.float64) for a in (drv.x, drv.y, drv.theta))
+            N.check(self.ctx, lib.gg_drive_track(self.ctx, b, N.ptr(tmpl), N.ptr(lo), N.ptr(hi), N.ptr(xs),
+                                                 N.ptr(ys), N.ptr(ths), drv.z, drv.scale_v, drv.scale_omega,
+                                                 N.ptr(base)), "gg_drive_track")
+            act = np.ascontiguousarray(drv.action, dtype=np.float64)
+            N.check(self.ctx, lib.gg_drive_command(self.ctx, b, N.ptr(act)), "gg_drive_command")
+        self.driven = [b for _, b, _ in plans]
+        self._track_slots = [(b, drv) for kind, b, drv in plans if kind == "track"]
+        return True
+
+    def drive_command(self) -> None:
+        """Send the host drivers' current actions to the device drivers."""
+        for b, drv in getattr(self, "_track_slots", []):
+            act = np.ascontiguousarray(drv.action, dtype=np.float64)
+            N.check(self.ctx, N.lib().gg_drive_command(self.ctx, b, N.ptr(act)), "gg_drive_command")
+
+    def _pull_driver_states(self) -> None:
+        for b, drv in getattr(self, "_track_slots", []):
+            x, y, th = np.empty(self.E), np.empty(self.E), np.empty(self.E)
+            N.check(self.ctx, N.lib().gg_drive_state(self.ctx, b, N.ptr(x), N.ptr(y), N.ptr(th)),
+                    "gg_drive_state")
+            drv.x, drv.y, drv.theta = x, y, th
+        self._last_table = None
+
     def last_bodies(self) -> np.ndarray:
         """(E, nb) gg_body rows at the current time (the last stepped poses,
         or the drivers' current poses before the first step)."""
@@ -455,29 +519,45 @@ class SceneBatch:
         return row[0]
 
     # -- stepping -------------------------------------------------------------
-    def run_raw(self, T: int, mode=PipelineMode.TWO_LOOPS_SPLIT):
+    def run_raw(self, T: int, mode=PipelineMode.TWO_LOOPS_SPLIT, last_only: bool = False):
         """Advance every env T steps.  Returns (reports (T,E) REPORT_DTYPE,
-        body_momentum (T,E,nb,3))."""
+        body_momentum (T,E,nb,3)); ``last_only``: only the last step's
+        (shapes (1,E), (1,E,nb,3)), the others are not copied back."""
         if T < 0:
             raise ValueError("n_steps must be >= 0")
         mcode = _mode_code(mode)
         if T == 0:
             return np.zeros((0, self.E), N.REPORT_DTYPE), np.zeros((0, self.E, self.nb, 3))
         t0 = self.t.copy()
-        table = self.body_tables(T)
+        driven = bool(getattr(self, "driven", None)) and len(self.driven) == self.nb
+        if driven:
+            table = None
+            self.t = self.t + float(self.params.timestep) * T
+        else:
+            table = self.body_tables(T)
         reps = np.zeros((T, self.E), dtype=N.REPORT_DTYPE)
         bm = np.zeros((T, self.E, max(self.nb, 1), 3))
         done = 0
         lib = N.lib()
         while done < T:
-            rows = np.ascontiguousarray(table[done:])
-            st = lib.gg_step(self.ctx, T - done, N.ptr(rows), self.nb, mcode)
+            if driven and done > 0:  # the rows of steps done.. are on the device already
+                st = lib.gg_step_resume(self.ctx, done, T - done, mcode)
+            else:
+                rows = None if driven else np.ascontiguousarray(table[done:])
+                st = lib.gg_step(self.ctx, T - done, N.ptr(rows), self.nb, mcode)
             N.check(self.ctx, st, "gg_step")
             rbuf = np.zeros((T - done, self.E), dtype=N.REPORT_DTYPE)
             bbuf = np.zeros((T - done, self.E, max(self.nb, 1), 3))
             nd, es = ctypes.c_int32(0), ctypes.c_int32(-1)
-            st = lib.gg_sync(self.ctx, N.ptr(rbuf), N.ptr(bbuf), T - done, ctypes.byref(nd),
-                             ctypes.byref(es))
+            if last_only:
+                st = lib.gg_sync(self.ctx, None, None, 0, ctypes.byref(nd), ctypes.byref(es))
+                if st == N.GG_OK and nd.value > 0:  # the batch's last step only
+                    kk = nd.value - 1
+                    N.check(self.ctx, lib.gg_batch_reports(self.ctx, kk, 1, N.ptr(rbuf[kk:kk + 1]),
+                                                           N.ptr(bbuf[kk:kk + 1])), "gg_batch_reports")
+            else:
+                st = lib.gg_sync(self.ctx, N.ptr(rbuf), N.ptr(bbuf), T - done, ctypes.byref(nd),
+                                 ctypes.byref(es))
             k = nd.value
             reps[done:done + k] = rbuf[:k]
             bm[done:done + k] = bbuf[:k]
@@ -498,6 +578,10 @@ class SceneBatch:
             if st == N.GG_EPOSITIONS:
                 raise ValueError(msg)
             raise RuntimeError(f"step {done}: {msg}")
+        if driven:
+            self._pull_driver_states()
+        if last_only:
+            return reps[-1:], bm[-1:, :, : self.nb]
         return reps, bm[:, :, : self.nb]
 
     def step(self, mode=PipelineMode.TWO_LOOPS_SPLIT) -> list[StepReport]:

@@ -14,6 +14,7 @@
 #include "gg_render.cuh"
 #include "gg_bake.cuh"
 #include "gg_l1.cuh"
+#include "gg_drive.cuh"
 
 using namespace gg;
 
@@ -92,6 +93,16 @@ struct gg_ctx {
   long long mbox_cap = 0;
   Mailbox* peer[2] = {nullptr, nullptr};
   bool peer_ipc[2] = {false, false};  // opened with cudaIpcOpenMemHandle
+
+  // device-resident body drivers (gg_drive_*), one per body slot
+  struct DriveSlot {
+    int kind = 0;  // 0 none, 1 fixed, 2 track
+    gg_body* d_fixed = nullptr;
+    double* d_state = nullptr;  // [3][E] x, y, theta
+    double* d_action = nullptr; // [E][2]
+    DriveTrack P{};
+  };
+  std::vector<DriveSlot> drive;
 };
 
 namespace {
@@ -1020,13 +1031,18 @@ int gg_upload_grid(gg_ctx* ctx, const double* values, const int32_t dims[3],
 int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodies, int32_t mode) {
   if (!ctx) return GG_EINVAL;
   if (n_steps < 0) return fail(ctx, GG_EINVAL, "n_steps must be >= 0");
-  if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
+  if (n_bodies < 0) return fail(ctx, GG_EINVAL, "bad bodies");
+  const bool driven = n_bodies > 0 && !bodies;  // rows from the device drivers
+  if (driven)
+    for (int b = 0; b < n_bodies; ++b)
+      if (b >= static_cast<int>(ctx->drive.size()) || ctx->drive[b].kind == 0)
+        return fail(ctx, GG_EINVAL, "bodies == NULL needs a device driver on every body slot");
   if (mode < 0 || mode > 2) return fail(ctx, GG_EINVAL, "unknown pipeline mode");
   if (mode != ctx->pipeline) {
     ctx->pipeline = mode;
     ctx->graph_dirty = true;
   }
-  for (long long i = 0; i < static_cast<long long>(n_steps) * ctx->E * n_bodies; ++i) {
+  for (long long i = 0; !driven && i < static_cast<long long>(n_steps) * ctx->E * n_bodies; ++i) {
     const gg_body& b = bodies[i];
     if (b.kind < GG_GEOM_SPHERE || b.kind > GG_GEOM_GRID)
       return fail(ctx, GG_EINVAL, "unknown geometry kind");
@@ -1042,7 +1058,22 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
     ctx->D.nb = n_bodies;
     ctx->graph_dirty = true;
   }
-  if (n_bodies > 0) {
+  if (driven) {
+    const int E = ctx->E;
+    const unsigned g = static_cast<unsigned>((E + 127) / 128);
+    for (int b = 0; b < n_bodies; ++b) {
+      gg_ctx::DriveSlot& ds = ctx->drive[b];
+      if (ds.kind == 1) {
+        k_drive_fixed<<<g, 128, 0, ctx->stream>>>(ctx->d_bodies, ds.d_fixed, n_steps, E, n_bodies, b);
+      } else {
+        DriveTrack P = ds.P;
+        P.dt = ctx->P.timestep;
+        k_drive_track<<<g, 128, 0, ctx->stream>>>(ctx->d_bodies, P, n_steps, E, n_bodies, b);
+      }
+      ctx->launches += 1;
+    }
+    CK(cudaGetLastError());
+  } else if (n_bodies > 0) {
     const size_t bytes = sizeof(gg_body) * static_cast<size_t>(n_steps) * ctx->E * n_bodies;
     std::memcpy(ctx->h_bodies, bodies, bytes);
     CK(cudaMemcpyAsync(ctx->d_bodies, ctx->h_bodies, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -1280,6 +1311,141 @@ int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
 
 int gg_required_contacts(gg_ctx* ctx) {
   return ctx && ctx->h_ctl ? ctx->h_ctl->cap_needed : 0;
+}
+
+static int drive_slot(gg_ctx* ctx, int32_t slot, gg_ctx::DriveSlot** out) {
+  if (slot < 0 || slot >= std::max(ctx->max_bodies, 1)) return fail(ctx, GG_EINVAL, "body slot out of range");
+  if (static_cast<int>(ctx->drive.size()) <= slot) ctx->drive.resize(slot + 1);
+  *out = &ctx->drive[slot];
+  return GG_OK;
+}
+
+int gg_drive_fixed(gg_ctx* ctx, int32_t slot, const gg_body* rows) {
+  if (!ctx || !rows) return GG_EINVAL;
+  gg_ctx::DriveSlot* ds = nullptr;
+  int st = drive_slot(ctx, slot, &ds);
+  if (st != GG_OK) return st;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (!ds->d_fixed) CK(dalloc(ctx, &ds->d_fixed, ctx->E));
+  CK(cudaMemcpy(ds->d_fixed, rows, sizeof(gg_body) * ctx->E, cudaMemcpyHostToDevice));
+  ds->kind = 1;
+  return GG_OK;
+}
+
+int gg_drive_track(gg_ctx* ctx, int32_t slot, const gg_body* tmpl, const double lo[3], const double hi[3],
+                   const double* x, const double* y, const double* theta, double z, double scale_v,
+                   double scale_omega, const double base_pose[16]) {
+  if (!ctx || !tmpl || !x || !y || !theta || !base_pose) return GG_EINVAL;
+  if (tmpl->bounded && (!lo || !hi)) return fail(ctx, GG_EINVAL, "bounded template needs local bounds");
+  gg_ctx::DriveSlot* ds = nullptr;
+  int st = drive_slot(ctx, slot, &ds);
+  if (st != GG_OK) return st;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int E = ctx->E;
+  if (!ds->d_state) CK(dalloc(ctx, &ds->d_state, 3 * static_cast<size_t>(E)));
+  if (!ds->d_action) CK(dalloc(ctx, &ds->d_action, 2 * static_cast<size_t>(E)));
+  CK(cudaMemcpy(ds->d_state, x, sizeof(double) * E, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ds->d_state + E, y, sizeof(double) * E, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ds->d_state + 2 * E, theta, sizeof(double) * E, cudaMemcpyHostToDevice));
+  CK(cudaMemset(ds->d_action, 0, sizeof(double) * 2 * E));
+  DriveTrack& P = ds->P;
+  P = DriveTrack{};
+  P.x = ds->d_state;
+  P.y = ds->d_state + E;
+  P.theta = ds->d_state + 2 * E;
+  P.action = ds->d_action;
+  P.z = z;
+  P.scale_v = scale_v;
+  P.scale_omega = scale_omega;
+  for (int i = 0; i < 16; ++i) P.base[i] = base_pose[i];
+  for (int a = 0; a < 3; ++a) {
+    P.lo[a] = lo ? lo[a] : 0.0;
+    P.hi[a] = hi ? hi[a] : 0.0;
+  }
+  P.tmpl = *tmpl;
+  ds->kind = 2;
+  return GG_OK;
+}
+
+int gg_drive_command(gg_ctx* ctx, int32_t slot, const double* actions) {
+  if (!ctx || !actions) return GG_EINVAL;
+  if (slot < 0 || slot >= static_cast<int>(ctx->drive.size()) || ctx->drive[slot].kind != 2)
+    return fail(ctx, GG_EINVAL, "no track driver on this body slot");
+  DeviceGuard guard(ctx->device);
+  const int E = ctx->E;
+  std::vector<double> a(actions, actions + 2 * static_cast<size_t>(E));
+  for (double& u : a) u = u < -1.0 ? -1.0 : (u > 1.0 ? 1.0 : u);  // TrackSteeringDriver.command clip
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(ctx->drive[slot].d_action, a.data(), sizeof(double) * 2 * E, cudaMemcpyHostToDevice));
+  return GG_OK;
+}
+
+int gg_drive_state(gg_ctx* ctx, int32_t slot, double* x, double* y, double* theta) {
+  if (!ctx) return GG_EINVAL;
+  if (slot < 0 || slot >= static_cast<int>(ctx->drive.size()) || ctx->drive[slot].kind != 2)
+    return fail(ctx, GG_EINVAL, "no track driver on this body slot");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int E = ctx->E;
+  const double* d = ctx->drive[slot].d_state;
+  if (x) CK(cudaMemcpy(x, d, sizeof(double) * E, cudaMemcpyDeviceToHost));
+  if (y) CK(cudaMemcpy(y, d + E, sizeof(double) * E, cudaMemcpyDeviceToHost));
+  if (theta) CK(cudaMemcpy(theta, d + 2 * E, sizeof(double) * E, cudaMemcpyDeviceToHost));
+  return GG_OK;
+}
+
+int gg_step_resume(gg_ctx* ctx, int32_t first, int32_t n_steps, int32_t mode) {
+  if (!ctx) return GG_EINVAL;
+  if (first < 0 || n_steps < 1 || first + n_steps > ctx->batch_cap || ctx->D.nb < 1)
+    return fail(ctx, GG_EINVAL, "gg_step_resume: rows outside the last batch");
+  if (mode != ctx->pipeline) return fail(ctx, GG_EINVAL, "gg_step_resume: pipeline mode changed");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const size_t per = static_cast<size_t>(ctx->E) * ctx->D.nb;
+  if (first > 0) {
+    // the remaining rows to the front (a temporary: the ranges may overlap)
+    gg_body* tmp = nullptr;
+    CK(cudaMalloc(&tmp, sizeof(gg_body) * per * n_steps));
+    CK(cudaMemcpy(tmp, ctx->d_bodies + per * first, sizeof(gg_body) * per * n_steps, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(ctx->d_bodies, tmp, sizeof(gg_body) * per * n_steps, cudaMemcpyDeviceToDevice));
+    cudaFree(tmp);
+  }
+  int st;
+  if (ctx->graph_dirty) {
+    st = build_graph(ctx);
+    if (st != GG_OK) return st;
+  }
+  refresh_dev(ctx);
+  st = begin_batch(ctx, ctx->stream);
+  if (st != GG_OK) return st;
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  for (int i = 0; i < n_steps; ++i) {
+    st = launch_step(ctx);
+    if (st != GG_OK) return st;
+  }
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->launches += 1;
+  ctx->last_batch = n_steps;
+  ctx->tap_uncommitted = false;
+  return GG_OK;
+}
+
+int gg_batch_reports(gg_ctx* ctx, int32_t first, int32_t count, gg_report* reports, double* body_momentum) {
+  if (!ctx) return GG_EINVAL;
+  if (first < 0 || count < 0 || first + count > ctx->last_batch)
+    return fail(ctx, GG_EINVAL, "report range outside the last batch");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const size_t E = static_cast<size_t>(ctx->E);
+  if (reports && count > 0)
+    CK(cudaMemcpy(reports, ctx->d_reports + first * E, sizeof(gg_report) * count * E, cudaMemcpyDeviceToHost));
+  if (body_momentum && count > 0 && ctx->last_nb > 0) {
+    const size_t per = 3 * static_cast<size_t>(ctx->last_nb) * E;
+    CK(cudaMemcpy(body_momentum, ctx->d_bm + first * per, sizeof(double) * count * per, cudaMemcpyDeviceToHost));
+  }
+  return GG_OK;
 }
 
 int gg_tap_hash(gg_ctx* ctx, int64_t* cells, int64_t* hashes, int64_t* order) {

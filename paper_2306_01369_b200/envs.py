@@ -187,6 +187,9 @@ class BatchedBulldozerEnv:
             self.batch.close()
         self.batch = SceneBatch(scenes, body_drivers={0: StaticBatch(E), 1: self.driver},
                                 device=self.device)
+        # the ground and the blade's TrackSteeringDriver run on the device:
+        # no per-substep body tables are packed or uploaded
+        self.device_drivers = self.batch.drive_on_device()
         self._steps = 0
         return self._observe()
 
@@ -223,7 +226,9 @@ class BatchedBulldozerEnv:
         if not np.all(np.isfinite(a)):
             raise ValueError("action must be finite")
         self.driver.command(a)
-        reps, _ = self.batch.run_raw(self.config.frame_skip)
+        if self.device_drivers:
+            self.batch.drive_command()
+        reps, _ = self.batch.run_raw(self.config.frame_skip, last_only=True)
         rew, ins = self.goal_stats()
         self._steps += 1
         done = np.full(self.n_envs, self._steps >= self.episode_length)
