@@ -183,14 +183,28 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
  *                    and the geometry's local contact bounds lo/hi for the
  *                    world AABB; each step advances the state by the context
  *                    timestep (heading first), then poses the body;
- *   gg_drive_command per-env actions [E][2], clipped to [-1, 1];
- *   gg_drive_state   the current state back to the host. */
+ *   gg_drive_chain   KinematicChain + ChainLinkDriver per env (kinematics.py:
+ *                    237-322): n_links links (parent index, prismatic flag,
+ *                    parent-to-joint 4x4 origin, unit axis, velocity limit),
+ *                    base pose, joint positions q [E][n_links]; each step the
+ *                    joint rates are the command clipped to the limits,
+ *                    q += dt * qd, then the forward kinematics of link_index
+ *                    gives the body pose and twist (ExcavationEnv.step,
+ *                    envs.py:336-341);
+ *   gg_drive_command per-env actions: track [E][2] (clipped to [-1, 1]),
+ *                    chain [E][n_links] joint-rate commands;
+ *   gg_drive_state / gg_drive_chain_state  the current state back to the host. */
 int gg_drive_fixed(gg_ctx* ctx, int32_t slot, const gg_body* rows);
 int gg_drive_track(gg_ctx* ctx, int32_t slot, const gg_body* tmpl, const double lo[3], const double hi[3],
                    const double* x, const double* y, const double* theta, double z, double scale_v,
                    double scale_omega, const double base_pose[16]);
+int gg_drive_chain(gg_ctx* ctx, int32_t slot, const gg_body* tmpl, const double lo[3], const double hi[3],
+                   int32_t n_links, int32_t link_index, const int32_t* parents, const int32_t* prismatic,
+                   const double* origins, const double* axes, const double* limits,
+                   const double base_pose[16], const double* q);
 int gg_drive_command(gg_ctx* ctx, int32_t slot, const double* actions);
 int gg_drive_state(gg_ctx* ctx, int32_t slot, double* x, double* y, double* theta);
+int gg_drive_chain_state(gg_ctx* ctx, int32_t slot, double* q);
 /* Re-run steps [first, first + n_steps) of the last batch from the body rows
  * it already holds (a device-driven batch after GG_ECAPACITY and
  * gg_set_max_contacts: the drivers have advanced past these rows). */

@@ -152,6 +152,8 @@ def _bind(lib: C.CDLL) -> None:
         "gg_drive_fixed": (C.c_int, [P, i32, P]),
         "gg_drive_track": (C.c_int, [P, i32, P, P, P, P, P, P, dbl, dbl, dbl, P]),
         "gg_drive_command": (C.c_int, [P, i32, P]),
+        "gg_drive_chain": (C.c_int, [P, i32, P, P, P, i32, i32, P, P, P, P, P, P, P]),
+        "gg_drive_chain_state": (C.c_int, [P, i32, P]),
         "gg_drive_state": (C.c_int, [P, i32, P, P, P]),
         "gg_batch_reports": (C.c_int, [P, i32, i32, P, P]),
         "gg_step_resume": (C.c_int, [P, i32, i32, i32]),

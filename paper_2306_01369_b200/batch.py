@@ -445,12 +445,12 @@ class SceneBatch:
         for b in range(self.nb):
             drv = self.body_drivers.get(b)
             slot = self._slots[b]
-            if isinstance(drv, TrackSteeringBatch):
+            if isinstance(drv, (TrackSteeringBatch, ChainBatch)):
                 same = (np.all(slot.kind == slot.kind[0]) and np.all(slot.shape == slot.shape[0])
                         and np.all(slot.grid_id == slot.grid_id[0]))
                 if not same:
                     return False
-                plans.append(("track", b, drv))
+                plans.append(("track" if isinstance(drv, TrackSteeringBatch) else "chain", b, drv))
             elif isinstance(drv, StaticBatch) or (
                     drv is None and all(isinstance(sc.bodies[b].driver, StaticDriver) for sc in self.scenes)):
                 plans.append(("fixed", b, drv))
@@ -472,28 +472,48 @@ class SceneBatch:
                 lo = np.ascontiguousarray(bounds[0], dtype=np.float64)
                 hi = np.ascontiguousarray(bounds[1], dtype=np.float64)
             base = np.ascontiguousarray(drv.base_pose, dtype=np.float64)
-            xs, ys, ths = (np.ascontiguousarray(a, dtype=np.float64) for a in (drv.x, drv.y, drv.theta))
-            N.check(self.ctx, lib.gg_drive_track(self.ctx, b, N.ptr(tmpl), N.ptr(lo), N.ptr(hi), N.ptr(xs),
-                                                 N.ptr(ys), N.ptr(ths), drv.z, drv.scale_v, drv.scale_omega,
-                                                 N.ptr(base)), "gg_drive_track")
-            act = np.ascontiguousarray(drv.action, dtype=np.float64)
-            N.check(self.ctx, lib.gg_drive_command(self.ctx, b, N.ptr(act)), "gg_drive_command")
+            if kind == "track":
+                xs, ys, ths = (np.ascontiguousarray(a, dtype=np.float64) for a in (drv.x, drv.y, drv.theta))
+                N.check(self.ctx, lib.gg_drive_track(self.ctx, b, N.ptr(tmpl), N.ptr(lo), N.ptr(hi), N.ptr(xs),
+                                                     N.ptr(ys), N.ptr(ths), drv.z, drv.scale_v,
+                                                     drv.scale_omega, N.ptr(base)), "gg_drive_track")
+            else:
+                links = drv.links
+                J = len(links)
+                par = np.array([l.parent for l in links], dtype=np.int32)
+                pri = np.array([0 if l.joint_type == "revolute" else 1 for l in links], dtype=np.int32)
+                org = np.ascontiguousarray(np.stack([np.asarray(l.origin, float) for l in links]).reshape(J, 16))
+                axs = np.ascontiguousarray(np.stack([np.asarray(l.axis, float) for l in links]))
+                q = np.ascontiguousarray(drv.q, dtype=np.float64)
+                N.check(self.ctx, lib.gg_drive_chain(self.ctx, b, N.ptr(tmpl), N.ptr(lo), N.ptr(hi), J,
+                                                     drv.link_index, N.ptr(par), N.ptr(pri), N.ptr(org),
+                                                     N.ptr(axs), N.ptr(np.ascontiguousarray(drv.limits)),
+                                                     N.ptr(base), N.ptr(q)), "gg_drive_chain")
         self.driven = [b for _, b, _ in plans]
-        self._track_slots = [(b, drv) for kind, b, drv in plans if kind == "track"]
+        self._track_slots = [(b, drv) for kind, b, drv in plans if kind in ("track", "chain")]
+        self.drive_command()
         return True
 
     def drive_command(self) -> None:
-        """Send the host drivers' current actions to the device drivers."""
+        """Send the host drivers' current commands (track actions, chain joint
+        rate commands) to the device drivers."""
         for b, drv in getattr(self, "_track_slots", []):
-            act = np.ascontiguousarray(drv.action, dtype=np.float64)
+            src = drv.action if isinstance(drv, TrackSteeringBatch) else drv.cmd
+            act = np.ascontiguousarray(src, dtype=np.float64)
             N.check(self.ctx, N.lib().gg_drive_command(self.ctx, b, N.ptr(act)), "gg_drive_command")
 
     def _pull_driver_states(self) -> None:
         for b, drv in getattr(self, "_track_slots", []):
-            x, y, th = np.empty(self.E), np.empty(self.E), np.empty(self.E)
-            N.check(self.ctx, N.lib().gg_drive_state(self.ctx, b, N.ptr(x), N.ptr(y), N.ptr(th)),
-                    "gg_drive_state")
-            drv.x, drv.y, drv.theta = x, y, th
+            if isinstance(drv, TrackSteeringBatch):
+                x, y, th = np.empty(self.E), np.empty(self.E), np.empty(self.E)
+                N.check(self.ctx, N.lib().gg_drive_state(self.ctx, b, N.ptr(x), N.ptr(y), N.ptr(th)),
+                        "gg_drive_state")
+                drv.x, drv.y, drv.theta = x, y, th
+            else:
+                q = np.empty((self.E, len(drv.links)))
+                N.check(self.ctx, N.lib().gg_drive_chain_state(self.ctx, b, N.ptr(q)), "gg_drive_chain_state")
+                drv.q = q
+                drv.qd = np.clip(drv.cmd, -drv.limits, drv.limits)
         self._last_table = None
 
     def last_bodies(self) -> np.ndarray:
@@ -530,7 +550,8 @@ class SceneBatch:
             return np.zeros((0, self.E), N.REPORT_DTYPE), np.zeros((0, self.E, self.nb, 3))
         t0 = self.t.copy()
         driven = bool(getattr(self, "driven", None)) and len(self.driven) == self.nb
-        if driven:
+        if driven:  # the host drivers' commands are the source of truth
+            self.drive_command()
             table = None
             self.t = self.t + float(self.params.timestep) * T
         else:

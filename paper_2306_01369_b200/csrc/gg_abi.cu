@@ -96,11 +96,12 @@ struct gg_ctx {
 
   // device-resident body drivers (gg_drive_*), one per body slot
   struct DriveSlot {
-    int kind = 0;  // 0 none, 1 fixed, 2 track
+    int kind = 0;  // 0 none, 1 fixed, 2 track, 3 chain
     gg_body* d_fixed = nullptr;
-    double* d_state = nullptr;  // [3][E] x, y, theta
-    double* d_action = nullptr; // [E][2]
+    double* d_state = nullptr;  // track: [3][E] x, y, theta; chain: [E][J] q
+    double* d_action = nullptr; // track: [E][2]; chain: [E][J] joint rate commands
     DriveTrack P{};
+    DriveChain C{};
   };
   std::vector<DriveSlot> drive;
 };
@@ -1065,6 +1066,10 @@ int gg_step(gg_ctx* ctx, int32_t n_steps, const gg_body* bodies, int32_t n_bodie
       gg_ctx::DriveSlot& ds = ctx->drive[b];
       if (ds.kind == 1) {
         k_drive_fixed<<<g, 128, 0, ctx->stream>>>(ctx->d_bodies, ds.d_fixed, n_steps, E, n_bodies, b);
+      } else if (ds.kind == 3) {
+        DriveChain C = ds.C;
+        C.dt = ctx->P.timestep;
+        k_drive_chain<<<g, 128, 0, ctx->stream>>>(ctx->d_bodies, C, n_steps, E, n_bodies, b);
       } else {
         DriveTrack P = ds.P;
         P.dt = ctx->P.timestep;
@@ -1369,16 +1374,78 @@ int gg_drive_track(gg_ctx* ctx, int32_t slot, const gg_body* tmpl, const double 
   return GG_OK;
 }
 
+int gg_drive_chain(gg_ctx* ctx, int32_t slot, const gg_body* tmpl, const double lo[3], const double hi[3],
+                   int32_t n_links, int32_t link_index, const int32_t* parents, const int32_t* prismatic,
+                   const double* origins, const double* axes, const double* limits,
+                   const double base_pose[16], const double* q) {
+  if (!ctx || !tmpl || !parents || !prismatic || !origins || !axes || !limits || !base_pose || !q)
+    return GG_EINVAL;
+  if (n_links < 1 || n_links > kChainMax || link_index < 0 || link_index >= n_links)
+    return fail(ctx, GG_EINVAL, "chain: 1..16 links and a link index among them");
+  for (int i = 0; i < n_links; ++i)
+    if (parents[i] >= i) return fail(ctx, GG_EINVAL, "chain: links must follow their parents");
+  if (tmpl->bounded && (!lo || !hi)) return fail(ctx, GG_EINVAL, "bounded template needs local bounds");
+  gg_ctx::DriveSlot* ds = nullptr;
+  int st = drive_slot(ctx, slot, &ds);
+  if (st != GG_OK) return st;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const size_t EJ = static_cast<size_t>(ctx->E) * n_links;
+  if (ds->d_state) dfree(ctx, ds->d_state);
+  if (ds->d_action) dfree(ctx, ds->d_action);
+  ds->d_state = nullptr;
+  ds->d_action = nullptr;
+  CK(dalloc(ctx, &ds->d_state, EJ));
+  CK(dalloc(ctx, &ds->d_action, EJ));
+  CK(cudaMemcpy(ds->d_state, q, sizeof(double) * EJ, cudaMemcpyHostToDevice));
+  CK(cudaMemset(ds->d_action, 0, sizeof(double) * EJ));
+  DriveChain& C = ds->C;
+  C = DriveChain{};
+  C.q = ds->d_state;
+  C.cmd = ds->d_action;
+  C.J = n_links;
+  C.link = link_index;
+  for (int i = 0; i < n_links; ++i) {
+    C.parent[i] = parents[i];
+    C.prismatic[i] = prismatic[i];
+    for (int r = 0; r < 12; ++r) C.origin[i][r] = origins[16 * i + r];
+    for (int a = 0; a < 3; ++a) C.axis[i][a] = axes[3 * i + a];
+    C.limit[i] = limits[i];
+  }
+  for (int r = 0; r < 12; ++r) C.base[r] = base_pose[r];
+  for (int a = 0; a < 3; ++a) {
+    C.lo[a] = lo ? lo[a] : 0.0;
+    C.hi[a] = hi ? hi[a] : 0.0;
+  }
+  C.tmpl = *tmpl;
+  ds->kind = 3;
+  return GG_OK;
+}
+
 int gg_drive_command(gg_ctx* ctx, int32_t slot, const double* actions) {
   if (!ctx || !actions) return GG_EINVAL;
-  if (slot < 0 || slot >= static_cast<int>(ctx->drive.size()) || ctx->drive[slot].kind != 2)
-    return fail(ctx, GG_EINVAL, "no track driver on this body slot");
+  if (slot < 0 || slot >= static_cast<int>(ctx->drive.size()) || ctx->drive[slot].kind < 2)
+    return fail(ctx, GG_EINVAL, "no track or chain driver on this body slot");
   DeviceGuard guard(ctx->device);
   const int E = ctx->E;
-  std::vector<double> a(actions, actions + 2 * static_cast<size_t>(E));
-  for (double& u : a) u = u < -1.0 ? -1.0 : (u > 1.0 ? 1.0 : u);  // TrackSteeringDriver.command clip
+  gg_ctx::DriveSlot& ds = ctx->drive[slot];
+  const size_t m = static_cast<size_t>(E) * (ds.kind == 2 ? 2 : ds.C.J);
+  std::vector<double> a(actions, actions + m);
+  if (ds.kind == 2)
+    for (double& u : a) u = u < -1.0 ? -1.0 : (u > 1.0 ? 1.0 : u);  // TrackSteeringDriver.command clip
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMemcpy(ctx->drive[slot].d_action, a.data(), sizeof(double) * 2 * E, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ds.d_action, a.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
+  return GG_OK;
+}
+
+int gg_drive_chain_state(gg_ctx* ctx, int32_t slot, double* q) {
+  if (!ctx || !q) return GG_EINVAL;
+  if (slot < 0 || slot >= static_cast<int>(ctx->drive.size()) || ctx->drive[slot].kind != 3)
+    return fail(ctx, GG_EINVAL, "no chain driver on this body slot");
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  const gg_ctx::DriveSlot& ds = ctx->drive[slot];
+  CK(cudaMemcpy(q, ds.d_state, sizeof(double) * ctx->E * ds.C.J, cudaMemcpyDeviceToHost));
   return GG_OK;
 }
 

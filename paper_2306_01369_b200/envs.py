@@ -226,8 +226,6 @@ class BatchedBulldozerEnv:
         if not np.all(np.isfinite(a)):
             raise ValueError("action must be finite")
         self.driver.command(a)
-        if self.device_drivers:
-            self.batch.drive_command()
         reps, _ = self.batch.run_raw(self.config.frame_skip, last_only=True)
         rew, ins = self.goal_stats()
         self._steps += 1
@@ -316,6 +314,8 @@ class BatchedExcavationEnv:
             self.batch.close()
         self.batch = SceneBatch(scenes, body_drivers={0: StaticBatch(E), 1: self.chain},
                                 device=self.device)
+        # the ground and the arm's forward kinematics run on the device
+        self.device_drivers = self.batch.drive_on_device()
         self._steps = 0
         return self._observe()
 
@@ -339,7 +339,7 @@ class BatchedExcavationEnv:
         if not np.all(np.isfinite(a)):
             raise ValueError("action must be finite")
         self.chain.command(np.clip(a, -1.0, 1.0) * self.chain.limits)
-        reps, _ = self.batch.run_raw(self.frame_skip)
+        reps, _ = self.batch.run_raw(self.frame_skip, last_only=True)
         self._steps += 1
         done = np.full(self.n_envs, self._steps >= self.episode_length)
         info = {"n_contacts": reps[-1]["n_contacts"].copy(), "t": self.batch.t.copy()}

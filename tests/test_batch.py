@@ -412,3 +412,39 @@ def test_closed_form_body_aabb_matches_corners():
     assert np.abs(col["aabb_lo"] - world.min(axis=2)).max() <= 1e-14
     assert np.abs(col["aabb_hi"] - world.max(axis=2)).max() <= 1e-14
     assert (col["bounded"] == 1).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_kind", ["bulldozer", "excavation"])
+def test_device_drivers_match_host_tables(env_kind):
+    """The device-resident drivers (gg_drive_track / gg_drive_chain) pose the
+    bodies like the host batch drivers: the same batch run once with host
+    body tables and once with device-generated rows gives the same state
+    (to the last bits of sin/cos), and the drivers' states agree."""
+    from paper_2306_01369_b200.envs import BatchedBulldozerEnv, BatchedExcavationEnv
+
+    E = 6
+    outs = []
+    for device in (False, True):
+        env = BatchedBulldozerEnv(E, render=False) if env_kind == "bulldozer" else BatchedExcavationEnv(E)
+        env.reset(np.arange(E))
+        if not device:
+            env.batch.driven = None
+            env.device_drivers = False
+        rng = np.random.default_rng(1)
+        for _ in range(3):
+            a = rng.uniform(-1, 1, (E, 2 if env_kind == "bulldozer" else 7))
+            if env_kind == "bulldozer":
+                env.driver.command(a)
+            else:
+                env.chain.command(np.clip(a, -1, 1) * env.chain.limits)
+            env.batch.run_raw(10)
+        x, v = env.batch.state()
+        drv = env.driver if env_kind == "bulldozer" else env.chain
+        st = np.stack([drv.x, drv.y, drv.theta], 1) if env_kind == "bulldozer" else drv.q
+        outs.append((x, v, st))
+        env.close()
+    (x0, v0, s0), (x1, v1, s1) = outs
+    np.testing.assert_allclose(s1, s0, rtol=0, atol=1e-12)
+    for e in range(E):
+        assert rel_err(x1[e], x0[e]) <= TOL and rel_err(v1[e], v0[e]) <= 1e-3
