@@ -179,6 +179,25 @@ class SlabTransport:
             for buf, h, m in back:
                 buf[:m].copy_(h)
 
+    def reduce_packed(self, sums: np.ndarray, maxes: np.ndarray, mins: np.ndarray):
+        """The StepReport reduction in ONE collective: every rank's packed
+        [sums | maxes | mins] float64 vector is all-gathered and reduced in
+        rank order (deterministic), instead of one all-reduce per operator."""
+        packed = np.concatenate([np.asarray(sums, np.float64).ravel(), np.asarray(maxes, np.float64).ravel(),
+                                 np.asarray(mins, np.float64).ravel()])
+        if self.world == 1:
+            rows = packed[None, :]
+        else:
+            torch = self.torch
+            dev = self.dev if self.on_device else torch.device("cpu")
+            t = torch.from_numpy(packed).to(dev)
+            out = torch.empty((self.world, len(packed)), dtype=torch.float64, device=dev)
+            with self._ctx():
+                self.dist.all_gather_into_tensor(out, t)
+            rows = out.cpu().numpy()
+        a, b = len(np.ravel(sums)), len(np.ravel(maxes))
+        return rows[:, :a].sum(axis=0), rows[:, a:a + b].max(axis=0), rows[:, a + b:].min(axis=0)
+
     def allreduce(self, vals: np.ndarray, op: str) -> np.ndarray:
         if self.world == 1:
             return vals
@@ -198,7 +217,7 @@ class SlabBed:
     def __init__(self, scene, rank: int = 0, world: int = 1, device: int = 0,
                  backend: str | None = None, cuts: np.ndarray | None = None,
                  capacity: float = 1.6, max_contacts: int = 16, resort_every: int = 8,
-                 halo: str = "host"):
+                 halo: str = "auto"):
         from .engine import Engine
 
         self.scene = scene
@@ -233,8 +252,10 @@ class SlabBed:
         self.tr = SlabTransport(rank, world, device, lib.gg_stream(self.ctx), backend)
         self.buf_cap = max(4096, self.cap // 2)
         self._alloc()
-        if halo not in ("host", "p2p"):
-            raise ValueError("halo must be 'host' or 'p2p'")
+        if halo not in ("auto", "host", "p2p"):
+            raise ValueError("halo must be 'auto', 'host' or 'p2p'")
+        if halo == "auto":  # peer memory whenever the ranks run NCCL on one node's GPUs
+            halo = "p2p" if self.tr.backend == "nccl" else "host"
         self.halo = halo if world > 1 else "host"
         self.seq = 0
         if self.halo == "p2p":
@@ -337,13 +358,11 @@ class SlabBed:
         return self._reduce(rep[0], bm[: self.nb])
 
     def _reduce(self, r, bm) -> StepReport:
-        tr = self.tr
-        s = tr.allreduce(np.array([r["n_contacts"], r["n_candidates"], r["n_body_contacts"],
-                                   r["n_coincident"], r["n_degenerate"], r["kinetic_energy"]],
-                                  dtype=np.float64), "sum")
-        mx = tr.allreduce(np.array([r["max_penetration"], r["max_cone_violation"]]), "max")
-        mn = tr.allreduce(np.array([r["min_normal_impulse"]]), "min")
-        bms = tr.allreduce(np.asarray(bm, dtype=np.float64).reshape(-1), "sum").reshape(-1, 3)
+        sums = np.concatenate([[r["n_contacts"], r["n_candidates"], r["n_body_contacts"], r["n_coincident"],
+                                r["n_degenerate"], r["kinetic_energy"]], np.asarray(bm, np.float64).ravel()])
+        s, mx, mn = self.tr.reduce_packed(sums, [r["max_penetration"], r["max_cone_violation"]],
+                                          [r["min_normal_impulse"]])
+        bms = s[6:].reshape(-1, 3)
         n_pp, n_cand = int(s[0]), int(s[1])
         m = float(mn[0])
         return StepReport(n_contacts=n_pp, n_candidates=n_cand,

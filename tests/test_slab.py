@@ -93,7 +93,8 @@ def _transport_worker(rank, world, port, out):
     r_hi = torch.zeros((8, REC_FLOATS))
     tr.exchange(s_lo, n_lo, s_hi, n_hi, r_lo, m_lo, r_hi, m_hi)
     red = tr.allreduce(np.array([rank, 1.0]), "sum")
-    out[rank] = (m_lo, m_hi, r_lo[:m_lo].numpy().copy(), r_hi[:m_hi].numpy().copy(), red)
+    packed = tr.reduce_packed([rank, 1.0], [float(rank)], [float(rank) + 3.0])
+    out[rank] = (m_lo, m_hi, r_lo[:m_lo].numpy().copy(), r_hi[:m_hi].numpy().copy(), red, packed)
     td.destroy_process_group()
 
 
@@ -104,7 +105,7 @@ def test_transport_gloo_neighbour_exchange(world):
     out = mgr.dict()
     mp.spawn(_transport_worker, args=(world, _port(), out), nprocs=world, join=True)
     for r in range(world):
-        m_lo, m_hi, r_lo, r_hi, red = out[r]
+        m_lo, m_hi, r_lo, r_hi, red, packed = out[r]
         if r > 0:  # from my lo neighbour: what it sent to ITS hi
             assert m_lo == (r - 1) + 2 and np.all(r_lo == (r - 1) + 0.5)
         else:
@@ -114,6 +115,8 @@ def test_transport_gloo_neighbour_exchange(world):
         else:
             assert m_hi == 0
         assert red[0] == sum(range(world)) and red[1] == world
+        s_, mx, mn = packed  # one all_gather: sums, maxes, mins
+        assert list(s_) == [sum(range(world)), world] and mx[0] == world - 1 and mn[0] == 3.0
 
 
 # ---------------------------------------------------------------------------
