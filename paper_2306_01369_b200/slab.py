@@ -191,10 +191,10 @@ class SlabTransport:
             torch = self.torch
             dev = self.dev if self.on_device else torch.device("cpu")
             t = torch.from_numpy(packed).to(dev)
-            out = torch.empty((self.world, len(packed)), dtype=torch.float64, device=dev)
+            out = [torch.empty(len(packed), dtype=torch.float64, device=dev) for _ in range(self.world)]
             with self._ctx():
-                self.dist.all_gather_into_tensor(out, t)
-            rows = out.cpu().numpy()
+                self.dist.all_gather(out, t)
+            rows = torch.stack(out).cpu().numpy()
         a, b = len(np.ravel(sums)), len(np.ravel(maxes))
         return rows[:, :a].sum(axis=0), rows[:, a:a + b].max(axis=0), rows[:, a + b:].min(axis=0)
 
