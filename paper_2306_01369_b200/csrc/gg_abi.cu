@@ -1131,6 +1131,9 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
   ctx->tap_uncommitted = true;
   CK(cudaMemcpy(ctx->h_ctl, D.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   if (ctx->h_ctl->err == GG_EPOSITIONS) return fail(ctx, GG_EPOSITIONS, "positions must be finite");
+  if (ctx->h_ctl->err == GG_EBUCKET)
+    return fail(ctx, GG_EINVAL, "hash table too small: the neighbour buckets of a particle hold more "
+                                "than 27 x 65534 particles (raise hashmap_size)");
   if (ctx->h_ctl->err == GG_ECAPACITY) {
     char buf[160];
     std::snprintf(buf, sizeof(buf), "contact capacity exceeded: an owner has %d contacts > %d slots",
@@ -1309,6 +1312,10 @@ int gg_sync(gg_ctx* ctx, gg_report* reports, double* body_momentum, int32_t cap,
                     "contact capacity exceeded: an owner has %d contacts > %d slots",
                     c.cap_needed, ctx->K);
       return fail(ctx, GG_ECAPACITY, buf);
+    case GG_EBUCKET:
+      return fail(ctx, GG_EINVAL,
+                  "hash table too small: the neighbour buckets of a particle hold more than "
+                  "27 x 65534 particles (raise hashmap_size)");
     default:
       return fail(ctx, c.err, "device error");
   }

@@ -40,6 +40,7 @@
 namespace gg {
 
 constexpr int kBlock = 256;
+constexpr int GG_EBUCKET = 6;  // device-internal: a bucket too long for the contact kernel's lists
 constexpr int kScanTile = 2048;  // elements per scan tile (256 thr x 8)
 constexpr int kMaxBad = 32;
 constexpr int kMaxFusedBlocks = 1024;  // neighbour-flag sweeps: block-set bitmask size
@@ -662,11 +663,22 @@ constexpr int kPassCap = GG_PASSCAP;  // prefilter passes queued per owner (more
 constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass that is no contact)
 constexpr int kWarps = kBlock / 32;
 
+#ifndef GG_LEN32
+#define GG_LEN32 0
+#endif
+#if GG_LEN32
+using NarrowLen = uint32_t;  // any bucket size (a tiny table may put every particle in one bucket)
+constexpr uint32_t kLenSentinel = 0xffffffffu;
+#else
+using NarrowLen = uint16_t;
+constexpr uint32_t kLenSentinel = 0xffffu;
+#endif
+
 template <int B>
 struct NarrowSmemT {
   static constexpr int kW = B / 32;
   uint32_t beg[28][B];        // compacted non-empty buckets + a sentinel
-  uint32_t len[28][B];        // bucket sizes (any n: a bucket may hold every particle)
+  NarrowLen len[28][B];       // bucket sizes
   uint32_t pass[kPassCap][B]; // Xh index of every prefilter pass, per owner, in order
   float4 pos[B];              // owner positions
   uint32_t off[kW][32];       // per-warp exclusive offsets of the owners' queue segments
@@ -909,6 +921,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       }
     }
     int nb = 0;
+    bool big = false;
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
       uint32_t hb[9], sb[9], eb[9];
@@ -922,10 +935,37 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       for (int j = 0; j < 9; ++j) {
         const bool keep = eb[j] > sb[j] && !((dupmask >> (g * 9 + j)) & 1u);
         if (keep) {
+          const uint32_t L = eb[j] - sb[j];
+          total += L;
+          big |= L >= kLenSentinel;
           sm.beg[nb][tid] = sb[j];
-          sm.len[nb][tid] = eb[j] - sb[j];
-          total += eb[j] - sb[j];
+          sm.len[nb][tid] = static_cast<NarrowLen>(L);
           ++nb;
+        }
+      }
+    }
+    if (big) {
+      // a bucket longer than the 16-bit list lengths (a tiny table with very
+      // many particles per bucket): rebuild the list with such buckets as
+      // consecutive entries of at most kLenSentinel - 1 (candidate order
+      // unchanged); more entries than the list holds is refused, never truncated
+      nb = 0;
+      for (int o = 0; o < 27; ++o) {
+        if ((dupmask >> o) & 1u) continue;
+        const uint32_t h = nb_hash(D, o, c0, c1, c2, tx, ty, tz);
+        uint32_t s0 = start[h];
+        for (uint32_t left = start[h + 1] - s0; left > 0;) {
+          const uint32_t c = left < kLenSentinel - 1 ? left : kLenSentinel - 1;
+          if (nb >= 27) {
+            raise_err(ctl, GG_EBUCKET);
+            left = 0;
+            break;
+          }
+          sm.beg[nb][tid] = s0;
+          sm.len[nb][tid] = static_cast<NarrowLen>(c);
+          ++nb;
+          s0 += c;
+          left -= c;
         }
       }
     }
@@ -934,7 +974,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     // candidates past the end without a guard (indices < n + kXhPad: Xh is
     // padded; never tested)
     sm.beg[nb][tid] = sm.beg[0][tid];
-    sm.len[nb][tid] = 0xffffffffu;
+    sm.len[nb][tid] = static_cast<NarrowLen>(kLenSentinel);
     const bool all = D.pipeline == 1;
     const float rej = D.reject_d2f;
     CandCursor cur;
