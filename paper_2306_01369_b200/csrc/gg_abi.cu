@@ -356,6 +356,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
         k_sweep<<<sweep_grid(ctx->n), kSweepBlock, 0, s>>>(D, it);
     }
     k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
+    k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ctx->n));
     if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
     CK(cudaGetLastError());
     return GG_OK;
@@ -442,7 +443,7 @@ bool use_staged_solve(const gg_ctx* ctx);
 
 int kernels_per_step(const gg_ctx* ctx, int resort) {
   if (use_fused_step(ctx)) return use_cluster_solve(ctx) ? 2 : 1;
-  const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 1;
+  const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 2;
   const int env_reports = (ctx->E > 1 && !use_persistent_solve(ctx)) ? 1 : 0;
   return 7 + solve + env_reports + (resort ? 6 : 0);
 }
@@ -528,6 +529,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     Dev Df = D;
     Df.env_kernel = ctx->E > 1 ? 1 : 0;
     k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(Df);
+    k_commit<<<1, kBlock, 0, s>>>(Df, finish_grid(ctx->n));
     if (Df.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(Df);
     mark(13);
   }
@@ -2397,7 +2399,8 @@ int gg_slab_finish(gg_ctx* ctx, gg_report* report, double* body_momentum) {
   DeviceGuard guard(ctx->device);
   cudaStream_t s = ctx->stream;
   k_finish<<<finish_grid(std::max<long long>(ctx->n_own, 1)), kFinishBlock, 0, s>>>(slab_dev(ctx));
-  ctx->launches += 1;
+  k_commit<<<1, kBlock, 0, s>>>(slab_dev(ctx), finish_grid(std::max<long long>(ctx->n_own, 1)));
+  ctx->launches += 2;
   CK(cudaGetLastError());
   int32_t nd = 0, es = -1;
   st = gg_sync(ctx, report, body_momentum, 1, &nd, &es);

@@ -1615,8 +1615,11 @@ __device__ __forceinline__ void write_report(const Dev& D, gg_report& R, const A
 // every block.
 // This thread integrates particles kb, kb + step, ... < ke (its particles
 // of the last sweep: another thread's w is not ordered before this read).
-__device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ctl, int kb, int kend,
-                                                           int kstep, double* smd, int* s_last) {
+// Symplectic Euler of this thread's particles kb, kb + kstep, ... < kend and
+// the block's kinetic-energy partial in D.part[blockIdx.x] (E == 1; E > 1
+// adds to the per-env fixed-point sums).  Called by every thread.
+__device__ __forceinline__ void integrate_range(const Dev& D, Ctl* ctl, int kb, int kend, int kstep,
+                                                double* smd) {
   const int cur = ctl->cur;
   const int step = ctl->step;
   const Layout L = layout(D, ctl);
@@ -1669,18 +1672,19 @@ __device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ct
     r = block_reduce<0>(ke, smd);
   else
     env_add_arr(D, kenv, kef, D.ke_fix);
-  if (threadIdx.x == 0) {
-    D.part[blockIdx.x] = r;
-    __threadfence();
-    *s_last = atomicAdd(&ctl->done_count, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!*s_last) return;
-  __threadfence();
+  if (threadIdx.x == 0) D.part[blockIdx.x] = r;
+}
+
+// The step's StepReport(s), body momenta and commit, by ONE block after all
+// integration blocks (nparts partials in D.part) are done: fixed-order
+// kinetic-energy sum, reports, reset of the per-step words, state flip.
+__device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, double* smd) {
+  const int cur = ctl->cur;
+  const int step = ctl->step;
   double ke_tot = 0.0;
   if (D.E == 1) {
     double v0 = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v0 += *((volatile double*)&D.part[b]);
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v0 += *((volatile double*)&D.part[b]);
     ke_tot = block_reduce<0>(v0, smd);
   }
   __shared__ int s_err;
@@ -1692,9 +1696,9 @@ __device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ct
     if (!s_err) D.bm_out[static_cast<long long>(step) * nbm + i] = static_cast<double>(f) / kMomScale;
     D.bm_fix[i] = 0ull;
   }
-  // every other block has finished (it incremented done_count last), so the
-  // barrier words and sweep flags can be reset here for the next launch
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+  // the barrier words and sweep flags of a persistent launch are reset here
+  // for the next one (every other block of it has finished)
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x)
     if (D.bflags) D.bflags[b] = 0u;
   if (D.E > 1 && !s_err && !D.env_kernel) {
     for (int e = threadIdx.x; e < D.E; e += blockDim.x) {
@@ -1719,6 +1723,22 @@ __device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ct
     if (D.resort) ctl->ucur ^= 1;
     ctl->step = step + 1;
   }
+}
+
+// Persistent kernels: integrate, then the last block to finish commits.
+// This thread integrates particles kb, kb + kstep, ... < kend (its particles
+// of the last sweep: another thread's w is not ordered before this read).
+__device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ctl, int kb, int kend,
+                                                           int kstep, double* smd, int* s_last) {
+  integrate_range(D, ctl, kb, kend, kstep, smd);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *s_last = atomicAdd(&ctl->done_count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();
+  commit_step(D, ctl, gridDim.x, smd);
 }
 
 __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int t0, int G,
@@ -1853,13 +1873,19 @@ __global__ void __launch_bounds__(kBlock) k_sweep_oneloop(Dev D, int s) {
   sweep_acc_flush(D, A, smd);
 }
 
+// Large-n integration: a pure stream (x, v, cinfo, w in; x, v out), one
+// particle per thread, a kinetic-energy partial per block; k_commit (one
+// block) then sums the partials in fixed order and commits the step.
 __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
   __shared__ double smd[32];
-  __shared__ int s_last;
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  integrate_and_finish(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, smd,
-                       &s_last);
+  integrate_range(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, D.n_own, gridDim.x * blockDim.x, smd);
+}
+
+__global__ void __launch_bounds__(kBlock) k_commit(Dev D, int nparts) {
+  __shared__ double smd[32];
+  commit_step(D, D.ctl, nparts, smd);
 }
 
 // ===========================================================================
