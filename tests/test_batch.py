@@ -265,6 +265,9 @@ def test_large_batch_sampled_envs_match_singles():
     E, T = 256, 80  # the bed reaches the floor after ~60 substeps
     env = BatchedBulldozerEnv(E, cfg)
     env.reset(np.arange(E))
+    # host-posed blades (the replayed singles get the same poses bit for bit;
+    # the device drivers' sin/cos may differ in the last bit, tested apart)
+    env.batch.driven = None
     acts = np.random.default_rng(0).uniform(-1, 1, size=(E, 2))
     env.driver.command(acts)
     twin = TrackSteeringBatch(np.full(E, -2.0), np.zeros(E), np.zeros(E), z=0.0,
