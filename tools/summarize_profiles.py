@@ -17,11 +17,11 @@ def line(name):
 
 
 rows = []
-for w in ("hero50k", "bed1m", "envs", "slab"):
+for w in ("bed1m", "bed1m_mode8", "hero50k", "envs", "slab"):
     z = line(w)
     if not z:
         continue
-    r, c = z.get("roofline") or {}, z.get("config") or {}
+    r, c = z.get("roofline") or {}, {**(z.get("config") or {}), **(z.get("run") or {})}
     cb = z.get("cpu_baseline") or {}
     rows.append(f"| {w} | {z['value']:.3e} | {z['ms_per_step']:.4f} | {z['e2e']['value']:.3e} | "
                 f"{r.get('kernel')} | {r.get('frac', 0):.3f} | "
@@ -29,11 +29,11 @@ for w in ("hero50k", "bed1m", "envs", "slab"):
                 f"{cb.get('value', float('nan')):.3g} | {c.get('c_pp', 0):.2f} | {c.get('c_b', 0):.3f} | "
                 f"{c.get('l2', '-')} |")
 ref = line("reference")
-clk = (line("hero50k") or {}).get("clocks", {})
-out = [f"# Round 1 profiles (1x B200, sm_100a, SM clock {clk.get('sm_mhz')} MHz of "
+clk = (line("bed1m") or line("hero50k") or {}).get("clocks", {})
+out = [f"# {d.name} profiles (1x B200, sm_100a, SM clock {clk.get('sm_mhz')} MHz of "
        f"{clk.get('sm_max_mhz')}, throttle reasons {clk.get('reasons')})", "",
-       "Bench lines: `bench_<workload>.json` (`python bench.py --workload <w>`; hero50k is the default "
-       "run: 2000 steps; bed1m: 500 steps after 50 warm-up steps from the GPU-settled bed).",
+       "Bench lines: `bench_<workload>.json` (`python bench.py --workload <w>`; bed1m is the default "
+       "workload (tools/gpu_round2.sh has the exact commands)).",
        "Launch lists: `launches_<workload>.csv` (ncu `gpu__time_duration.sum --clock-control none`, "
        "cold cache, serialised), summarised in `launches_summary.txt`.",
        "Full-set ncu captures of the top kernels: `ncu_full_summary.txt` (per kernel: duration, DRAM "
@@ -47,10 +47,12 @@ out = [f"# Round 1 profiles (1x B200, sm_100a, SM clock {clk.get('sm_mhz')} MHz 
        "|---|---|---|---|---|---|---|---|---|---|---|", *rows, ""]
 if ref:
     out.append(f"Reference arm (`bench.py --impl reference`, oracle port, "
-               f"{ref['cpu_baseline']['cores']} core): {ref['value']:.3e} particle-steps/s on hero50k.")
+               f"{ref['cpu_baseline']['cores']} core, {ref['cpu_baseline'].get('host_cores')} host cores): "
+               f"{ref['value']:.3e} particle-steps/s on {ref['config']['workload']} "
+               f"({ref['cpu_baseline']['sample']}).")
 # where the time goes: kernel shares of each workload's step (bench roofline pass)
 out += ["", "## Kernel time shares (device, per step)", ""]
-for w in ("hero50k", "bed1m", "envs"):
+for w in ("bed1m", "bed1m_mode8", "hero50k", "envs"):
     z = line(w)
     if not z:
         continue
