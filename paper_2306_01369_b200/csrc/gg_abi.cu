@@ -71,6 +71,7 @@ struct gg_ctx {
   int pipeline = 0;        // PipelineMode of the captured graphs (GG_MODE_*)
   int fused_grid = 0;      // co-resident blocks of k_step_fused
   int staged_grid = 0;     // co-resident blocks of k_solve_staged (one per SM)
+  int nflags = 1;          // length of D.bflags
   size_t staged_smem = 0;  // its dynamic shared memory per block
   bool cluster_ok = false; // a 16-CTA cluster of k_solve_cluster can be resident
   long long since_resort = 1 << 30;  // force a re-sort after upload
@@ -151,6 +152,14 @@ int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock)
 #endif
 constexpr int kSweepBlock = GG_SWEEP_BLOCK;  // k_sweep block size (<= kBlock)
 int sweep_grid(long long n) { return static_cast<int>((n + kSweepBlock - 1) / kSweepBlock); }
+// one per-particle sweep launch over particles [0, n): record-major by default
+void launch_sweep(const Dev& D, int it, long long n, cudaStream_t s) {
+#if GG_SWEEP_RM
+  k_sweep_rm<<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+#else
+  k_sweep<<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+#endif
+}
 #ifndef GG_FINISH_BLOCK
 #define GG_FINISH_BLOCK 256
 #endif
@@ -267,7 +276,7 @@ int ensure_batch(gg_ctx* ctx, int steps, int nb) {
 int begin_batch(gg_ctx* ctx, cudaStream_t s) {
   CK(cudaMemsetAsync(ctx->D.cnt, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->D.nh_tot), s));  // every env's table
   CK(cudaMemsetAsync(ctx->D.tile, 0, sizeof(uint32_t) * static_cast<size_t>(ctx->ntiles), s));
-  CK(cudaMemsetAsync(ctx->D.bflags, 0, sizeof(unsigned) * std::max(ctx->fused_grid, 1), s));
+  CK(cudaMemsetAsync(ctx->D.bflags, 0, sizeof(unsigned) * ctx->nflags, s));
   const long long work = std::max<long long>(ctx->E, static_cast<long long>(ctx->E) * std::max(ctx->max_bodies, 1) * 3);
   k_batch_begin<<<static_cast<int>(std::min<long long>(148, (work + 255) / 256)), 256, 0, s>>>(ctx->D);
   CK(cudaGetLastError());
@@ -353,7 +362,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
       if (D.pipeline == GG_MODE_ONE_LOOP)
         k_sweep_oneloop<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
       else
-        k_sweep<<<sweep_grid(ctx->n), kSweepBlock, 0, s>>>(D, it);
+        launch_sweep(D, it, ctx->n, s);
     }
     k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
     k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ctx->n));
@@ -523,7 +532,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
       if (D.pipeline == GG_MODE_ONE_LOOP)
         k_sweep_oneloop<<<nbn, kBlock, 0, s>>>(D, it);
       else
-        k_sweep<<<sweep_grid(ctx->n), kSweepBlock, 0, s>>>(D, it);
+        launch_sweep(D, it, ctx->n, s);
       mark(12);
     }
     Dev Df = D;
@@ -823,7 +832,10 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   // (values never tested); zeroed so every read is of initialised memory
   CK(dalloc(ctx, &D.Xh, n + kXhPad));
   CK(cudaMemset(D.Xh, 0, sizeof(float4) * (n + kXhPad)));
-  CK(dalloc(ctx, &D.bflags, static_cast<size_t>(std::max(ctx->fused_grid, 1))));
+  // one flag per block of any persistent launch (the commit of each resets
+  // its grid's flags)
+  ctx->nflags = std::max({ctx->fused_grid, ctx->solve_grid, ctx->staged_grid, kClusterCTAs, 1});
+  CK(dalloc(ctx, &D.bflags, static_cast<size_t>(ctx->nflags)));
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks,
                                                           finish_grid(n), kClusterCTAs,
                                                           ctx->staged_grid}))));
@@ -2348,7 +2360,7 @@ int gg_slab_sweep(gg_ctx* ctx, int32_t sweep) {
   if (sweep < 0 || sweep >= ctx->D.S) return fail(ctx, GG_EINVAL, "sweep index out of range");
   DeviceGuard guard(ctx->device);
   if (ctx->n_own > 0)
-    k_sweep<<<sweep_grid(ctx->n_own), kSweepBlock, 0, ctx->stream>>>(slab_dev(ctx), sweep);
+    launch_sweep(slab_dev(ctx), sweep, ctx->n_own, ctx->stream);
   ctx->launches += 1;
   CK(cudaGetLastError());
   return GG_OK;

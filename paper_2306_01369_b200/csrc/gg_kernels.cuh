@@ -1678,7 +1678,10 @@ __device__ __forceinline__ void integrate_range(const Dev& D, Ctl* ctl, int kb, 
 // The step's StepReport(s), body momenta and commit, by ONE block after all
 // integration blocks (nparts partials in D.part) are done: fixed-order
 // kinetic-energy sum, reports, reset of the per-step words, state flip.
-__device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, double* smd) {
+// nflags: sweep flags of the persistent launch to reset (its grid size; 0
+// after the per-sweep kernels, whose k_finish grid is larger than bflags).
+__device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, double* smd,
+                                            int nflags) {
   const int cur = ctl->cur;
   const int step = ctl->step;
   double ke_tot = 0.0;
@@ -1698,7 +1701,7 @@ __device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, 
   }
   // the barrier words and sweep flags of a persistent launch are reset here
   // for the next one (every other block of it has finished)
-  for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+  for (int b = threadIdx.x; b < nflags; b += blockDim.x)
     if (D.bflags) D.bflags[b] = 0u;
   if (D.E > 1 && !s_err && !D.env_kernel) {
     for (int e = threadIdx.x; e < D.E; e += blockDim.x) {
@@ -1738,7 +1741,7 @@ __device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ct
   __syncthreads();
   if (!*s_last) return;
   __threadfence();
-  commit_step(D, ctl, gridDim.x, smd);
+  commit_step(D, ctl, gridDim.x, smd, gridDim.x);
 }
 
 __device__ __forceinline__ void integrate_and_finish(const Dev& D, Ctl* ctl, int t0, int G,
@@ -1847,6 +1850,123 @@ __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
   sweep_acc_flush_nobar(D, A);
 }
 
+// Record-major sweep (the large-n default).  A warp sweeps the 32 particles
+// whose records the contact kernel allocated as one warp-contiguous block:
+// record 0 of each particle sits at its fixed index, records 1.. of all 32
+// owners are laid end to end in lane order from the warp base (= lane 0's CSR
+// offset).  The warp walks those CSR records 32 at a time, ONE RECORD PER LANE
+// (a particle with six contacts no longer keeps 31 lanes idle), the owner of
+// record r found by a 5-step shuffle search over the lanes' inclusive record
+// counts, and the owner's w fetched by shuffle.  Each lane's impulse goes to
+// shared memory and the owner adds its records' impulses in record order —
+// the same float64 sums, in the same order, as sweep_particle_h, so every
+// schedule stays bitwise identical.  Latency: head -> {own w, partner 0, the
+// first chunk of records} -> partners of the chunk, whatever the counts (the
+// per-particle loop paid two dependent round trips per extra record).
+// Warps whose lanes belong to two envs take the per-particle path.
+#ifndef GG_SWEEP_BLOCK
+#define GG_SWEEP_BLOCK 64
+#endif
+#ifndef GG_SWEEP_RM
+#define GG_SWEEP_RM 1
+#endif
+constexpr int kSweepBlockK = GG_SWEEP_BLOCK;
+static_assert(kSweepBlockK % 32 == 0 && kSweepBlockK <= kBlock, "sweep block: whole warps");
+#ifndef GG_SWEEP_RM_MINB
+#define GG_SWEEP_RM_MINB 16
+#endif
+__global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev D, int s) {
+  static_assert(kFixedSlots == 1, "record-major sweep: one fixed record slot per particle");
+  __shared__ double s_imp[kSweepBlockK / 32][3][32];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const bool live = k < D.n_own;
+  SweepHead h;
+  h.ci = make_int2(0, 0);
+  if (live) h.load(D, k);
+  const Ctl* ctl = D.ctl;
+  if (*((volatile const int*)&ctl->err) != 0) return;  // uniform: nothing raises during sweeps
+  const float4* Win = (s == 0) ? layout(D, ctl).v : D.W[(s - 1) & 1];
+  float4* Wout = D.W[s & 1];
+  SweepAcc A;
+  sweep_acc_init_nobar(D, A, k);
+  int e0 = 0;
+  if (D.E > 1 && !warp_env_uniform(env_of(D, live ? k : D.n - 1), &e0)) {
+    if (live) sweep_particle_h(D, k, h, Win, Wout, A);
+    sweep_acc_flush_nobar(D, A);
+    return;
+  }
+  const int c = h.ci.y;
+  const uint32_t m = c > 1 ? static_cast<uint32_t>(c - 1) : 0u;  // this owner's CSR records
+  uint32_t incl = m;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);  // CSR records of the warp
+  const uint32_t excl = incl - m;
+  const long long wb = __shfl_sync(0xffffffffu, static_cast<long long>(h.ci.x), 0);
+  // requested together: own w, record 0's partner, the first chunk's records
+  float4 wf = make_float4(0.f, 0.f, 0.f, 0.f), q0 = wf;
+  const bool has0 = c > 0 && h.j[0] != kNullContact;
+  if (c > 0) wf = Win[k];
+  if (has0) q0 = (h.j[0] >= 0) ? Win[h.j[0]] : D.cvb[k];
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  int j = kNullContact;
+  if (static_cast<uint32_t>(lane) < T) {
+    g = D.cgeo[wb + lane];
+    j = D.coth[wb + lane];
+  }
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  if (has0) contact_impulse(D, wf.x, wf.y, wf.z, h.g[0], h.j[0], q0, ax, ay, az, A);
+  for (uint32_t cb = 0; cb < T; cb += 32) {
+    const uint32_t r = cb + lane;
+    const bool mine = r < T && j != kNullContact;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (mine) q = (j >= 0) ? Win[j] : D.cvb[wb + r];
+    // owner of record r: the first lane whose inclusive count exceeds r
+    int o = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, o + st - 1);
+      if (v <= r) o += st;
+    }
+    o = o < 31 ? o : 31;
+    const float owx = __shfl_sync(0xffffffffu, wf.x, o);
+    const float owy = __shfl_sync(0xffffffffu, wf.y, o);
+    const float owz = __shfl_sync(0xffffffffu, wf.z, o);
+    // the next chunk's records, requested before this chunk's arithmetic
+    const float4 gc = g;
+    const int jc = j;
+    if (cb + 32 + lane < T) {
+      g = D.cgeo[wb + cb + 32 + lane];
+      j = D.coth[wb + cb + 32 + lane];
+    }
+    double ix = 0.0, iy = 0.0, iz = 0.0;
+    if (mine) contact_impulse(D, owx, owy, owz, gc, jc, q, ix, iy, iz, A);
+    s_imp[wi][0][lane] = ix;
+    s_imp[wi][1][lane] = iy;
+    s_imp[wi][2][lane] = iz;
+    __syncwarp();
+    // the owner adds its records of this chunk in record order (a null
+    // record adds +0.0, which leaves a sum that started at +0.0 unchanged)
+    const uint32_t a0 = excl > cb ? excl : cb;
+    const uint32_t a1 = incl < cb + 32 ? incl : cb + 32;
+    for (uint32_t rr = a0; rr < a1; ++rr) {
+      ax += s_imp[wi][0][rr - cb];
+      ay += s_imp[wi][1][rr - cb];
+      az += s_imp[wi][2][rr - cb];
+    }
+    __syncwarp();
+  }
+  if (c > 0)
+    Wout[k] = make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
+                          static_cast<float>(static_cast<double>(wf.y) + ay),
+                          static_cast<float>(static_cast<double>(wf.z) + az), 0.f);
+  sweep_acc_flush_nobar(D, A);
+}
+
 // ONE_LOOP sweep (its own kernel: the inline collision test would cost the
 // record-reading sweep its registers)
 __global__ void __launch_bounds__(kBlock) k_sweep_oneloop(Dev D, int s) {
@@ -1885,7 +2005,7 @@ __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
 
 __global__ void __launch_bounds__(kBlock) k_commit(Dev D, int nparts) {
   __shared__ double smd[32];
-  commit_step(D, D.ctl, nparts, smd);
+  commit_step(D, D.ctl, nparts, smd, 0);
 }
 
 // ===========================================================================

@@ -261,6 +261,10 @@ def test_large_batch_sampled_envs_match_singles():
     """256 envs x 2000 particles (the config-3 env size) in one context:
     sampled envs' counters and states equal single-context runs fed the same
     blade poses."""
+    # a utility context first (as when the parity tests run before this one):
+    # it moves the batch's allocations, which exposed an out-of-bounds write
+    # of the per-sweep commit kernel into the neighbouring buffer
+    gg.spatial_hash(np.zeros((1, 3), np.int64), 64)
     cfg = BulldozerEnvConfig(n_particles=2000, radius=0.025)
     E, T = 256, 80  # the bed reaches the floor after ~60 substeps
     env = BatchedBulldozerEnv(E, cfg)
