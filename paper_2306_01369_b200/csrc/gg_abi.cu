@@ -217,10 +217,12 @@ int alloc_slots(gg_ctx* ctx, int K) {
   D.coth = nullptr;
   D.cvb = nullptr;
   // K records per particle on average: record 0 of particle k at index k,
-  // the block allocator hands out [n, K * n) (per-owner counts are not
-  // limited by K)
-  const size_t slots = static_cast<size_t>(std::max(K, kFixedSlots + 1)) *
-                       static_cast<size_t>(std::max<long long>(ctx->n, 1));
+  // then one region of 32 x (K - 1) records per warp of 32 particles (a
+  // warp's owners share it: per-owner counts are not limited by K)
+  K = std::max(K, kFixedSlots + 1);
+  const long long n1 = std::max<long long>(ctx->n, 1);
+  const long long wcap = 32ll * (K - kFixedSlots);
+  const size_t slots = static_cast<size_t>(kFixedSlots * n1 + ((n1 + 31) / 32) * wcap);
   CK(dalloc(ctx, &D.cgeo, slots));
   CK(dalloc(ctx, &D.coth, slots));
   CK(dalloc(ctx, &D.cvb, slots));
@@ -232,7 +234,8 @@ int alloc_slots(gg_ctx* ctx, int K) {
   ctx->K = K;
   D.K = K;
   D.cap_tot = static_cast<long long>(slots);
-  D.nrec0 = static_cast<long long>(kFixedSlots) * std::max<long long>(ctx->n, 1);
+  D.nrec0 = static_cast<long long>(kFixedSlots) * n1;
+  D.wcap = wcap;
   ctx->graph_dirty = true;
   return GG_OK;
 }
@@ -353,6 +356,11 @@ int env_report_blocks(const gg_ctx* ctx) {
   return static_cast<int>(std::min<long long>(4 * 148, (work + kBlock - 1) / kBlock));
 }
 
+// The contact kernel of a step over particles [0, nn)
+void launch_narrow(gg_ctx* ctx, const Dev& D, long long nn, cudaStream_t s) {
+  k_narrow<<<narrow_blocks(nn), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+}
+
 int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
   if (!use_persistent_solve(ctx)) {
     // one thread per particle: S sweep launches + integrate/report
@@ -440,7 +448,7 @@ int enqueue_step(gg_ctx* ctx, int resort) {
   const Dev D = pass_dev(ctx, resort, 0);
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
-  k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+  launch_narrow(ctx, D, ctx->n, s);
   CK(cudaGetLastError());
   return launch_solve(ctx, D, s);
 }
@@ -522,7 +530,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     }
   }
   const Dev D = pass_dev(ctx, resort, 0);
-  k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+  launch_narrow(ctx, D, ctx->n, s);
   mark(8);
   if (use_persistent_solve(ctx)) {
     if (launch_solve(ctx, D, s) != GG_OK) return -1;
@@ -735,6 +743,13 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
     while (p2 * 2 <= n_h) p2 *= 2;
     D.mmask = static_cast<uint32_t>(p2 - 1);
     D.mspan = static_cast<uint32_t>(p2);
+    int bits = 0;
+    while (bits < 10 && (1ll << (3 * (bits + 1))) <= p2) ++bits;
+    D.mbits = bits;
+    // until a state is uploaded: the window centred on the origin, wrapping
+    D.mlo[0] = D.mlo[1] = D.mlo[2] = -(1 << bits) / 2;
+    D.msh[0] = D.msh[1] = D.msh[2] = 0;
+    D.mclamp = 0;
   }
   fill_params(ctx);
   D.nb = 0;
@@ -943,6 +958,53 @@ static int ensure_stage(gg_ctx* ctx) {
   return GG_OK;
 }
 
+// The Morton window (Dev::mlo, msh) of a state with positions x (row stride
+// `stride` values, n rows): per axis the 0.05% .. 99.95% cell quantiles,
+// shifted right until they fit the key's bits per axis.  Only the physical
+// order (locality) depends on it, never a result.  Marks the graphs dirty
+// when it changes.
+void set_morton_window(gg_ctx* ctx, const float* xf, const double* xd, long long n, int stride) {
+  if (n <= 0) return;
+  const int bits = ctx->D.mbits;
+  const long long sample = std::min<long long>(n, 1 << 18);
+  const long long stepi = std::max<long long>(1, n / sample);
+  std::vector<long long> c;
+  c.reserve(static_cast<size_t>(sample) + 1);
+  int lo[3], sh[3];
+  for (int a = 0; a < 3; ++a) {
+    c.clear();
+    for (long long i = 0; i < n; i += stepi) {
+      const double q = (xf ? static_cast<double>(xf[i * stride + a]) : xd[i * stride + a]) / ctx->D.two_r;
+      if (!std::isfinite(q) || std::fabs(q) > 1e9) continue;
+      c.push_back(static_cast<long long>(std::copysign(std::floor(std::fabs(q) + 0.5), q)));
+    }
+    if (c.empty()) {
+      lo[a] = 0;
+      sh[a] = 0;
+      continue;
+    }
+    const size_t m = c.size();
+    const size_t klo = m / 2000, khi = m - 1 - m / 2000;
+    std::nth_element(c.begin(), c.begin() + klo, c.end());
+    const long long qlo = c[klo];
+    std::nth_element(c.begin(), c.begin() + khi, c.end());
+    const long long qhi = c[khi];
+    const long long ext = qhi - qlo + 3;  // + the halo cells either side
+    int s = 0;
+    while ((ext >> s) >= (1ll << bits) && s < 20) ++s;
+    lo[a] = static_cast<int>(qlo - 1);
+    sh[a] = s;
+  }
+  bool changed = ctx->D.mclamp != 1;
+  ctx->D.mclamp = 1;
+  for (int a = 0; a < 3; ++a) {
+    changed |= ctx->D.mlo[a] != lo[a] || ctx->D.msh[a] != sh[a];
+    ctx->D.mlo[a] = lo[a];
+    ctx->D.msh[a] = sh[a];
+  }
+  if (changed) ctx->graph_dirty = true;
+}
+
 int gg_set_state_f64(gg_ctx* ctx, const double* x, const double* v) {
   if (!ctx || !x || !v) return fail(ctx, GG_EINVAL, "null argument");
   DeviceGuard guard(ctx->device);
@@ -951,6 +1013,7 @@ int gg_set_state_f64(gg_ctx* ctx, const double* x, const double* v) {
   const size_t bytes = sizeof(double) * 3 * static_cast<size_t>(ctx->n);
   CK(cudaMemcpyAsync(ctx->d_stage, x, bytes, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_stage + 3 * ctx->n, v, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->slab_on) set_morton_window(ctx, nullptr, x, ctx->n, 3);
   ctx->since_resort = 1 << 30;
   k_load_f64<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, ctx->d_stage,
                                                         ctx->d_stage + 3 * ctx->n);
@@ -979,6 +1042,12 @@ int gg_get_state_f64(gg_ctx* ctx, double* x, double* v) {
 int gg_set_state_f32x4_dev(gg_ctx* ctx, const void* x4, const void* v4) {
   if (!ctx || !x4 || !v4) return fail(ctx, GG_EINVAL, "null argument");
   DeviceGuard guard(ctx->device);
+  if (!ctx->slab_on && ctx->n > 0) {
+    std::vector<float> hx(4 * static_cast<size_t>(ctx->n));
+    CK(cudaMemcpyAsync(hx.data(), x4, sizeof(float) * hx.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    set_morton_window(ctx, hx.data(), nullptr, ctx->n, 4);
+  }
   ctx->since_resort = 1 << 30;
   k_load_f4<<<ctx->nblocks, kBlock, 0, ctx->stream>>>(ctx->D, static_cast<const float4*>(x4),
                                                        static_cast<const float4*>(v4));
@@ -2345,7 +2414,7 @@ int gg_slab_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies) {
     st = enqueue_sort_pass(ctx, D, s);
     ctx->nblocks = nb_save;
     if (st != GG_OK) return st;
-    k_narrow<<<narrow_blocks(ctx->n_cur), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+    launch_narrow(ctx, D, ctx->n_cur, s);
   }
   ctx->launches += 9;
   ctx->last_batch = 1;

@@ -107,6 +107,14 @@ struct Dev {
   HashCfg H;         // the per-env table (n_h buckets)
   uint32_t mmask;  // Morton key mask (power of two <= n_h, minus one)
   uint32_t mspan;  // mmask + 1: Morton key range per env
+  // Morton window: the key of cell c is built from (c - mlo) >> msh per axis,
+  // so the bulk of the bed spans at most the key's bits per axis and the
+  // low-bit key does not wrap (wrapping interleaves cells 2^b apart and
+  // breaks the locality of the physical order).  Set by the host from the
+  // uploaded state; 0 / 0 = the plain low-bit key.
+  int mlo[3], msh[3];
+  int mbits;   // bits per axis of the curve key: 3 * mbits <= log2(mspan)
+  int mclamp;  // 1: cells outside the window clamp to its faces (else wrap)
   unsigned long long* ke_fix;  // [E] fixed-point sum |v|^2 (E > 1)
   double r, two_r, contact_d2, coinc_d2, mass, mu, alpha, dt, gamma, bias_coef;
   float reject_d2f;  // float32 pre-filter: d2_f32 > this  =>  d2 >= contact_d2 exactly
@@ -137,6 +145,7 @@ struct Dev {
   // CSR entries allocated from nrec0 = kFixedSlots * n on.  A sweep fetches a
   // particle's first contacts together with its cinfo instead of after it.
   long long nrec0;
+  long long wcap;  // CSR records per warp region (32 x (K - kFixedSlots))
   // k_solve_staged: particles per block and contact records staged in each
   // block's shared memory (the rest are read from global memory)
   int stage_pb, stage_cap;
@@ -413,6 +422,48 @@ __global__ void k_batch_begin(Dev D) {
 // handle one index; block phases (ph_scan_*, ph_contacts) contain
 // __syncthreads and must be called by every thread of the block.  The
 // standalone kernels and the fused small-n kernel are thin drivers.
+
+// Hilbert key of a cell (the physical-order key, R passes): consecutive keys
+// are always face-adjacent cells, so a block of consecutive particles fills
+// a compact region — the Morton curve's jumps across its tile boundaries put
+// a quarter of 256-particle blocks into boxes of thousands of cells.
+// Skilling's transpose form (AxestoTranspose), then the bits interleaved
+// axis 0 first.  Cells are taken relative to the window (Dev::mlo, msh).
+__device__ __forceinline__ uint32_t curve_key(const Dev& D, long long c0, long long c1, long long c2) {
+  const int b = D.mbits;
+  if (b <= 0) return 0u;
+  const long long top = (1ll << b) - 1;
+  long long q[3] = {(c0 - D.mlo[0]) >> D.msh[0], (c1 - D.mlo[1]) >> D.msh[1], (c2 - D.mlo[2]) >> D.msh[2]};
+  uint32_t X[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const long long v = D.mclamp ? (q[a] < 0 ? 0 : (q[a] > top ? top : q[a])) : (q[a] & top);
+    X[a] = static_cast<uint32_t>(v);
+  }
+  const uint32_t M = 1u << (b - 1);
+  for (uint32_t Q = M; Q > 1; Q >>= 1) {
+    const uint32_t P = Q - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (X[i] & Q) {
+        X[0] ^= P;
+      } else {
+        const uint32_t t = (X[0] ^ X[i]) & P;
+        X[0] ^= t;
+        X[i] ^= t;
+      }
+    }
+  }
+  X[1] ^= X[0];
+  X[2] ^= X[1];
+  uint32_t t = 0;
+  for (uint32_t Q = M; Q > 1; Q >>= 1)
+    if (X[2] & Q) t ^= Q - 1;
+  X[0] ^= t;
+  X[1] ^= t;
+  X[2] ^= t;
+  return (spread3(X[0]) << 2) | (spread3(X[1]) << 1) | spread3(X[2]);
+}
 // ===========================================================================
 
 // R1/H1: key + bucket occupancy.  R (Morton key) reads the committed state;
@@ -427,7 +478,7 @@ __device__ __forceinline__ void ph_count(const Dev& D, Ctl* ctl, int i, bool mor
   const long long c1 = cell_coord(p.y, D.two_r);
   const long long c2 = cell_coord(p.z, D.two_r);
   const uint32_t env = static_cast<uint32_t>(env_of(D, i));
-  const uint32_t h = morton ? env * D.mspan + morton_key(c0, c1, c2, D.mmask)
+  const uint32_t h = morton ? env * D.mspan + curve_key(D, c0, c1, c2)
                             : env * static_cast<uint32_t>(D.H.n_h) + hash_cell(c0, c1, c2, D.H);
   D.key[i] = h;
   D.arrive[i] = atomicAdd(&D.cnt[h], 1u);
@@ -683,7 +734,6 @@ struct NarrowSmemT {
   float4 pos[B];              // owner positions
   uint32_t off[kW][32];       // per-warp exclusive offsets of the owners' queue segments
   uint8_t qown[kW][32 * kPassCap];  // per-warp queue: owner lane of each entry
-  unsigned long long wrec[kW];      // per-warp record totals -> bases (block allocation)
   double d[32];
   unsigned long long u[32];
 };
@@ -726,8 +776,8 @@ struct CandCursor {
 // c_slots: records (= contacts, or every candidate in TWO_LOOPS_FUSED);
 // c_pp: contacts.
 template <class SM>
-__device__ __forceinline__ void scan_exact(const Dev& D, const SM& sm, int tid, int k,
-                                           float4 pf, uint32_t total, bool write, long long off,
+__device__ __forceinline__ void scan_exact(const Dev& D, const SM& sm, const float4* cand, int tid,
+                                           int k, float4 pf, uint32_t total, bool write, long long off,
                                            int& c_slots, int& c_pp, unsigned long long& n_coinc,
                                            double& max_psi) {
   const double px = pf.x, py = pf.y, pz = pf.z;
@@ -738,7 +788,7 @@ __device__ __forceinline__ void scan_exact(const Dev& D, const SM& sm, int tid, 
   n_coinc = 0;
   for (uint32_t i = 0; i < total; ++i) {
     const uint32_t mi = cur.next(sm, tid, i + 1 < total);
-    const float4 qf = D.Xh[mi];
+    const float4 qf = cand[mi];
     const int q = __float_as_int(qf.w);
     if (q == k) continue;
     const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
@@ -856,6 +906,127 @@ __device__ __forceinline__ void acc_contacts(const Dev& D, int env, unsigned lon
   }
 }
 
+// Phase B of the contact kernel (after a phase A filled sm.pass / the
+// candidate lists): warp-cooperative exact test of the queued prefilter
+// passes, body contacts, one record allocation per block, the records, the
+// counters.  `cand` is the array the queue and lists index (the
+// bucket-ordered copy Xh).  Called by every thread of the block.
+template <class SM>
+__device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base, SM& sm,
+                                                const float4* cand, bool live, int k, int env,
+                                                float4 pf, uint32_t total, uint32_t npass,
+                                                unsigned long long n_cand, unsigned long long n_coinc,
+                                                unsigned long long n_deg) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5, wb = w * 32;
+  sm.pos[tid] = pf;
+  // ---- phase B: warp-cooperative exact test, one pass --------------------------
+  // Every queued candidate (a prefilter pass) gets a record slot: its owner's
+  // offset + its index in the owner's queue, so slots are known before the
+  // exact test runs.  The rare pass that is not a contact (coincident, or
+  // inside the prefilter's 1e-5 margin) leaves a null record the sweeps skip.
+  const uint32_t np = npass < kPassCap ? npass : kPassCap;
+  const bool ovf = npass > kPassCap;
+  uint32_t incl = np;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t excl = incl - np;
+  const uint32_t Tw = __shfl_sync(0xffffffffu, incl, 31);
+  sm.off[w][lane] = excl;
+  for (uint32_t i = 0; i < np; ++i) sm.qown[w][excl + i] = static_cast<uint8_t>(lane);
+  int c_pp = 0;           // hits counted by this lane (queue entries it tested)
+  int c_own = np;         // record slots this owner needs for pp contacts
+  double max_psi = 0.0;
+  if (ovf) {  // more prefilter passes than the queue holds: exact inline count
+    int s_ex = 0, c_ex = 0;
+    unsigned long long co_ex = 0;
+    scan_exact(D, sm, cand, tid, k, pf, total, false, 0, s_ex, c_ex, co_ex, max_psi);
+    c_own = s_ex;
+  }
+  // this env's bodies at this step: bodies[step][env][nb]
+  const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
+  const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, k, 0, 0, n_deg, max_psi) : 0;
+  // ---- allocation: a fixed region per warp -----------------------------------
+  // (records 0 .. kFixedSlots-1 of each owner are its fixed slots; records
+  // kFixedSlots.. of the warp's 32 owners are laid end to end, in lane
+  // order, from nrec0 + warp * wcap — an address the sweeps know without
+  // reading anything, so they request a warp's records with its heads)
+  const int tot = c_own + c_b;
+  const int talloc = tot > kFixedSlots ? tot - kFixedSlots : 0;
+  int wincl = talloc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+    if (lane >= o) wincl += y;
+  }
+  const long long wbase = D.nrec0 + (static_cast<long long>(base + wb) >> 5) * D.wcap;
+  const long long my_off = wbase + (wincl - talloc);
+  const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
+  const bool fits = wtot <= D.wcap;
+  if (!fits && lane == 0) {
+    // slots per particle that would hold this warp's records
+    const long long need = (static_cast<long long>(wtot) + 31) / 32 + kFixedSlots + 1;
+    atomicMax(&ctl->cap_needed, static_cast<int>(need < (1 << 30) ? need : (1 << 30)));
+    raise_err(ctl, GG_ECAPACITY);
+  }
+  __syncwarp();  // sm.pos / off / qown / pass of the warp's lanes
+  const uint32_t* offw = sm.off[w];
+  if (fits) {
+    // pp records, cooperatively in queue order
+    const bool uni = (D.E == 1) || __all_sync(0xffffffffu, env == __shfl_sync(0xffffffffu, env, 0));
+    for (uint32_t r = 0; r * 32 < Tw; ++r) {
+      const uint32_t idx = r * 32 + lane;
+      const int o = idx < Tw ? sm.qown[w][idx] : 0;
+      const long long oo = __shfl_sync(0xffffffffu, my_off, o);
+      const bool oovf = __shfl_sync(0xffffffffu, ovf, o);
+      if (idx < Tw && !oovf) {
+        const uint32_t i = idx - offw[o];
+        const long long dst = ridx(D, base + wb + o, oo, static_cast<int>(i));
+        const float4 qf = cand[sm.pass[i][wb + o]];
+        const float4 of = sm.pos[wb + o];
+        double dx, dy, dz;
+        const double d2 = pp_d2(of.x, of.y, of.z, qf, dx, dy, dz);
+        const bool coi = !(d2 >= D.coinc_d2);
+        if (!coi && d2 < D.contact_d2) {
+          const double psi = pp_write(D, dst, dx, dy, dz, d2, __float_as_int(qf.w));
+          if (uni) {
+            max_psi = nmax(max_psi, psi);
+            ++c_pp;
+          } else {  // warp straddles two envs (rare): the owner's env directly
+            Acc* a = D.acc + env_of(D, base + wb + o);
+            if (psi > 0.0) atomicMax(&a->max_psi_bits, dbits(psi));
+            atomicAdd(&a->n_pp, 1ull);
+          }
+        } else {
+          D.coth[dst] = kNullContact;
+          if (coi) {
+            if (uni)
+              ++n_coinc;
+            else
+              atomicAdd(&D.acc[env_of(D, base + wb + o)].n_coinc, 1ull);
+          }
+        }
+      }
+    }
+    if (live) {
+      if (ovf) {
+        int s_ex = 0, c_ex = 0;
+        unsigned long long co_ex = 0;
+        scan_exact(D, sm, cand, tid, k, pf, total, true, my_off, s_ex, c_ex, co_ex, max_psi);
+        c_pp += c_ex;
+        n_coinc += co_ex;
+      }
+      if (c_b > 0) body_contacts(D, bodies, pf, true, k, my_off, c_own, n_deg, max_psi);
+      D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
+    }
+  }
+  acc_contacts(D, env, static_cast<unsigned long long>(c_pp), n_cand, n_coinc,
+               static_cast<unsigned long long>(c_b), n_deg, max_psi);
+}
+
 // K5+K6: all contacts of particles base .. base+blockDim (contact.py:244-300).
 //
 // Phase A (per thread): the 27 neighbour-bucket bounds (three batches of 9
@@ -874,13 +1045,11 @@ __device__ __forceinline__ void acc_contacts(const Dev& D, int env, unsigned lon
 template <class SM>
 __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, int count,
                                             SM& sm) {
-  constexpr int kWarps = SM::kW;
   // plain (coherent) loads: in the fused kernel these buffers are written
   // earlier in the same launch, so the read-only (.nc) path is not allowed
   const float4* LX = layout(D, ctl).x;
   const float4* Xh = D.Xh;
   const int tid = threadIdx.x;
-  const int lane = tid & 31, w = tid >> 5, wb = w * 32;
   const int k = base + tid;
   const bool live = tid < count && k < D.n_own;
   const int env = env_of(D, live ? k : D.n - 1);
@@ -1003,121 +1172,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       }
     }
   }
-  sm.pos[tid] = pf;
-  // ---- phase B: warp-cooperative exact test, one pass --------------------------
-  // Every queued candidate (a prefilter pass) gets a record slot: its owner's
-  // offset + its index in the owner's queue, so slots are known before the
-  // exact test runs.  The rare pass that is not a contact (coincident, or
-  // inside the prefilter's 1e-5 margin) leaves a null record the sweeps skip.
-  const uint32_t np = npass < kPassCap ? npass : kPassCap;
-  const bool ovf = npass > kPassCap;
-  uint32_t incl = np;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const uint32_t excl = incl - np;
-  const uint32_t Tw = __shfl_sync(0xffffffffu, incl, 31);
-  sm.off[w][lane] = excl;
-  for (uint32_t i = 0; i < np; ++i) sm.qown[w][excl + i] = static_cast<uint8_t>(lane);
-  int c_pp = 0;           // hits counted by this lane (queue entries it tested)
-  int c_own = np;         // record slots this owner needs for pp contacts
-  double max_psi = 0.0;
-  if (ovf) {  // more prefilter passes than the queue holds: exact inline count
-    int s_ex = 0, c_ex = 0;
-    unsigned long long co_ex = 0;
-    scan_exact(D, sm, tid, k, pf, total, false, 0, s_ex, c_ex, co_ex, max_psi);
-    c_own = s_ex;
-  }
-  // this env's bodies at this step: bodies[step][env][nb]
-  const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
-  const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, k, 0, 0, n_deg, max_psi) : 0;
-  // ---- allocation: one atomic per block ----------------------------------------
-  // (records 0 .. kFixedSlots-1 of each owner are its fixed slots; the rest
-  // come from the cursor)
-  const int tot = c_own + c_b;
-  const int talloc = tot > kFixedSlots ? tot - kFixedSlots : 0;
-  int wincl = talloc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, wincl, o);
-    if (lane >= o) wincl += y;
-  }
-  if (lane == 31) sm.wrec[w] = static_cast<unsigned long long>(wincl);
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long run = 0;
-    for (int q = 0; q < kWarps; ++q) {
-      const unsigned long long t = sm.wrec[q];
-      sm.wrec[q] = run;
-      run += t;
-    }
-    const unsigned long long b0 = run ? atomicAdd(&ctl->ccursor, run) : 0ull;
-    for (int q = 0; q < kWarps; ++q) sm.wrec[q] += b0;
-    if (static_cast<long long>(b0 + run) > D.cap_tot) {
-      const long long need = (static_cast<long long>(b0 + run) + D.n - 1) / D.n + 1;
-      atomicMax(&ctl->cap_needed, static_cast<int>(need < (1 << 30) ? need : (1 << 30)));
-      raise_err(ctl, GG_ECAPACITY);
-    }
-  }
-  __syncthreads();
-  const unsigned long long wbase = sm.wrec[w];
-  const long long my_off = static_cast<long long>(wbase) + (wincl - talloc);
-  const int wtot = __shfl_sync(0xffffffffu, wincl, 31);
-  const bool fits = static_cast<long long>(wbase) + wtot <= D.cap_tot;
-  const uint32_t* offw = sm.off[w];
-  if (fits) {
-    // pp records, cooperatively in queue order
-    const bool uni = (D.E == 1) || __all_sync(0xffffffffu, env == __shfl_sync(0xffffffffu, env, 0));
-    for (uint32_t r = 0; r * 32 < Tw; ++r) {
-      const uint32_t idx = r * 32 + lane;
-      const int o = idx < Tw ? sm.qown[w][idx] : 0;
-      const long long oo = __shfl_sync(0xffffffffu, my_off, o);
-      const bool oovf = __shfl_sync(0xffffffffu, ovf, o);
-      if (idx < Tw && !oovf) {
-        const uint32_t i = idx - offw[o];
-        const long long dst = ridx(D, base + wb + o, oo, static_cast<int>(i));
-        const float4 qf = Xh[sm.pass[i][wb + o]];
-        const float4 of = sm.pos[wb + o];
-        double dx, dy, dz;
-        const double d2 = pp_d2(of.x, of.y, of.z, qf, dx, dy, dz);
-        const bool coi = !(d2 >= D.coinc_d2);
-        if (!coi && d2 < D.contact_d2) {
-          const double psi = pp_write(D, dst, dx, dy, dz, d2, __float_as_int(qf.w));
-          if (uni) {
-            max_psi = nmax(max_psi, psi);
-            ++c_pp;
-          } else {  // warp straddles two envs (rare): the owner's env directly
-            Acc* a = D.acc + env_of(D, base + wb + o);
-            if (psi > 0.0) atomicMax(&a->max_psi_bits, dbits(psi));
-            atomicAdd(&a->n_pp, 1ull);
-          }
-        } else {
-          D.coth[dst] = kNullContact;
-          if (coi) {
-            if (uni)
-              ++n_coinc;
-            else
-              atomicAdd(&D.acc[env_of(D, base + wb + o)].n_coinc, 1ull);
-          }
-        }
-      }
-    }
-    if (live) {
-      if (ovf) {
-        int s_ex = 0, c_ex = 0;
-        unsigned long long co_ex = 0;
-        scan_exact(D, sm, tid, k, pf, total, true, my_off, s_ex, c_ex, co_ex, max_psi);
-        c_pp += c_ex;
-        n_coinc += co_ex;
-      }
-      if (c_b > 0) body_contacts(D, bodies, pf, true, k, my_off, c_own, n_deg, max_psi);
-      D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
-    }
-  }
-  acc_contacts(D, env, static_cast<unsigned long long>(c_pp), n_cand, n_coinc,
-               static_cast<unsigned long long>(c_b), n_deg, max_psi);
+  contacts_finish(D, ctl, base, sm, Xh, live, k, env, pf, total, npass, n_cand, n_coinc, n_deg);
 }
 
 // ---------------------------------------------------------------------------
@@ -1621,7 +1676,6 @@ __device__ __forceinline__ void write_report(const Dev& D, gg_report& R, const A
 __device__ __forceinline__ void integrate_range(const Dev& D, Ctl* ctl, int kb, int kend, int kstep,
                                                 double* smd) {
   const int cur = ctl->cur;
-  const int step = ctl->step;
   const Layout L = layout(D, ctl);
   const float4* Wf = D.W[(D.S - 1) & 1];
   double ke = 0.0;
@@ -1884,6 +1938,18 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
   SweepHead h;
   h.ci = make_int2(0, 0);
   if (live) h.load(D, k);
+  // the warp's CSR region is at a fixed address (contacts_finish): its first
+  // 32 records are requested together with the heads
+  const long long wb = D.nrec0 + static_cast<long long>(k >> 5) * D.wcap;
+#ifndef GG_SWEEP_PREFETCH
+#define GG_SWEEP_PREFETCH 1
+#endif
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  int j = kNullContact;
+  if (GG_SWEEP_PREFETCH) {
+    g = D.cgeo[wb + lane];
+    j = D.coth[wb + lane];
+  }
   const Ctl* ctl = D.ctl;
   if (*((volatile const int*)&ctl->err) != 0) return;  // uniform: nothing raises during sweeps
   const float4* Win = (s == 0) ? layout(D, ctl).v : D.W[(s - 1) & 1];
@@ -1906,25 +1972,35 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
   }
   const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);  // CSR records of the warp
   const uint32_t excl = incl - m;
-  const long long wb = __shfl_sync(0xffffffffu, static_cast<long long>(h.ci.x), 0);
-  // requested together: own w, record 0's partner, the first chunk's records
+  if (!GG_SWEEP_PREFETCH && static_cast<uint32_t>(lane) < T) {
+    g = D.cgeo[wb + lane];
+    j = D.coth[wb + lane];
+  }
+  if (static_cast<uint32_t>(lane) >= T) j = kNullContact;  // past the warp's records
+  // requested together: own w, record 0's partner, the first chunk's partners
   float4 wf = make_float4(0.f, 0.f, 0.f, 0.f), q0 = wf;
   const bool has0 = c > 0 && h.j[0] != kNullContact;
   if (c > 0) wf = Win[k];
   if (has0) q0 = (h.j[0] >= 0) ? Win[h.j[0]] : D.cvb[k];
-  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-  int j = kNullContact;
-  if (static_cast<uint32_t>(lane) < T) {
-    g = D.cgeo[wb + lane];
-    j = D.coth[wb + lane];
-  }
+  // ... and the first chunk's partners, in the same round trip
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j != kNullContact) q = (j >= 0) ? Win[j] : D.cvb[wb + lane];
   double ax = 0.0, ay = 0.0, az = 0.0;
   if (has0) contact_impulse(D, wf.x, wf.y, wf.z, h.g[0], h.j[0], q0, ax, ay, az, A);
   for (uint32_t cb = 0; cb < T; cb += 32) {
     const uint32_t r = cb + lane;
-    const bool mine = r < T && j != kNullContact;
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (mine) q = (j >= 0) ? Win[j] : D.cvb[wb + r];
+    const bool mine = j != kNullContact;  // (r < T: j is null past the records)
+    // this chunk's record and partner; the next chunk's requested now
+    const float4 gc = g, qc = q;
+    const int jc = j;
+    if (cb + 32 < T) {
+      j = kNullContact;
+      if (cb + 32 + lane < T) {
+        g = D.cgeo[wb + cb + 32 + lane];
+        j = D.coth[wb + cb + 32 + lane];
+      }
+      if (j != kNullContact) q = (j >= 0) ? Win[j] : D.cvb[wb + cb + 32 + lane];
+    }
     // owner of record r: the first lane whose inclusive count exceeds r
     int o = 0;
 #pragma unroll
@@ -1936,15 +2012,8 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
     const float owx = __shfl_sync(0xffffffffu, wf.x, o);
     const float owy = __shfl_sync(0xffffffffu, wf.y, o);
     const float owz = __shfl_sync(0xffffffffu, wf.z, o);
-    // the next chunk's records, requested before this chunk's arithmetic
-    const float4 gc = g;
-    const int jc = j;
-    if (cb + 32 + lane < T) {
-      g = D.cgeo[wb + cb + 32 + lane];
-      j = D.coth[wb + cb + 32 + lane];
-    }
     double ix = 0.0, iy = 0.0, iz = 0.0;
-    if (mine) contact_impulse(D, owx, owy, owz, gc, jc, q, ix, iy, iz, A);
+    if (mine) contact_impulse(D, owx, owy, owz, gc, jc, qc, ix, iy, iz, A);
     s_imp[wi][0][lane] = ix;
     s_imp[wi][1][lane] = iy;
     s_imp[wi][2][lane] = iz;
