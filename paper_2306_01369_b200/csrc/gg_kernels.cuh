@@ -1741,7 +1741,9 @@ __device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, 
   double ke_tot = 0.0;
   if (D.E == 1) {
     double v0 = 0.0;
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v0 += *((volatile double*)&D.part[b]);
+    // L2 loads (another block / kernel wrote them; not volatile, so a
+    // thread's loads are in flight together)
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v0 += __ldcg(&D.part[b]);
     ke_tot = block_reduce<0>(v0, smd);
   }
   __shared__ int s_err;
@@ -1749,7 +1751,7 @@ __device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, 
   __syncthreads();
   const long long nbm = static_cast<long long>(D.E) * D.nb * 3;
   for (long long i = threadIdx.x; !D.env_kernel && i < nbm; i += blockDim.x) {
-    const long long f = static_cast<long long>(*((volatile unsigned long long*)&D.bm_fix[i]));
+    const long long f = static_cast<long long>(__ldcg(&D.bm_fix[i]));
     if (!s_err) D.bm_out[static_cast<long long>(step) * nbm + i] = static_cast<double>(f) / kMomScale;
     D.bm_fix[i] = 0ull;
   }
