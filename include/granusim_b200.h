@@ -454,6 +454,20 @@ int64_t gg_slab_owned(const gg_ctx* ctx);
 int gg_slab_mailbox(gg_ctx* ctx, int64_t cap, void* handle_out);
 int gg_slab_connect(gg_ctx* ctx, int32_t side, const void* handle);
 int gg_slab_halo_p2p(gg_ctx* ctx, int32_t sweep, uint64_t seq);
+/* Migration + ghost exchange through the same mailboxes (replaces
+ * migrate_pack/unpack + ghost_pack/unpack + the host count and record
+ * exchanges): pack kernels store straight into the neighbours' mailboxes,
+ * counts and flags are published on the device, and the host reads the new
+ * counts back ONCE.  seq (migrants) and seq + 1 (ghosts): advance by 2 per
+ * step on every rank.  resort != 0 re-sorts the owned particles first.
+ * info[6] = migrants sent lo, hi, received lo, hi; ghosts received lo, hi.
+ * The reference has no multi-GPU path: parity is "same as one GPU"
+ * (stepper.py:57-135 on the whole bed). */
+int gg_slab_exchange_p2p(gg_ctx* ctx, uint64_t seq, int32_t resort, int64_t info[6]);
+/* The step's S sweeps (solve_contacts_pja, contact.py:463-501) with the
+ * peer-memory halo between them, in one call; halo sequence numbers
+ * seq + 1 .. seq + S - 1. */
+int gg_slab_solve_p2p(gg_ctx* ctx, uint64_t seq);
 int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, int64_t* n_own);
 
 #ifdef __cplusplus

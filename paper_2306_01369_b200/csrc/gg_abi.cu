@@ -85,6 +85,8 @@ struct gg_ctx {
   long long ghost_in[2] = {0, 0};   // ghosts received from lo / hi
   long long ghost_out[2] = {0, 0};  // boundary particles sent to lo / hi
   unsigned long long* d_scnt = nullptr;  // [4] slab counters
+  unsigned long long* d_x = nullptr;     // [kXCount] device-side exchange counts
+  unsigned long long* h_x = nullptr;     // pinned mirror
   unsigned long long* h_scnt = nullptr;  // pinned mirror
   int* d_holes = nullptr;
   int* d_movers = nullptr;
@@ -890,6 +892,7 @@ int gg_destroy(gg_ctx* ctx) {
     if (ctx->h_bodies) cudaFreeHost(ctx->h_bodies);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
     if (ctx->h_scnt) cudaFreeHost(ctx->h_scnt);
+    if (ctx->h_x) cudaFreeHost(ctx->h_x);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -2259,6 +2262,7 @@ int gg_slab_load(gg_ctx* ctx, const double* x, const double* v, const int32_t* g
   ctx->n_own = ctx->n_cur = n_own;
   ctx->ghost_in[0] = ctx->ghost_in[1] = 0;
   if (n_own == 0) return GG_OK;
+  set_morton_window(ctx, nullptr, x, n_own, 3);
   const size_t b = sizeof(double) * 3 * static_cast<size_t>(n_own);
   CK(cudaMemcpyAsync(ctx->d_stage, x, b, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_stage + 3 * ctx->n, v, b, cudaMemcpyHostToDevice, ctx->stream));
@@ -2616,7 +2620,7 @@ int gg_slab_mailbox(gg_ctx* ctx, int64_t cap, void* handle_out) {
     dfree(ctx, ctx->mbox);
     ctx->mbox = nullptr;
   }
-  const size_t bytes = sizeof(Mailbox) + sizeof(float4) * 4 * static_cast<size_t>(cap);
+  const size_t bytes = mailbox_bytes(cap);
   if (!ctx->mbox) {
     // plain cudaMalloc (IPC-exportable), zeroed flags
     void* p = nullptr;
@@ -2647,6 +2651,102 @@ int gg_slab_connect(gg_ctx* ctx, int32_t side, const void* handle) {
   CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   ctx->peer[side] = static_cast<Mailbox*>(p);
   ctx->peer_ipc[side] = true;
+  return GG_OK;
+}
+
+// Migration and ghost exchange through the neighbours' mailboxes, counts on
+// the device, one host read-back (gg_slab.cuh, "Device-side exchange").
+// Sequence numbers seq (migrants) and seq + 1 (ghosts): the caller advances
+// seq by 2 per step, identically on every rank.  resort != 0 re-sorts the
+// owned particles first (the physical order never changes a result).
+// info[6]: migrants sent lo, hi, received lo, hi; ghosts received lo, hi.
+int gg_slab_exchange_p2p(gg_ctx* ctx, uint64_t seq, int32_t resort, int64_t info[6]) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (!ctx->mbox) return fail(ctx, GG_EINVAL, "gg_slab_mailbox has not been called");
+  if ((ctx->slab.has_lo && !ctx->peer[0]) || (ctx->slab.has_hi && !ctx->peer[1]))
+    return fail(ctx, GG_EINVAL, "slab neighbour mailbox not connected");
+  if (resort) {
+    st = gg_slab_resort(ctx);
+    if (st != GG_OK) return st;
+  }
+  DeviceGuard guard(ctx->device);
+  if (!ctx->d_x) {
+    CK(dalloc(ctx, &ctx->d_x, kXCount));
+    CK(cudaMallocHost(&ctx->h_x, sizeof(unsigned long long) * kXCount));
+  }
+  const long long cap = ctx->mbox_cap;
+  cudaStream_t s = ctx->stream;
+  unsigned long long* X = ctx->d_x;
+  ctx->n_cur = ctx->n_own;
+  const long long n0 = ctx->n_own;
+  const Dev D = slab_dev(ctx);
+  Dev Dcap = D;
+  Dcap.n = static_cast<int>(ctx->n);  // append bound: the particle capacity
+  const int has_lo = ctx->slab.has_lo ? 1 : 0, has_hi = ctx->slab.has_hi ? 1 : 0;
+  const unsigned long long tmo = 20000000000ull;  // 20 s
+  CK(cudaMemsetAsync(X, 0, sizeof(unsigned long long) * kXCount, s));
+  // migrants -> the neighbours' kind-0 boxes (I am my lo neighbour's hi side)
+  SlabRec* m_lo = ctx->peer[0] ? mailbox_rec(ctx->peer[0], cap, 0, 1) : nullptr;
+  SlabRec* m_hi = ctx->peer[1] ? mailbox_rec(ctx->peer[1], cap, 0, 0) : nullptr;
+  if (n0 > 0) k_slab_emigrate<<<blocks_for(n0), kBlock, 0, s>>>(D, ctx->slab, m_lo, m_hi, cap, X);
+  k_x_signal<<<1, 32, 0, s>>>(ctx->peer[0], ctx->peer[1], 0, seq, X);
+  k_x_wait<<<1, 32, 0, s>>>(D, ctx->mbox, 0, seq, has_lo, has_hi, X, 5, tmo);
+  if (n0 > 0) {
+    k_x_holes<<<blocks_for(n0), kBlock, 0, s>>>(D, X, ctx->d_holes, ctx->d_movers, X);
+    k_x_fill<<<blocks_for(n0), kBlock, 0, s>>>(D, ctx->d_holes, ctx->d_movers, X);
+  }
+  k_x_append<<<blocks_for(2 * cap), kBlock, 0, s>>>(Dcap, ctx->mbox, cap, 0, X, 4, 5);
+  // ghosts: the boundary cells of the new owned set -> kind-1 boxes
+  SlabRec* g_lo = ctx->peer[0] ? mailbox_rec(ctx->peer[0], cap, 1, 1) : nullptr;
+  SlabRec* g_hi = ctx->peer[1] ? mailbox_rec(ctx->peer[1], cap, 1, 0) : nullptr;
+  k_slab_ghosts<<<blocks_for(n0 + 2 * cap), kBlock, 0, s>>>(D, ctx->slab, g_lo, g_hi, ctx->d_map[0],
+                                                          ctx->d_map[1], std::min<long long>(cap, ctx->n),
+                                                          X + 8, X + 7);
+  k_x_signal<<<1, 32, 0, s>>>(ctx->peer[0], ctx->peer[1], 1, seq + 1, X + 8);
+  k_x_wait<<<1, 32, 0, s>>>(D, ctx->mbox, 1, seq + 1, has_lo, has_hi, X, 10, tmo);
+  k_x_append<<<blocks_for(2 * cap), kBlock, 0, s>>>(Dcap, ctx->mbox, cap, 1, X, 7, 10);
+  ctx->launches += 10;
+  CK(cudaGetLastError());
+  int err = 0;
+  CK(cudaMemcpyAsync(ctx->h_x, X, sizeof(unsigned long long) * kXCount, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&err, &ctx->D.ctl->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long* h = ctx->h_x;
+  if (h[0] > static_cast<unsigned long long>(cap) || h[1] > static_cast<unsigned long long>(cap) ||
+      h[8] > static_cast<unsigned long long>(cap) || h[9] > static_cast<unsigned long long>(cap))
+    return fail(ctx, GG_ECAPACITY, "slab mailbox too small for this step's migrants or ghosts");
+  if (err == GG_ECAPACITY) return fail(ctx, GG_ECAPACITY, "slab particle capacity exceeded");
+  if (err) return fail(ctx, GG_ECUDA, "slab exchange: a neighbour did not answer (timeout)");
+  ctx->n_own = static_cast<long long>(h[7]);
+  ctx->ghost_out[0] = static_cast<long long>(h[8]);
+  ctx->ghost_out[1] = static_cast<long long>(h[9]);
+  ctx->ghost_in[0] = static_cast<long long>(h[10]);
+  ctx->ghost_in[1] = static_cast<long long>(h[11]);
+  ctx->n_cur = ctx->n_own + ctx->ghost_in[0] + ctx->ghost_in[1];
+  if (info) {
+    info[0] = static_cast<int64_t>(h[0]);
+    info[1] = static_cast<int64_t>(h[1]);
+    info[2] = static_cast<int64_t>(h[5]);
+    info[3] = static_cast<int64_t>(h[6]);
+    info[4] = static_cast<int64_t>(h[10]);
+    info[5] = static_cast<int64_t>(h[11]);
+  }
+  return GG_OK;
+}
+
+// The S sweeps of a slab step with the per-sweep peer-memory halo between
+// them (gg_slab_sweep / gg_slab_halo_p2p in one call: no host work between
+// sweeps).  seq: the halo sequence number before the first sweep; the call
+// uses seq + 1 .. seq + S - 1.
+int gg_slab_solve_p2p(gg_ctx* ctx, uint64_t seq) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  for (int sweep = 0; sweep < ctx->D.S; ++sweep) {
+    st = gg_slab_sweep(ctx, sweep);
+    if (st == GG_OK && sweep < ctx->D.S - 1) st = gg_slab_halo_p2p(ctx, sweep, seq + 1 + sweep);
+    if (st != GG_OK) return st;
+  }
   return GG_OK;
 }
 

@@ -1926,6 +1926,9 @@ __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
 #ifndef GG_SWEEP_RM
 #define GG_SWEEP_RM 1
 #endif
+#ifndef GG_RM_MAXT
+#define GG_RM_MAXT 64
+#endif
 constexpr int kSweepBlockK = GG_SWEEP_BLOCK;
 static_assert(kSweepBlockK % 32 == 0 && kSweepBlockK <= kBlock, "sweep block: whole warps");
 #ifndef GG_SWEEP_RM_MINB
@@ -1973,6 +1976,14 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
     if (lane >= o) incl += y;
   }
   const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);  // CSR records of the warp
+  // a densely packed warp (more than GG_RM_MAXT CSR records: every lane has
+  // several) keeps its lanes busy record by record — the per-particle loop
+  // is cheaper there than chunk after chunk of owner searches and sums
+  if (T > GG_RM_MAXT) {
+    if (live) sweep_particle_h(D, k, h, Win, Wout, A);
+    sweep_acc_flush_nobar(D, A);
+    return;
+  }
   const uint32_t excl = incl - m;
   if (!GG_SWEEP_PREFETCH && static_cast<uint32_t>(lane) < T) {
     g = D.cgeo[wb + lane];

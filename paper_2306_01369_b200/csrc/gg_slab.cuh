@@ -53,6 +53,7 @@ __global__ void k_slab_emigrate(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
     r.x = make_float4(x.x, x.y, x.z, __int_as_float(D.UID[u][k]));
     r.v = D.V[cur][k];
     (side ? send_hi : send_lo)[slot] = r;
+    __threadfence_system();  // the record may be a peer's mailbox (gg_slab_exchange_p2p)
   }
   D.UID[u][k] = -1;
 }
@@ -94,12 +95,14 @@ __global__ void k_slab_append(Dev D, const SlabRec* __restrict__ in, int m, int 
 // G1: the owned particles in the boundary cells, packed for the neighbours;
 // map_* keeps their physical index for the per-sweep halo (no re-sort
 // happens inside a slab step, so the map stays valid for the whole step).
+// n_dev: the owned count on the device (after a device-side migration), else D.n_own.
 __global__ void k_slab_ghosts(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
                               SlabRec* __restrict__ send_hi, int* __restrict__ map_lo,
                               int* __restrict__ map_hi, long long cap,
-                              unsigned long long* __restrict__ cnt) {
+                              unsigned long long* __restrict__ cnt,
+                              const unsigned long long* __restrict__ n_dev = nullptr) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= D.n_own) return;
+  if (k >= (n_dev ? static_cast<int>(*n_dev) : D.n_own)) return;
   const int cur = D.ctl->cur, u = D.ctl->ucur;
   const float4 x = D.X[cur][k];
   const long long cx = cell_coord(x.x, D.two_r);
@@ -123,6 +126,7 @@ __global__ void k_slab_ghosts(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
       map_hi[s] = k;
     }
   }
+  if (n_dev) __threadfence_system();  // peer mailbox records before the signal
 }
 
 // H: w of sweep s for the mapped boundary particles -> out; in -> ghosts.
@@ -189,13 +193,22 @@ namespace gg {
 // push of that sweep before sweeping again).
 // ---------------------------------------------------------------------------
 struct Mailbox {
-  unsigned long long flag[2];  // [side]: last sequence number delivered from the lo / hi neighbour
-  unsigned long long pad[6];
-  // float4 data[2 parity][2 side][cap] follows
+  unsigned long long flag[2];       // [side]: last halo sequence delivered from the lo / hi neighbour
+  unsigned long long xflag[2];      // [side]: last exchange sequence (migrants, then ghosts)
+  unsigned long long xcount[2][2];  // [kind][side]: records delivered (kind 0 migrants, 1 ghosts)
+  // float4 halo[2 parity][2 side][cap], then SlabRec rec[2 kind][2 side][cap]
 };
+static_assert(sizeof(Mailbox) == 64, "mailbox header");
 
 __device__ __forceinline__ float4* mailbox_data(Mailbox* m, long long cap, int parity, int side) {
   return reinterpret_cast<float4*>(m + 1) + (static_cast<long long>(parity) * 2 + side) * cap;
+}
+__host__ __device__ __forceinline__ SlabRec* mailbox_rec(Mailbox* m, long long cap, int kind, int side) {
+  return reinterpret_cast<SlabRec*>(reinterpret_cast<float4*>(m + 1) + 4 * cap) +
+         (static_cast<long long>(kind) * 2 + side) * cap;
+}
+__host__ __device__ __forceinline__ size_t mailbox_bytes(long long cap) {
+  return sizeof(Mailbox) + (sizeof(float4) + sizeof(SlabRec)) * 4 * static_cast<size_t>(cap);
 }
 
 // block 0 -> the lo neighbour (its side 1), block 1 -> the hi neighbour (its side 0)
@@ -255,6 +268,109 @@ __global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine,
   const int at = D.n_own + (side == 0 ? 0 : n_lo);
   float4* W = D.W[s & 1];
   for (int i = threadIdx.x; i < m; i += blockDim.x) W[at + i] = src[i];
+}
+
+
+// ---------------------------------------------------------------------------
+// Device-side exchange of migrants and ghosts (gg_slab_exchange_p2p): the
+// pack kernels write straight into the neighbours' mailboxes (peer memory),
+// then ONE thread per side publishes the count and a system-scope release
+// flag; the receiver waits for both flags (bounded) and appends from its own
+// mailbox.  Every count lives on the device (X below); the host reads them
+// once, after both exchanges.  No host round trip, no NCCL call.
+//   X[0], X[1]  migrants sent lo / hi         X[2] holes, X[3] movers
+//   X[4]        owned after the departures    X[5], X[6] migrants received lo / hi
+//   X[7]        owned after the arrivals      X[8], X[9] ghosts sent lo / hi
+//   X[10], X[11] ghosts received lo / hi
+// ---------------------------------------------------------------------------
+constexpr int kXCount = 12;
+
+// publish this rank's records of `kind` to the neighbours: count, then flag
+__global__ void k_x_signal(Mailbox* peer_lo, Mailbox* peer_hi, int kind, unsigned long long seq,
+                           const unsigned long long* __restrict__ sent) {
+  if (threadIdx.x != 0) return;
+  for (int side = 0; side < 2; ++side) {
+    Mailbox* p = side == 0 ? peer_lo : peer_hi;
+    if (!p) continue;
+    const int their = side == 0 ? 1 : 0;  // I am their hi (resp. lo) neighbour
+    volatile unsigned long long* c = &p->xcount[kind][their];
+    *c = sent[side];
+    __threadfence_system();
+    asm volatile("st.release.sys.u64 [%0], %1;" ::"l"(&p->xflag[their]), "l"(seq) : "memory");
+  }
+}
+
+// wait for the neighbours' flags, read the counts they sent (0 without a
+// neighbour) into X[at], X[at + 1]; the departures' survivors count first
+__global__ void k_x_wait(Dev D, Mailbox* mine, int kind, unsigned long long seq, int has_lo, int has_hi,
+                         unsigned long long* __restrict__ X, int at, unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  for (int side = 0; side < 2; ++side) {
+    unsigned long long got = 0;
+    if (side == 0 ? has_lo : has_hi) {
+      unsigned long long t0, t, v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        asm volatile("ld.relaxed.sys.u64 %0, [%1];" : "=l"(v) : "l"(&mine->xflag[side]) : "memory");
+        if (v >= seq) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {  // a neighbour died: fail instead of hanging the GPU
+          raise_err(D.ctl, GG_ECUDA);
+          break;
+        }
+        __nanosleep(200);
+      }
+      asm volatile("ld.acquire.sys.u64 %0, [%1];" : "=l"(v) : "l"(&mine->xflag[side]) : "memory");
+      got = *((volatile unsigned long long*)&mine->xcount[kind][side]);
+    }
+    X[at + side] = got;
+  }
+  if (kind == 0) X[4] = static_cast<unsigned long long>(D.n_own) - X[0] - X[1];
+}
+
+// holes below the survivors' count and survivors above it (k_slab_holes with
+// the device count)
+__global__ void k_x_holes(Dev D, const unsigned long long* __restrict__ X, int* __restrict__ holes,
+                          int* __restrict__ movers, unsigned long long* __restrict__ cnt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= D.n_own) return;
+  const int n_stay = static_cast<int>(X[4]);
+  const int uid = D.UID[D.ctl->ucur][k];
+  if (k < n_stay && uid < 0) holes[atomicAdd(cnt + 2, 1ull)] = k;
+  if (k >= n_stay && uid >= 0) movers[atomicAdd(cnt + 3, 1ull)] = k;
+}
+
+__global__ void k_x_fill(Dev D, const int* __restrict__ holes, const int* __restrict__ movers,
+                         const unsigned long long* __restrict__ X) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int>(X[2])) return;
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  const int h = holes[i], s = movers[i];
+  D.X[cur][h] = D.X[cur][s];
+  D.V[cur][h] = D.V[cur][s];
+  D.UID[u][h] = D.UID[u][s];
+}
+
+// append the mailbox's records of `kind` (lo side first) at X[base];
+// kind 0 also sets X[7] = owned after the arrivals.  Grid: 2 * cap threads.
+__global__ void k_x_append(Dev D, Mailbox* mine, long long cap, int kind,
+                           unsigned long long* __restrict__ X, int base, int in_at) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long m_lo = static_cast<long long>(X[in_at]), m_hi = static_cast<long long>(X[in_at + 1]);
+  if (kind == 0 && t == 0) X[7] = X[4] + m_lo + m_hi;
+  const int side = t < cap ? 0 : 1;
+  const long long i = side == 0 ? t : t - cap;
+  if (i >= (side == 0 ? m_lo : m_hi) || i >= cap) return;
+  const long long at = static_cast<long long>(X[base]) + (side == 0 ? 0 : m_lo) + i;
+  if (at >= D.n) {  // capacity (D.n = the context's particle capacity here)
+    raise_err(D.ctl, GG_ECAPACITY);
+    return;
+  }
+  const SlabRec r = mailbox_rec(mine, cap, kind, side)[i];
+  const int cur = D.ctl->cur, u = D.ctl->ucur;
+  D.X[cur][at] = make_float4(r.x.x, r.x.y, r.x.z, 0.f);
+  D.V[cur][at] = make_float4(r.v.x, r.v.y, r.v.z, 0.f);
+  D.UID[u][at] = __float_as_int(r.x.w);
 }
 
 }  // namespace gg

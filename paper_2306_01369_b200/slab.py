@@ -18,11 +18,20 @@ bitwise identical to the one-GPU run (tests/test_slab.py).
 when the hash aliases: a rank hashes only its owned and ghost particles, so
 far-away particles of other slabs that share a bucket with a neighbour cell
 are missing from its candidate counts.  Aliases are never contacts (a
-contact is within 2r, i.e. within +-1 cell), so nothing else changes.  The library only packs and unpacks device buffers
-(gg_slab_* in include/granusim_b200.h); this module moves them with
-torch.distributed point-to-point operations — NCCL on device buffers over
-NVLink in production, or gloo staged through host memory (tests, and several
-ranks sharing one GPU).
+contact is within 2r, i.e. within +-1 cell), so nothing else changes.
+
+Two transports.  ``halo="p2p"`` (the default under NCCL): every rank exports a
+mailbox through CUDA IPC and opens its neighbours'; migrants and ghosts are
+packed by kernels straight into the neighbours' mailboxes, counts and
+system-scope release flags are published on the device, the receiver waits
+on the device and appends (gg_slab_exchange_p2p: one host read-back of the
+new counts per step), and the S sweeps run with their per-sweep w halo pushed
+into the same mailboxes (gg_slab_solve_p2p: one call, no host work between
+sweeps) — no NCCL call on the step path, three host synchronisations per step
+(exchange counts, StepReport, its reduction).  ``halo="host"``: the library
+packs and unpacks device buffers (gg_slab_* pack/unpack) and this module
+moves them with torch.distributed point-to-point operations — NCCL on device
+buffers, or gloo staged through host memory (tests on CPU).
 """
 
 from __future__ import annotations
@@ -257,7 +266,8 @@ class SlabBed:
         if halo == "auto":  # peer memory whenever the ranks run NCCL on one node's GPUs
             halo = "p2p" if self.tr.backend == "nccl" else "host"
         self.halo = halo if world > 1 else "host"
-        self.seq = 0
+        self.seq = 0   # halo sequence (one per inner sweep)
+        self.xseq = 0  # exchange sequence (two per step: migrants, ghosts)
         if self.halo == "p2p":
             self._connect_mailboxes()
 
@@ -323,18 +333,33 @@ class SlabBed:
             body.update(t)
             self.engine.body_row(body, float(sc.params.radius), row[b])
         sc.t = t
+        resort = self.steps % self.resort_every == 0
+        S = int(self.params.solver_iterations)
+        if self.halo == "p2p":
+            # 1-2. (re-sort,) migration and ghosts through the neighbours'
+            # mailboxes, counts on the device, one read-back; 3. the sweeps
+            # with their peer-memory halos in one call
+            info = np.zeros(6, dtype=np.int64)
+            self.xseq += 2
+            N.check(self.ctx, lib.gg_slab_exchange_p2p(self.ctx, self.xseq - 1, int(resort), N.ptr(info)),
+                    "slab exchange")
+            self.migrated += int(info[0] + info[1])
+            self.ghosts = (int(info[4]), int(info[5]))
+            N.check(self.ctx, lib.gg_slab_detect(self.ctx, N.ptr(row), self.nb), "slab detect")
+            N.check(self.ctx, lib.gg_slab_solve_p2p(self.ctx, self.seq), "slab solve")
+            self.seq += S - 1
+            return self._finish(lib)
         # 1. migration, 2. (re-sort) + ghosts
         sent, _ = self._swap(lib.gg_slab_migrate_pack, lib.gg_slab_migrate_unpack,
                              (self.s_lo, self.s_hi), (self.r_lo, self.r_hi))
         self.migrated += sent[0] + sent[1]
-        if self.steps % self.resort_every == 0:
+        if resort:
             N.check(self.ctx, lib.gg_slab_resort(self.ctx), "slab resort")
         n_out, (g_lo, g_hi) = self._swap(lib.gg_slab_ghost_pack, lib.gg_slab_ghost_unpack,
                                          (self.s_lo, self.s_hi), (self.r_lo, self.r_hi))
         self.ghosts = (g_lo, g_hi)
         # 3. step with per-sweep halo exchange of w
         N.check(self.ctx, lib.gg_slab_detect(self.ctx, N.ptr(row), self.nb), "slab detect")
-        S = int(self.params.solver_iterations)
         for s in range(S):
             N.check(self.ctx, lib.gg_slab_sweep(self.ctx, s), "slab sweep")
             if s < S - 1 and self.halo == "p2p":
@@ -347,6 +372,9 @@ class SlabBed:
                                  self.h_rhi, g_hi)
                 N.check(self.ctx, lib.gg_slab_halo_unpack(self.ctx, s, self._p(self.h_rlo),
                                                           self._p(self.h_rhi)), "halo unpack")
+        return self._finish(lib)
+
+    def _finish(self, lib) -> StepReport:
         rep = np.zeros(1, dtype=N.REPORT_DTYPE)
         bm = np.zeros((max(self.nb, 1), 3))
         st = lib.gg_slab_finish(self.ctx, N.ptr(rep), N.ptr(bm))
