@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent copies of the scene per GPU instead of one slab-decomposed bed")
     ap.add_argument("--slab-particles", type=int, default=8_000_000)
+    ap.add_argument("--halo", choices=["auto", "host", "p2p"], default="auto",
+                    help="N > 1 single-bed exchange: peer-memory mailboxes (p2p; auto under NCCL) "
+                         "or torch.distributed point-to-point (host)")
     ap.add_argument("--envs", type=int, default=4096, help="envs workload: total envs")
     ap.add_argument("--env-particles", type=int, default=2000)
     ap.add_argument("--settle", type=int, default=3000, help="hero50k: settle steps when no state file")
@@ -683,7 +686,7 @@ def run_slab(args, dist: Dist):
             return s2
 
     bed = SlabBed(scene(), rank=dist.rank, world=dist.world, device=dev,
-                  backend=dist.backend if dist.world > 1 else None)
+                  backend=dist.backend if dist.world > 1 else None, halo=args.halo)
     lib = N.lib()
     K, W = args.steps, args.warmup
     for _ in range(W):
@@ -723,7 +726,7 @@ def run_slab(args, dist: Dist):
     dist.barrier()
     t0 = time.perf_counter()
     bed2 = SlabBed(scene(), rank=dist.rank, world=dist.world, device=dev,
-                   backend=dist.backend if dist.world > 1 else None)
+                   backend=dist.backend if dist.world > 1 else None, halo=args.halo)
     for _ in range(K):
         bed2.step()
     Xg, _ = bed2.gather()
@@ -745,7 +748,7 @@ def run_slab(args, dist: Dist):
                 "dtype": "f32 state / f64 contact geometry", "data": "synthetic",
                 "config": desc,
                 "run": {"parallelism": f"slabs x{dist.world}", "n_h": bed.n_h, "c_pp": c_pp,
-                        "c_b": c_b, "max_owned": owned, "backend": dist.backend,
+                        "c_b": c_b, "max_owned": owned, "backend": dist.backend, "halo": bed.halo,
                         "l2": "not flushed: the state exceeds L2"},
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches}

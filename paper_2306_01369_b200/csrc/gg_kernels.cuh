@@ -1651,16 +1651,21 @@ __device__ __forceinline__ void env_add_arr(const Dev& D, int env, unsigned long
 }
 
 __device__ __forceinline__ void write_report(const Dev& D, gg_report& R, const Acc* a, double ke_sum) {
-  const volatile Acc* va = a;
-  R.n_contacts = static_cast<long long>(va->n_pp);
-  R.n_candidates = static_cast<long long>(va->n_cand);
-  R.n_body_contacts = static_cast<long long>(va->n_body);
-  R.n_coincident = static_cast<long long>(va->n_coinc);
-  R.n_degenerate = static_cast<long long>(va->n_deg);
-  R.max_penetration = __longlong_as_double(static_cast<long long>(va->max_psi_bits));
+  // L2 loads, all in flight together (other blocks / kernels wrote them;
+  // volatile loads would be one round trip each)
+  const unsigned long long n_pp = __ldcg(&a->n_pp), n_cand = __ldcg(&a->n_cand),
+                           n_body = __ldcg(&a->n_body), n_coinc = __ldcg(&a->n_coinc),
+                           n_deg = __ldcg(&a->n_deg), psi = __ldcg(&a->max_psi_bits),
+                           viol = __ldcg(&a->max_viol_bits), b1 = __ldcg(&a->min_b1_bits);
+  R.n_contacts = static_cast<long long>(n_pp);
+  R.n_candidates = static_cast<long long>(n_cand);
+  R.n_body_contacts = static_cast<long long>(n_body);
+  R.n_coincident = static_cast<long long>(n_coinc);
+  R.n_degenerate = static_cast<long long>(n_deg);
+  R.max_penetration = __longlong_as_double(static_cast<long long>(psi));
   R.kinetic_energy = 0.5 * D.mass * ke_sum;
-  R.max_cone_violation = __longlong_as_double(static_cast<long long>(va->max_viol_bits));
-  R.min_normal_impulse = __longlong_as_double(static_cast<long long>(va->min_b1_bits));
+  R.max_cone_violation = __longlong_as_double(static_cast<long long>(viol));
+  R.min_normal_impulse = __longlong_as_double(static_cast<long long>(b1));
 }
 
 // Symplectic Euler (stepper.py:102-106), SolverError check
@@ -1743,7 +1748,16 @@ __device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, 
     double v0 = 0.0;
     // L2 loads (another block / kernel wrote them; not volatile, so a
     // thread's loads are in flight together)
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v0 += __ldcg(&D.part[b]);
+    // (eight loads per round in flight; the sum keeps the strided order)
+    int b = threadIdx.x;
+    for (; b + 7 * static_cast<int>(blockDim.x) < nparts; b += 8 * blockDim.x) {
+      double t[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t[q] = __ldcg(&D.part[b + q * blockDim.x]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v0 += t[q];
+    }
+    for (; b < nparts; b += blockDim.x) v0 += __ldcg(&D.part[b]);
     ke_tot = block_reduce<0>(v0, smd);
   }
   __shared__ int s_err;
