@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import threading
 
 import numpy as np
@@ -24,7 +25,7 @@ from . import _native as N
 from .errors import SolverError
 from .sdf import geometry_kind, geometry_shape
 
-DEFAULT_MAX_CONTACTS = 16
+DEFAULT_MAX_CONTACTS = int(os.environ.get("GG_MAX_CONTACTS", 16))  # record slots per particle (grown x2 on overflow)
 
 
 def default_table_size(n_p: int) -> int:
