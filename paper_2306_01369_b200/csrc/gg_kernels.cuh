@@ -725,9 +725,15 @@ using NarrowLen = uint16_t;
 constexpr uint32_t kLenSentinel = 0xffffu;
 #endif
 
-template <int B>
+// B threads per block; Depth candidates in flight per thread; the 27
+// neighbour-bucket bounds requested in Groups rounds.  The large-n kernel
+// (throughput) and the fused small-n kernel (latency) are tuned apart.
+template <int B, int Depth = GG_KDEPTH, int Groups = 3>
 struct NarrowSmemT {
   static constexpr int kW = B / 32;
+  static constexpr int kDepth = Depth;
+  static constexpr int kGroups = Groups;
+  static_assert(27 % Groups == 0, "bucket rounds");
   uint32_t beg[28][B];        // compacted non-empty buckets + a sentinel
   NarrowLen len[28][B];       // bucket sizes
   uint32_t pass[kPassCap][B]; // Xh index of every prefilter pass, per owner, in order
@@ -737,7 +743,13 @@ struct NarrowSmemT {
   double d[32];
   unsigned long long u[32];
 };
-using NarrowSmem = NarrowSmemT<kBlock>;
+#ifndef GG_FUSED_KDEPTH
+#define GG_FUSED_KDEPTH GG_KDEPTH
+#endif
+#ifndef GG_FUSED_GROUPS
+#define GG_FUSED_GROUPS 3
+#endif
+using NarrowSmem = NarrowSmemT<kBlock, GG_FUSED_KDEPTH, GG_FUSED_GROUPS>;  // the fused kernel's
 #ifndef GG_NARROW_BLOCK
 #define GG_NARROW_BLOCK 256
 #endif
@@ -906,6 +918,16 @@ __device__ __forceinline__ void acc_contacts(const Dev& D, int env, unsigned lon
   }
 }
 
+// contact-kernel sub-phase stamps of block 0, thread 0 (tstamp[48 + i];
+// phase timer only)
+__device__ __forceinline__ void cstamp(const Dev& D, int i) {
+  if (D.tstamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    D.tstamp[48 + i] = t;
+  }
+}
+
 // Phase B of the contact kernel (after a phase A filled sm.pass / the
 // candidate lists): warp-cooperative exact test of the queued prefilter
 // passes, body contacts, one record allocation per block, the records, the
@@ -920,6 +942,7 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
   const int tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5, wb = w * 32;
   sm.pos[tid] = pf;
+  cstamp(D, 3);
   // ---- phase B: warp-cooperative exact test, one pass --------------------------
   // Every queued candidate (a prefilter pass) gets a record slot: its owner's
   // offset + its index in the owner's queue, so slots are known before the
@@ -948,7 +971,9 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
   }
   // this env's bodies at this step: bodies[step][env][nb]
   const gg_body* bodies = D.bodies + (static_cast<long long>(ctl->step) * D.E + env) * D.nb;
+  cstamp(D, 4);
   const int c_b = (live && D.nb > 0) ? body_contacts(D, bodies, pf, false, k, 0, 0, n_deg, max_psi) : 0;
+  cstamp(D, 5);
   // ---- allocation: a fixed region per warp -----------------------------------
   // (records 0 .. kFixedSlots-1 of each owner are its fixed slots; records
   // kFixedSlots.. of the warp's 32 owners are laid end to end, in lane
@@ -1023,6 +1048,7 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
       D.cinfo[k] = make_int2(static_cast<int>(my_off), tot);
     }
   }
+  cstamp(D, 6);
   acc_contacts(D, env, static_cast<unsigned long long>(c_pp), n_cand, n_coinc,
                static_cast<unsigned long long>(c_b), n_deg, max_psi);
 }
@@ -1053,6 +1079,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   const int k = base + tid;
   const bool live = tid < count && k < D.n_own;
   const int env = env_of(D, live ? k : D.n - 1);
+  cstamp(D, 0);
   unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
   uint32_t total = 0, npass = 0;
   float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1091,18 +1118,19 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     }
     int nb = 0;
     bool big = false;
+    constexpr int kPerG = 27 / SM::kGroups;
 #pragma unroll
-    for (int g = 0; g < 3; ++g) {
-      uint32_t hb[9], sb[9], eb[9];
+    for (int g = 0; g < SM::kGroups; ++g) {
+      uint32_t hb[kPerG], sb[kPerG], eb[kPerG];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        hb[j] = nb_hash(D, g * 9 + j, c0, c1, c2, tx, ty, tz);
+      for (int j = 0; j < kPerG; ++j) {
+        hb[j] = nb_hash(D, g * kPerG + j, c0, c1, c2, tx, ty, tz);
         sb[j] = start[hb[j]];
         eb[j] = start[hb[j] + 1];
       }
 #pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const bool keep = eb[j] > sb[j] && !((dupmask >> (g * 9 + j)) & 1u);
+      for (int j = 0; j < kPerG; ++j) {
+        const bool keep = eb[j] > sb[j] && !((dupmask >> (g * kPerG + j)) & 1u);
         if (keep) {
           const uint32_t L = eb[j] - sb[j];
           total += L;
@@ -1138,6 +1166,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         }
       }
     }
+    cstamp(D, 1);
     n_cand = total - 1;  // minus the self pair (one per particle, broadphase.py:441-447)
     // sentinel after the last bucket: the cursor may run up to kDepth - 1
     // candidates past the end without a guard (indices < n + kXhPad: Xh is
@@ -1148,7 +1177,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     const float rej = D.reject_d2f;
     CandCursor cur;
     cur.init(sm, tid);
-    constexpr int kDepth = GG_KDEPTH;  // candidates in flight per thread
+    constexpr int kDepth = SM::kDepth;  // candidates in flight per thread
     static_assert(kDepth <= kXhPad, "the sentinel bucket reads up to kDepth - 1 entries past n");
     for (uint32_t i = 0; i < total; i += kDepth) {
       uint32_t mi[kDepth];
@@ -1172,7 +1201,9 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       }
     }
   }
+  cstamp(D, 2);
   contacts_finish(D, ctl, base, sm, Xh, live, k, env, pf, total, npass, n_cand, n_coinc, n_deg);
+  cstamp(D, 7);
 }
 
 // ---------------------------------------------------------------------------

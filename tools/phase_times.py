@@ -28,6 +28,11 @@ for resort in (False, True):
     eng.run_batch(table, nb, 0)
     st = np.zeros(64, dtype=np.uint64)
     lib.gg_phase_timer(eng.ctx, 1, N.ptr(st), 64)
+    sub = st[48:56].astype(np.int64)
+    if (sub > 0).all():  # contact-kernel sub-phases of block 0, thread 0
+        print("  contacts sub-phases (us): bucket lists, candidates, (phase B start), exact test, body count, records, counters:",
+              np.round(np.diff(sub) / 1000.0, 2).tolist())
+    st[48:] = 0
     k = int(np.nonzero(st)[0].max()) + 1
     d = np.diff(st[:k].astype(np.int64)) / 1000.0
     print(f"resort={resort} total {(int(st[k-1]) - int(st[0])) / 1000:.1f} us; phases (us):", np.round(d, 2).tolist())
