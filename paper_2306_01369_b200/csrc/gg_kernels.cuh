@@ -919,9 +919,13 @@ __device__ __forceinline__ void acc_contacts(const Dev& D, int env, unsigned lon
 }
 
 // contact-kernel sub-phase stamps of block 0, thread 0 (tstamp[48 + i];
-// phase timer only)
+// phase timer, debug builds with -DGG_CSTAMP=1 only: the check costs the
+// large-n contact kernel registers)
+#ifndef GG_CSTAMP
+#define GG_CSTAMP 0
+#endif
 __device__ __forceinline__ void cstamp(const Dev& D, int i) {
-  if (D.tstamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (GG_CSTAMP && D.tstamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     D.tstamp[48 + i] = t;

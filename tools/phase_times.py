@@ -29,7 +29,7 @@ for resort in (False, True):
     st = np.zeros(64, dtype=np.uint64)
     lib.gg_phase_timer(eng.ctx, 1, N.ptr(st), 64)
     sub = st[48:56].astype(np.int64)
-    if (sub > 0).all():  # contact-kernel sub-phases of block 0, thread 0
+    if (sub > 0).all():  # contact-kernel sub-phases of block 0, thread 0 (library built with -DGG_CSTAMP=1)
         print("  contacts sub-phases (us): bucket lists, candidates, (phase B start), exact test, body count, records, counters:",
               np.round(np.diff(sub) / 1000.0, 2).tolist())
     st[48:] = 0
