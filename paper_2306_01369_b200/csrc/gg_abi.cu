@@ -149,6 +149,12 @@ void dfree(gg_ctx* ctx, void* p) {
 }
 
 int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock); }
+// up to this many scan tiles (2048 buckets each) k_scan_apply sums its
+// predecessor tiles itself and k_scan_top is not launched
+#ifndef GG_SCAN_TOP_FREE
+#define GG_SCAN_TOP_FREE 2048
+#endif
+constexpr int kScanTopFree = GG_SCAN_TOP_FREE;
 #ifndef GG_SWEEP_BLOCK
 #define GG_SWEEP_BLOCK 64
 #endif
@@ -403,8 +409,8 @@ int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
   // bucket/tile counts are zero on entry: the previous scatter zeroed them
   k_count<<<nbn, kBlock, 0, s>>>(D);
   k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
-  k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
-  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+  if (ctx->ntiles > kScanTopFree) k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+  k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D, ctx->ntiles <= kScanTopFree ? 1 : 0);
   k_scatter<<<nbn, kBlock, 0, s>>>(D);
   if (D.key_morton)
     k_resort<<<nbn, kBlock, 0, s>>>(D);
@@ -464,7 +470,8 @@ int kernels_per_step(const gg_ctx* ctx, int resort) {
   if (use_fused_step(ctx)) return use_cluster_solve(ctx) ? 2 : 1;
   const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 2;
   const int env_reports = (ctx->E > 1 && !use_persistent_solve(ctx)) ? 1 : 0;
-  return 7 + solve + env_reports + (resort ? 6 : 0);
+  const int top = ctx->ntiles > kScanTopFree ? 1 : 0;  // k_scan_top per sort pass
+  return 6 + top + solve + env_reports + (resort ? 5 + top : 0);
 }
 
 // Same schedule as enqueue_step, with an event after every kernel so each
@@ -517,9 +524,9 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     mark(1);
     k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
     mark(2);
-    k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
+    if (ctx->ntiles > kScanTopFree) k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
     mark(3);
-    k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D);
+    k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D, ctx->ntiles <= kScanTopFree ? 1 : 0);
     mark(4);
     k_scatter<<<nbn, kBlock, 0, s>>>(D);
     mark(5);

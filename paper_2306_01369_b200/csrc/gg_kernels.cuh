@@ -1953,10 +1953,13 @@ __global__ void __launch_bounds__(1024) k_scan_top(Dev D, int ntiles) {
   ph_scan_top(D, ntiles, sm);
 }
 
-__global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D) {
+// tile_counts != 0: tile[] still holds the per-tile totals (no k_scan_top
+// ran): each block sums its predecessors' totals itself — one launch fewer
+// for up to a few thousand tiles
+__global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D, int tile_counts) {
   __shared__ uint32_t sm[32];
   if (D.ctl->err) return;
-  ph_scan_apply(D, blockIdx.x, sm, false);
+  ph_scan_apply(D, blockIdx.x, sm, tile_counts != 0);
 }
 
 __global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
