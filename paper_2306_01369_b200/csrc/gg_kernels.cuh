@@ -701,7 +701,7 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
 }
 
 #ifndef GG_PASSCAP
-#define GG_PASSCAP 16
+#define GG_PASSCAP 12
 #endif
 constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidate copy
 #ifndef GG_KDEPTH
@@ -754,7 +754,10 @@ using NarrowSmem = NarrowSmemT<kBlock, GG_FUSED_KDEPTH, GG_FUSED_GROUPS>;  // th
 #define GG_NARROW_BLOCK 256
 #endif
 constexpr int kNarrowBlock = GG_NARROW_BLOCK;  // k_narrow block size (large-n contact kernel)
-using NarrowSmemN = NarrowSmemT<kNarrowBlock>;
+#ifndef GG_NARROW_GROUPS
+#define GG_NARROW_GROUPS 3
+#endif
+using NarrowSmemN = NarrowSmemT<kNarrowBlock, GG_KDEPTH, GG_NARROW_GROUPS>;
 
 // Iterate over a thread's concatenated candidate list (its compacted
 // neighbour buckets) — the cursor of the flat candidate loop.
