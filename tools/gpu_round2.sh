@@ -20,7 +20,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --c
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $O/launches_envs.csv python bench.py --workload envs --steps 10 --warmup 2 --no-cpu-baseline --profile-steps 1 > /dev/null 2>&1
 python tools/launches.py $O/launches_bed1m.csv $O/launches_hero50k.csv $O/launches_envs.csv > $O/launches_summary.txt 2>&1
 # full-set captures of the top kernels
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_narrow|k_sweep|k_finish|k_commit|k_fill|k_count|k_scatter' -s 60 -c 16 -o $O/full_bed1m python bench.py --steps 20 --warmup 5 --no-cpu-baseline --profile-steps 1 > $O/ncu_bed1m.log 2>&1; tail -1 $O/ncu_bed1m.log
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_narrow|k_sweep|k_finish|k_commit|k_fill|k_count|k_scatter|k_scan' -s 60 -c 18 -o $O/full_bed1m python bench.py --steps 20 --warmup 5 --no-cpu-baseline --profile-steps 1 > $O/ncu_bed1m.log 2>&1; tail -1 $O/ncu_bed1m.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_step_fused' -s 3 -c 1 -o $O/full_hero50k python bench.py --workload hero50k --steps 5 --warmup 2 --no-cpu-baseline --profile-steps 1 > $O/ncu_hero.log 2>&1; tail -1 $O/ncu_hero.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_solve_staged' -s 3 -c 1 -o $O/full_bed1m_staged python bench.py --solve-mode 8 --steps 5 --warmup 3 --no-cpu-baseline --profile-steps 1 > $O/ncu_staged.log 2>&1; tail -1 $O/ncu_staged.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_narrow|k_sweep|k_finish' -s 30 -c 12 -o $O/full_envs python bench.py --workload envs --steps 10 --warmup 2 --no-cpu-baseline --profile-steps 1 > $O/ncu_envs.log 2>&1; tail -1 $O/ncu_envs.log
