@@ -2,7 +2,7 @@
 # DRAM traffic of a sweep inside a step (records and w warm in L2 or not)
 mkdir -p gpurun_out/ws
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct -k regex:'k_sweep_rm|k_narrow|k_finish' -s 40 -c 13 --csv python bench.py --steps 8 --warmup 3 --no-cpu-baseline --profile-steps 1 > gpurun_out/ws/warm.csv 2> gpurun_out/ws/warm.err
+timeout 900 ncu --replay-mode application --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct -k regex:'k_sweep_rm|k_narrow|k_finish' -s 40 -c 13 --csv python bench.py --steps 8 --warmup 3 --no-cpu-baseline --profile-steps 1 > gpurun_out/ws/warm.csv 2> gpurun_out/ws/warm.err
 python - <<'PY'
 import csv
 rows = list(csv.reader(open('gpurun_out/ws/warm.csv')))
