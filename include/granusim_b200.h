@@ -468,6 +468,15 @@ int gg_slab_exchange_p2p(gg_ctx* ctx, uint64_t seq, int32_t resort, int64_t info
  * peer-memory halo between them, in one call; halo sequence numbers
  * seq + 1 .. seq + S - 1. */
 int gg_slab_solve_p2p(gg_ctx* ctx, uint64_t seq);
+/* The whole slab step on the peer-memory transport — exchange, contacts,
+ * sweeps with their halos, integration and commit — replayed as ONE CUDA
+ * graph per re-sort flag (stepper.py:57-135 on the rank's slab): the counts
+ * stay on the device, the mailbox sequence numbers come from a device step
+ * counter, and the host synchronises once, to read the rank's StepReport
+ * (report, body_momentum [n_bodies][3]).  info[6] as gg_slab_exchange_p2p's.
+ * A bed uses either this or the per-call entry points above, not both. */
+int gg_slab_step_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t resort,
+                     gg_report* report, double* body_momentum, int64_t info[6]);
 int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, int64_t* n_own);
 
 #ifdef __cplusplus

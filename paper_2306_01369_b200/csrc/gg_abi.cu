@@ -87,6 +87,10 @@ struct gg_ctx {
   unsigned long long* d_scnt = nullptr;  // [4] slab counters
   unsigned long long* d_x = nullptr;     // [kXCount] device-side exchange counts
   unsigned long long* h_x = nullptr;     // pinned mirror
+  int* d_n = nullptr;                    // [2] {n, n_own} of a graph-replayed slab step
+  unsigned long long* d_step = nullptr;  // slab steps replayed (the mailbox sequence numbers)
+  cudaGraphExec_t sgexec[2] = {nullptr, nullptr};  // slab step graphs (plain, re-sort)
+  unsigned long long sgkey = 0;          // what the slab graphs were built for
   unsigned long long* h_scnt = nullptr;  // pinned mirror
   int* d_holes = nullptr;
   int* d_movers = nullptr;
@@ -230,7 +234,11 @@ int alloc_slots(gg_ctx* ctx, int K) {
   K = std::max(K, kFixedSlots + 1);
   const long long n1 = std::max<long long>(ctx->n, 1);
   const long long wcap = 32ll * (K - kFixedSlots);
-  const size_t slots = static_cast<size_t>(kFixedSlots * n1 + ((n1 + 31) / 32) * wcap);
+  // regions for every warp of a kBlock-rounded grid: a sweep warp past the
+  // last particle still requests its region's first records (speculatively,
+  // with the heads) and must stay inside the allocation
+  const long long nwarps = ((n1 + kBlock - 1) / kBlock) * (kBlock / 32);
+  const size_t slots = static_cast<size_t>(kFixedSlots * n1 + nwarps * wcap);
   CK(dalloc(ctx, &D.cgeo, slots));
   CK(dalloc(ctx, &D.coth, slots));
   CK(dalloc(ctx, &D.cvb, slots));
@@ -889,8 +897,10 @@ int gg_destroy(gg_ctx* ctx) {
   {
     DeviceGuard guard(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (int g = 0; g < 2; ++g)
+    for (int g = 0; g < 2; ++g) {
       if (ctx->gexec[g]) cudaGraphExecDestroy(ctx->gexec[g]);
+      if (ctx->sgexec[g]) cudaGraphExecDestroy(ctx->sgexec[g]);
+    }
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
     for (int side = 0; side < 2; ++side)
       if (ctx->peer_ipc[side] && ctx->peer[side]) cudaIpcCloseMemHandle(ctx->peer[side]);
@@ -2740,6 +2750,185 @@ int gg_slab_exchange_p2p(gg_ctx* ctx, uint64_t seq, int32_t resort, int64_t info
     info[5] = static_cast<int64_t>(h[11]);
   }
   return GG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The whole slab step on the peer-memory transport as ONE CUDA graph (one per
+// re-sort flag), replayed every step: nothing in it depends on the host.  The
+// particle counts live on the device (Dev::dn, grids sized for the
+// capacity), the mailbox sequence numbers derive from a device step counter,
+// capacity and timeout failures raise the error word.  The host stages the
+// body rows, launches the graph and reads the report back: one
+// synchronisation per step.
+// ---------------------------------------------------------------------------
+static unsigned long long slab_graph_key(const gg_ctx* ctx) {
+  const Dev& D = ctx->D;
+  unsigned long long k = 1469598103934665603ull;
+  auto mix = [&](unsigned long long v) { k = (k ^ v) * 1099511628211ull; };
+  mix(static_cast<unsigned long long>(D.nb));
+  mix(reinterpret_cast<uintptr_t>(D.bodies));
+  mix(reinterpret_cast<uintptr_t>(D.grids));
+  mix(reinterpret_cast<uintptr_t>(D.gvals));
+  mix(reinterpret_cast<uintptr_t>(D.cgeo));
+  mix(static_cast<unsigned long long>(D.wcap));
+  mix(static_cast<unsigned long long>(D.S));
+  mix(static_cast<unsigned long long>(ctx->pipeline));
+  mix(reinterpret_cast<uintptr_t>(ctx->mbox));
+  mix(static_cast<unsigned long long>(ctx->mbox_cap));
+  mix(reinterpret_cast<uintptr_t>(ctx->peer[0]));
+  mix(reinterpret_cast<uintptr_t>(ctx->peer[1]));
+  for (int a = 0; a < 3; ++a) mix(static_cast<unsigned long long>(D.mlo[a] * 64 + D.msh[a]));
+  return k;
+}
+
+static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
+  const long long cap = ctx->mbox_cap;
+  const long long ncap = ctx->n;  // particle capacity
+  Dev D = ctx->D;
+  D.n = D.n_own = static_cast<int>(ncap);
+  D.dn = ctx->d_n;
+  D.resort = 0;
+  D.key_morton = 0;
+  D.pipeline = ctx->pipeline;
+  unsigned long long* X = ctx->d_x;
+  const unsigned long long* dstep = ctx->d_step;
+  const int has_lo = ctx->slab.has_lo ? 1 : 0, has_hi = ctx->slab.has_hi ? 1 : 0;
+  const unsigned long long tmo = 20000000000ull;  // 20 s
+  k_batch_begin<<<1, 256, 0, s>>>(D);
+  k_x_prep<<<1, 32, 0, s>>>(X, ctx->d_n);
+  if (resort) {  // (results never depend on the physical order)
+    Dev R = D;
+    R.resort = 1;
+    R.key_morton = 1;
+    k_slab_set_n<<<1, 1, 0, s>>>(R);
+    int st = enqueue_sort_pass(ctx, R, s);
+    if (st != GG_OK) return st;
+    k_slab_commit_sorted<<<blocks_for(ncap), kBlock, 0, s>>>(R);
+  }
+  // migrants, then ghosts, through the neighbours' mailboxes
+  SlabRec* m_lo = ctx->peer[0] ? mailbox_rec(ctx->peer[0], cap, 0, 1) : nullptr;
+  SlabRec* m_hi = ctx->peer[1] ? mailbox_rec(ctx->peer[1], cap, 0, 0) : nullptr;
+  k_slab_emigrate<<<blocks_for(ncap), kBlock, 0, s>>>(D, ctx->slab, m_lo, m_hi, cap, X);
+  k_x_signal<<<1, 32, 0, s>>>(ctx->peer[0], ctx->peer[1], 0, 1, X, dstep, ctx->D.ctl, cap);
+  k_x_wait<<<1, 32, 0, s>>>(D, ctx->mbox, 0, 1, has_lo, has_hi, X, 5, tmo, dstep);
+  k_x_holes<<<blocks_for(ncap), kBlock, 0, s>>>(D, X, ctx->d_holes, ctx->d_movers, X);
+  k_x_fill<<<blocks_for(ncap), kBlock, 0, s>>>(D, ctx->d_holes, ctx->d_movers, X);
+  k_x_append<<<blocks_for(2 * cap), kBlock, 0, s>>>(D, ctx->mbox, cap, 0, X, 4, 5);
+  SlabRec* g_lo = ctx->peer[0] ? mailbox_rec(ctx->peer[0], cap, 1, 1) : nullptr;
+  SlabRec* g_hi = ctx->peer[1] ? mailbox_rec(ctx->peer[1], cap, 1, 0) : nullptr;
+  k_slab_ghosts<<<blocks_for(ncap), kBlock, 0, s>>>(D, ctx->slab, g_lo, g_hi, ctx->d_map[0], ctx->d_map[1],
+                                                    std::min<long long>(cap, ncap), X + 8, X + 7);
+  k_x_signal<<<1, 32, 0, s>>>(ctx->peer[0], ctx->peer[1], 1, 2, X + 8, dstep, ctx->D.ctl, cap);
+  k_x_wait<<<1, 32, 0, s>>>(D, ctx->mbox, 1, 2, has_lo, has_hi, X, 10, tmo, dstep);
+  k_x_append<<<blocks_for(2 * cap), kBlock, 0, s>>>(D, ctx->mbox, cap, 1, X, 7, 10);
+  k_x_counts<<<1, 32, 0, s>>>(X, ctx->d_n);
+  // contacts, sweeps with the per-sweep halo, integration and commit
+  k_slab_set_n<<<1, 1, 0, s>>>(D);
+  int st = enqueue_sort_pass(ctx, D, s);
+  if (st != GG_OK) return st;
+  launch_narrow(ctx, D, ncap, s);
+  const int S = D.S;
+  for (int sweep = 0; sweep < S; ++sweep) {
+    launch_sweep(D, sweep, ncap, s);
+    if (sweep < S - 1) {
+      const unsigned long long seq = static_cast<unsigned long long>(sweep) + 1;
+      k_halo_push<<<2, 1024, 0, s>>>(D, sweep, seq, ctx->peer[0], ctx->peer[1], cap, ctx->d_map[0],
+                                     ctx->d_map[1], 0, 0, X, dstep, static_cast<unsigned long long>(S - 1));
+      k_halo_pull<<<2, 1024, 0, s>>>(D, sweep, seq, ctx->mbox, cap, 0, 0, has_lo, has_hi, tmo, X, dstep,
+                                     static_cast<unsigned long long>(S - 1));
+    }
+  }
+  k_finish<<<finish_grid(ncap), kFinishBlock, 0, s>>>(D);
+  k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ncap));
+  k_x_done<<<1, 32, 0, s>>>(ctx->d_step);
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+static int build_slab_graphs(gg_ctx* ctx) {
+  for (int g = 0; g < 2; ++g) {
+    if (ctx->sgexec[g]) {
+      cudaGraphExecDestroy(ctx->sgexec[g]);
+      ctx->sgexec[g] = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int st = enqueue_slab_step(ctx, g, ctx->stream);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (st != GG_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture (slab step)");
+    e = cudaGraphInstantiate(&ctx->sgexec[g], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate (slab step)");
+  }
+  ctx->sgkey = slab_graph_key(ctx);
+  return GG_OK;
+}
+
+// One slab step on the peer-memory transport (replaces exchange_p2p +
+// detect + solve_p2p + finish): bodies for this step, re-sort flag; the
+// rank's StepReport (its owned particles) and body momentum; info[6] as
+// gg_slab_exchange_p2p's.
+int gg_slab_step_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t resort,
+                     gg_report* report, double* body_momentum, int64_t info[6]) {
+  int st = slab_check(ctx);
+  if (st != GG_OK) return st;
+  if (!ctx->mbox) return fail(ctx, GG_EINVAL, "gg_slab_mailbox has not been called");
+  if ((ctx->slab.has_lo && !ctx->peer[0]) || (ctx->slab.has_hi && !ctx->peer[1]))
+    return fail(ctx, GG_EINVAL, "slab neighbour mailbox not connected");
+  if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
+  for (int b = 0; b < n_bodies; ++b)
+    if (bodies[b].kind < GG_GEOM_SPHERE || bodies[b].kind > GG_GEOM_GRID ||
+        (bodies[b].kind == GG_GEOM_GRID && (bodies[b].grid_id < 0 || bodies[b].grid_id >= (int)ctx->grids.size())))
+      return fail(ctx, GG_EINVAL, "bad body");
+  DeviceGuard guard(ctx->device);
+  if (!ctx->d_x) {
+    CK(dalloc(ctx, &ctx->d_x, kXCount));
+    CK(cudaMallocHost(&ctx->h_x, sizeof(unsigned long long) * kXCount));
+  }
+  if (!ctx->d_n) {  // first graph step: the device takes over the counts
+    CK(dalloc(ctx, &ctx->d_n, 2));
+    CK(dalloc(ctx, &ctx->d_step, 1));
+    const int nn[2] = {static_cast<int>(ctx->n_own), static_cast<int>(ctx->n_own)};
+    CK(cudaMemcpy(ctx->d_n, nn, sizeof(nn), cudaMemcpyHostToDevice));
+    CK(cudaMemset(ctx->d_step, 0, sizeof(unsigned long long)));
+  }
+  st = stage_bodies(ctx, 1, bodies, n_bodies);
+  if (st != GG_OK) return st;
+  if (!ctx->sgexec[0] || ctx->sgkey != slab_graph_key(ctx)) {
+    st = build_slab_graphs(ctx);
+    if (st != GG_OK) return st;
+  }
+  CK(cudaGraphLaunch(ctx->sgexec[resort ? 1 : 0], ctx->stream));
+  ctx->launches += 40 + 3 * ctx->D.S;
+  ctx->last_batch = 1;
+  ctx->last_nb = n_bodies;
+  int dn[2] = {0, 0};
+  CK(cudaMemcpyAsync(ctx->h_x, ctx->d_x, sizeof(unsigned long long) * kXCount, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(dn, ctx->d_n, sizeof(dn), cudaMemcpyDeviceToHost, ctx->stream));
+  int32_t nd = 0, es = -1;
+  st = gg_sync(ctx, report, body_momentum, 1, &nd, &es);  // synchronises the stream
+  const unsigned long long* h = ctx->h_x;
+  ctx->n_own = ctx->n_cur = dn[1];
+  ctx->ghost_out[0] = static_cast<long long>(h[8]);
+  ctx->ghost_out[1] = static_cast<long long>(h[9]);
+  ctx->ghost_in[0] = ctx->ghost_in[1] = 0;  // dropped after the commit
+  if (info) {
+    info[0] = static_cast<int64_t>(h[0]);
+    info[1] = static_cast<int64_t>(h[1]);
+    info[2] = static_cast<int64_t>(h[5]);
+    info[3] = static_cast<int64_t>(h[6]);
+    info[4] = static_cast<int64_t>(h[10]);
+    info[5] = static_cast<int64_t>(h[11]);
+  }
+  if (st == GG_ECAPACITY && ctx->h_ctl->cap_needed == 0)
+    return fail(ctx, GG_ECAPACITY, "slab mailbox or particle capacity exceeded by migrants or ghosts");
+  if (st == GG_OK && nd != 1) return fail(ctx, GG_ECUDA, "slab step did not commit");
+  return st;
 }
 
 // The S sweeps of a slab step with the per-sweep peer-memory halo between

@@ -103,6 +103,10 @@ struct Dev {
   // contacts, are not swept (their w arrives by halo exchange) and are not
   // integrated.  n_own == n otherwise.
   int n_own;
+  // Slab steps replayed as a CUDA graph: the particle counts change on the
+  // device every step (migration, ghosts), so kernels take them from dn
+  // ({n, n_own}) and grids are sized for the capacity.  nullptr otherwise.
+  const int* dn;
   long long nh_tot;  // E * n_h: length of cnt / start
   HashCfg H;         // the per-env table (n_h buckets)
   uint32_t mmask;  // Morton key mask (power of two <= n_h, minus one)
@@ -164,6 +168,10 @@ struct Dev {
   Ctl* ctl;
 };
 
+
+// live particle counts: the device's (graph-replayed slab step) or the Dev's
+__device__ __forceinline__ int live_n(const Dev& D) { return D.dn ? __ldcg(D.dn) : D.n; }
+__device__ __forceinline__ int live_own(const Dev& D) { return D.dn ? __ldcg(D.dn + 1) : D.n_own; }
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void raise_err(Ctl* ctl, int code) {
@@ -1084,7 +1092,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   const float4* Xh = D.Xh;
   const int tid = threadIdx.x;
   const int k = base + tid;
-  const bool live = tid < count && k < D.n_own;
+  const bool live = tid < count && k < live_own(D);
   const int env = env_of(D, live ? k : D.n - 1);
   cstamp(D, 0);
   unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
@@ -1778,7 +1786,8 @@ __device__ __forceinline__ void integrate_range(const Dev& D, Ctl* ctl, int kb, 
   double ke = 0.0;
   unsigned long long kef = 0;  // E > 1: this thread's fixed-point sum for env kenv
   int kenv = env_of(D, kb < D.n ? kb : D.n - 1);
-  const int klim = kend < D.n_own ? kend : D.n_own;
+  const int own = live_own(D);
+  const int klim = kend < own ? kend : own;
   for (int k = kb; k < klim; k += kstep) {
     const float4 xo = L.x[k];
     const float4 vo = L.v[k];
@@ -1941,7 +1950,7 @@ __global__ void __launch_bounds__(kBlock) k_count(Dev D) {
   Ctl* ctl = D.ctl;
   if (ctl->err) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < D.n) ph_count(D, ctl, i, D.key_morton != 0);
+  if (i < live_n(D)) ph_count(D, ctl, i, D.key_morton != 0);
 }
 
 __global__ void __launch_bounds__(kBlock) k_scan_tiles(Dev D) {
@@ -1968,20 +1977,20 @@ __global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D, int tile_counts) {
 __global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
   if (D.ctl->err) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < D.n) ph_scatter(D, i);
+  if (i < live_n(D)) ph_scatter(D, i);
   ph_zero_counts(D, i, static_cast<long long>(gridDim.x) * blockDim.x);
 }
 
 __global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
   if (D.ctl->err) return;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < D.n) ph_resort(D, D.ctl, k);
+  if (k < live_n(D)) ph_resort(D, D.ctl, k);
 }
 
 __global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
   if (D.ctl->err) return;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < D.n) ph_fill(D, D.ctl, k);
+  if (k < live_n(D)) ph_fill(D, D.ctl, k);
 }
 
 // NarrowSmem (> 48 KB) is dynamic shared memory: launch with sizeof(NarrowSmem)
@@ -2003,7 +2012,7 @@ __global__ void __launch_bounds__(kNarrowBlock, GG_NARROW_MINB) k_narrow(Dev D) 
 #endif
 __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = k < D.n_own;
+  const bool live = k < live_own(D);
   SweepHead h;
   if (live) h.load(D, k);
   const Ctl* ctl = D.ctl;
@@ -2048,7 +2057,7 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
   __shared__ double s_imp[kSweepBlockK / 32][3][32];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const bool live = k < D.n_own;
+  const bool live = k < live_own(D);
   L2Pol pol;
   pol.init();
   SweepHead h;
@@ -2200,7 +2209,7 @@ __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
   __shared__ double smd[32];
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  integrate_range(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, D.n_own, gridDim.x * blockDim.x, smd);
+  integrate_range(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, live_own(D), gridDim.x * blockDim.x, smd);
 }
 
 __global__ void __launch_bounds__(kBlock) k_commit(Dev D, int nparts) {

@@ -39,7 +39,7 @@ __global__ void k_slab_emigrate(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
                                 SlabRec* __restrict__ send_hi, long long cap,
                                 unsigned long long* __restrict__ cnt) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= D.n_own) return;
+  if (k >= live_own(D)) return;
   const int cur = D.ctl->cur, u = D.ctl->ucur;
   const float4 x = D.X[cur][k];
   const long long cx = cell_coord(x.x, D.two_r);
@@ -142,12 +142,12 @@ __global__ void k_slab_halo_unpack(Dev D, int s, const float4* __restrict__ in, 
 }
 
 // start[E * n_h] = n for the current particle count (n varies per step)
-__global__ void k_slab_set_n(Dev D) { D.start[D.nh_tot] = static_cast<uint32_t>(D.n); }
+__global__ void k_slab_set_n(Dev D) { D.start[D.nh_tot] = static_cast<uint32_t>(live_n(D)); }
 
 // copy a Morton-re-sorted owned set (Xs, V0, UID[u^1]) back to the committed buffers
 __global__ void k_slab_commit_sorted(Dev D) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= D.n) return;
+  if (k >= live_n(D)) return;
   const int cur = D.ctl->cur, u = D.ctl->ucur;
   D.X[cur][k] = D.Xs[k];
   D.V[cur][k] = D.V0[k];
@@ -212,12 +212,18 @@ __host__ __device__ __forceinline__ size_t mailbox_bytes(long long cap) {
 }
 
 // block 0 -> the lo neighbour (its side 1), block 1 -> the hi neighbour (its side 0)
+// X != nullptr (graph-replayed step): the ghost counts are X[8], X[9] and the
+// sequence number is dstep * seq_mult + seq (a device step counter)
 __global__ void k_halo_push(Dev D, int s, unsigned long long seq, Mailbox* peer_lo, Mailbox* peer_hi,
                             long long cap, const int* __restrict__ map_lo, const int* __restrict__ map_hi,
-                            int n_lo, int n_hi) {
+                            int n_lo, int n_hi, const unsigned long long* __restrict__ X = nullptr,
+                            const unsigned long long* __restrict__ dstep = nullptr,
+                            unsigned long long seq_mult = 0) {
   const int side = blockIdx.x;  // 0: push to lo, 1: push to hi
   Mailbox* peer = side == 0 ? peer_lo : peer_hi;
-  const int m = side == 0 ? n_lo : n_hi;
+  if (dstep) seq += *dstep * seq_mult;
+  int m = side == 0 ? n_lo : n_hi;
+  if (X) m = static_cast<int>(min(X[8 + side], static_cast<unsigned long long>(cap)));
   if (peer == nullptr) return;  // block-uniform
   const int* map = side == 0 ? map_lo : map_hi;
   float4* dst = mailbox_data(peer, cap, s & 1, side == 0 ? 1 : 0);
@@ -239,8 +245,15 @@ __global__ void k_halo_push(Dev D, int s, unsigned long long seq, Mailbox* peer_
 // asymmetric.
 __global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine, long long cap,
                             int n_lo, int n_hi, int has_lo, int has_hi,
-                            unsigned long long timeout_ns) {
+                            unsigned long long timeout_ns, const unsigned long long* __restrict__ X = nullptr,
+                            const unsigned long long* __restrict__ dstep = nullptr,
+                            unsigned long long seq_mult = 0) {
   const int side = blockIdx.x;
+  if (dstep) seq += *dstep * seq_mult;
+  if (X) {
+    n_lo = static_cast<int>(min(X[10], static_cast<unsigned long long>(cap)));
+    n_hi = static_cast<int>(min(X[11], static_cast<unsigned long long>(cap)));
+  }
   const int m = side == 0 ? n_lo : n_hi;
   if (!(side == 0 ? has_lo : has_hi)) return;  // block-uniform: no neighbour on this side
   __shared__ int s_ok;
@@ -265,7 +278,7 @@ __global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine,
   __syncthreads();
   if (!s_ok || m == 0) return;
   const float4* src = mailbox_data(mine, cap, s & 1, side);
-  const int at = D.n_own + (side == 0 ? 0 : n_lo);
+  const int at = live_own(D) + (side == 0 ? 0 : n_lo);
   float4* W = D.W[s & 1];
   for (int i = threadIdx.x; i < m; i += blockDim.x) W[at + i] = src[i];
 }
@@ -287,8 +300,15 @@ constexpr int kXCount = 12;
 
 // publish this rank's records of `kind` to the neighbours: count, then flag
 __global__ void k_x_signal(Mailbox* peer_lo, Mailbox* peer_hi, int kind, unsigned long long seq,
-                           const unsigned long long* __restrict__ sent) {
+                           const unsigned long long* __restrict__ sent,
+                           const unsigned long long* __restrict__ dstep = nullptr, Ctl* ctl = nullptr,
+                           long long cap = 0) {
   if (threadIdx.x != 0) return;
+  if (dstep) seq += *dstep * 2;
+  // records beyond the mailbox were not delivered: the step fails (the host
+  // path checks the counts it reads back; a replayed graph reads none)
+  if (ctl && (sent[0] > static_cast<unsigned long long>(cap) || sent[1] > static_cast<unsigned long long>(cap)))
+    raise_err(ctl, GG_ECAPACITY);
   for (int side = 0; side < 2; ++side) {
     Mailbox* p = side == 0 ? peer_lo : peer_hi;
     if (!p) continue;
@@ -303,8 +323,10 @@ __global__ void k_x_signal(Mailbox* peer_lo, Mailbox* peer_hi, int kind, unsigne
 // wait for the neighbours' flags, read the counts they sent (0 without a
 // neighbour) into X[at], X[at + 1]; the departures' survivors count first
 __global__ void k_x_wait(Dev D, Mailbox* mine, int kind, unsigned long long seq, int has_lo, int has_hi,
-                         unsigned long long* __restrict__ X, int at, unsigned long long timeout_ns) {
+                         unsigned long long* __restrict__ X, int at, unsigned long long timeout_ns,
+                         const unsigned long long* __restrict__ dstep = nullptr) {
   if (threadIdx.x != 0) return;
+  if (dstep) seq += *dstep * 2;
   for (int side = 0; side < 2; ++side) {
     unsigned long long got = 0;
     if (side == 0 ? has_lo : has_hi) {
@@ -325,7 +347,7 @@ __global__ void k_x_wait(Dev D, Mailbox* mine, int kind, unsigned long long seq,
     }
     X[at + side] = got;
   }
-  if (kind == 0) X[4] = static_cast<unsigned long long>(D.n_own) - X[0] - X[1];
+  if (kind == 0) X[4] = static_cast<unsigned long long>(live_own(D)) - X[0] - X[1];
 }
 
 // holes below the survivors' count and survivors above it (k_slab_holes with
@@ -333,7 +355,7 @@ __global__ void k_x_wait(Dev D, Mailbox* mine, int kind, unsigned long long seq,
 __global__ void k_x_holes(Dev D, const unsigned long long* __restrict__ X, int* __restrict__ holes,
                           int* __restrict__ movers, unsigned long long* __restrict__ cnt) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= D.n_own) return;
+  if (k >= live_own(D)) return;
   const int n_stay = static_cast<int>(X[4]);
   const int uid = D.UID[D.ctl->ucur][k];
   if (k < n_stay && uid < 0) holes[atomicAdd(cnt + 2, 1ull)] = k;
@@ -371,6 +393,25 @@ __global__ void k_x_append(Dev D, Mailbox* mine, long long cap, int kind,
   D.X[cur][at] = make_float4(r.x.x, r.x.y, r.x.z, 0.f);
   D.V[cur][at] = make_float4(r.v.x, r.v.y, r.v.z, 0.f);
   D.UID[u][at] = __float_as_int(r.x.w);
+}
+
+
+// Graph-replayed slab step: the step's counts on the device.  k_x_prep:
+// exchange counters cleared, ghosts of the previous step dropped
+// (n = n_own); k_x_counts: the new counts after both exchanges; k_x_done: the
+// device step counter the sequence numbers derive from.
+__global__ void k_x_prep(unsigned long long* __restrict__ X, int* __restrict__ dn) {
+  const int t = threadIdx.x;
+  if (t < kXCount) X[t] = 0ull;
+  if (t == 0) dn[0] = dn[1];
+}
+__global__ void k_x_counts(const unsigned long long* __restrict__ X, int* __restrict__ dn) {
+  if (threadIdx.x != 0) return;
+  dn[1] = static_cast<int>(X[7]);
+  dn[0] = static_cast<int>(X[7] + X[10] + X[11]);
+}
+__global__ void k_x_done(unsigned long long* __restrict__ dstep) {
+  if (threadIdx.x == 0) *dstep += 1;
 }
 
 }  // namespace gg

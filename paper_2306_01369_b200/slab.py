@@ -24,11 +24,11 @@ Two transports.  ``halo="p2p"`` (the default under NCCL): every rank exports a
 mailbox through CUDA IPC and opens its neighbours'; migrants and ghosts are
 packed by kernels straight into the neighbours' mailboxes, counts and
 system-scope release flags are published on the device, the receiver waits
-on the device and appends (gg_slab_exchange_p2p: one host read-back of the
-new counts per step), and the S sweeps run with their per-sweep w halo pushed
-into the same mailboxes (gg_slab_solve_p2p: one call, no host work between
-sweeps) — no NCCL call on the step path, three host synchronisations per step
-(exchange counts, StepReport, its reduction).  ``halo="host"``: the library
+on the device and appends, and the S sweeps run with their per-sweep w halo
+pushed into the same mailboxes; the particle counts stay on the device and
+the whole step is replayed as one CUDA graph (gg_slab_step_p2p) — no NCCL
+call on the step path, one host synchronisation per step (the rank's
+StepReport) plus the report reduction.  ``halo="host"``: the library
 packs and unpacks device buffers (gg_slab_* pack/unpack) and this module
 moves them with torch.distributed point-to-point operations — NCCL on device
 buffers, or gloo staged through host memory (tests on CPU).
@@ -266,8 +266,6 @@ class SlabBed:
         if halo == "auto":  # peer memory whenever the ranks run NCCL on one node's GPUs
             halo = "p2p" if self.tr.backend == "nccl" else "host"
         self.halo = halo if world > 1 else "host"
-        self.seq = 0   # halo sequence (one per inner sweep)
-        self.xseq = 0  # exchange sequence (two per step: migrants, ghosts)
         if self.halo == "p2p":
             self._connect_mailboxes()
 
@@ -336,19 +334,23 @@ class SlabBed:
         resort = self.steps % self.resort_every == 0
         S = int(self.params.solver_iterations)
         if self.halo == "p2p":
-            # 1-2. (re-sort,) migration and ghosts through the neighbours'
-            # mailboxes, counts on the device, one read-back; 3. the sweeps
-            # with their peer-memory halos in one call
+            # the whole step — (re-sort,) migration and ghosts through the
+            # neighbours' mailboxes, contacts, sweeps with their peer-memory
+            # halos, integration, commit — as one CUDA graph replay; one
+            # synchronisation, for the rank's report
             info = np.zeros(6, dtype=np.int64)
-            self.xseq += 2
-            N.check(self.ctx, lib.gg_slab_exchange_p2p(self.ctx, self.xseq - 1, int(resort), N.ptr(info)),
-                    "slab exchange")
+            rep = np.zeros(1, dtype=N.REPORT_DTYPE)
+            bm = np.zeros((max(self.nb, 1), 3))
+            st = lib.gg_slab_step_p2p(self.ctx, N.ptr(row), self.nb, int(resort), N.ptr(rep), N.ptr(bm),
+                                      N.ptr(info))
+            if st != N.GG_OK:
+                from .engine import raise_status
+
+                raise_status(st, N.last_error(self.ctx), self.steps)
             self.migrated += int(info[0] + info[1])
             self.ghosts = (int(info[4]), int(info[5]))
-            N.check(self.ctx, lib.gg_slab_detect(self.ctx, N.ptr(row), self.nb), "slab detect")
-            N.check(self.ctx, lib.gg_slab_solve_p2p(self.ctx, self.seq), "slab solve")
-            self.seq += S - 1
-            return self._finish(lib)
+            self.steps += 1
+            return self._reduce(rep[0], bm[: self.nb])
         # 1. migration, 2. (re-sort) + ghosts
         sent, _ = self._swap(lib.gg_slab_migrate_pack, lib.gg_slab_migrate_unpack,
                              (self.s_lo, self.s_hi), (self.r_lo, self.r_hi))
@@ -362,10 +364,7 @@ class SlabBed:
         N.check(self.ctx, lib.gg_slab_detect(self.ctx, N.ptr(row), self.nb), "slab detect")
         for s in range(S):
             N.check(self.ctx, lib.gg_slab_sweep(self.ctx, s), "slab sweep")
-            if s < S - 1 and self.halo == "p2p":
-                self.seq += 1
-                N.check(self.ctx, lib.gg_slab_halo_p2p(self.ctx, s, self.seq), "halo p2p")
-            elif s < S - 1 and self.world > 1:
+            if s < S - 1 and self.world > 1:
                 N.check(self.ctx, lib.gg_slab_halo_pack(self.ctx, s, self._p(self.h_slo),
                                                         self._p(self.h_shi)), "halo pack")
                 self.tr.exchange(self.h_slo, n_out[0], self.h_shi, n_out[1], self.h_rlo, g_lo,
