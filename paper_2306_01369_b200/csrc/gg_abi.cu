@@ -167,9 +167,15 @@ int sweep_grid(long long n) { return static_cast<int>((n + kSweepBlock - 1) / kS
 // one per-particle sweep launch over particles [0, n): record-major by default
 void launch_sweep(const Dev& D, int it, long long n, cudaStream_t s) {
 #if GG_SWEEP_RM
-  k_sweep_rm<<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+  if (D.dn)
+    k_sweep_rm<true><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+  else
+    k_sweep_rm<false><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
 #else
-  k_sweep<<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+  if (D.dn)
+    k_sweep<true><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+  else
+    k_sweep<false><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
 #endif
 }
 #ifndef GG_FINISH_BLOCK
@@ -374,7 +380,10 @@ int env_report_blocks(const gg_ctx* ctx) {
 
 // The contact kernel of a step over particles [0, nn)
 void launch_narrow(gg_ctx* ctx, const Dev& D, long long nn, cudaStream_t s) {
-  k_narrow<<<narrow_blocks(nn), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+  if (D.dn)
+    k_narrow<true><<<narrow_blocks(nn), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+  else
+    k_narrow<false><<<narrow_blocks(nn), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
 }
 
 int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
@@ -388,7 +397,7 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
       else
         launch_sweep(D, it, ctx->n, s);
     }
-    k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
+    k_finish<false><<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
     k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ctx->n));
     if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
     CK(cudaGetLastError());
@@ -415,15 +424,26 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
 int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
   const int nbn = ctx->nblocks;
   // bucket/tile counts are zero on entry: the previous scatter zeroed them
-  k_count<<<nbn, kBlock, 0, s>>>(D);
+  if (D.dn)
+    k_count<true><<<nbn, kBlock, 0, s>>>(D);
+  else
+    k_count<false><<<nbn, kBlock, 0, s>>>(D);
   k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
   if (ctx->ntiles > kScanTopFree) k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
   k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D, ctx->ntiles <= kScanTopFree ? 1 : 0);
-  k_scatter<<<nbn, kBlock, 0, s>>>(D);
-  if (D.key_morton)
-    k_resort<<<nbn, kBlock, 0, s>>>(D);
-  else
-    k_fill<<<nbn, kBlock, 0, s>>>(D);
+  if (D.dn) {
+    k_scatter<true><<<nbn, kBlock, 0, s>>>(D);
+    if (D.key_morton)
+      k_resort<true><<<nbn, kBlock, 0, s>>>(D);
+    else
+      k_fill<true><<<nbn, kBlock, 0, s>>>(D);
+  } else {
+    k_scatter<false><<<nbn, kBlock, 0, s>>>(D);
+    if (D.key_morton)
+      k_resort<false><<<nbn, kBlock, 0, s>>>(D);
+    else
+      k_fill<false><<<nbn, kBlock, 0, s>>>(D);
+  }
   CK(cudaGetLastError());
   return GG_OK;
 }
@@ -528,7 +548,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
   }
   for (int pass = resort ? 0 : 1; pass < 2; ++pass) {
     const Dev D = pass_dev(ctx, resort, pass == 0 ? 1 : 0);
-    k_count<<<nbn, kBlock, 0, s>>>(D);
+    k_count<false><<<nbn, kBlock, 0, s>>>(D);
     mark(1);
     k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
     mark(2);
@@ -536,13 +556,13 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     mark(3);
     k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D, ctx->ntiles <= kScanTopFree ? 1 : 0);
     mark(4);
-    k_scatter<<<nbn, kBlock, 0, s>>>(D);
+    k_scatter<false><<<nbn, kBlock, 0, s>>>(D);
     mark(5);
     if (pass == 0) {
-      k_resort<<<nbn, kBlock, 0, s>>>(D);
+      k_resort<false><<<nbn, kBlock, 0, s>>>(D);
       mark(6);
     } else {
-      k_fill<<<nbn, kBlock, 0, s>>>(D);
+      k_fill<false><<<nbn, kBlock, 0, s>>>(D);
       mark(7);
     }
   }
@@ -562,7 +582,7 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
     }
     Dev Df = D;
     Df.env_kernel = ctx->E > 1 ? 1 : 0;
-    k_finish<<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(Df);
+    k_finish<false><<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(Df);
     k_commit<<<1, kBlock, 0, s>>>(Df, finish_grid(ctx->n));
     if (Df.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(Df);
     mark(13);
@@ -788,7 +808,9 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   CK(cudaMemset(D.cinfo, 0, sizeof(int2) * n));
   CK(dalloc(ctx, &D.bad, n));
   CK(cudaMemset(D.bad, 0, sizeof(int) * n));
-  CK(cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(k_narrow<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(sizeof(NarrowSmemN))));
+  CK(cudaFuncSetAttribute(k_narrow<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(sizeof(NarrowSmemN))));
   CK(cudaFuncSetAttribute(k_step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(sizeof(NarrowSmem))));
@@ -1227,7 +1249,7 @@ int gg_detect(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, gg_report* o
   if (st != GG_OK) return st;
   st = enqueue_sort_pass(ctx, D, s);
   if (st != GG_OK) return st;
-  k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
+  k_narrow<false><<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), s>>>(D);
   ctx->launches += 9;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
@@ -1740,7 +1762,7 @@ std::string nonfinite_message(gg_ctx* ctx, int err_step, std::vector<int> bad) {
     cudaStream_t st = ctx->stream;
     ok = begin_batch(ctx, st) == GG_OK && enqueue_sort_pass(ctx, D, st) == GG_OK;
     if (ok) {
-      k_narrow<<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), st>>>(D);
+      k_narrow<false><<<narrow_blocks(ctx->n), kNarrowBlock, sizeof(NarrowSmemN), st>>>(D);
       ctx->launches += 9;
       ok = cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess &&
            collect_contacts(ctx, recs) == GG_OK;
@@ -2500,7 +2522,7 @@ int gg_slab_finish(gg_ctx* ctx, gg_report* report, double* body_momentum) {
   if (st != GG_OK) return st;
   DeviceGuard guard(ctx->device);
   cudaStream_t s = ctx->stream;
-  k_finish<<<finish_grid(std::max<long long>(ctx->n_own, 1)), kFinishBlock, 0, s>>>(slab_dev(ctx));
+  k_finish<false><<<finish_grid(std::max<long long>(ctx->n_own, 1)), kFinishBlock, 0, s>>>(slab_dev(ctx));
   k_commit<<<1, kBlock, 0, s>>>(slab_dev(ctx), finish_grid(std::max<long long>(ctx->n_own, 1)));
   ctx->launches += 2;
   CK(cudaGetLastError());
@@ -2838,7 +2860,7 @@ static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
                                      static_cast<unsigned long long>(S - 1));
     }
   }
-  k_finish<<<finish_grid(ncap), kFinishBlock, 0, s>>>(D);
+  k_finish<true><<<finish_grid(ncap), kFinishBlock, 0, s>>>(D);
   k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ncap));
   k_x_done<<<1, 32, 0, s>>>(ctx->d_step);
   CK(cudaGetLastError());

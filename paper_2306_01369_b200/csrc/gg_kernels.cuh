@@ -170,8 +170,15 @@ struct Dev {
 
 
 // live particle counts: the device's (graph-replayed slab step) or the Dev's
-__device__ __forceinline__ int live_n(const Dev& D) { return D.dn ? __ldcg(D.dn) : D.n; }
-__device__ __forceinline__ int live_own(const Dev& D) { return D.dn ? __ldcg(D.dn + 1) : D.n_own; }
+// (DC: the kernel instantiation replayed in the slab graph; the others read
+// the by-value Dev and pay nothing for it)
+template <bool DC>
+__device__ __forceinline__ int live_n(const Dev& D) { return DC ? __ldcg(D.dn) : D.n; }
+template <bool DC>
+__device__ __forceinline__ int live_own(const Dev& D) { return DC ? __ldcg(D.dn + 1) : D.n_own; }
+// the slab kernels shared by the graph and the per-call paths decide at run time
+__device__ __forceinline__ int live_n_rt(const Dev& D) { return D.dn ? __ldcg(D.dn) : D.n; }
+__device__ __forceinline__ int live_own_rt(const Dev& D) { return D.dn ? __ldcg(D.dn + 1) : D.n_own; }
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void raise_err(Ctl* ctl, int code) {
@@ -1083,7 +1090,7 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
 //   owner stay in candidate order, then bodies in index order, so results
 //   do not depend on where the allocator put them.
 // Particles base .. base + count - 1 (count <= blockDim.x) belong to this block.
-template <class SM>
+template <class SM, bool DC = false>
 __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, int count,
                                             SM& sm) {
   // plain (coherent) loads: in the fused kernel these buffers are written
@@ -1092,7 +1099,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   const float4* Xh = D.Xh;
   const int tid = threadIdx.x;
   const int k = base + tid;
-  const bool live = tid < count && k < live_own(D);
+  const bool live = tid < count && k < live_own<DC>(D);
   const int env = env_of(D, live ? k : D.n - 1);
   cstamp(D, 0);
   unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
@@ -1779,14 +1786,13 @@ __device__ __forceinline__ void write_report(const Dev& D, gg_report& R, const A
 // the block's kinetic-energy partial in D.part[blockIdx.x] (E == 1; E > 1
 // adds to the per-env fixed-point sums).  Called by every thread.
 __device__ __forceinline__ void integrate_range(const Dev& D, Ctl* ctl, int kb, int kend, int kstep,
-                                                double* smd) {
+                                                double* smd, int own) {
   const int cur = ctl->cur;
   const Layout L = layout(D, ctl);
   const float4* Wf = D.W[(D.S - 1) & 1];
   double ke = 0.0;
   unsigned long long kef = 0;  // E > 1: this thread's fixed-point sum for env kenv
   int kenv = env_of(D, kb < D.n ? kb : D.n - 1);
-  const int own = live_own(D);
   const int klim = kend < own ? kend : own;
   for (int k = kb; k < klim; k += kstep) {
     const float4 xo = L.x[k];
@@ -1904,7 +1910,7 @@ __device__ __forceinline__ void commit_step(const Dev& D, Ctl* ctl, int nparts, 
 // of the last sweep: another thread's w is not ordered before this read).
 __device__ __forceinline__ void integrate_and_finish_range(const Dev& D, Ctl* ctl, int kb, int kend,
                                                            int kstep, double* smd, int* s_last) {
-  integrate_range(D, ctl, kb, kend, kstep, smd);
+  integrate_range(D, ctl, kb, kend, kstep, smd, D.n_own);
   if (threadIdx.x == 0) {
     __threadfence();
     *s_last = atomicAdd(&ctl->done_count, 1u) == gridDim.x - 1;
@@ -1946,11 +1952,12 @@ __global__ void __launch_bounds__(kBlock) k_env_reports(Dev D) {
 // ===========================================================================
 // Large-n drivers: one kernel per phase, one thread per element.
 // ===========================================================================
+template <bool DC>
 __global__ void __launch_bounds__(kBlock) k_count(Dev D) {
   Ctl* ctl = D.ctl;
   if (ctl->err) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < live_n(D)) ph_count(D, ctl, i, D.key_morton != 0);
+  if (i < live_n<DC>(D)) ph_count(D, ctl, i, D.key_morton != 0);
 }
 
 __global__ void __launch_bounds__(kBlock) k_scan_tiles(Dev D) {
@@ -1974,33 +1981,37 @@ __global__ void __launch_bounds__(kBlock) k_scan_apply(Dev D, int tile_counts) {
   ph_scan_apply(D, blockIdx.x, sm, tile_counts != 0);
 }
 
+template <bool DC>
 __global__ void __launch_bounds__(kBlock) k_scatter(Dev D) {
   if (D.ctl->err) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < live_n(D)) ph_scatter(D, i);
+  if (i < live_n<DC>(D)) ph_scatter(D, i);
   ph_zero_counts(D, i, static_cast<long long>(gridDim.x) * blockDim.x);
 }
 
+template <bool DC>
 __global__ void __launch_bounds__(kBlock) k_resort(Dev D) {
   if (D.ctl->err) return;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < live_n(D)) ph_resort(D, D.ctl, k);
+  if (k < live_n<DC>(D)) ph_resort(D, D.ctl, k);
 }
 
+template <bool DC>
 __global__ void __launch_bounds__(kBlock) k_fill(Dev D) {
   if (D.ctl->err) return;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < live_n(D)) ph_fill(D, D.ctl, k);
+  if (k < live_n<DC>(D)) ph_fill(D, D.ctl, k);
 }
 
 // NarrowSmem (> 48 KB) is dynamic shared memory: launch with sizeof(NarrowSmem)
 extern __shared__ __align__(16) unsigned char g_dsmem[];
 
+template <bool DC>
 __global__ void __launch_bounds__(kNarrowBlock, GG_NARROW_MINB) k_narrow(Dev D) {
   NarrowSmemN& sm = *reinterpret_cast<NarrowSmemN*>(g_dsmem);
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  ph_contacts(D, ctl, blockIdx.x * blockDim.x, blockDim.x, sm);
+  ph_contacts<NarrowSmemN, DC>(D, ctl, blockIdx.x * blockDim.x, blockDim.x, sm);
 }
 
 // One sweep, one thread per particle, no block barriers: the particle's
@@ -2010,9 +2021,10 @@ __global__ void __launch_bounds__(kNarrowBlock, GG_NARROW_MINB) k_narrow(Dev D) 
 #ifndef GG_SWEEP_MINB
 #define GG_SWEEP_MINB 4
 #endif
+template <bool DC>
 __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = k < live_own(D);
+  const bool live = k < live_own<DC>(D);
   SweepHead h;
   if (live) h.load(D, k);
   const Ctl* ctl = D.ctl;
@@ -2052,12 +2064,13 @@ static_assert(kSweepBlockK % 32 == 0 && kSweepBlockK <= kBlock, "sweep block: wh
 #ifndef GG_SWEEP_RM_MINB
 #define GG_SWEEP_RM_MINB 16
 #endif
+template <bool DC>
 __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev D, int s) {
   static_assert(kFixedSlots == 1, "record-major sweep: one fixed record slot per particle");
   __shared__ double s_imp[kSweepBlockK / 32][3][32];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const bool live = k < live_own(D);
+  const bool live = k < live_own<DC>(D);
   L2Pol pol;
   pol.init();
   SweepHead h;
@@ -2205,11 +2218,13 @@ __global__ void __launch_bounds__(kBlock) k_sweep_oneloop(Dev D, int s) {
 // Large-n integration: a pure stream (x, v, cinfo, w in; x, v out), one
 // particle per thread, a kinetic-energy partial per block; k_commit (one
 // block) then sums the partials in fixed order and commits the step.
+template <bool DC>
 __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
   __shared__ double smd[32];
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
-  integrate_range(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, live_own(D), gridDim.x * blockDim.x, smd);
+  const int own = live_own<DC>(D);
+  integrate_range(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, own, gridDim.x * blockDim.x, smd, own);
 }
 
 __global__ void __launch_bounds__(kBlock) k_commit(Dev D, int nparts) {

@@ -39,7 +39,7 @@ __global__ void k_slab_emigrate(Dev D, SlabCfg C, SlabRec* __restrict__ send_lo,
                                 SlabRec* __restrict__ send_hi, long long cap,
                                 unsigned long long* __restrict__ cnt) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= live_own(D)) return;
+  if (k >= live_own_rt(D)) return;
   const int cur = D.ctl->cur, u = D.ctl->ucur;
   const float4 x = D.X[cur][k];
   const long long cx = cell_coord(x.x, D.two_r);
@@ -142,12 +142,12 @@ __global__ void k_slab_halo_unpack(Dev D, int s, const float4* __restrict__ in, 
 }
 
 // start[E * n_h] = n for the current particle count (n varies per step)
-__global__ void k_slab_set_n(Dev D) { D.start[D.nh_tot] = static_cast<uint32_t>(live_n(D)); }
+__global__ void k_slab_set_n(Dev D) { D.start[D.nh_tot] = static_cast<uint32_t>(live_n_rt(D)); }
 
 // copy a Morton-re-sorted owned set (Xs, V0, UID[u^1]) back to the committed buffers
 __global__ void k_slab_commit_sorted(Dev D) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= live_n(D)) return;
+  if (k >= live_n_rt(D)) return;
   const int cur = D.ctl->cur, u = D.ctl->ucur;
   D.X[cur][k] = D.Xs[k];
   D.V[cur][k] = D.V0[k];
@@ -278,7 +278,7 @@ __global__ void k_halo_pull(Dev D, int s, unsigned long long seq, Mailbox* mine,
   __syncthreads();
   if (!s_ok || m == 0) return;
   const float4* src = mailbox_data(mine, cap, s & 1, side);
-  const int at = live_own(D) + (side == 0 ? 0 : n_lo);
+  const int at = live_own_rt(D) + (side == 0 ? 0 : n_lo);
   float4* W = D.W[s & 1];
   for (int i = threadIdx.x; i < m; i += blockDim.x) W[at + i] = src[i];
 }
@@ -347,7 +347,7 @@ __global__ void k_x_wait(Dev D, Mailbox* mine, int kind, unsigned long long seq,
     }
     X[at + side] = got;
   }
-  if (kind == 0) X[4] = static_cast<unsigned long long>(live_own(D)) - X[0] - X[1];
+  if (kind == 0) X[4] = static_cast<unsigned long long>(live_own_rt(D)) - X[0] - X[1];
 }
 
 // holes below the survivors' count and survivors above it (k_slab_holes with
@@ -355,7 +355,7 @@ __global__ void k_x_wait(Dev D, Mailbox* mine, int kind, unsigned long long seq,
 __global__ void k_x_holes(Dev D, const unsigned long long* __restrict__ X, int* __restrict__ holes,
                           int* __restrict__ movers, unsigned long long* __restrict__ cnt) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= live_own(D)) return;
+  if (k >= live_own_rt(D)) return;
   const int n_stay = static_cast<int>(X[4]);
   const int uid = D.UID[D.ctl->ucur][k];
   if (k < n_stay && uid < 0) holes[atomicAdd(cnt + 2, 1ull)] = k;
