@@ -2827,7 +2827,9 @@ static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
     if (st != GG_OK) return st;
     k_slab_commit_sorted<<<blocks_for(ncap), kBlock, 0, s>>>(R);
   }
+  const bool alone = !has_lo && !has_hi;  // one rank: nothing to exchange
   // migrants, then ghosts, through the neighbours' mailboxes
+  if (!alone) {
   SlabRec* m_lo = ctx->peer[0] ? mailbox_rec(ctx->peer[0], cap, 0, 1) : nullptr;
   SlabRec* m_hi = ctx->peer[1] ? mailbox_rec(ctx->peer[1], cap, 0, 0) : nullptr;
   k_slab_emigrate<<<blocks_for(ncap), kBlock, 0, s>>>(D, ctx->slab, m_lo, m_hi, cap, X);
@@ -2844,6 +2846,7 @@ static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
   k_x_wait<<<1, 32, 0, s>>>(D, ctx->mbox, 1, 2, has_lo, has_hi, X, 10, tmo, dstep);
   k_x_append<<<blocks_for(2 * cap), kBlock, 0, s>>>(D, ctx->mbox, cap, 1, X, 7, 10);
   k_x_counts<<<1, 32, 0, s>>>(X, ctx->d_n);
+  }
   // contacts, sweeps with the per-sweep halo, integration and commit
   k_slab_set_n<<<1, 1, 0, s>>>(D);
   int st = enqueue_sort_pass(ctx, D, s);
@@ -2852,7 +2855,7 @@ static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
   const int S = D.S;
   for (int sweep = 0; sweep < S; ++sweep) {
     launch_sweep(D, sweep, ncap, s);
-    if (sweep < S - 1) {
+    if (sweep < S - 1 && !alone) {
       const unsigned long long seq = static_cast<unsigned long long>(sweep) + 1;
       k_halo_push<<<2, 1024, 0, s>>>(D, sweep, seq, ctx->peer[0], ctx->peer[1], cap, ctx->d_map[0],
                                      ctx->d_map[1], 0, 0, X, dstep, static_cast<unsigned long long>(S - 1));

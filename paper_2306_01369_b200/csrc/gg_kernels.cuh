@@ -2008,6 +2008,8 @@ extern __shared__ __align__(16) unsigned char g_dsmem[];
 
 template <bool DC>
 __global__ void __launch_bounds__(kNarrowBlock, GG_NARROW_MINB) k_narrow(Dev D) {
+  // capacity-sized grid (slab graph): blocks past the owned particles leave
+  if (DC && static_cast<int>(blockIdx.x * blockDim.x) >= live_own<true>(D)) return;
   NarrowSmemN& sm = *reinterpret_cast<NarrowSmemN*>(g_dsmem);
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
@@ -2023,6 +2025,7 @@ __global__ void __launch_bounds__(kNarrowBlock, GG_NARROW_MINB) k_narrow(Dev D) 
 #endif
 template <bool DC>
 __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
+  if (DC && static_cast<int>(blockIdx.x * blockDim.x) >= live_own<true>(D)) return;  // (slab graph)
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = k < live_own<DC>(D);
   SweepHead h;
@@ -2066,6 +2069,7 @@ static_assert(kSweepBlockK % 32 == 0 && kSweepBlockK <= kBlock, "sweep block: wh
 #endif
 template <bool DC>
 __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev D, int s) {
+  if (DC && static_cast<int>(blockIdx.x * blockDim.x) >= live_own<true>(D)) return;  // (slab graph)
   static_assert(kFixedSlots == 1, "record-major sweep: one fixed record slot per particle");
   __shared__ double s_imp[kSweepBlockK / 32][3][32];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2224,6 +2228,10 @@ __global__ void __launch_bounds__(kBlock) k_finish(Dev D) {
   Ctl* ctl = D.ctl;
   if (block_should_exit(ctl)) return;
   const int own = live_own<DC>(D);
+  if (DC && static_cast<int>(blockIdx.x * blockDim.x) >= own) {  // (slab graph: capacity grid)
+    if (threadIdx.x == 0) D.part[blockIdx.x] = 0.0;
+    return;
+  }
   integrate_range(D, ctl, blockIdx.x * blockDim.x + threadIdx.x, own, gridDim.x * blockDim.x, smd, own);
 }
 

@@ -242,7 +242,8 @@ class SlabBed:
         lo, hi, has_lo, has_hi = slab_bounds(self.cuts, rank)
         mine = np.nonzero(owner_of(cx, self.cuts) == rank)[0]
         self.nb = len(scene.bodies)
-        self.cap = int(math.ceil(capacity * max(len(mine), 1) + 4096))
+        # (alone, a rank neither receives migrants nor ghosts)
+        self.cap = int(math.ceil((capacity if world > 1 else 1.0) * max(len(mine), 1) + 4096))
         self.resort_every = resort_every
         self.steps = 0
         self.migrated = 0  # particles this rank sent to its neighbours
@@ -263,9 +264,9 @@ class SlabBed:
         self._alloc()
         if halo not in ("auto", "host", "p2p"):
             raise ValueError("halo must be 'auto', 'host' or 'p2p'")
-        if halo == "auto":  # peer memory whenever the ranks run NCCL on one node's GPUs
-            halo = "p2p" if self.tr.backend == "nccl" else "host"
-        self.halo = halo if world > 1 else "host"
+        if halo == "auto":  # peer memory whenever the ranks run NCCL on one node's GPUs (or alone)
+            halo = "p2p" if (self.tr.backend == "nccl" or world == 1) else "host"
+        self.halo = halo
         if self.halo == "p2p":
             self._connect_mailboxes()
 
@@ -280,6 +281,8 @@ class SlabBed:
         cap = int(self.tr.allreduce(np.array([float(self.buf_cap)]), "max")[0])
         h = np.zeros(64, dtype=np.uint8)
         N.check(self.ctx, lib.gg_slab_mailbox(self.ctx, cap, N.ptr(h)), "mailbox")
+        if self.world == 1:  # no neighbours: the mailbox only backs the graph-replayed step
+            return
         handles = [None] * self.world
         td.all_gather_object(handles, h.tobytes())
         for side, peer in ((0, self.rank - 1), (1, self.rank + 1)):
