@@ -84,7 +84,7 @@ def parse():
     ap.add_argument("--pipeline", default="two-loops-split",
                     choices=["two-loops-split", "two-loops-fused", "one-loop"],
                     help="PipelineMode (loop structure; same results): the paper's Fig. 6 comparison")
-    ap.add_argument("--resort-every", type=int, default=8)
+    ap.add_argument("--resort-every", type=int, default=32)
     return ap.parse_args()
 
 

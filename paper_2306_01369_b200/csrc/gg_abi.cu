@@ -66,7 +66,7 @@ struct gg_ctx {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   bool graph_dirty = true;
   int solve_grid = 0;      // co-resident blocks of k_solve
-  int resort_every = 8;    // physical re-sort period (steps)
+  int resort_every = 32;   // physical re-sort period (steps; particles move << a cell per step)
   int solve_mode = 0;      // 0 auto, 1 coop solve, 2 plain persistent solve, 3 per-sweep, 4 fused step
   int pipeline = 0;        // PipelineMode of the captured graphs (GG_MODE_*)
   int fused_grid = 0;      // co-resident blocks of k_step_fused

@@ -225,7 +225,7 @@ class SlabBed:
 
     def __init__(self, scene, rank: int = 0, world: int = 1, device: int = 0,
                  backend: str | None = None, cuts: np.ndarray | None = None,
-                 capacity: float = 1.6, max_contacts: int = 16, resort_every: int = 8,
+                 capacity: float = 1.6, max_contacts: int = 16, resort_every: int = 32,
                  halo: str = "auto"):
         from .engine import Engine
 
