@@ -28,6 +28,21 @@ def val(d, key, scale=None):
     return x * mul
 
 
+def add_solve(ent, S=10):
+    """the logical k_solve of one step: S sweeps (record-major k_sweep_rm, or
+    k_sweep) + k_finish (+ k_commit)"""
+    sw = ent.get("k_sweep_rm") or ent.get("k_sweep")
+    fi = ent.get("k_finish")
+    if not sw or not fi:
+        return
+    co = ent.get("k_commit", {"dram_bytes_per_launch": 0.0, "ncu_us_per_launch": 0.0})
+    ent["k_solve"] = {"dram_bytes_per_launch": S * sw["dram_bytes_per_launch"] + fi["dram_bytes_per_launch"]
+                                               + co["dram_bytes_per_launch"],
+                      "ncu_us_per_launch": S * sw["ncu_us_per_launch"] + fi["ncu_us_per_launch"]
+                                           + co["ncu_us_per_launch"],
+                      "launches": 1, "source": f"{S} x sweep + k_finish + k_commit (cold-cache ncu replays)"}
+
+
 def main():
     out_path = sys.argv[1]
     try:
@@ -46,12 +61,7 @@ def main():
             ent[name] = {"dram_bytes_per_launch": sum(b for b, _ in lst) / len(lst),
                          "ncu_us_per_launch": sum(t for _, t in lst) / len(lst), "launches": len(lst),
                          "source": rep.split("/")[-1]}
-        if "k_sweep" in per and "k_finish" in per:
-            sw, fi = ent["k_sweep"], ent["k_finish"]
-            S = 10
-            ent["k_solve"] = {"dram_bytes_per_launch": S * sw["dram_bytes_per_launch"] + fi["dram_bytes_per_launch"],
-                              "ncu_us_per_launch": S * sw["ncu_us_per_launch"] + fi["ncu_us_per_launch"],
-                              "launches": 1, "source": "10 x k_sweep + k_finish (cold-cache ncu replays)"}
+        add_solve(ent)
     json.dump(summary, open(out_path, "w"), indent=1, sort_keys=True)
     print(json.dumps(summary, indent=1, sort_keys=True))
 
