@@ -160,7 +160,7 @@ int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock)
 #endif
 constexpr int kScanTopFree = GG_SCAN_TOP_FREE;
 #ifndef GG_SWEEP_BLOCK
-#define GG_SWEEP_BLOCK 64
+#define GG_SWEEP_BLOCK 32
 #endif
 constexpr int kSweepBlock = GG_SWEEP_BLOCK;  // k_sweep block size (<= kBlock)
 int sweep_grid(long long n) { return static_cast<int>((n + kSweepBlock - 1) / kSweepBlock); }

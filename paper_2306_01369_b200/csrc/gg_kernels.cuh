@@ -2054,7 +2054,7 @@ __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
 // per-particle loop paid two dependent round trips per extra record).
 // Warps whose lanes belong to two envs take the per-particle path.
 #ifndef GG_SWEEP_BLOCK
-#define GG_SWEEP_BLOCK 64
+#define GG_SWEEP_BLOCK 32
 #endif
 #ifndef GG_SWEEP_RM
 #define GG_SWEEP_RM 1
@@ -2065,7 +2065,7 @@ __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
 constexpr int kSweepBlockK = GG_SWEEP_BLOCK;
 static_assert(kSweepBlockK % 32 == 0 && kSweepBlockK <= kBlock, "sweep block: whole warps");
 #ifndef GG_SWEEP_RM_MINB
-#define GG_SWEEP_RM_MINB 16
+#define GG_SWEEP_RM_MINB 32
 #endif
 template <bool DC>
 __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev D, int s) {
