@@ -153,6 +153,11 @@ void dfree(gg_ctx* ctx, void* p) {
 }
 
 int blocks_for(long long n) { return static_cast<int>((n + kBlock - 1) / kBlock); }
+#ifndef GG_SORT_BLOCK
+#define GG_SORT_BLOCK 256
+#endif
+constexpr int kSortBlock = GG_SORT_BLOCK;  // count / scatter / fill / resort block size
+static_assert(kBlock % kSortBlock == 0, "sort blocks tile the kBlock grid");
 // up to this many scan tiles (2048 buckets each) k_scan_apply sums its
 // predecessor tiles itself and k_scan_top is not launched
 #ifndef GG_SCAN_TOP_FREE
@@ -422,27 +427,29 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
 }
 
 int enqueue_sort_pass(gg_ctx* ctx, const Dev& D, cudaStream_t s) {
-  const int nbn = ctx->nblocks;
+  // the per-particle sort kernels in kSortBlock-thread blocks (the same
+  // threads as ctx->nblocks x kBlock)
+  const int nbn = ctx->nblocks * (kBlock / kSortBlock);
   // bucket/tile counts are zero on entry: the previous scatter zeroed them
   if (D.dn)
-    k_count<true><<<nbn, kBlock, 0, s>>>(D);
+    k_count<true><<<nbn, kSortBlock, 0, s>>>(D);
   else
-    k_count<false><<<nbn, kBlock, 0, s>>>(D);
+    k_count<false><<<nbn, kSortBlock, 0, s>>>(D);
   k_scan_tiles<<<ctx->ntiles, kBlock, 0, s>>>(D);
   if (ctx->ntiles > kScanTopFree) k_scan_top<<<1, 1024, 0, s>>>(D, ctx->ntiles);
   k_scan_apply<<<ctx->ntiles, kBlock, 0, s>>>(D, ctx->ntiles <= kScanTopFree ? 1 : 0);
   if (D.dn) {
-    k_scatter<true><<<nbn, kBlock, 0, s>>>(D);
+    k_scatter<true><<<nbn, kSortBlock, 0, s>>>(D);
     if (D.key_morton)
-      k_resort<true><<<nbn, kBlock, 0, s>>>(D);
+      k_resort<true><<<nbn, kSortBlock, 0, s>>>(D);
     else
-      k_fill<true><<<nbn, kBlock, 0, s>>>(D);
+      k_fill<true><<<nbn, kSortBlock, 0, s>>>(D);
   } else {
-    k_scatter<false><<<nbn, kBlock, 0, s>>>(D);
+    k_scatter<false><<<nbn, kSortBlock, 0, s>>>(D);
     if (D.key_morton)
-      k_resort<false><<<nbn, kBlock, 0, s>>>(D);
+      k_resort<false><<<nbn, kSortBlock, 0, s>>>(D);
     else
-      k_fill<false><<<nbn, kBlock, 0, s>>>(D);
+      k_fill<false><<<nbn, kSortBlock, 0, s>>>(D);
   }
   CK(cudaGetLastError());
   return GG_OK;
