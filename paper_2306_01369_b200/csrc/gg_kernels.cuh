@@ -720,7 +720,7 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
 #endif
 constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidate copy
 #ifndef GG_KDEPTH
-#define GG_KDEPTH 6
+#define GG_KDEPTH 8
 #endif
 #ifndef GG_NARROW_MINB
 #define GG_NARROW_MINB 2
@@ -759,7 +759,7 @@ struct NarrowSmemT {
   unsigned long long u[32];
 };
 #ifndef GG_FUSED_KDEPTH
-#define GG_FUSED_KDEPTH GG_KDEPTH
+#define GG_FUSED_KDEPTH 6
 #endif
 #ifndef GG_FUSED_GROUPS
 #define GG_FUSED_GROUPS 3
