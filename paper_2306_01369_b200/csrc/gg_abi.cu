@@ -91,6 +91,7 @@ struct gg_ctx {
   unsigned long long* d_step = nullptr;  // slab steps replayed (the mailbox sequence numbers)
   cudaGraphExec_t sgexec[2] = {nullptr, nullptr};  // slab step graphs (plain, re-sort)
   unsigned long long sgkey = 0;          // what the slab graphs were built for
+  unsigned long long pgen = 0;           // bumped by every parameter / schedule change
   unsigned long long* h_scnt = nullptr;  // pinned mirror
   int* d_holes = nullptr;
   int* d_movers = nullptr;
@@ -954,6 +955,7 @@ int gg_set_params(gg_ctx* ctx, const gg_params* params) {
   ctx->P = *params;
   fill_params(ctx);
   ctx->graph_dirty = true;
+  ++ctx->pgen;
   return GG_OK;
 }
 
@@ -970,6 +972,7 @@ int gg_set_solve_mode(gg_ctx* ctx, int32_t mode) {
   if (!ctx || mode < 0 || mode > 8) return fail(ctx, GG_EINVAL, "solve mode must be 0..8");
   ctx->solve_mode = mode;
   ctx->graph_dirty = true;
+  ++ctx->pgen;
   return GG_OK;
 }
 
@@ -2806,6 +2809,7 @@ static unsigned long long slab_graph_key(const gg_ctx* ctx) {
   mix(static_cast<unsigned long long>(ctx->mbox_cap));
   mix(reinterpret_cast<uintptr_t>(ctx->peer[0]));
   mix(reinterpret_cast<uintptr_t>(ctx->peer[1]));
+  mix(ctx->pgen);
   for (int a = 0; a < 3; ++a) mix(static_cast<unsigned long long>(D.mlo[a] * 64 + D.msh[a]));
   return k;
 }
