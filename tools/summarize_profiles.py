@@ -73,9 +73,9 @@ if ncu.exists():
         if ln.endswith(".ncu-rep"):
             cap = Path(ln.strip()).stem
             continue
-        m = re.match(r"\s+--- (\S+)\(", ln)
+        m = re.match(r"\s+--- (?:void )?([A-Za-z_][A-Za-z_0-9]*)(<[^>]*>)?\(", ln)
         if m:
-            cur = (cap, m.group(1))
+            cur = (cap, m.group(1) + ("" if m.group(2) in (None, "<0>") else m.group(2)))
             if cur not in rows:
                 rows[cur] = {}
             continue
