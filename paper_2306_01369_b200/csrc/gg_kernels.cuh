@@ -1739,6 +1739,129 @@ struct RegContacts {
   }
 };
 
+// Record-major, register-resident sweeps for the fused kernel (one particle
+// per thread): a warp keeps its 32 particles' record 0 (one per lane) and its
+// first 64 CSR records (two per lane, ONE RECORD PER LANE per chunk) in
+// registers across the sweeps, like k_sweep_rm does per launch: a particle
+// with many contacts no longer makes its whole warp wait through a serial
+// loop.  The owner adds its records' impulses in record order (record 0,
+// then the CSR ones), exactly the sums of RegContacts::sweep.  A warp with
+// more than 64 CSR records re-reads its records every sweep
+// (sweep_particle_h).  Called by every lane of the warp.
+#ifndef GG_FUSED_RM
+#define GG_FUSED_RM 1
+#endif
+struct RegChunks {
+  int c;                  // this lane's particle's record count
+  uint32_t incl, excl, T;  // CSR records: inclusive / exclusive lane prefix, warp total
+  float4 g0, g1, g2;       // record 0; CSR records lane and 32 + lane
+  int j0, j1, j2;
+  long long wb;            // the warp's CSR region
+  float wx, wy, wz;        // this particle's w
+  bool fallback;           // T > 64: per-particle sweeps from memory
+
+  __device__ __forceinline__ void load(const Dev& D, int k, bool live, float4 w0) {
+    const int lane = threadIdx.x & 31;
+    c = 0;
+    j0 = j1 = j2 = kNullContact;
+    g0 = g1 = g2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+      const int2 ci = D.cinfo[k];
+      c = ci.y;
+      g0 = D.cgeo[k];
+      j0 = c > 0 ? D.coth[k] : kNullContact;
+    }
+    const uint32_t m = c > 1 ? static_cast<uint32_t>(c - 1) : 0u;
+    incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    T = __shfl_sync(0xffffffffu, incl, 31);
+    excl = incl - m;
+    wb = D.nrec0 + static_cast<long long>(k >> 5) * D.wcap;
+    fallback = T > 64;
+    if (!fallback) {
+      if (static_cast<uint32_t>(lane) < T) {
+        g1 = D.cgeo[wb + lane];
+        j1 = D.coth[wb + lane];
+      }
+      if (static_cast<uint32_t>(lane) + 32 < T) {
+        g2 = D.cgeo[wb + 32 + lane];
+        j2 = D.coth[wb + 32 + lane];
+      }
+    }
+    wx = w0.x;
+    wy = w0.y;
+    wz = w0.z;
+  }
+
+  // the chunk whose lane-record is (g, j) at record index cb + lane: impulses
+  // to shared memory, then each owner adds its records of the chunk in order
+  __device__ __forceinline__ void chunk(const Dev& D, const float4* Win, uint32_t cb, float4 g, int j,
+                                        double& ax, double& ay, double& az, SweepAcc& A,
+                                        double (*imp)[32]) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t r = cb + lane;
+    const bool mine = r < T && j != kNullContact;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (mine) q = (j >= 0) ? Win[j] : D.cvb[wb + r];
+    int o = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, o + st - 1);
+      if (v <= r) o += st;
+    }
+    o = o < 31 ? o : 31;
+    const float owx = __shfl_sync(0xffffffffu, wx, o);
+    const float owy = __shfl_sync(0xffffffffu, wy, o);
+    const float owz = __shfl_sync(0xffffffffu, wz, o);
+    double ix = 0.0, iy = 0.0, iz = 0.0;
+    if (mine) contact_impulse(D, owx, owy, owz, g, j, q, ix, iy, iz, A);
+    imp[0][lane] = ix;
+    imp[1][lane] = iy;
+    imp[2][lane] = iz;
+    __syncwarp();
+    const uint32_t a0 = excl > cb ? excl : cb;
+    const uint32_t a1 = incl < cb + 32 ? incl : cb + 32;
+    for (uint32_t rr = a0; rr < a1; ++rr) {
+      ax += imp[0][rr - cb];
+      ay += imp[1][rr - cb];
+      az += imp[2][rr - cb];
+    }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void sweep(const Dev& D, int k, bool live, const float4* Win, float4* Wout,
+                                        SweepAcc& A, double (*imp)[32]) {
+    if (fallback) {  // (warp-uniform)
+      if (live && c > 0) {
+        SweepHead h;
+        h.load(D, k);
+        sweep_particle_h(D, k, h, Win, Wout, A);
+      }
+      return;
+    }
+    const bool has0 = c > 0 && j0 != kNullContact;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (has0) q0 = (j0 >= 0) ? Win[j0] : D.cvb[k];
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    if (has0) contact_impulse(D, wx, wy, wz, g0, j0, q0, ax, ay, az, A);
+    if (T > 0) chunk(D, Win, 0, g1, j1, ax, ay, az, A, imp);
+    if (T > 32) chunk(D, Win, 32, g2, j2, ax, ay, az, A, imp);
+    if (c > 0) {
+      const float4 out = make_float4(static_cast<float>(static_cast<double>(wx) + ax),
+                                     static_cast<float>(static_cast<double>(wy) + ay),
+                                     static_cast<float>(static_cast<double>(wz) + az), 0.f);
+      Wout[k] = out;
+      wx = out.x;
+      wy = out.y;
+      wz = out.z;
+    }
+  }
+};
+
 // per-env kinetic energy (E > 1): sum |v|^2 in 64-bit fixed point (2^-32),
 // exact and order-independent like the body momentum
 constexpr double kKeScale = 4294967296.0;  // 2^32
@@ -2339,7 +2462,16 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
     __shared__ int s_nnb;
     RegContacts RC;
     RC.c = 0;
-    if (ok && kr_live) RC.load(D, kr, L.v[kr]);
+    const bool rm = GG_FUSED_RM && D.sweep_barrier;  // record-major register sweeps
+    // the chunk impulses live in the contact phase's pass queue (free now)
+    static_assert(sizeof(NarrowSmem::pass) >= sizeof(double) * 3 * 32 * (kBlock / 32), "impulse scratch");
+    double(*s_fimp)[3][32] = reinterpret_cast<double(*)[3][32]>(&sm.pass[0][0]);
+    RegChunks RK;
+    if (rm) {
+      RK.load(D, kr, ok && kr_live, kr_live ? L.v[kr] : make_float4(0.f, 0.f, 0.f, 0.f));
+    } else if (ok && kr_live) {
+      RC.load(D, kr, L.v[kr]);
+    }
     if (!D.sweep_barrier) {  // neighbour-block list for the flag-synchronised sweeps
       for (int w = threadIdx.x; w < kMaxFusedBlocks / 32; w += blockDim.x) s_nbmask[w] = 0u;
       __syncthreads();
@@ -2386,7 +2518,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
         ok = ok && s_flag == 0;
         stamp(D, ts);
       }
-      if (ok && kr_live) RC.sweep(D, kr, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+      if (rm) {
+        if (ok) RK.sweep(D, kr, kr_live, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A, s_fimp[threadIdx.x >> 5]);
+      } else if (ok && kr_live) {
+        RC.sweep(D, kr, (s == 0) ? L.v : D.W[(s - 1) & 1], D.W[s & 1], A);
+      }
       if (!D.sweep_barrier) {
         __syncthreads();
         if (threadIdx.x == 0)
