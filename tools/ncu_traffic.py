@@ -28,6 +28,15 @@ def val(d, key, scale=None):
     return x * mul
 
 
+def kname(raw):
+    """'void gg::k_sweep_rm<false>(gg::Dev, int)' -> 'k_sweep_rm' (the names
+    bench.py looks up; templated and plain kernels alike)"""
+    n = raw.split("(")[0].replace("gg::", "").strip()
+    if n.startswith("void "):
+        n = n[5:]
+    return n.split("<")[0].strip()
+
+
 def add_solve(ent, S=10):
     """the logical k_solve of one step: S sweeps (record-major k_sweep_rm, or
     k_sweep) + k_finish (+ k_commit)"""
@@ -43,7 +52,20 @@ def add_solve(ent, S=10):
                       "launches": 1, "source": f"{S} x sweep + k_finish + k_commit (cold-cache ncu replays)"}
 
 
+def renormalize(path):
+    """re-key an existing summary by kname() and recompute k_solve"""
+    summary = json.load(open(path))
+    for wl, ent in summary.items():
+        summary[wl] = {kname(k): v for k, v in ent.items() if k != "k_solve"}
+        add_solve(summary[wl])
+    json.dump(summary, open(path, "w"), indent=1, sort_keys=True)
+
+
 def main():
+    if sys.argv[1] == "--renormalize":
+        for p in sys.argv[2:]:
+            renormalize(p)
+        return
     out_path = sys.argv[1]
     try:
         summary = json.load(open(out_path))
@@ -53,7 +75,7 @@ def main():
         wl, rep = arg.split("=", 1)
         per = defaultdict(list)
         for d in rows(rep):
-            name = d["Kernel Name"][0].split("(")[0].replace("gg::", "")
+            name = kname(d["Kernel Name"][0])
             by = val(d, "dram__bytes_read.sum") + val(d, "dram__bytes_write.sum")
             per[name].append((by, val(d, "gpu__time_duration.sum")))
         ent = summary.setdefault(wl, {})
