@@ -112,3 +112,12 @@ def test_both_arms_print_the_same_config():
     a = json.loads(ours.stdout.strip().splitlines()[-1])
     b = json.loads(ref.stdout.strip().splitlines()[-1])
     assert a["config"] == b["config"] and a["metric"] == b["metric"] and a["unit"] == b["unit"]
+
+
+def test_roofline_traffic_resolves_for_each_top_kernel():
+    """roofline.traffic comes from the committed profiles/ncu_summary.json;
+    kernel names there are normalised (templated kernels included) so the
+    lookup the bench line makes finds a number for every top kernel."""
+    for kernel, wl in (("k_solve", "bed1m"), ("k_solve", "envs"), ("k_step_fused", "hero50k")):
+        t = bench.ncu_traffic(kernel, wl)
+        assert t is not None and t > 0, (kernel, wl)
