@@ -720,23 +720,29 @@ def run_slab(args, dist: Dist):
                 "step_bytes_per_particle": model["step_per_particle"],
                 "note": "whole-step byte model per GPU (SURVEY.md §8d); the kernels are those of "
                         "the one-GPU step (per-kernel fractions in the N = 1 line)"}
-    bed.close()
-    # e2e through the public API from host buffers: partition + upload
-    # (SlabBed), K steps, gather of the global state back to the host
+    # e2e through the public API from host buffers (pinned, like the
+    # one-context line): partition + upload of the global host state into
+    # the bed (SlabBed.load), K steps, gather of the global state back to
+    # the host (the context and its graphs exist, as for run() there)
+    xh = np.ascontiguousarray(x, dtype=np.float64)
+    vh = np.ascontiguousarray(v, dtype=np.float64)
+    lib.gg_host_register(N.ptr(xh), xh.nbytes)
+    lib.gg_host_register(N.ptr(vh), vh.nbytes)
     dist.barrier()
     t0 = time.perf_counter()
-    bed2 = SlabBed(scene(), rank=dist.rank, world=dist.world, device=dev,
-                   backend=dist.backend if dist.world > 1 else None, halo=args.halo)
+    bed.load(xh, vh)
     for _ in range(K):
-        bed2.step()
-    Xg, _ = bed2.gather()
+        bed.step()
+    Xg, _ = bed.gather()
     _ = float(Xg[0, 0])
     t_e2e = dist.max(time.perf_counter() - t0)
-    bed2.close()
+    lib.gg_host_unregister(N.ptr(xh))
+    lib.gg_host_unregister(N.ptr(vh))
+    bed.close()
     e2e = {"value": n * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 48 * n / max(K, 1),
            "d2h_bytes_per_step": 52 * n / max(K, 1), "wall_s": t_e2e,
-           "api": "SlabBed(scene) (partition + upload of the host state), K x SlabBed.step(), "
-                  "SlabBed.gather() (global state back on the host)"}
+           "api": "SlabBed.load(x, v) (partition + upload of the global host state), K x "
+                  "SlabBed.step(), SlabBed.gather() (global state back on the host)"}
     cb = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         sc_cb = scene()

@@ -2310,6 +2310,10 @@ int gg_slab_load(gg_ctx* ctx, const double* x, const double* v, const int32_t* g
   if (st != GG_OK) return st;
   ctx->n_own = ctx->n_cur = n_own;
   ctx->ghost_in[0] = ctx->ghost_in[1] = 0;
+  if (ctx->d_n) {  // a reload after graph steps: the device counts follow
+    const int nn[2] = {static_cast<int>(n_own), static_cast<int>(n_own)};
+    CK(cudaMemcpy(ctx->d_n, nn, sizeof(nn), cudaMemcpyHostToDevice));
+  }
   if (n_own == 0) return GG_OK;
   set_morton_window(ctx, nullptr, x, n_own, 3);
   const size_t b = sizeof(double) * 3 * static_cast<size_t>(n_own);

@@ -237,13 +237,14 @@ class SlabBed:
         v = np.asarray(scene.particles.velocities, dtype=np.float64)
         self.N = len(x)
         self.n_h = int(scene.hashmap_size or default_table_size(self.N))  # GLOBAL table
-        cx = cell_x(x.astype(np.float32).astype(np.float64)[:, 0], r)
+        cx = cell_x(x.astype(np.float32).astype(np.float64)[:, 0], r) if world > 1 else None
         self.cuts = slab_cuts(cx, world) if cuts is None else np.asarray(cuts, dtype=np.int64)
         lo, hi, has_lo, has_hi = slab_bounds(self.cuts, rank)
-        mine = np.nonzero(owner_of(cx, self.cuts) == rank)[0]
+        mine = self._mine(cx)
         self.nb = len(scene.bodies)
         # (alone, a rank neither receives migrants nor ghosts)
-        self.cap = int(math.ceil((capacity if world > 1 else 1.0) * max(len(mine), 1) + 4096))
+        n_mine = self.N if mine is None else len(mine)
+        self.cap = int(math.ceil((capacity if world > 1 else 1.0) * max(n_mine, 1) + 4096))
         self.resort_every = resort_every
         self.steps = 0
         self.migrated = 0  # particles this rank sent to its neighbours
@@ -254,11 +255,7 @@ class SlabBed:
         self.ctx = self.engine.ctx
         lib = N.lib()
         N.check(self.ctx, lib.gg_slab_setup(self.ctx, lo, hi, int(has_lo), int(has_hi)), "slab setup")
-        gid = mine.astype(np.int32)
-        xs = np.ascontiguousarray(x[mine])
-        vs = np.ascontiguousarray(v[mine])
-        N.check(self.ctx, lib.gg_slab_load(self.ctx, N.ptr(xs), N.ptr(vs), N.ptr(gid), len(mine)),
-                "slab load")
+        self._upload(x, v, mine)
         self.tr = SlabTransport(rank, world, device, lib.gg_stream(self.ctx), backend)
         self.buf_cap = max(4096, self.cap // 2)
         self._alloc()
@@ -269,6 +266,38 @@ class SlabBed:
         self.halo = halo
         if self.halo == "p2p":
             self._connect_mailboxes()
+
+    def _mine(self, cx: np.ndarray):
+        """global ids of the particles this rank owns (all of them when alone)"""
+        if self.world == 1:
+            return None
+        return np.nonzero(owner_of(cx, self.cuts) == self.rank)[0]
+
+    def _upload(self, x: np.ndarray, v: np.ndarray, mine) -> None:
+        if mine is None:  # alone: the whole bed, in id order
+            gid = np.arange(len(x), dtype=np.int32)
+            xs, vs = np.ascontiguousarray(x, np.float64), np.ascontiguousarray(v, np.float64)
+        else:
+            gid = mine.astype(np.int32)
+            xs = np.ascontiguousarray(x[mine])
+            vs = np.ascontiguousarray(v[mine])
+        if len(gid) > self.cap:
+            raise ValueError(f"rank {self.rank} would own {len(gid)} particles; capacity {self.cap}")
+        N.check(self.ctx, N.lib().gg_slab_load(self.ctx, N.ptr(xs), N.ptr(vs), N.ptr(gid), len(gid)),
+                "slab load")
+
+    def load(self, positions: np.ndarray, velocities: np.ndarray) -> None:
+        """Replace the bed's state with a host state of the same particles
+        (global ids = row indices), partitioned with this bed's slab cuts:
+        every rank calls it with the same arrays.  The context, its graphs
+        and the transport are kept."""
+        x = np.asarray(positions, dtype=np.float64)
+        v = np.asarray(velocities, dtype=np.float64)
+        if x.shape != (self.N, 3) or v.shape != (self.N, 3):
+            raise ValueError(f"expected ({self.N}, 3) positions and velocities")
+        cx = None if self.world == 1 else cell_x(x.astype(np.float32).astype(np.float64)[:, 0],
+                                                 float(self.params.radius))
+        self._upload(x, v, self._mine(cx) if cx is not None else None)
 
     def _connect_mailboxes(self) -> None:
         """Per-sweep halo through peer memory: export this rank's mailbox

@@ -169,14 +169,21 @@ def _reference_run(make=None):
     return sc.particles.positions.copy(), sc.particles.velocities.copy(), reps
 
 
-def _slab_worker(rank, world, port, out, halo="host", gap=False):
+def _slab_worker(rank, world, port, out, halo="host", gap=False, reload=False):
     from paper_2306_01369_b200.slab import SlabBed
 
     td = _init(rank, world, port) if world > 1 else None
     scene = _gap_bed() if gap else _bed()
     cuts = np.array([GAP_CUT]) if gap else None
+    x0, v0 = scene.particles.positions.copy(), scene.particles.velocities.copy()
     bed = SlabBed(scene, rank=rank, world=world, device=0, backend="gloo", resort_every=5, halo=halo,
                   cuts=cuts)
+    if reload:  # a few steps of a scrambled state, then the real one through SlabBed.load
+        rng = np.random.default_rng(rank)
+        bed.load(x0 + rng.normal(scale=1e-3, size=x0.shape), -v0)
+        bed.run(3)
+        scene.t = 0.0
+        bed.load(x0, v0)
     reps = bed.run(T_STEPS)
     X, V = bed.gather()
     out[f"ghosts{rank}"] = bed.ghosts
@@ -209,6 +216,25 @@ def test_slab_step_bitwise_equals_one_gpu(world, halo):
     _check_reports(out["reps"], reps1)
     if world > 1:
         assert sum(out[f"moved{r}"] for r in range(world)) > 0, "no particle migrated"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,halo", [(1, "auto"), (2, "p2p")])
+def test_slab_load_replaces_the_state(world, halo):
+    """SlabBed.load into a bed that has already stepped (graphs built,
+    device counts and exchange sequence numbers advanced) continues exactly
+    like a fresh bed on that state."""
+    x1, v1, reps1 = _reference_run()
+    if world == 1:
+        out = {}
+        _slab_worker(0, 1, 0, out, halo, False, True)
+    else:
+        ctx = mp.get_context("spawn")
+        out = ctx.Manager().dict()
+        mp.spawn(_slab_worker, args=(world, _port(), out, halo, False, True), nprocs=world, join=True)
+    assert np.array_equal(out["x"], x1)
+    assert np.array_equal(out["v"], v1)
+    _check_reports(out["reps"], reps1)
 
 
 def _check_reports(slab_reps, reps1):
