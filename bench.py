@@ -689,8 +689,7 @@ def run_slab(args, dist: Dist):
                   backend=dist.backend if dist.world > 1 else None, halo=args.halo)
     lib = N.lib()
     K, W = args.steps, args.warmup
-    for _ in range(W):
-        bed.step()
+    bed.run(W)
     stream = torch.cuda.ExternalStream(lib.gg_stream(bed.ctx), device=torch.device("cuda", dev))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -700,7 +699,7 @@ def run_slab(args, dist: Dist):
     dist.barrier()
     torch.cuda.synchronize(dev)
     e0.record(stream)
-    reps = [bed.step() for _ in range(K)]
+    reps = bed.run(K)  # (peer-memory transport: K steps back to back on the device)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     dist.barrier()
@@ -731,8 +730,7 @@ def run_slab(args, dist: Dist):
     dist.barrier()
     t0 = time.perf_counter()
     bed.load(xh, vh)
-    for _ in range(K):
-        bed.step()
+    bed.run(K)
     Xg, _ = bed.gather()
     _ = float(Xg[0, 0])
     t_e2e = dist.max(time.perf_counter() - t0)
@@ -741,8 +739,8 @@ def run_slab(args, dist: Dist):
     bed.close()
     e2e = {"value": n * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 48 * n / max(K, 1),
            "d2h_bytes_per_step": 52 * n / max(K, 1), "wall_s": t_e2e,
-           "api": "SlabBed.load(x, v) (partition + upload of the global host state), K x "
-                  "SlabBed.step(), SlabBed.gather() (global state back on the host)"}
+           "api": "SlabBed.load(x, v) (partition + upload of the global host state), "
+                  "SlabBed.run(K), SlabBed.gather() (global state back on the host)"}
     cb = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         sc_cb = scene()

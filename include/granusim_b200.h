@@ -477,6 +477,15 @@ int gg_slab_solve_p2p(gg_ctx* ctx, uint64_t seq);
  * A bed uses either this or the per-call entry points above, not both. */
 int gg_slab_step_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t resort,
                      gg_report* report, double* body_momentum, int64_t info[6]);
+/* n_steps slab steps (run, stepper.py:162-189, on the rank's slab) replayed
+ * back to back on the device: one batch reset, then the step graph per step
+ * with the bodies staged up front (bodies [n_steps][n_bodies]) and the
+ * re-sort flag of each step (resort [n_steps]); one synchronisation at the
+ * end for reports [n_steps] and body_momentum [n_steps][n_bodies][3].
+ * info[7]: the last step's info[6] as gg_slab_step_p2p's, then the particles
+ * this rank sent to its neighbours over the batch. */
+int gg_slab_run_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t n_steps,
+                    const int32_t* resort, gg_report* reports, double* body_momentum, int64_t info[7]);
 int gg_slab_get(gg_ctx* ctx, double* x, double* v, int32_t* gid, int64_t cap, int64_t* n_own);
 
 #ifdef __cplusplus

@@ -135,6 +135,7 @@ def _bind(lib: C.CDLL) -> None:
         "gg_slab_exchange_p2p": (C.c_int, [P, C.c_uint64, i32, P]),
         "gg_slab_solve_p2p": (C.c_int, [P, C.c_uint64]),
         "gg_slab_step_p2p": (C.c_int, [P, P, i32, i32, P, P, P]),
+        "gg_slab_run_p2p": (C.c_int, [P, P, i32, i32, P, P, P, P]),
         "gg_destroy": (C.c_int, [P]),
         "gg_last_error": (C.c_char_p, [P]),
         "gg_set_params": (C.c_int, [P, C.POINTER(GGParams)]),

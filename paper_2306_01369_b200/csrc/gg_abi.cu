@@ -89,7 +89,9 @@ struct gg_ctx {
   unsigned long long* h_x = nullptr;     // pinned mirror
   int* d_n = nullptr;                    // [2] {n, n_own} of a graph-replayed slab step
   unsigned long long* d_step = nullptr;  // slab steps replayed (the mailbox sequence numbers)
-  cudaGraphExec_t sgexec[2] = {nullptr, nullptr};  // slab step graphs (plain, re-sort)
+  // slab step graphs: [batched][re-sort] (batched: without the per-step
+  // batch reset, replayed K times after one k_batch_begin)
+  cudaGraphExec_t sgexec[4] = {nullptr, nullptr, nullptr, nullptr};
   unsigned long long sgkey = 0;          // what the slab graphs were built for
   unsigned long long pgen = 0;           // bumped by every parameter / schedule change
   unsigned long long* h_scnt = nullptr;  // pinned mirror
@@ -927,10 +929,10 @@ int gg_destroy(gg_ctx* ctx) {
   {
     DeviceGuard guard(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (int g = 0; g < 2; ++g) {
+    for (int g = 0; g < 2; ++g)
       if (ctx->gexec[g]) cudaGraphExecDestroy(ctx->gexec[g]);
+    for (int g = 0; g < 4; ++g)
       if (ctx->sgexec[g]) cudaGraphExecDestroy(ctx->sgexec[g]);
-    }
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
     for (int side = 0; side < 2; ++side)
       if (ctx->peer_ipc[side] && ctx->peer[side]) cudaIpcCloseMemHandle(ctx->peer[side]);
@@ -2806,6 +2808,8 @@ static unsigned long long slab_graph_key(const gg_ctx* ctx) {
   mix(reinterpret_cast<uintptr_t>(D.grids));
   mix(reinterpret_cast<uintptr_t>(D.gvals));
   mix(reinterpret_cast<uintptr_t>(D.cgeo));
+  mix(reinterpret_cast<uintptr_t>(D.reports));
+  mix(reinterpret_cast<uintptr_t>(D.bm_out));
   mix(static_cast<unsigned long long>(D.wcap));
   mix(static_cast<unsigned long long>(D.S));
   mix(static_cast<unsigned long long>(ctx->pipeline));
@@ -2818,7 +2822,7 @@ static unsigned long long slab_graph_key(const gg_ctx* ctx) {
   return k;
 }
 
-static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
+static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s, bool begin) {
   const long long cap = ctx->mbox_cap;
   const long long ncap = ctx->n;  // particle capacity
   Dev D = ctx->D;
@@ -2831,7 +2835,7 @@ static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
   const unsigned long long* dstep = ctx->d_step;
   const int has_lo = ctx->slab.has_lo ? 1 : 0, has_hi = ctx->slab.has_hi ? 1 : 0;
   const unsigned long long tmo = 20000000000ull;  // 20 s
-  k_batch_begin<<<1, 256, 0, s>>>(D);
+  if (begin) k_batch_begin<<<1, 256, 0, s>>>(D);
   k_x_prep<<<1, 32, 0, s>>>(X, ctx->d_n);
   if (resort) {  // (results never depend on the physical order)
     Dev R = D;
@@ -2880,20 +2884,20 @@ static int enqueue_slab_step(gg_ctx* ctx, int resort, cudaStream_t s) {
   }
   k_finish<true><<<finish_grid(ncap), kFinishBlock, 0, s>>>(D);
   k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ncap));
-  k_x_done<<<1, 32, 0, s>>>(ctx->d_step);
+  k_x_done<<<1, 32, 0, s>>>(ctx->d_step, X);
   CK(cudaGetLastError());
   return GG_OK;
 }
 
 static int build_slab_graphs(gg_ctx* ctx) {
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < 4; ++g) {
     if (ctx->sgexec[g]) {
       cudaGraphExecDestroy(ctx->sgexec[g]);
       ctx->sgexec[g] = nullptr;
     }
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    int st = enqueue_slab_step(ctx, g, ctx->stream);
+    int st = enqueue_slab_step(ctx, g & 1, ctx->stream, g < 2);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
     if (st != GG_OK) {
       if (graph) cudaGraphDestroy(graph);
@@ -2912,36 +2916,46 @@ static int build_slab_graphs(gg_ctx* ctx) {
 // detect + solve_p2p + finish): bodies for this step, re-sort flag; the
 // rank's StepReport (its owned particles) and body momentum; info[6] as
 // gg_slab_exchange_p2p's.
-int gg_slab_step_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t resort,
-                     gg_report* report, double* body_momentum, int64_t info[6]) {
+// checks, device counters, the staged body rows of n_steps steps and the
+// slab graphs (built on first use and whenever what they captured changed)
+static int slab_p2p_prepare(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t n_steps) {
   int st = slab_check(ctx);
   if (st != GG_OK) return st;
   if (!ctx->mbox) return fail(ctx, GG_EINVAL, "gg_slab_mailbox has not been called");
   if ((ctx->slab.has_lo && !ctx->peer[0]) || (ctx->slab.has_hi && !ctx->peer[1]))
     return fail(ctx, GG_EINVAL, "slab neighbour mailbox not connected");
+  if (n_steps < 1) return fail(ctx, GG_EINVAL, "n_steps must be >= 1");
   if (n_bodies < 0 || (n_bodies > 0 && !bodies)) return fail(ctx, GG_EINVAL, "bad bodies");
-  for (int b = 0; b < n_bodies; ++b)
+  for (long long b = 0; b < static_cast<long long>(n_bodies) * n_steps; ++b)
     if (bodies[b].kind < GG_GEOM_SPHERE || bodies[b].kind > GG_GEOM_GRID ||
         (bodies[b].kind == GG_GEOM_GRID && (bodies[b].grid_id < 0 || bodies[b].grid_id >= (int)ctx->grids.size())))
       return fail(ctx, GG_EINVAL, "bad body");
-  DeviceGuard guard(ctx->device);
   if (!ctx->d_x) {
     CK(dalloc(ctx, &ctx->d_x, kXCount));
     CK(cudaMallocHost(&ctx->h_x, sizeof(unsigned long long) * kXCount));
   }
   if (!ctx->d_n) {  // first graph step: the device takes over the counts
     CK(dalloc(ctx, &ctx->d_n, 2));
-    CK(dalloc(ctx, &ctx->d_step, 1));
+    CK(dalloc(ctx, &ctx->d_step, 2));  // {steps replayed, particles emigrated}
     const int nn[2] = {static_cast<int>(ctx->n_own), static_cast<int>(ctx->n_own)};
     CK(cudaMemcpy(ctx->d_n, nn, sizeof(nn), cudaMemcpyHostToDevice));
-    CK(cudaMemset(ctx->d_step, 0, sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->d_step, 0, 2 * sizeof(unsigned long long)));
   }
-  st = stage_bodies(ctx, 1, bodies, n_bodies);
+  st = stage_bodies(ctx, n_steps, bodies, n_bodies);
   if (st != GG_OK) return st;
   if (!ctx->sgexec[0] || ctx->sgkey != slab_graph_key(ctx)) {
     st = build_slab_graphs(ctx);
     if (st != GG_OK) return st;
   }
+  return GG_OK;
+}
+
+int gg_slab_step_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t resort,
+                     gg_report* report, double* body_momentum, int64_t info[6]) {
+  if (!ctx) return GG_EINVAL;
+  DeviceGuard guard(ctx->device);
+  int st = slab_p2p_prepare(ctx, bodies, n_bodies, 1);
+  if (st != GG_OK) return st;
   CK(cudaGraphLaunch(ctx->sgexec[resort ? 1 : 0], ctx->stream));
   ctx->launches += 40 + 3 * ctx->D.S;
   ctx->last_batch = 1;
@@ -2968,6 +2982,56 @@ int gg_slab_step_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32
   if (st == GG_ECAPACITY && ctx->h_ctl->cap_needed == 0)
     return fail(ctx, GG_ECAPACITY, "slab mailbox or particle capacity exceeded by migrants or ghosts");
   if (st == GG_OK && nd != 1) return fail(ctx, GG_ECUDA, "slab step did not commit");
+  return st;
+}
+
+// n_steps slab steps on the peer-memory transport, replayed back to back
+// (one batch reset, then the batched step graph per step; the host only
+// stages the bodies of every step up front and reads the reports once):
+// bodies[n_steps][n_bodies], resort[n_steps]; reports[n_steps] and
+// body_momentum[n_steps][n_bodies][3] of this rank's particles; info[7]: the
+// last step's info (as gg_slab_step_p2p's) and, in info[6], the particles
+// this rank sent to its neighbours over the whole batch.
+int gg_slab_run_p2p(gg_ctx* ctx, const gg_body* bodies, int32_t n_bodies, int32_t n_steps,
+                    const int32_t* resort, gg_report* reports, double* body_momentum, int64_t info[7]) {
+  if (!ctx) return GG_EINVAL;
+  if (!resort || !reports) return fail(ctx, GG_EINVAL, "null resort flags or reports");
+  DeviceGuard guard(ctx->device);
+  int st = slab_p2p_prepare(ctx, bodies, n_bodies, n_steps);  // (synchronises the stream)
+  if (st != GG_OK) return st;
+  unsigned long long ds0[2] = {0ull, 0ull};
+  CK(cudaMemcpy(ds0, ctx->d_step, sizeof(ds0), cudaMemcpyDeviceToHost));
+  k_batch_begin<<<1, 256, 0, ctx->stream>>>(ctx->D);
+  CK(cudaGetLastError());
+  for (int i = 0; i < n_steps; ++i) CK(cudaGraphLaunch(ctx->sgexec[2 + (resort[i] ? 1 : 0)], ctx->stream));
+  ctx->launches += 1 + static_cast<long long>(n_steps) * (39 + 3 * ctx->D.S);
+  ctx->last_batch = n_steps;
+  ctx->last_nb = n_bodies;
+  int dn[2] = {0, 0};
+  unsigned long long ds1[2] = {0ull, 0ull};
+  CK(cudaMemcpyAsync(ctx->h_x, ctx->d_x, sizeof(unsigned long long) * kXCount, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(dn, ctx->d_n, sizeof(dn), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ds1, ctx->d_step, sizeof(ds1), cudaMemcpyDeviceToHost, ctx->stream));
+  int32_t nd = 0, es = -1;
+  st = gg_sync(ctx, reports, body_momentum, n_steps, &nd, &es);  // synchronises the stream
+  const unsigned long long* h = ctx->h_x;
+  ctx->n_own = ctx->n_cur = dn[1];
+  ctx->ghost_out[0] = static_cast<long long>(h[8]);
+  ctx->ghost_out[1] = static_cast<long long>(h[9]);
+  ctx->ghost_in[0] = ctx->ghost_in[1] = 0;
+  if (info) {
+    info[0] = static_cast<int64_t>(h[0]);
+    info[1] = static_cast<int64_t>(h[1]);
+    info[2] = static_cast<int64_t>(h[5]);
+    info[3] = static_cast<int64_t>(h[6]);
+    info[4] = static_cast<int64_t>(h[10]);
+    info[5] = static_cast<int64_t>(h[11]);
+    info[6] = static_cast<int64_t>(ds1[1] - ds0[1]);
+  }
+  if (st == GG_ECAPACITY && ctx->h_ctl->cap_needed == 0)
+    return fail(ctx, GG_ECAPACITY, "slab mailbox or particle capacity exceeded by migrants or ghosts");
+  if (st == GG_OK && nd != n_steps) return fail(ctx, GG_ECUDA, "slab batch did not commit every step");
   return st;
 }
 

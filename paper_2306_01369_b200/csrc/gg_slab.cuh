@@ -410,8 +410,11 @@ __global__ void k_x_counts(const unsigned long long* __restrict__ X, int* __rest
   dn[1] = static_cast<int>(X[7]);
   dn[0] = static_cast<int>(X[7] + X[10] + X[11]);
 }
-__global__ void k_x_done(unsigned long long* __restrict__ dstep) {
-  if (threadIdx.x == 0) *dstep += 1;
+__global__ void k_x_done(unsigned long long* __restrict__ dstep, const unsigned long long* __restrict__ X) {
+  if (threadIdx.x == 0) {
+    dstep[0] += 1;
+    dstep[1] += X[0] + X[1];  // emigrants of this step (a running total)
+  }
 }
 
 }  // namespace gg

@@ -417,23 +417,71 @@ class SlabBed:
         return self._reduce(rep[0], bm[: self.nb])
 
     def _reduce(self, r, bm) -> StepReport:
-        sums = np.concatenate([[r["n_contacts"], r["n_candidates"], r["n_body_contacts"], r["n_coincident"],
-                                r["n_degenerate"], r["kinetic_energy"]], np.asarray(bm, np.float64).ravel()])
-        s, mx, mn = self.tr.reduce_packed(sums, [r["max_penetration"], r["max_cone_violation"]],
-                                          [r["min_normal_impulse"]])
-        bms = s[6:].reshape(-1, 3)
-        n_pp, n_cand = int(s[0]), int(s[1])
-        m = float(mn[0])
-        return StepReport(n_contacts=n_pp, n_candidates=n_cand,
-                          candidate_hit_rate=n_pp / max(n_cand, 1),
-                          max_penetration=float(mx[0]), kinetic_energy=float(s[5]),
-                          n_body_contacts=int(s[2]), n_coincident_skipped=int(s[3]),
-                          n_degenerate_skipped=int(s[4]), max_cone_violation=float(mx[1]),
-                          min_normal_impulse=m if np.isfinite(m) else 0.0,
-                          body_momentum=bms, step_index=self.steps - 1)
+        rr = np.zeros(1, dtype=N.REPORT_DTYPE)
+        rr[0] = r
+        return self._reduce_many(rr, np.asarray(bm, np.float64)[None])[0]
+
+    def _reduce_many(self, reps, bms) -> list[StepReport]:
+        """StepReports of len(reps) consecutive steps ending at self.steps - 1,
+        reduced over the ranks in ONE collective (per-step sums, maxes and
+        mins side by side)."""
+        K = len(reps)
+        nb = self.nb
+        cnt = np.stack([reps["n_contacts"], reps["n_candidates"], reps["n_body_contacts"],
+                        reps["n_coincident"], reps["n_degenerate"]], axis=1).astype(np.float64)
+        sums = np.concatenate([cnt, np.asarray(reps["kinetic_energy"], np.float64)[:, None],
+                               np.asarray(bms, np.float64)[:, :nb].reshape(K, 3 * nb)], axis=1)
+        maxes = np.stack([reps["max_penetration"], reps["max_cone_violation"]], axis=1)
+        mins = np.asarray(reps["min_normal_impulse"], np.float64)[:, None]
+        s, mx, mn = self.tr.reduce_packed(sums, maxes, mins)
+        s, mx, mn = s.reshape(K, -1), mx.reshape(K, 2), mn.reshape(K, 1)
+        out = []
+        for i in range(K):
+            n_pp, n_cand = int(s[i, 0]), int(s[i, 1])
+            m = float(mn[i, 0])
+            out.append(StepReport(n_contacts=n_pp, n_candidates=n_cand,
+                                  candidate_hit_rate=n_pp / max(n_cand, 1),
+                                  max_penetration=float(mx[i, 0]), kinetic_energy=float(s[i, 5]),
+                                  n_body_contacts=int(s[i, 2]), n_coincident_skipped=int(s[i, 3]),
+                                  n_degenerate_skipped=int(s[i, 4]), max_cone_violation=float(mx[i, 1]),
+                                  min_normal_impulse=m if np.isfinite(m) else 0.0,
+                                  body_momentum=s[i, 6:].reshape(-1, 3),
+                                  step_index=self.steps - K + i))
+        return out
 
     def run(self, n_steps: int) -> list[StepReport]:
-        return [self.step() for _ in range(n_steps)]
+        """``step`` n_steps times.  On the peer-memory transport the steps are
+        replayed back to back on the device (bodies of every step staged up
+        front, one synchronisation and one report collective for the batch);
+        the results are those of n_steps ``step`` calls, bit for bit."""
+        if n_steps < 0:
+            raise ValueError("n_steps must be >= 0")
+        if self.halo != "p2p" or n_steps < 2:
+            return [self.step() for _ in range(n_steps)]
+        lib = N.lib()
+        sc = self.scene
+        K, nbx = n_steps, max(self.nb, 1)
+        rows = np.zeros((K, nbx), dtype=N.BODY_DTYPE)
+        for i in range(K):  # body poses at t + dt of every step (stepper.py:65-67)
+            t = sc.t + sc.params.timestep
+            for b, body in enumerate(sc.bodies):
+                body.update(t)
+                self.engine.body_row(body, float(sc.params.radius), rows[i, b])
+            sc.t = t
+        resort = np.array([(self.steps + i) % self.resort_every == 0 for i in range(K)], dtype=np.int32)
+        info = np.zeros(7, dtype=np.int64)
+        reps = np.zeros(K, dtype=N.REPORT_DTYPE)
+        bm = np.zeros((K, nbx, 3))
+        st = lib.gg_slab_run_p2p(self.ctx, N.ptr(rows), self.nb, K, N.ptr(resort), N.ptr(reps), N.ptr(bm),
+                                 N.ptr(info))
+        if st != N.GG_OK:
+            from .engine import raise_status
+
+            raise_status(st, N.last_error(self.ctx), self.steps)
+        self.migrated += int(info[6])
+        self.ghosts = (int(info[4]), int(info[5]))
+        self.steps += K
+        return self._reduce_many(reps, bm)
 
     # -- state -----------------------------------------------------------------
     def owned_state(self):
