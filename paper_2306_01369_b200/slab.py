@@ -207,6 +207,39 @@ class SlabTransport:
         a, b = len(np.ravel(sums)), len(np.ravel(maxes))
         return rows[:, :a].sum(axis=0), rows[:, a:a + b].max(axis=0), rows[:, a + b:].min(axis=0)
 
+    def gather_rows(self, rows: np.ndarray) -> np.ndarray:
+        """Every rank's (n_r, w) float64 rows, concatenated in rank order, on
+        every rank: ONE all-gather of buffers padded to the longest (device
+        buffers under NCCL), instead of pickled objects."""
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        if self.world == 1:
+            return rows
+        torch = self.torch
+        n = rows.shape[0]
+        counts = self.allreduce_list(n)
+        nmax = max(max(counts), 1)
+        dev = self.dev if self.on_device else torch.device("cpu")
+        pad = np.zeros((nmax, rows.shape[1]))
+        pad[:n] = rows
+        t = torch.from_numpy(pad).to(dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        with self._ctx():
+            self.dist.all_gather(out, t)
+        got = torch.stack(out).cpu().numpy()
+        return np.concatenate([got[r, :counts[r]] for r in range(self.world)])
+
+    def allreduce_list(self, n: int) -> list[int]:
+        """every rank's integer n, in rank order"""
+        if self.world == 1:
+            return [int(n)]
+        torch = self.torch
+        dev = self.dev if self.on_device else torch.device("cpu")
+        t = torch.tensor([float(n)], dtype=torch.float64, device=dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        with self._ctx():
+            self.dist.all_gather(out, t)
+        return [int(o.item()) for o in out]
+
     def allreduce(self, vals: np.ndarray, op: str) -> np.ndarray:
         if self.world == 1:
             return vals
@@ -505,12 +538,9 @@ class SlabBed:
             V = np.zeros((self.N, 3))
             X[gid], V[gid] = x, v
             return X, V
-        import torch.distributed as td
-
-        parts = [None] * self.world
-        td.all_gather_object(parts, (x, v, gid))
+        rows = self.tr.gather_rows(np.concatenate([x, v, gid[:, None].astype(np.float64)], axis=1))
+        g = rows[:, 6].astype(np.int64)
         X = np.zeros((self.N, 3))
         V = np.zeros((self.N, 3))
-        for px, pv, pg in parts:
-            X[pg], V[pg] = px, pv
+        X[g], V[g] = rows[:, :3], rows[:, 3:6]
         return X, V

@@ -94,7 +94,8 @@ def _transport_worker(rank, world, port, out):
     tr.exchange(s_lo, n_lo, s_hi, n_hi, r_lo, m_lo, r_hi, m_hi)
     red = tr.allreduce(np.array([rank, 1.0]), "sum")
     packed = tr.reduce_packed([rank, 1.0], [float(rank)], [float(rank) + 3.0])
-    out[rank] = (m_lo, m_hi, r_lo[:m_lo].numpy().copy(), r_hi[:m_hi].numpy().copy(), red, packed)
+    rows = tr.gather_rows(np.full((rank, 7), float(rank)))  # ragged: rank 0 sends none
+    out[rank] = (m_lo, m_hi, r_lo[:m_lo].numpy().copy(), r_hi[:m_hi].numpy().copy(), red, packed, rows)
     td.destroy_process_group()
 
 
@@ -105,7 +106,9 @@ def test_transport_gloo_neighbour_exchange(world):
     out = mgr.dict()
     mp.spawn(_transport_worker, args=(world, _port(), out), nprocs=world, join=True)
     for r in range(world):
-        m_lo, m_hi, r_lo, r_hi, red, packed = out[r]
+        m_lo, m_hi, r_lo, r_hi, red, packed, rows = out[r]
+        want = np.concatenate([np.full((q, 7), float(q)) for q in range(world)])
+        assert rows.shape == want.shape and np.array_equal(rows, want)  # rank order, every rank
         if r > 0:  # from my lo neighbour: what it sent to ITS hi
             assert m_lo == (r - 1) + 2 and np.all(r_lo == (r - 1) + 0.5)
         else:
