@@ -1415,6 +1415,36 @@ __device__ __forceinline__ void sweep_acc_flush_nobar(const Dev& D, SweepAcc& A)
 // --fmad=false so that contact DECISIONS follow numpy's operation order;
 // the solver's arithmetic only has to meet the 1e-5 parity bar, and every
 // schedule evaluates this same function, so they stay bitwise identical).
+// The owner's adds of its records' impulses in chunk [cb, cb + 32): records
+// a0 .. a1 - 1 in order.  GG_OWNER_UNIFORM: every lane runs the warp's
+// largest count with predicated adds (no divergent loop); the same adds in
+// the same order either way.
+#ifndef GG_OWNER_UNIFORM
+#define GG_OWNER_UNIFORM 1
+#endif
+__device__ __forceinline__ void owner_sums(const double (*imp)[32], uint32_t a0, uint32_t a1, uint32_t cb,
+                                           double& ax, double& ay, double& az) {
+  if (GG_OWNER_UNIFORM) {
+    const uint32_t cnt = a1 > a0 ? a1 - a0 : 0u;
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, cnt);
+    const uint32_t b = a1 > a0 ? a0 - cb : 0u;
+    for (uint32_t q = 0; q < mx; ++q) {
+      const bool on = q < cnt;
+      const uint32_t i = on ? b + q : 0u;
+      const double vx = imp[0][i], vy = imp[1][i], vz = imp[2][i];
+      ax = on ? ax + vx : ax;
+      ay = on ? ay + vy : ay;
+      az = on ? az + vz : az;
+    }
+  } else {
+    for (uint32_t rr = a0; rr < a1; ++rr) {
+      ax += imp[0][rr - cb];
+      ay += imp[1][rr - cb];
+      az += imp[2][rr - cb];
+    }
+  }
+}
+
 __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
                                                 float4 g, int j, float4 q, double& ax, double& ay,
                                                 double& az, SweepAcc& A) {
@@ -1825,11 +1855,7 @@ struct RegChunks {
     __syncwarp();
     const uint32_t a0 = excl > cb ? excl : cb;
     const uint32_t a1 = incl < cb + 32 ? incl : cb + 32;
-    for (uint32_t rr = a0; rr < a1; ++rr) {
-      ax += imp[0][rr - cb];
-      ay += imp[1][rr - cb];
-      az += imp[2][rr - cb];
-    }
+    owner_sums(imp, a0, a1, cb, ax, ay, az);
     __syncwarp();
   }
 
@@ -2300,11 +2326,7 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
     // record adds +0.0, which leaves a sum that started at +0.0 unchanged)
     const uint32_t a0 = excl > cb ? excl : cb;
     const uint32_t a1 = incl < cb + 32 ? incl : cb + 32;
-    for (uint32_t rr = a0; rr < a1; ++rr) {
-      ax += s_imp[wi][0][rr - cb];
-      ay += s_imp[wi][1][rr - cb];
-      az += s_imp[wi][2][rr - cb];
-    }
+    owner_sums(s_imp[wi], a0, a1, cb, ax, ay, az);
     __syncwarp();
   }
   if (c > 0)
