@@ -725,6 +725,9 @@ constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidat
 #ifndef GG_NARROW_MINB
 #define GG_NARROW_MINB 2
 #endif
+#ifndef GG_PASS_PRED
+#define GG_PASS_PRED 1
+#endif
 constexpr int kPassCap = GG_PASSCAP;  // prefilter passes queued per owner (more: exact inline path)
 constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass that is no contact)
 constexpr int kWarps = kBlock / 32;
@@ -1214,12 +1217,23 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         // float32 pre-filter, conservative by a 1e-5 relative margin (the
         // float32 estimate is within ~4e-7 relative of the exact square)
         const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
+#if GG_PASS_PRED
+        // branch-free: every candidate is stored at the queue's next slot
+        // (a candidate that does not pass leaves a value the next pass
+        // overwrites, or one past the queue's end that nothing reads), and
+        // only passes advance it — no divergent branch per candidate
+        const bool valid = (i + u < total) & (__float_as_int(qf.w) != k);
+        const bool pass = valid & ((fx * fx + fy * fy + fz * fz <= rej) | all);
+        if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
+        npass += pass ? 1u : 0u;
+#else
         const bool pass = i + u < total && __float_as_int(qf.w) != k &&
                           (fx * fx + fy * fy + fz * fz <= rej || all);
         if (pass) {
           if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
           ++npass;
         }
+#endif
       }
     }
   }
