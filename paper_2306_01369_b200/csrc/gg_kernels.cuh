@@ -1156,6 +1156,17 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
 #pragma unroll
       for (int j = 0; j < kPerG; ++j) {
         const bool keep = eb[j] > sb[j] && !((dupmask >> (g * kPerG + j)) & 1u);
+#if GG_PASS_PRED
+        // branch-free: stored at the list's next entry, kept buckets advance
+        // it (a dropped one is overwritten by the next kept bucket or by the
+        // sentinel)
+        const uint32_t L = keep ? eb[j] - sb[j] : 0u;
+        total += L;
+        big |= L >= kLenSentinel;
+        sm.beg[nb][tid] = sb[j];
+        sm.len[nb][tid] = static_cast<NarrowLen>(L);
+        nb += keep ? 1 : 0;
+#else
         if (keep) {
           const uint32_t L = eb[j] - sb[j];
           total += L;
@@ -1164,6 +1175,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
           sm.len[nb][tid] = static_cast<NarrowLen>(L);
           ++nb;
         }
+#endif
       }
     }
     if (big) {
