@@ -1147,9 +1147,22 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
 #pragma unroll
     for (int g = 0; g < SM::kGroups; ++g) {
       uint32_t hb[kPerG], sb[kPerG], eb[kPerG];
+      // the table kind is tested once per round, not once per bucket
+      if (D.H.pow2) {
+#pragma unroll
+        for (int j = 0; j < kPerG; ++j) {
+          const int o = g * kPerG + j, ox = o / 9, oy = (o / 3) % 3, oz = o % 3;
+          hb[j] = (tx[ox] ^ ty[oy] ^ tz[oz]) & D.H.mask;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kPerG; ++j) {
+          const int o = g * kPerG + j;
+          hb[j] = hash_cell64(c0 + o / 9 - 1, c1 + (o / 3) % 3 - 1, c2 + o % 3 - 1, D.H.n_h);
+        }
+      }
 #pragma unroll
       for (int j = 0; j < kPerG; ++j) {
-        hb[j] = nb_hash(D, g * kPerG + j, c0, c1, c2, tx, ty, tz);
         sb[j] = start[hb[j]];
         eb[j] = start[hb[j] + 1];
       }
