@@ -1449,17 +1449,18 @@ __device__ __forceinline__ void sweep_acc_flush_nobar(const Dev& D, SweepAcc& A)
   }
 }
 
-// The impulse of one contact record on its owner (contact.py:463-488), in
-// float64 with explicit fused multiply-adds (the library is built with
-// --fmad=false so that contact DECISIONS follow numpy's operation order;
-// the solver's arithmetic only has to meet the 1e-5 parity bar, and every
-// schedule evaluates this same function, so they stay bitwise identical).
 // The owner's adds of its records' impulses in chunk [cb, cb + 32): records
 // a0 .. a1 - 1 in order.  GG_OWNER_UNIFORM: every lane runs the warp's
 // largest count with predicated adds (no divergent loop); the same adds in
 // the same order either way.
 #ifndef GG_OWNER_UNIFORM
 #define GG_OWNER_UNIFORM 1
+#endif
+#ifndef GG_SLIDE_PRED
+#define GG_SLIDE_PRED 0
+#endif
+#ifndef GG_MINE_PRED
+#define GG_MINE_PRED 0
 #endif
 __device__ __forceinline__ void owner_sums(const double (*imp)[32], uint32_t a0, uint32_t a1, uint32_t cb,
                                            double& ax, double& ay, double& az) {
@@ -1484,9 +1485,16 @@ __device__ __forceinline__ void owner_sums(const double (*imp)[32], uint32_t a0,
   }
 }
 
+// The impulse of one contact record on its owner (contact.py:463-488), in
+// float64 with explicit fused multiply-adds (the library is built with
+// --fmad=false so that contact DECISIONS follow numpy's operation order;
+// the solver's arithmetic only has to meet the 1e-5 parity bar, and every
+// schedule evaluates this same function, so they stay bitwise identical).
 __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double wy, double wz,
                                                 float4 g, int j, float4 q, double& ax, double& ay,
-                                                double& az, SweepAcc& A) {
+                                                double& az, SweepAcc& A, bool on = true) {
+  // on == false: evaluated but without effect (a lane with no record in a
+  // warp-uniform call; its inputs may be anything)
   const double eff = (j >= 0) ? 0.5 : 1.0;  // both partners mobile (contact.py:457-460)
   const double e1x = g.x, e1y = g.y, e1z = g.z;
   const double ng = -D.gamma;
@@ -1500,6 +1508,18 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
   double btx = fma(un, e1x, -ux), bty = fma(un, e1y, -uy), btz = fma(un, e1z, -uz);
   const double tn2 = fma(btz, btz, fma(bty, bty, btx * btx));
   const double lim = D.mu * b1;
+#if GG_SLIDE_PRED
+  {  // sliding: the projection below as selects (no divergent branch)
+    const bool slide = tn2 > lim * lim;
+    const double inv = rsqrt(slide ? tn2 : 1.0);
+    const double sc = lim * inv;
+    btx = slide ? btx * sc : btx;
+    bty = slide ? bty * sc : bty;
+    btz = slide ? btz * sc : btz;
+    const double viol = fma(tn2 * inv, sc, -lim);
+    A.maxviol = (on && slide && viol > A.maxviol) ? viol : A.maxviol;
+  }
+#else
   if (tn2 > lim * lim) {  // sliding: project onto the Coulomb cone
     // scale = lim / |bt| with one reciprocal square root (tn2 > lim^2 >= 0,
     // so tn2 > 0); 1-ulp accurate, far inside the 1e-5 parity bar
@@ -1509,16 +1529,17 @@ __device__ __forceinline__ void contact_impulse(const Dev& D, double wx, double 
     bty *= sc;
     btz *= sc;
     const double viol = fma(tn2 * inv, sc, -lim);
-    if (viol > A.maxviol) A.maxviol = viol;
+    if (on && viol > A.maxviol) A.maxviol = viol;
   }
+#endif
   const double ix = fma(e1x, b1, btx) * eff;
   const double iy = fma(e1y, b1, bty) * eff;
   const double iz = fma(e1z, b1, btz) * eff;
-  ax += ix;
-  ay += iy;
-  az += iz;
-  if (b1 < A.minb1) A.minb1 = b1;
-  if (j < 0) {  // reaction momentum on the body (contact.py:489-495)
+  ax = on ? ax + ix : ax;
+  ay = on ? ay + iy : ay;
+  az = on ? az + iz : az;
+  A.minb1 = (on && b1 < A.minb1) ? b1 : A.minb1;
+  if (on && j < 0) {  // reaction momentum on the body (contact.py:489-495)
     const int b = -j - 1;
     const unsigned long long fx = to_fix(-D.mass * ix), fy = to_fix(-D.mass * iy),
                              fz = to_fix(-D.mass * iz);
@@ -1887,7 +1908,10 @@ struct RegChunks {
     const float owy = __shfl_sync(0xffffffffu, wy, o);
     const float owz = __shfl_sync(0xffffffffu, wz, o);
     double ix = 0.0, iy = 0.0, iz = 0.0;
-    if (mine) contact_impulse(D, owx, owy, owz, g, j, q, ix, iy, iz, A);
+    if (GG_MINE_PRED)
+      contact_impulse(D, owx, owy, owz, g, j, q, ix, iy, iz, A, mine);
+    else if (mine)
+      contact_impulse(D, owx, owy, owz, g, j, q, ix, iy, iz, A);
     imp[0][lane] = ix;
     imp[1][lane] = iy;
     imp[2][lane] = iz;
@@ -2356,7 +2380,10 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
     const float owy = __shfl_sync(0xffffffffu, wf.y, o);
     const float owz = __shfl_sync(0xffffffffu, wf.z, o);
     double ix = 0.0, iy = 0.0, iz = 0.0;
-    if (mine) contact_impulse(D, owx, owy, owz, gc, jc, qc, ix, iy, iz, A);
+    if (GG_MINE_PRED)
+      contact_impulse(D, owx, owy, owz, gc, jc, qc, ix, iy, iz, A, mine);
+    else if (mine)
+      contact_impulse(D, owx, owy, owz, gc, jc, qc, ix, iy, iz, A);
     s_imp[wi][0][lane] = ix;
     s_imp[wi][1][lane] = iy;
     s_imp[wi][2][lane] = iz;
