@@ -728,6 +728,12 @@ constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidat
 #ifndef GG_PASS_PRED
 #define GG_PASS_PRED 1
 #endif
+#ifndef GG_CULL
+#define GG_CULL 1  // large-n contact kernel
+#endif
+#ifndef GG_FUSED_CULL
+#define GG_FUSED_CULL 0  // fused small-n kernel (measured slower there: a latency-bound chain)
+#endif
 constexpr int kPassCap = GG_PASSCAP;  // prefilter passes queued per owner (more: exact inline path)
 constexpr int kNullContact = 0x7fffffff;  // partner of a null record (a pass that is no contact)
 constexpr int kWarps = kBlock / 32;
@@ -1093,7 +1099,7 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
 //   owner stay in candidate order, then bodies in index order, so results
 //   do not depend on where the allocator put them.
 // Particles base .. base + count - 1 (count <= blockDim.x) belong to this block.
-template <class SM, bool DC = false>
+template <class SM, bool DC = false, bool CULL = (GG_CULL != 0)>
 __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, int count,
                                             SM& sm) {
   // plain (coherent) loads: in the fused kernel these buffers are written
@@ -1107,6 +1113,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
   cstamp(D, 0);
   unsigned long long n_cand = 0, n_coinc = 0, n_deg = 0;
   uint32_t total = 0, npass = 0;
+  uint32_t ttest = 0;  // candidates in the walked buckets (total less the culled ones)
   float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
   // ---- phase A ------------------------------------------------------------
   if (live) {
@@ -1125,6 +1132,28 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
       tz[d] = hash_term32(c2 + d - 1, kP2);
     }
     const bool dedup = !D.H.pow2 || may_alias(tx, ty, tz, D.H.mask);
+    // Geometric bucket culling: neighbour cell o's members lie in its box, so
+    // none is within reach if the box's nearest point is farther than the
+    // prefilter radius (+0.1%): such a bucket still counts its members as
+    // candidates (n_candidates) but is not walked.  Every prefilter pass
+    // survives, so the queue, the records and the results are unchanged.
+    // Off where one bucket may serve two neighbour cells (dedup) and where
+    // every candidate gets a record (TWO_LOOPS_FUSED).
+    const bool cull_on = CULL && !dedup && D.pipeline != 1;
+    float fq[3][3];  // per axis: squared distance to the lower / own / upper neighbour cell
+    {
+      const double pc[3] = {px, py, pz};
+      const long long cc[3] = {c0, c1, c2};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double lo = pc[a] - (static_cast<double>(cc[a]) - 0.5) * D.two_r;
+        const double hi = (static_cast<double>(cc[a]) + 0.5) * D.two_r - pc[a];
+        fq[a][0] = static_cast<float>(lo * lo);
+        fq[a][1] = 0.f;
+        fq[a][2] = static_cast<float>(hi * hi);
+      }
+    }
+    const float cull_d2 = D.reject_d2f * 1.001f;
     // bit o: neighbour o's bucket was already visited at an earlier offset
     // (rare: only particles whose 27 cells can alias run this loop; a real
     // branch, not predicated code every lane would issue)
@@ -1173,16 +1202,21 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         // branch-free: stored at the list's next entry, kept buckets advance
         // it (a dropped one is overwritten by the next kept bucket or by the
         // sentinel)
+        const int o = g * kPerG + j;  // (a constant: both loops are unrolled)
+        const bool reach = !cull_on || fq[0][o / 9] + fq[1][(o / 3) % 3] + fq[2][o % 3] <= cull_d2;
         const uint32_t L = keep ? eb[j] - sb[j] : 0u;
         total += L;
         big |= L >= kLenSentinel;
+        const uint32_t Lt = reach ? L : 0u;
+        ttest += Lt;
         sm.beg[nb][tid] = sb[j];
-        sm.len[nb][tid] = static_cast<NarrowLen>(L);
-        nb += keep ? 1 : 0;
+        sm.len[nb][tid] = static_cast<NarrowLen>(Lt);
+        nb += (keep && reach) ? 1 : 0;
 #else
         if (keep) {
           const uint32_t L = eb[j] - sb[j];
           total += L;
+          ttest += L;
           big |= L >= kLenSentinel;
           sm.beg[nb][tid] = sb[j];
           sm.len[nb][tid] = static_cast<NarrowLen>(L);
@@ -1215,6 +1249,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
           left -= c;
         }
       }
+      ttest = total;  // (every bucket walked)
     }
     cstamp(D, 1);
     n_cand = total - 1;  // minus the self pair (one per particle, broadphase.py:441-447)
@@ -1229,7 +1264,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     cur.init(sm, tid);
     constexpr int kDepth = SM::kDepth;  // candidates in flight per thread
     static_assert(kDepth <= kXhPad, "the sentinel bucket reads up to kDepth - 1 entries past n");
-    for (uint32_t i = 0; i < total; i += kDepth) {
+    for (uint32_t i = 0; i < ttest; i += kDepth) {
       uint32_t mi[kDepth];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) mi[u] = cur.next(sm, tid, true);
@@ -1247,12 +1282,12 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
         // (a candidate that does not pass leaves a value the next pass
         // overwrites, or one past the queue's end that nothing reads), and
         // only passes advance it — no divergent branch per candidate
-        const bool valid = (i + u < total) & (__float_as_int(qf.w) != k);
+        const bool valid = (i + u < ttest) & (__float_as_int(qf.w) != k);
         const bool pass = valid & ((fx * fx + fy * fy + fz * fz <= rej) | all);
         if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
         npass += pass ? 1u : 0u;
 #else
-        const bool pass = i + u < total && __float_as_int(qf.w) != k &&
+        const bool pass = i + u < ttest && __float_as_int(qf.w) != k &&
                           (fx * fx + fy * fy + fz * fz <= rej || all);
         if (pass) {
           if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
@@ -1263,7 +1298,7 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     }
   }
   cstamp(D, 2);
-  contacts_finish(D, ctl, base, sm, Xh, live, k, env, pf, total, npass, n_cand, n_coinc, n_deg);
+  contacts_finish(D, ctl, base, sm, Xh, live, k, env, pf, ttest, npass, n_cand, n_coinc, n_deg);
   cstamp(D, 7);
 }
 
@@ -2528,7 +2563,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   const bool kr_live = one_per_thread && kr < D.n_own;
   if (ok) {
     for (int base = blockIdx.x * blockDim.x; base < D.n; base += G)
-      ph_contacts(D, ctl, base, blockDim.x, sm);
+      ph_contacts<NarrowSmem, false, (GG_FUSED_CULL != 0)>(D, ctl, base, blockDim.x, sm);
   }
   stamp(D, ts);
   // split schedule: k_solve_cluster runs the sweeps and the commit (and
