@@ -896,6 +896,16 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   // (values never tested); zeroed so every read is of initialised memory
   CK(dalloc(ctx, &D.Xh, n + kXhPad));
   CK(cudaMemset(D.Xh, 0, sizeof(float4) * (n + kXhPad)));
+  {  // far padding after the particles: the contact kernel's list sentinel
+     // reads it, and nothing there ever passes the prefilter
+    float4 far[kXhPad];
+    const int none = -1;  // (w: no particle)
+    float wn;
+    std::memcpy(&wn, &none, sizeof(wn));
+    for (int i = 0; i < kXhPad; ++i) far[i] = make_float4(1e30f, 1e30f, 1e30f, wn);
+    CK(cudaMemcpy(D.Xh + n, far, sizeof(far), cudaMemcpyHostToDevice));
+    D.xh_pad = static_cast<int>(n);
+  }
   // one flag per block of any persistent launch (the commit of each resets
   // its grid's flags)
   ctx->nflags = std::max({ctx->fused_grid, ctx->solve_grid, ctx->staged_grid, kClusterCTAs, 1});

@@ -142,6 +142,7 @@ struct Dev {
   int* coth;        // partner: physical index, or -(body + 1)
   float4* cvb;      // body surface velocity (body records)
   int2* cinfo;      // per particle {CSR offset of its record 1, record count}
+  int xh_pad;       // Xh's allocated length: Xh[xh_pad .. xh_pad + kXhPad) is far padding
   int* bad;         // [n] uid + 1 of a particle whose correction was non-finite (0: fine)
   long long cap_tot;  // record capacity
   // Records 0 .. kFixedSlots-1 of particle k live at fixed indices i * n + k
@@ -731,6 +732,9 @@ constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidat
 #ifndef GG_CULL
 #define GG_CULL 1  // large-n contact kernel
 #endif
+#ifndef GG_FAR_SENTINEL
+#define GG_FAR_SENTINEL 1
+#endif
 #ifndef GG_FUSED_CULL
 #define GG_FUSED_CULL 0  // fused small-n kernel (measured slower there: a latency-bound chain)
 #endif
@@ -1084,6 +1088,53 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
                static_cast<unsigned long long>(c_b), n_deg, max_psi);
 }
 
+// The flat candidate loop of phase A over the thread's bucket list (ttest
+// candidates, kDepth in flight): the float32 prefilter, passes queued in
+// sm.pass.  CHK: every candidate is checked against ttest; without it the
+// sentinel entry points at Xh's far padding (GG_FAR_SENTINEL), whose
+// entries never pass the prefilter — not usable when every candidate passes
+// (TWO_LOOPS_FUSED).
+template <bool CHK, class SM>
+__device__ __forceinline__ void cand_loop(SM& sm, int tid, int k, float4 pf, const float4* Xh, uint32_t ttest,
+                                          float rej, bool all, uint32_t& npass) {
+  CandCursor cur;
+  cur.init(sm, tid);
+  constexpr int kDepth = SM::kDepth;  // candidates in flight per thread
+  static_assert(kDepth <= kXhPad, "the sentinel bucket reads up to kDepth - 1 entries past n");
+  for (uint32_t i = 0; i < ttest; i += kDepth) {
+    uint32_t mi[kDepth];
+#pragma unroll
+    for (int u = 0; u < kDepth; ++u) mi[u] = cur.next(sm, tid, true);
+    float4 qv[kDepth];
+#pragma unroll
+    for (int u = 0; u < kDepth; ++u) qv[u] = Xh[mi[u]];
+#pragma unroll
+    for (int u = 0; u < kDepth; ++u) {
+      const float4 qf = qv[u];
+      // float32 pre-filter, conservative by a 1e-5 relative margin (the
+      // float32 estimate is within ~4e-7 relative of the exact square)
+      const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
+#if GG_PASS_PRED
+      // branch-free: every candidate is stored at the queue's next slot
+      // (a candidate that does not pass leaves a value the next pass
+      // overwrites, or one past the queue's end that nothing reads), and
+      // only passes advance it — no divergent branch per candidate
+      const bool valid = (!CHK || i + u < ttest) & (__float_as_int(qf.w) != k);
+      const bool pass = valid & ((fx * fx + fy * fy + fz * fz <= rej) | all);
+      if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
+      npass += pass ? 1u : 0u;
+#else
+      const bool pass = (!CHK || i + u < ttest) && __float_as_int(qf.w) != k &&
+                        (fx * fx + fy * fy + fz * fz <= rej || all);
+      if (pass) {
+        if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
+        ++npass;
+      }
+#endif
+    }
+  }
+}
+
 // K5+K6: all contacts of particles base .. base+blockDim (contact.py:244-300).
 //
 // Phase A (per thread): the 27 neighbour-bucket bounds (three batches of 9
@@ -1099,7 +1150,7 @@ __device__ __forceinline__ void contacts_finish(const Dev& D, Ctl* ctl, int base
 //   owner stay in candidate order, then bodies in index order, so results
 //   do not depend on where the allocator put them.
 // Particles base .. base + count - 1 (count <= blockDim.x) belong to this block.
-template <class SM, bool DC = false, bool CULL = (GG_CULL != 0)>
+template <class SM, bool DC = false, bool CULL = (GG_CULL != 0), bool FAR = (GG_FAR_SENTINEL != 0)>
 __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, int count,
                                             SM& sm) {
   // plain (coherent) loads: in the fused kernel these buffers are written
@@ -1256,46 +1307,14 @@ __device__ __forceinline__ void ph_contacts(const Dev& D, Ctl* ctl, int base, in
     // sentinel after the last bucket: the cursor may run up to kDepth - 1
     // candidates past the end without a guard (indices < n + kXhPad: Xh is
     // padded; never tested)
-    sm.beg[nb][tid] = sm.beg[0][tid];
+    sm.beg[nb][tid] = FAR ? static_cast<uint32_t>(D.xh_pad) : sm.beg[0][tid];
     sm.len[nb][tid] = static_cast<NarrowLen>(kLenSentinel);
     const bool all = D.pipeline == 1;
     const float rej = D.reject_d2f;
-    CandCursor cur;
-    cur.init(sm, tid);
-    constexpr int kDepth = SM::kDepth;  // candidates in flight per thread
-    static_assert(kDepth <= kXhPad, "the sentinel bucket reads up to kDepth - 1 entries past n");
-    for (uint32_t i = 0; i < ttest; i += kDepth) {
-      uint32_t mi[kDepth];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) mi[u] = cur.next(sm, tid, true);
-      float4 qv[kDepth];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) qv[u] = Xh[mi[u]];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) {
-        const float4 qf = qv[u];
-        // float32 pre-filter, conservative by a 1e-5 relative margin (the
-        // float32 estimate is within ~4e-7 relative of the exact square)
-        const float fx = pf.x - qf.x, fy = pf.y - qf.y, fz = pf.z - qf.z;
-#if GG_PASS_PRED
-        // branch-free: every candidate is stored at the queue's next slot
-        // (a candidate that does not pass leaves a value the next pass
-        // overwrites, or one past the queue's end that nothing reads), and
-        // only passes advance it — no divergent branch per candidate
-        const bool valid = (i + u < ttest) & (__float_as_int(qf.w) != k);
-        const bool pass = valid & ((fx * fx + fy * fy + fz * fz <= rej) | all);
-        if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
-        npass += pass ? 1u : 0u;
-#else
-        const bool pass = i + u < ttest && __float_as_int(qf.w) != k &&
-                          (fx * fx + fy * fy + fz * fz <= rej || all);
-        if (pass) {
-          if (npass < kPassCap) sm.pass[npass][tid] = mi[u];
-          ++npass;
-        }
-#endif
-      }
-    }
+    if (FAR && !all)
+      cand_loop<false>(sm, tid, k, pf, Xh, ttest, rej, all, npass);
+    else
+      cand_loop<true>(sm, tid, k, pf, Xh, ttest, rej, all, npass);
   }
   cstamp(D, 2);
   contacts_finish(D, ctl, base, sm, Xh, live, k, env, pf, ttest, npass, n_cand, n_coinc, n_deg);
@@ -2563,7 +2582,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_step_fused(Dev D) {
   const bool kr_live = one_per_thread && kr < D.n_own;
   if (ok) {
     for (int base = blockIdx.x * blockDim.x; base < D.n; base += G)
-      ph_contacts<NarrowSmem, false, (GG_FUSED_CULL != 0)>(D, ctl, base, blockDim.x, sm);
+      ph_contacts<NarrowSmem, false, (GG_FUSED_CULL != 0), false>(D, ctl, base, blockDim.x, sm);
   }
   stamp(D, ts);
   // split schedule: k_solve_cluster runs the sweeps and the commit (and
