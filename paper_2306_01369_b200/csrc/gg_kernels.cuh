@@ -721,7 +721,7 @@ __device__ __forceinline__ double pp_write(const Dev& D, long long dst, double d
 #endif
 constexpr int kXhPad = 16;  // padding entries after the bucket-ordered candidate copy
 #ifndef GG_KDEPTH
-#define GG_KDEPTH 8
+#define GG_KDEPTH 6
 #endif
 #ifndef GG_NARROW_MINB
 #define GG_NARROW_MINB 2
