@@ -493,3 +493,32 @@ def test_huge_bucket_tiny_table():
     assert int(rep1["n_candidates"]) == n * (n - 1)
     assert np.array_equal(cs1.directed(), cs2.directed())
     assert int(rep1["n_contacts"]) == int(rep2["n_contacts"]) > 0
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_contacts_at_reach_across_cell_edges_and_corners(seed):
+    """Pairs at 2r (1 -/+ 1e-6) in random directions from random points of a
+    cell: partners land in the edge and corner neighbour cells at the limit
+    of reach, where the contact kernel's geometric bucket culling decides.
+    Directed contacts and counters bit-exact against the oracle."""
+    r = 0.05
+    rng = np.random.default_rng(seed)
+    m = 1500
+    base = np.stack(np.meshgrid(np.arange(12), np.arange(12), np.arange(11), indexing="ij"), -1)
+    base = base.reshape(-1, 3)[:m] * (20 * r)  # pairs 10 cells apart
+    p = base + rng.uniform(-r, r, size=(m, 3))  # anywhere in its cell (cell size 2r)
+    u = rng.normal(size=(m, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    scale = np.where(rng.random(m) < 0.5, 1.0 - 1e-6, 1.0 + 1e-6)[:, None]
+    q = p + u * (2.0 * r) * scale
+    x = np.concatenate([p, q]).astype(np.float32).astype(np.float64)
+    n_h = gg.default_table_size(len(x))
+    params = gg.MaterialParams(radius=r, timestep=5e-4)
+    cs, rep = device_detect(x, r, n_h, [], params=params)
+    oc, _ = O.detect(x, r, n_h, [])
+    got = directed_rows(cs.owner, cs.kind, cs.other)
+    want = directed_rows(oc.owner, oc.kind, oc.other)
+    assert len(want) > 0.8 * m  # about half the pairs touch, both directions each
+    assert np.array_equal(got, want)
+    assert int(rep["n_candidates"]) == int(oc.n_candidates)
+    assert int(rep["n_coincident"]) == int(oc.n_coincident)
