@@ -53,6 +53,37 @@ __global__ void k_cluster_barriers(int iters, int* out) {
   if (acc == -1) *out = acc;
 }
 
+// hierarchical grid barrier: a hardware cluster barrier, then ONE global
+// arrival per cluster (its rank-0 CTA), then a second cluster barrier that
+// releases the cluster; every CTA then makes one acquire load of the counter
+// (gpu-scope visibility of the other clusters' writes in its own L1)
+__global__ void k_hier_barriers(int iters, int csize) {
+  unsigned target = 0;
+  const unsigned nclusters = gridDim.x / csize;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = 0; i < iters; ++i) {
+    target += nclusters;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (rank == 0 && threadIdx.x == 0) {
+      unsigned v;
+      asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(v) : "l"(&g_count) : "memory");
+      v += 1;
+      while ((int)(v - target) < 0)
+        asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&g_count) : "memory");
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&g_count) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (rank != 0 && threadIdx.x == 0) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&g_count) : "memory");
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_chain(const int* __restrict__ next, int steps, int* out) {
   int p = threadIdx.x + blockIdx.x * blockDim.x;
   for (int i = 0; i < steps; ++i) p = next[p];
@@ -97,6 +128,35 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       printf("grid %d barrier variant %d: %.2f us per barrier (%s)\n", grid, var, ms * 1000 / iters,
              cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // 2a. hierarchical barriers (cluster + one global arrival per cluster)
+  for (int cs : {2, 4, 8}) {
+    for (int grid : {148, 296}) {
+      if (grid % cs) continue;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(256);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeCooperative;
+      attr[1].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      k_reset<<<1, 1, 0, s>>>();
+      cudaLaunchKernelEx(&cfg, k_hier_barriers, 10, cs);
+      k_reset<<<1, 1, 0, s>>>();
+      cudaEventRecord(a, s);
+      cudaLaunchKernelEx(&cfg, k_hier_barriers, iters, cs);
+      cudaEventRecord(b, s);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+      printf("grid %d hierarchical barrier, clusters of %d (cooperative): %.2f us per barrier (%s)\n", grid, cs,
+             ms * 1000 / iters, cudaGetErrorString(cudaGetLastError()));
     }
   }
   // 2b. cluster barriers
