@@ -824,6 +824,25 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
                           static_cast<int>(sizeof(NarrowSmemN))));
   CK(cudaFuncSetAttribute(k_step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(sizeof(NarrowSmem))));
+#ifndef GG_SWEEP_CARVE
+#define GG_SWEEP_CARVE -1
+#endif
+#ifndef GG_NARROW_CARVE
+#define GG_NARROW_CARVE -1
+#endif
+  // shared-memory carve-out preference (percent of the unified L1/shared
+  // array; -1 leaves the driver's choice)
+  if (GG_SWEEP_CARVE >= 0) {
+    CK(cudaFuncSetAttribute(k_sweep_rm<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            GG_SWEEP_CARVE));
+    CK(cudaFuncSetAttribute(k_sweep_rm<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            GG_SWEEP_CARVE));
+    CK(cudaFuncSetAttribute(k_finish<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            GG_SWEEP_CARVE));
+  }
+  if (GG_NARROW_CARVE >= 0)
+    CK(cudaFuncSetAttribute(k_narrow<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            GG_NARROW_CARVE));
   CK(dalloc(ctx, &D.acc, E));
   D.ke_fix = nullptr;
   if (E > 1) {
