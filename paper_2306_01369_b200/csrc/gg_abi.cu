@@ -171,11 +171,27 @@ constexpr int kScanTopFree = GG_SCAN_TOP_FREE;
 #define GG_SWEEP_BLOCK 32
 #endif
 constexpr int kSweepBlock = GG_SWEEP_BLOCK;  // k_sweep block size (<= kBlock)
+#ifndef GG_FINISH_BLOCK
+#define GG_FINISH_BLOCK 256
+#endif
+constexpr int kFinishBlockFin = GG_FINISH_BLOCK;
 int sweep_grid(long long n) { return static_cast<int>((n + kSweepBlock - 1) / kSweepBlock); }
 // one per-particle sweep launch over particles [0, n): record-major by default
-void launch_sweep(const Dev& D, int it, long long n, cudaStream_t s) {
+#ifndef GG_SWEEP_FIN
+#define GG_SWEEP_FIN 0  // measured slower; bitwise equal either way
+#endif
+// the last record-major sweep integrates too (no k_finish launch): one bed
+// (E == 1), not the slab graph's device-count variant
+bool sweep_fin(const Dev& D) {
+  return GG_SWEEP_RM && GG_SWEEP_FIN && kFinishBlockFin == kFinGroup && D.E == 1 && !D.dn &&
+         D.S >= 1 && D.pipeline != GG_MODE_ONE_LOOP;
+}
+// fin: the caller launches no k_finish after the last sweep (sweep_fin(D))
+void launch_sweep(const Dev& D, int it, long long n, cudaStream_t s, bool fin = false) {
 #if GG_SWEEP_RM
-  if (D.dn)
+  if (fin && it == D.S - 1)
+    k_sweep_rm<false, true><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
+  else if (D.dn)
     k_sweep_rm<true><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
   else
     k_sweep_rm<false><<<sweep_grid(n), kSweepBlock, 0, s>>>(D, it);
@@ -403,9 +419,9 @@ int launch_solve(gg_ctx* ctx, const Dev& D0, cudaStream_t s) {
       if (D.pipeline == GG_MODE_ONE_LOOP)
         k_sweep_oneloop<<<ctx->nblocks, kBlock, 0, s>>>(D, it);
       else
-        launch_sweep(D, it, ctx->n, s);
+        launch_sweep(D, it, ctx->n, s, sweep_fin(D));
     }
-    k_finish<false><<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
+    if (!sweep_fin(D)) k_finish<false><<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(D);
     k_commit<<<1, kBlock, 0, s>>>(D, finish_grid(ctx->n));
     if (D.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(D);
     CK(cudaGetLastError());
@@ -506,7 +522,7 @@ bool use_staged_solve(const gg_ctx* ctx);
 
 int kernels_per_step(const gg_ctx* ctx, int resort) {
   if (use_fused_step(ctx)) return use_cluster_solve(ctx) ? 2 : 1;
-  const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + 2;
+  const int solve = use_persistent_solve(ctx) ? 1 : ctx->D.S + (sweep_fin(ctx->D) ? 1 : 2);
   const int env_reports = (ctx->E > 1 && !use_persistent_solve(ctx)) ? 1 : 0;
   const int top = ctx->ntiles > kScanTopFree ? 1 : 0;  // k_scan_top per sort pass
   return 6 + top + solve + env_reports + (resort ? 5 + top : 0);
@@ -587,12 +603,12 @@ int enqueue_step_profiled(gg_ctx* ctx, int resort, cudaEvent_t* ev, int* kind_of
       if (D.pipeline == GG_MODE_ONE_LOOP)
         k_sweep_oneloop<<<nbn, kBlock, 0, s>>>(D, it);
       else
-        launch_sweep(D, it, ctx->n, s);
+        launch_sweep(D, it, ctx->n, s, sweep_fin(D));
       mark(12);
     }
     Dev Df = D;
     Df.env_kernel = ctx->E > 1 ? 1 : 0;
-    k_finish<false><<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(Df);
+    if (!sweep_fin(D)) k_finish<false><<<finish_grid(ctx->n), kFinishBlock, 0, s>>>(Df);
     k_commit<<<1, kBlock, 0, s>>>(Df, finish_grid(ctx->n));
     if (Df.env_kernel) k_env_reports<<<env_report_blocks(ctx), kBlock, 0, s>>>(Df);
     mark(13);
@@ -932,6 +948,9 @@ int gg_create_batched(int device, const gg_params* params, int32_t n_envs, int64
   CK(dalloc(ctx, &D.part, static_cast<size_t>(std::max({ctx->solve_grid, ctx->fused_grid, ctx->nblocks,
                                                           finish_grid(n), kClusterCTAs,
                                                           ctx->staged_grid}))));
+  CK(dalloc(ctx, &D.wpart, static_cast<size_t>(sweep_grid(n) * (kSweepBlock / 32))));
+  CK(dalloc(ctx, &D.gcnt, static_cast<size_t>(finish_grid(n))));
+  CK(cudaMemset(D.gcnt, 0, sizeof(unsigned) * finish_grid(n)));
   CK(dalloc(ctx, &D.bm_fix, static_cast<size_t>(std::max(ctx->max_bodies, 1)) * 3 * E));
   CK(dalloc(ctx, &D.stage_seg, static_cast<size_t>(std::max(ctx->staged_grid, 1))));
   CK(cudaMemset(D.bm_fix, 0, sizeof(unsigned long long) * std::max(ctx->max_bodies, 1) * 3 * E));

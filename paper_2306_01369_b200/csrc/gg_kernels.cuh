@@ -163,6 +163,8 @@ struct Dev {
   unsigned long long* tstamp;  // optional phase timestamps of the fused kernel (64)
   unsigned* bflags;  // [fused grid] per-block sweep progress (fused kernel)
   double* part;     // [nblocks_solve] per-block kinetic-energy partials
+  double* wpart;    // [n / 32] per-warp kinetic-energy partials (last sweep integrates)
+  unsigned* gcnt;   // [n / 256] warps of a 256-particle group done (reset by the last)
   unsigned long long* bm_fix;  // [nb][3] fixed-point body momentum of the step
   gg_report* reports;
   double* bm_out;  // [batch][nb][3]
@@ -2305,6 +2307,63 @@ __global__ void __launch_bounds__(kBlock, GG_SWEEP_MINB) k_sweep(Dev D, int s) {
   sweep_acc_flush_nobar(D, A);
 }
 
+// The last sweep integrates (GG_SWEEP_FIN, E == 1, one bed): the particle's
+// symplectic Euler step exactly as integrate_range with w from registers, and
+// the kinetic-energy partials in k_finish's order — a warp sum per 32
+// particles, then the 8 warps of each 256-particle group added in warp order
+// by the group's last warp (k_finish's block_reduce; warps past n add +0.0
+// there, which leaves the sum unchanged) — so k_commit sums the same
+// partials and every schedule stays bitwise identical.  Called by all lanes.
+constexpr int kFinGroup = 256;  // = k_finish's block size
+__device__ __forceinline__ void sweep_integrate(const Dev& D, int k, bool live, bool has, float4 wf) {
+  Ctl* ctl = D.ctl;
+  double v2 = 0.0;
+  if (live) {
+    const int cur = ctl->cur;
+    const Layout L = layout(D, ctl);
+    const float4 xo = L.x[k];
+    const float4 vo = L.v[k];
+    if (!has) wf = vo;
+    const double dvx = has ? (double)wf.x - (double)vo.x : 0.0;
+    const double dvy = has ? (double)wf.y - (double)vo.y : 0.0;
+    const double dvz = has ? (double)wf.z - (double)vo.z : 0.0;
+    if (!isfinite(dvx) || !isfinite(dvy) || !isfinite(dvz)) {
+      const int slot = atomicAdd(&ctl->n_bad, 1);
+      if (slot < kMaxBad) ctl->bad_uid[slot] = L.uid[k];
+      if (D.bad) D.bad[k] = L.uid[k] + 1;
+      raise_err(ctl, GG_ENONFINITE);
+    }
+    const double vx = __dadd_rn((double)vo.x, __dadd_rn(D.gdt0, dvx));
+    const double vy = __dadd_rn((double)vo.y, __dadd_rn(D.gdt1, dvy));
+    const double vz = __dadd_rn((double)vo.z, __dadd_rn(D.gdt2, dvz));
+    const double x = __dadd_rn((double)xo.x, __dmul_rn(D.dt, vx));
+    const double y = __dadd_rn((double)xo.y, __dmul_rn(D.dt, vy));
+    double z = __dadd_rn((double)xo.z, __dmul_rn(D.dt, vz));
+    if (D.has_boundary && z < D.z_min) z = __dadd_rn(z, D.band);  // stepper.py:138-144
+    D.X[cur ^ 1][k] = make_float4(static_cast<float>(x), static_cast<float>(y),
+                                  static_cast<float>(z), 0.f);
+    D.V[cur ^ 1][k] = make_float4(static_cast<float>(vx), static_cast<float>(vy),
+                                  static_cast<float>(vz), 0.f);
+    v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+  }
+  const double ws = warp_sum(v2);
+  if ((threadIdx.x & 31) == 0) {
+    constexpr int kW = kFinGroup / 32;
+    const int w = k >> 5, g = w / kW;
+    const int nwarps = (D.n_own + 31) >> 5;
+    const int nw = min(kW, nwarps - g * kW);
+    D.wpart[w] = ws;
+    __threadfence();
+    if (atomicAdd(&D.gcnt[g], 1u) == static_cast<unsigned>(nw - 1)) {
+      __threadfence();
+      double r = __ldcg(&D.wpart[g * kW]);
+      for (int q = 1; q < nw; ++q) r += __ldcg(&D.wpart[g * kW + q]);
+      D.part[g] = r;
+      D.gcnt[g] = 0u;
+    }
+  }
+}
+
 // Record-major sweep (the large-n default).  A warp sweeps the 32 particles
 // whose records the contact kernel allocated as one warp-contiguous block:
 // record 0 of each particle sits at its fixed index, records 1.. of all 32
@@ -2333,7 +2392,7 @@ static_assert(kSweepBlockK % 32 == 0 && kSweepBlockK <= kBlock, "sweep block: wh
 #ifndef GG_SWEEP_RM_MINB
 #define GG_SWEEP_RM_MINB 32
 #endif
-template <bool DC>
+template <bool DC, bool FIN = false>
 __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev D, int s) {
   if (DC && static_cast<int>(blockIdx.x * blockDim.x) >= live_own<true>(D)) return;  // (slab graph)
   static_assert(kFixedSlots == 1, "record-major sweep: one fixed record slot per particle");
@@ -2363,6 +2422,19 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
     j = ld_hint(&D.coth[wb + lane], pol.first, kHintRec);
   }
   const Ctl* ctl = D.ctl;
+#ifndef GG_FIN_PREFETCH
+#define GG_FIN_PREFETCH 1
+#endif
+  if (FIN && GG_FIN_PREFETCH && live) {  // the integration's x, v into L1 while the sweep runs
+    const Layout L = layout(D, ctl);
+#if defined(GG_FIN_L2) && GG_FIN_L2
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(L.x + k));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(L.v + k));
+#else
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(L.x + k));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(L.v + k));
+#endif
+  }
   if (*((volatile const int*)&ctl->err) != 0) return;  // uniform: nothing raises during sweeps
   const float4* Win = (s == 0) ? layout(D, ctl).v : D.W[(s - 1) & 1];
   float4* Wout = D.W[s & 1];
@@ -2372,6 +2444,7 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
   if (D.E > 1 && !warp_env_uniform(env_of(D, live ? k : D.n - 1), &e0)) {
     if (live) sweep_particle_h(D, k, h, Win, Wout, A);
     sweep_acc_flush_nobar(D, A);
+    if (FIN) sweep_integrate(D, k, live, h.ci.y > 0, h.ci.y > 0 ? Wout[k] : make_float4(0.f, 0.f, 0.f, 0.f));
     return;
   }
   const int c = h.ci.y;
@@ -2389,6 +2462,7 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
   if (T > GG_RM_MAXT) {
     if (live) sweep_particle_h(D, k, h, Win, Wout, A);
     sweep_acc_flush_nobar(D, A);
+    if (FIN) sweep_integrate(D, k, live, c > 0, c > 0 ? Wout[k] : make_float4(0.f, 0.f, 0.f, 0.f));
     return;
   }
   const uint32_t excl = incl - m;
@@ -2449,13 +2523,12 @@ __global__ void __launch_bounds__(kSweepBlockK, GG_SWEEP_RM_MINB) k_sweep_rm(Dev
     owner_sums(s_imp[wi], a0, a1, cb, ax, ay, az);
     __syncwarp();
   }
-  if (c > 0)
-    st_hint(&Wout[k],
-            make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
-                        static_cast<float>(static_cast<double>(wf.y) + ay),
-                        static_cast<float>(static_cast<double>(wf.z) + az), 0.f),
-            pol.last, kHintW);
+  const float4 wn = make_float4(static_cast<float>(static_cast<double>(wf.x) + ax),
+                                 static_cast<float>(static_cast<double>(wf.y) + ay),
+                                 static_cast<float>(static_cast<double>(wf.z) + az), 0.f);
+  if (c > 0 && !FIN) st_hint(&Wout[k], wn, pol.last, kHintW);
   sweep_acc_flush_nobar(D, A);
+  if (FIN) sweep_integrate(D, k, live, c > 0, wn);
 }
 
 // ONE_LOOP sweep (its own kernel: the inline collision test would cost the
